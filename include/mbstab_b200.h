@@ -1,0 +1,204 @@
+/*
+ * mbstab_b200.h -- C ABI of the B200-native multi-RHS BiCGStab hot path.
+ *
+ * Plain pointers and sizes only; every function returns an int status
+ * (MBG_OK == 0) and never throws.  mbg_last_error() returns the message of
+ * the last failure on the calling thread.  The C++ API in mbstab_b200.hpp
+ * wraps these calls and rethrows std::invalid_argument / std::runtime_error,
+ * matching the reference's error behaviour.
+ *
+ * Each entry point names the reference interface it replaces (paths relative
+ * to the reference tree, proj/...):
+ *
+ *   mbg_csr_upload        core::CsrMatrix + validate()     include/mbstab/core/csr.hpp:13-30,
+ *                                                           src/core/csr.cpp:8-32
+ *   mbg_mv_*              core::MultiVector                include/mbstab/core/types.hpp:13-35
+ *   mbg_spmv              core::spmv                       include/mbstab/core/spmv.hpp:16-17,
+ *                                                           src/core/spmv.cpp:54-74
+ *   mbg_spmv_traffic_bytes core::spmv_traffic_bytes        src/core/spmv.cpp:10-16
+ *   mbg_execute_group     kernels::execute_group           include/mbstab/kernels/execute.hpp:26-30,
+ *                                                           src/kernels/execute.cpp:123-172
+ *   mbg_analyze_traffic   kernels::analyze_traffic         include/mbstab/kernels/statement.hpp:65
+ *   mbg_split_basic_traffic kernels::split_basic (+ analyze) include/mbstab/kernels/statement.hpp:73
+ *   mbg_solve             solvers::solve (missing in the reference: proj/CMakeLists.txt:31;
+ *                                           contract SPEC.md:227-235)
+ *   mbg_method_schedule   solvers::method_schedule (missing: CMakeLists.txt:32)
+ *   mbg_gen_*             core::gen_poisson_7pt            src/core/generators.cpp:37-67
+ *                         and the BASELINE.json config generators
+ *
+ * Numerics contract: no FMA contraction anywhere; SpMV
+ * sums each (row, column) sequentially in CSR order from 0.0; updates sum
+ * terms in statement order from 0.0; dot products are exact (correctly
+ * rounded), hence independent of launch shape and GPU count.
+ */
+#ifndef MBSTAB_B200_H
+#define MBSTAB_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MBG_OK 0
+#define MBG_ERR_INVALID 1    /* std::invalid_argument in the reference */
+#define MBG_ERR_RUNTIME 2    /* std::runtime_error (CUDA / NCCL failure) */
+#define MBG_ERR_BREAKDOWN 3  /* solver breakdown */
+
+#define MBG_MAX_TERMS 8
+
+typedef struct mbg_ctx mbg_ctx;
+typedef struct mbg_csr mbg_csr;
+typedef struct mbg_mv mbg_mv;
+
+/* ---- errors / version ------------------------------------------------- */
+const char* mbg_last_error(void);
+const char* mbg_version(void);
+
+/* ---- context: one CUDA device, its streams and (optionally) a NCCL comm */
+int mbg_ctx_create(int device, mbg_ctx** out);
+int mbg_ctx_destroy(mbg_ctx* ctx);
+int mbg_ctx_synchronize(mbg_ctx* ctx);
+/* Multi-GPU: join a communicator of `world` ranks (one process per GPU).
+ * nccl_id is the 128-byte ncclUniqueId created by rank 0 (mbg_comm_unique_id)
+ * and broadcast by the caller (e.g. torch.distributed). */
+int mbg_comm_unique_id(unsigned char out_id[128]);
+int mbg_ctx_init_comm(mbg_ctx* ctx, int rank, int world, const unsigned char nccl_id[128]);
+
+/* ---- CSR matrix ----------------------------------------------------------
+ * Square CSR, offsets int64[n+1], cols int32[nnz] strictly increasing per
+ * row, vals fp64[nnz].  Validated like CsrMatrix::validate (csr.cpp:8-32). */
+int mbg_csr_validate(int64_t n, const int64_t* offsets, const int32_t* cols, int64_t nnz);
+int mbg_csr_upload(mbg_ctx* ctx, int64_t n, const int64_t* offsets, const int32_t* cols,
+                   const double* vals, mbg_csr** out);
+/* Partitioned upload for multi-GPU (one process per GPU): rows are split in
+ * nparts contiguous blocks, part p owning global rows [bounds[p], bounds[p+1]);
+ * this context's rank owns part my_part.  The full host CSR is given; the halo
+ * plan (renumbered local CSR, per-peer send lists and receive windows,
+ * interior / boundary row split) is built from its column pattern. */
+int mbg_csr_upload_partitioned(mbg_ctx* ctx, int64_t n, const int64_t* offsets, const int32_t* cols,
+                               const double* vals, int nparts, const int64_t* bounds, int my_part,
+                               mbg_csr** out);
+/* Host-only view of the same halo plan (no device): call once with
+ * loc_off == NULL for the sizes, then with buffers of n_own+1, nnz_local,
+ * n_halo, npeers and sum(peer_send_count) entries. */
+int mbg_halo_plan(int64_t n, const int64_t* offsets, const int32_t* cols, const double* vals, int nparts,
+                  const int64_t* bounds, int my_part, int64_t* n_own, int64_t* n_halo, int64_t* nnz_local,
+                  int32_t* loc_off, int32_t* loc_col, double* loc_val, int64_t* halo_global, int* npeers,
+                  int* peer_part, int64_t* peer_send_count, int32_t* peer_send_rows,
+                  int64_t* peer_recv_offset, int64_t* peer_recv_count);
+int mbg_csr_free(mbg_csr* a);
+int64_t mbg_csr_rows(const mbg_csr* a);   /* local rows */
+int64_t mbg_csr_nnz(const mbg_csr* a);    /* local nnz */
+
+/* ---- multivector: n x m fp64, row-interleaved (element (i,c) at i*m+c) -- */
+int mbg_mv_alloc(mbg_ctx* ctx, int64_t n, int m, mbg_mv** out);
+int mbg_mv_free(mbg_mv* v);
+int mbg_mv_upload(mbg_mv* v, const double* host);     /* n*m doubles */
+int mbg_mv_download(const mbg_mv* v, double* host);   /* n*m doubles */
+int mbg_mv_fill(mbg_mv* v, double value);
+double* mbg_mv_device_ptr(mbg_mv* v);
+
+/* ---- SpMV / SpMM --------------------------------------------------------
+ * y(i,c) = sum_k A(i,k) x(k,c); throws invalid on shape mismatch or x == y
+ * (spmv.cpp:20-25).  Enqueued on the context stream. */
+int mbg_spmv(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* x, mbg_mv* y);
+double mbg_spmv_traffic_bytes(int64_t n, int64_t nnz, int m);           /* Eq. (3) */
+double mbg_spmv_compulsory_bytes(int64_t n, int64_t nnz, int m);        /* x once */
+
+/* ---- statement groups (statement.hpp:13-45) ------------------------------ */
+#define MBG_STMT_UPDATE 0
+#define MBG_STMT_DOT 1
+typedef struct mbg_statement {
+    int kind;                                  /* MBG_STMT_UPDATE / MBG_STMT_DOT */
+    int out;                                   /* update: output vector id */
+    int nterms;                                /* update: number of terms */
+    int term_vec[MBG_MAX_TERMS];               /* update: operand vector ids */
+    const double* term_coeff[MBG_MAX_TERMS];   /* update: host arrays of m coeffs */
+    int left, right, slot;                     /* dot: operands and result slot */
+} mbg_statement;
+
+/* Traffic in whole-vector-transfer units (statement.cpp:25-56). */
+int mbg_analyze_traffic(const mbg_statement* stmts, int nstmts, int* reads, int* writes);
+/* split_basic(group) followed by analyze_traffic of each piece, summed
+ * (statement.cpp:58-85); also returns the number of pieces. */
+int mbg_split_basic_traffic(const mbg_statement* stmts, int nstmts, int first_temp_id,
+                            int* reads, int* writes, int* ngroups);
+/* Single-pass fused execution on the GPU (execute.cpp:123-172).
+ * vectors[id] are device multivectors of identical shape; dot_results is a
+ * HOST array of nslots*m doubles: slot s, column c at s*m+c (exact dots). */
+int mbg_execute_group(mbg_ctx* ctx, const mbg_statement* stmts, int nstmts, mbg_mv* const* vectors,
+                      int nvectors, double* dot_results, int nslots);
+
+/* ---- solver --------------------------------------------- */
+#define MBG_BICGSTAB 0
+#define MBG_RBICGSTAB 1
+#define MBG_PIPEBICGSTAB 2
+#define MBG_MERGED 0
+#define MBG_BASIC 1
+
+typedef struct mbg_report {
+    int iterations;
+    int converged;
+    int breakdown;          /* 0 none; 1 alpha (delta), 2 omega, 3 beta */
+    int breakdown_iter;
+    int breakdown_col;
+    /* traffic counted like TrafficCounter (types.hpp:95-109) */
+    int64_t vector_reads;
+    int64_t vector_writes;
+    double spmv_bytes;          /* Eq. (3) */
+    double compulsory_bytes;    /* roofline byte model */
+    int64_t reductions;         /* reduction points executed */
+    int64_t gpu_launches;       /* kernels launched by the solve loop */
+    double loop_ms;             /* device time of the iteration loop */
+} mbg_report;
+
+/* X holds x0 on entry and the solution on exit.  hist: host array of
+ * (max_iters+1)*m doubles or NULL; row j = relative recursive residual h_j.
+ * fixed != 0: run exactly max_iters iterations (benchmark mode). */
+int mbg_solve(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* b, mbg_mv* x, int method,
+              int formulation, double tol, int fixed, int max_iters, double* hist,
+              mbg_report* report);
+/* Same solve with HOST b/x buffers (n*m doubles): uploads b and x0, solves,
+ * downloads x.  The reference-facing end-to-end entry point. */
+int mbg_solve_host(mbg_ctx* ctx, const mbg_csr* a, int m, const double* b_host, double* x_host,
+                   int method, int formulation, double tol, int fixed, int max_iters,
+                   double* hist, mbg_report* report);
+
+/* Profiling solve (bench.py roofline): identical numerics, launched without a
+ * graph with CUDA events around every kernel of the iteration loop; writes
+ * {"label": [launches, total_ms, algorithmic_bytes_per_launch], ...} to json. */
+int mbg_solve_profile(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* b, mbg_mv* x, int method,
+                      int formulation, double tol, int fixed, int max_iters, char* json, int cap,
+                      mbg_report* report);
+
+/* Per-iteration schedule totals: vector reads/writes,
+ * SpMVs, reduction points and dots per reduction (up to 8 entries). */
+int mbg_method_schedule(int method, int formulation, int* reads, int* writes, int* spmvs,
+                        int* nreductions, int* dots_per_reduction);
+
+/* ---- config generators (host) --------------------------------------------
+ * kind 0 Poisson 7-pt (gen_poisson_7pt), 1 conv-diff 7-pt, 2 27-pt perturbed.
+ * Two-phase: call with NULL cols/vals to get nnz (offsets may be NULL too). */
+int mbg_gen_stencil(int kind, int nx, int ny, int nz, uint64_t seed, int64_t* nnz,
+                    int64_t* offsets, int32_t* cols, double* vals);
+int mbg_gen_banded(int64_t n, int64_t band, int kmin, int kmax, uint64_t seed, int64_t* nnz,
+                   int64_t* offsets, int32_t* cols, double* vals);
+int mbg_gen_rhs(int64_t n, int m, uint64_t seed, double* b);
+
+/* ---- exact-dot limb format (host hooks for partition tests) ----------------
+ * A slot is mbg_exact_slot_words() int64 words per column.  accumulate adds
+ * RN(a(i,c)*b(i,c)) exactly into D[c]; slots from different row ranges or
+ * ranks combine by int64 addition; round gives the correctly rounded sum. */
+int mbg_exact_slot_words(void);
+int mbg_exact_accumulate_host(int64_t n, int m, const double* a, const double* b, int64_t* D);
+int mbg_exact_round_host(const int64_t* D, int count, double* out);
+
+/* number of kernels this context has launched (telemetry) */
+int64_t mbg_ctx_launches(const mbg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

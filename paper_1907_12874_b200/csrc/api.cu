@@ -1,0 +1,539 @@
+// api.cpp -- the C ABI (include/mbstab_b200.h): context, containers, SpMV,
+// execute_group and solve.  No exception crosses the boundary; invalid usage
+// maps to MBG_ERR_INVALID with the reference's message text.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "comm.hpp"
+#include "common.hpp"
+#include "kernels.hpp"
+#include "solver.hpp"
+
+namespace mbg {
+
+static thread_local std::string g_error;
+void set_error(const std::string& msg) { g_error = msg; }
+
+template <class F>
+static int guarded(F&& f) {
+    try {
+        f();
+        return MBG_OK;
+    } catch (const Invalid& e) {
+        set_error(e.what());
+        return MBG_ERR_INVALID;
+    } catch (const Breakdown& e) {
+        set_error(e.what());
+        return MBG_ERR_BREAKDOWN;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return MBG_ERR_RUNTIME;
+    }
+}
+
+static void use(mbg_ctx* ctx) {
+    if (!ctx) throw Invalid("null context");
+    MBG_CUDA(cudaSetDevice(ctx->device));
+}
+
+// CsrMatrix::validate (csr.cpp:8-32), same messages.
+static void validate_csr(int64_t n, const int64_t* off, const int32_t* col, int64_t nnz) {
+    if (n < 0) throw Invalid("csr: negative row count");
+    if (!off) throw Invalid("csr: row_offsets length must be n_rows+1");
+    if (off[0] != 0) throw Invalid("csr: row_offsets[0] must be 0");
+    if (off[n] != nnz) throw Invalid("csr: row_offsets back must equal nnz");
+    for (int64_t i = 0; i < n; ++i) {
+        if (off[i] > off[i + 1])
+            throw Invalid("csr: row_offsets not non-decreasing at row " + std::to_string(i));
+        for (int64_t k = off[i]; k < off[i + 1]; ++k) {
+            const int32_t c = col[k];
+            if (c < 0 || c >= n) throw Invalid("csr: column index out of range in row " + std::to_string(i));
+            if (k > off[i] && col[k - 1] >= c)
+                throw Invalid("csr: column indices not strictly increasing in row " + std::to_string(i));
+        }
+    }
+}
+
+template <class T>
+static void upload(DevBuf<T>& d, const T* h, size_t n, cudaStream_t st) {
+    d.alloc(n);
+    if (n) MBG_CUDA(cudaMemcpyAsync(d.p, h, n * sizeof(T), cudaMemcpyHostToDevice, st));
+}
+
+}  // namespace mbg
+
+using namespace mbg;
+
+extern "C" const char* mbg_last_error(void) { return g_error.c_str(); }
+extern "C" const char* mbg_version(void) { return "mbstab_b200 0.1 (sm_100a)"; }
+
+extern "C" int mbg_ctx_create(int device, mbg_ctx** out) {
+    return guarded([&] {
+        if (!out) throw Invalid("null output");
+        int ndev = 0;
+        MBG_CUDA(cudaGetDeviceCount(&ndev));
+        if (device < 0 || device >= ndev) throw Invalid("ctx_create: no such CUDA device");
+        MBG_CUDA(cudaSetDevice(device));
+        auto* c = new mbg_ctx();
+        c->device = device;
+        MBG_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+        MBG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        MBG_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        *out = c;
+    });
+}
+
+extern "C" int mbg_ctx_destroy(mbg_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamSynchronize(ctx->side);
+        comm_destroy(ctx);
+        ctx->scratch_i64.release();
+        ctx->scratch_f64.release();
+        ctx->scratch_ctl.release();
+        ctx->pool.clear();
+        cudaStreamDestroy(ctx->stream);
+        cudaStreamDestroy(ctx->side);
+        delete ctx;
+    });
+}
+
+extern "C" int mbg_ctx_synchronize(mbg_ctx* ctx) {
+    return guarded([&] {
+        use(ctx);
+        MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+        MBG_CUDA(cudaStreamSynchronize(ctx->side));
+    });
+}
+
+extern "C" int mbg_csr_validate(int64_t n, const int64_t* off, const int32_t* col, int64_t nnz) {
+    return guarded([&] { validate_csr(n, off, col, nnz); });
+}
+
+static void csr_to_device(mbg_ctx* ctx, mbg_csr* a, int64_t n, const int64_t* off, const int32_t* col,
+                          const double* val) {
+    const int64_t nnz = off[n];
+    if (nnz > INT32_MAX) throw Invalid("csr: nnz >= 2^31 needs 64-bit offsets (not supported)");
+    std::vector<int32_t> off32(n + 1);
+    for (int64_t i = 0; i <= n; ++i) off32[i] = static_cast<int32_t>(off[i]);
+    upload(a->off, off32.data(), off32.size(), ctx->stream);
+    upload(a->col, col, nnz, ctx->stream);
+    upload(a->val, val, nnz, ctx->stream);
+    MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+    a->n = n;
+    a->nnz = nnz;
+}
+
+extern "C" int mbg_csr_upload(mbg_ctx* ctx, int64_t n, const int64_t* off, const int32_t* col,
+                              const double* val, mbg_csr** out) {
+    return guarded([&] {
+        use(ctx);
+        if (!out) throw Invalid("null output");
+        validate_csr(n, off, col, off ? off[n] : 0);
+        auto* a = new mbg_csr();
+        try {
+            a->ctx = ctx;
+            a->n_global = n;
+            csr_to_device(ctx, a, n, off, col, val);
+        } catch (...) {
+            delete a;
+            throw;
+        }
+        *out = a;
+    });
+}
+
+// Partitioned upload: parts given by bounds[nparts+1]; this context's rank is
+// my_part.  Builds the halo plan from the full host CSR.
+extern "C" int mbg_csr_upload_partitioned(mbg_ctx* ctx, int64_t n, const int64_t* off, const int32_t* col,
+                                          const double* val, int nparts, const int64_t* bounds, int my_part,
+                                          mbg_csr** out) {
+    return guarded([&] {
+        use(ctx);
+        if (!out) throw Invalid("null output");
+        validate_csr(n, off, col, off ? off[n] : 0);
+        HaloPlan pl = build_halo_plan(n, off, col, val, nparts, bounds, my_part);
+        auto* a = new mbg_csr();
+        try {
+            a->ctx = ctx;
+            a->n_global = n;
+            a->row_begin = bounds[my_part];
+            a->n = pl.n_own;
+            a->nnz = pl.nnz;
+            a->n_halo = pl.n_halo;
+            upload(a->off, pl.off.data(), pl.off.size(), ctx->stream);
+            upload(a->col, pl.col.data(), pl.col.size(), ctx->stream);
+            upload(a->val, pl.val.data(), pl.val.size(), ctx->stream);
+            if (nparts > 1) {
+                upload(a->interior_rows, pl.interior.data(), pl.interior.size(), ctx->stream);
+                upload(a->boundary_rows, pl.boundary.data(), pl.boundary.size(), ctx->stream);
+                a->n_interior = static_cast<int64_t>(pl.interior.size());
+                a->n_boundary = static_cast<int64_t>(pl.boundary.size());
+                for (auto& p : pl.peers) {
+                    mbg_csr::Peer q;
+                    q.rank = p.part;
+                    q.send_count = static_cast<int64_t>(p.send_rows.size());
+                    q.recv_count = p.recv_count;
+                    q.recv_offset = p.recv_offset;
+                    upload(q.send_rows, p.send_rows.data(), p.send_rows.size(), ctx->stream);
+                    a->peers.push_back(std::move(q));
+                }
+            }
+            MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+        } catch (...) {
+            delete a;
+            throw;
+        }
+        *out = a;
+    });
+}
+
+// Host-only halo plan for tests of the partition logic (no device needed).
+extern "C" int mbg_halo_plan(int64_t n, const int64_t* off, const int32_t* col, const double* val, int nparts,
+                             const int64_t* bounds, int my_part, int64_t* n_own, int64_t* n_halo,
+                             int64_t* nnz_local, int32_t* loc_off, int32_t* loc_col, double* loc_val,
+                             int64_t* halo_global, int* npeers, int* peer_part, int64_t* peer_send_count,
+                             int32_t* peer_send_rows, int64_t* peer_recv_offset, int64_t* peer_recv_count) {
+    return guarded([&] {
+        HaloPlan pl = build_halo_plan(n, off, col, val, nparts, bounds, my_part);
+        *n_own = pl.n_own;
+        *n_halo = pl.n_halo;
+        *nnz_local = pl.nnz;
+        *npeers = static_cast<int>(pl.peers.size());
+        if (!loc_off) return;  // sizes only
+        std::memcpy(loc_off, pl.off.data(), pl.off.size() * sizeof(int32_t));
+        std::memcpy(loc_col, pl.col.data(), pl.col.size() * sizeof(int32_t));
+        std::memcpy(loc_val, pl.val.data(), pl.val.size() * sizeof(double));
+        std::memcpy(halo_global, pl.halo_global.data(), pl.halo_global.size() * sizeof(int64_t));
+        int64_t so = 0;
+        for (size_t i = 0; i < pl.peers.size(); ++i) {
+            const auto& p = pl.peers[i];
+            peer_part[i] = p.part;
+            peer_send_count[i] = static_cast<int64_t>(p.send_rows.size());
+            peer_recv_offset[i] = p.recv_offset;
+            peer_recv_count[i] = p.recv_count;
+            std::memcpy(peer_send_rows + so, p.send_rows.data(), p.send_rows.size() * sizeof(int32_t));
+            so += static_cast<int64_t>(p.send_rows.size());
+        }
+    });
+}
+
+extern "C" int mbg_csr_free(mbg_csr* a) {
+    return guarded([&] {
+        if (!a) return;
+        if (a->ctx) cudaSetDevice(a->ctx->device);
+        delete a;
+    });
+}
+
+extern "C" int64_t mbg_csr_rows(const mbg_csr* a) { return a ? a->n : -1; }
+extern "C" int64_t mbg_csr_nnz(const mbg_csr* a) { return a ? a->nnz : -1; }
+
+extern "C" int mbg_mv_alloc(mbg_ctx* ctx, int64_t n, int m, mbg_mv** out) {
+    return guarded([&] {
+        use(ctx);
+        if (!out) throw Invalid("null output");
+        if (n < 0 || m < 1) throw Invalid("multivector: bad shape");
+        auto* v = new mbg_mv();
+        v->ctx = ctx;
+        v->n = n;
+        v->n_alloc = n;
+        v->m = m;
+        try {
+            v->data.alloc(static_cast<size_t>(n) * m);
+            if (n) MBG_CUDA(cudaMemsetAsync(v->data.p, 0, static_cast<size_t>(n) * m * sizeof(double), ctx->stream));
+            MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+        } catch (...) {
+            delete v;
+            throw;
+        }
+        *out = v;
+    });
+}
+
+extern "C" int mbg_mv_free(mbg_mv* v) {
+    return guarded([&] {
+        if (!v) return;
+        if (v->ctx) cudaSetDevice(v->ctx->device);
+        delete v;
+    });
+}
+
+extern "C" int mbg_mv_upload(mbg_mv* v, const double* host) {
+    return guarded([&] {
+        if (!v) throw Invalid("null multivector");
+        use(v->ctx);
+        const size_t cnt = static_cast<size_t>(v->n) * v->m;
+        if (cnt) MBG_CUDA(cudaMemcpyAsync(v->data.p, host, cnt * sizeof(double), cudaMemcpyHostToDevice, v->ctx->stream));
+        MBG_CUDA(cudaStreamSynchronize(v->ctx->stream));
+    });
+}
+
+extern "C" int mbg_mv_download(const mbg_mv* v, double* host) {
+    return guarded([&] {
+        if (!v) throw Invalid("null multivector");
+        use(v->ctx);
+        const size_t cnt = static_cast<size_t>(v->n) * v->m;
+        if (cnt) MBG_CUDA(cudaMemcpyAsync(host, v->data.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, v->ctx->stream));
+        MBG_CUDA(cudaStreamSynchronize(v->ctx->stream));
+    });
+}
+
+__global__ void mv_fill_kernel(double* p, int64_t n, double v) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+
+extern "C" int mbg_mv_fill(mbg_mv* v, double value) {
+    return guarded([&] {
+        if (!v) throw Invalid("null multivector");
+        use(v->ctx);
+        const int64_t cnt = v->n * v->m;
+        if (cnt) {
+            mv_fill_kernel<<<v->ctx->num_sms * 4, 256, 0, v->ctx->stream>>>(v->data.p, cnt, value);
+            MBG_CUDA(cudaGetLastError());
+            v->ctx->launches++;
+        }
+        MBG_CUDA(cudaStreamSynchronize(v->ctx->stream));
+    });
+}
+
+extern "C" double* mbg_mv_device_ptr(mbg_mv* v) { return v ? v->data.p : nullptr; }
+
+// core::spmv (spmv.cpp:54-74): shape / aliasing checks, then the SpMM.
+extern "C" int mbg_spmv(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* x, mbg_mv* y) {
+    return guarded([&] {
+        use(ctx);
+        if (!a || !x || !y) throw Invalid("spmv: null argument");
+        if (x->n != a->n || y->n != a->n || x->m != y->m) throw Invalid("spmv: dimension mismatch");
+        if (x == y || x->data.p == y->data.p) throw Invalid("spmv: x and y must be distinct storage");
+        const int m = x->m;
+        double* xin = x->data.p;
+        if (a->n_halo) {
+            // partitioned: stage x in a buffer with halo room
+            ctx->scratch_f64.ensure(static_cast<size_t>(a->n + a->n_halo) * m);
+            MBG_CUDA(cudaMemcpyAsync(ctx->scratch_f64.p, xin, static_cast<size_t>(a->n) * m * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, ctx->stream));
+            xin = ctx->scratch_f64.p;
+        }
+        ctx->launches += apply_operator(ctx, a, m, xin, y->data.p, nullptr);
+        MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+// kernels::execute_group (execute.cpp:123-172), exact dots.
+extern "C" int mbg_execute_group(mbg_ctx* ctx, const mbg_statement* st, int ns, mbg_mv* const* vectors,
+                                 int nvec, double* dot_results, int nslots) {
+    return guarded([&] {
+        use(ctx);
+        if (ns < 0 || (ns > 0 && !st)) throw Invalid("execute_group: bad statement array");
+        if (ns == 0) return;  // empty group: no-op (execute.cpp:129)
+        if (ns > GEN_MAX_STMT) throw Invalid("execute_group: too many statements");
+        if (nvec > GEN_MAX_VEC) throw Invalid("execute_group: too many vectors");
+        auto vec = [&](int id) -> mbg_mv* {
+            if (id < 0 || id >= nvec || !vectors[id]) throw Invalid("execute_group: unbound vector id");
+            return vectors[id];
+        };
+        int64_t n = -1;
+        int m = -1;
+        auto note = [&](mbg_mv* v) {
+            if (n < 0) { n = v->n; m = v->m; }
+            else if (v->n != n || v->m != m) throw Invalid("execute_group: shape mismatch");
+        };
+        GenericGroup g{};
+        g.nstmt = ns;
+        std::vector<double> coef;
+        int used_slots = 0;
+        int nterm_total = 0;
+        for (int i = 0; i < ns; ++i) {
+            if (st[i].kind == MBG_STMT_UPDATE) {
+                note(vec(st[i].out));
+                if (st[i].nterms < 0 || st[i].nterms > MBG_MAX_TERMS) throw Invalid("execute_group: too many terms");
+                g.kind[i] = MBG_STMT_UPDATE;
+                g.out[i] = st[i].out;
+                g.nterms[i] = st[i].nterms;
+                g.tfirst[i] = nterm_total;
+                for (int t = 0; t < st[i].nterms; ++t) {
+                    note(vec(st[i].term_vec[t]));
+                    if (!st[i].term_coeff[t]) throw Invalid("execute_group: coefficient width mismatch");
+                    g.term_vec[nterm_total + t] = st[i].term_vec[t];
+                }
+                nterm_total += st[i].nterms;
+            } else if (st[i].kind == MBG_STMT_DOT) {
+                note(vec(st[i].left));
+                note(vec(st[i].right));
+                if (st[i].slot < 0 || st[i].slot >= nslots) throw Invalid("execute_group: dot slot out of range");
+                if (st[i].slot >= GEN_MAX_SLOT) throw Invalid("execute_group: too many dot slots");
+                g.kind[i] = MBG_STMT_DOT;
+                g.left[i] = st[i].left;
+                g.right[i] = st[i].right;
+                g.dslot[i] = st[i].slot;
+                used_slots = std::max(used_slots, st[i].slot + 1);
+            } else {
+                throw Invalid("execute_group: unknown statement kind");
+            }
+        }
+        coef.resize(static_cast<size_t>(nterm_total) * m);
+        for (int i = 0, t0 = 0; i < ns; ++i)
+            if (st[i].kind == MBG_STMT_UPDATE) {
+                for (int t = 0; t < st[i].nterms; ++t)
+                    std::memcpy(&coef[static_cast<size_t>(t0 + t) * m], st[i].term_coeff[t], m * sizeof(double));
+                t0 += st[i].nterms;
+            }
+        g.len = n * m;
+        g.m = m;
+        for (int i = 0; i < nvec; ++i) g.vec[i] = vectors[i] ? vectors[i]->data.p : nullptr;
+        g.nslots = used_slots;
+        const int max_blocks = ctx->num_sms * 8;
+        const size_t slot_words = static_cast<size_t>(used_slots) * m * NSLOT;
+        const size_t part_words = static_cast<size_t>(used_slots) * m * max_blocks * KEXP;
+        ctx->scratch_i64.ensure(2 * slot_words + 1);
+        ctx->scratch_f64.ensure(part_words + coef.size() + static_cast<size_t>(used_slots) * m + 1);
+        int64_t* slots = ctx->scratch_i64.p;
+        int64_t* D = slots + slot_words;
+        double* part = ctx->scratch_f64.p;
+        double* dcoef = part + part_words;
+        double* rounded = dcoef + coef.size();
+        if (slot_words) MBG_CUDA(cudaMemsetAsync(slots, 0, slot_words * sizeof(int64_t), ctx->stream));
+        if (!coef.empty())
+            MBG_CUDA(cudaMemcpyAsync(dcoef, coef.data(), coef.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                     ctx->stream));
+        g.coef = dcoef;
+        g.slot = slots;
+        g.part = part;
+        int nblocks = 0;
+        launch_generic_group(ctx->stream, g, ctx->num_sms, &nblocks);
+        ctx->launches++;
+        if (used_slots) {
+            for (int s0 = 0; s0 < used_slots; s0 += GMAX_DOT) {
+                FoldArgs f{};
+                f.m = m;
+                f.nblocks = nblocks;
+                const int cnt = std::min(GMAX_DOT, used_slots - s0);
+                for (int s = 0; s < cnt; ++s) {
+                    f.slot[s] = slots + static_cast<size_t>(s0 + s) * m * NSLOT;
+                    f.part[s] = part + static_cast<size_t>(s0 + s) * m * nblocks * KEXP;
+                    f.D[s] = D + static_cast<size_t>(s0 + s) * m * NSLOT;
+                }
+                launch_fold(ctx->stream, f, cnt);
+                ctx->launches++;
+            }
+            if (ctx->comm) comm_allreduce_i64(ctx, D, slot_words, ctx->stream);
+            launch_round(ctx->stream, D, used_slots, m, rounded);
+            ctx->launches++;
+            std::vector<double> h(static_cast<size_t>(used_slots) * m);
+            MBG_CUDA(cudaMemcpyAsync(h.data(), rounded, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+            MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+            for (int i = 0; i < ns; ++i)
+                if (st[i].kind == MBG_STMT_DOT)
+                    std::memcpy(dot_results + static_cast<size_t>(st[i].slot) * m,
+                                h.data() + static_cast<size_t>(st[i].slot) * m, m * sizeof(double));
+        } else {
+            MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
+    });
+}
+
+static void check_solve_args(mbg_ctx* ctx, const mbg_csr* a, int m, double tol, int fixed, int max_iters) {
+    use(ctx);
+    if (!a) throw Invalid("solve: null matrix");
+    if (m < 1) throw Invalid("solve: shape mismatch");
+    if (max_iters < 0) throw Invalid("solve: negative iteration count");
+    if (!fixed && !(tol > 0.0)) throw Invalid("solve: tol must be > 0 in converge mode");
+}
+
+static void do_solve(mbg_ctx* ctx, const mbg_csr* a, int m, const double* b, double* x, int method,
+                     int formulation, double tol, int fixed, int max_iters, double* hist, mbg_report* report) {
+    Solver s(ctx, a, m, method, formulation, tol, fixed, max_iters);
+    s.run(b, x);
+    mbg_report rep;
+    s.report(hist, &rep);
+    ctx->launches += rep.gpu_launches;
+    if (report) *report = rep;
+    if (rep.breakdown) {
+        static const char* what[] = {"", "delta (alpha)", "psi (omega)", "beta"};
+        throw Breakdown("solve: breakdown at iteration " + std::to_string(rep.breakdown_iter) + ", column " +
+                        std::to_string(rep.breakdown_col) + ": " + what[rep.breakdown & 3] +
+                        " denominator zero or non-finite");
+    }
+}
+
+extern "C" int mbg_solve(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* b, mbg_mv* x, int method, int formulation,
+                         double tol, int fixed, int max_iters, double* hist, mbg_report* report) {
+    return guarded([&] {
+        if (!b || !x) throw Invalid("solve: null multivector");
+        check_solve_args(ctx, a, b->m, tol, fixed, max_iters);
+        if (b->n != a->n || x->n != a->n || b->m != x->m) throw Invalid("solve: shape mismatch");
+        do_solve(ctx, a, b->m, b->data.p, x->data.p, method, formulation, tol, fixed, max_iters, hist, report);
+    });
+}
+
+extern "C" int mbg_solve_host(mbg_ctx* ctx, const mbg_csr* a, int m, const double* b_host, double* x_host,
+                              int method, int formulation, double tol, int fixed, int max_iters, double* hist,
+                              mbg_report* report) {
+    return guarded([&] {
+        check_solve_args(ctx, a, m, tol, fixed, max_iters);
+        if (!b_host || !x_host) throw Invalid("solve: null host buffer");
+        const size_t cnt = static_cast<size_t>(a->n) * m;
+        DevBuf<double> db(cnt), dx(cnt);
+        MBG_CUDA(cudaMemcpyAsync(db.p, b_host, cnt * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        MBG_CUDA(cudaMemcpyAsync(dx.p, x_host, cnt * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        try {
+            do_solve(ctx, a, m, db.p, dx.p, method, formulation, tol, fixed, max_iters, hist, report);
+        } catch (const Breakdown&) {
+            MBG_CUDA(cudaMemcpy(x_host, dx.p, cnt * sizeof(double), cudaMemcpyDeviceToHost));
+            throw;
+        }
+        MBG_CUDA(cudaMemcpy(x_host, dx.p, cnt * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
+// Profiling solve: same numerics, no graph, CUDA events around every launch.
+extern "C" int mbg_solve_profile(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* b, mbg_mv* x, int method,
+                                 int formulation, double tol, int fixed, int max_iters, char* json, int cap,
+                                 mbg_report* report) {
+    return guarded([&] {
+        if (!b || !x) throw Invalid("solve: null multivector");
+        check_solve_args(ctx, a, b->m, tol, fixed, max_iters);
+        if (b->n != a->n || x->n != a->n || b->m != x->m) throw Invalid("solve: shape mismatch");
+        Solver s(ctx, a, b->m, method, formulation, tol, fixed, max_iters);
+        s.enable_profile();
+        s.run(b->data.p, x->data.p);
+        mbg_report rep;
+        s.report(nullptr, &rep);
+        if (report) *report = rep;
+        const std::string js = s.profile_json();
+        if (json && cap > 0) {
+            std::strncpy(json, js.c_str(), static_cast<size_t>(cap) - 1);
+            json[cap - 1] = 0;
+        }
+    });
+}
+
+// ---- test hooks: host-side exact accumulation in the device limb format ----
+extern "C" int mbg_exact_accumulate_host(int64_t n, int m, const double* a, const double* b, int64_t* D) {
+    return guarded([&] {
+        for (int64_t i = 0; i < n; ++i)
+            for (int c = 0; c < m; ++c) {
+                const double p = a[i * m + c] * b[i * m + c];
+                digits_add(D + static_cast<int64_t>(c) * NSLOT, p);
+            }
+    });
+}
+
+extern "C" int mbg_exact_round_host(const int64_t* D, int count, double* out) {
+    return guarded([&] {
+        for (int i = 0; i < count; ++i) out[i] = digits_round(D + static_cast<int64_t>(i) * NSLOT);
+    });
+}
+
+extern "C" int mbg_exact_slot_words(void) { return NSLOT; }
+
+extern "C" int64_t mbg_ctx_launches(const mbg_ctx* ctx) { return ctx ? ctx->launches : -1; }

@@ -1,0 +1,132 @@
+// common.hpp -- shared host-side plumbing of the B200 library: error
+// handling across the C ABI, CUDA checks and the context / container structs.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "mbstab_b200.h"
+
+namespace mbg {
+
+// The reference throws std::invalid_argument for API misuse (spmv.cpp:20-25,
+// execute.cpp:42-82, csr.cpp:8-32) and the C ABI maps it to MBG_ERR_INVALID.
+struct Invalid : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct Breakdown : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void set_error(const std::string& msg);
+
+#define MBG_CUDA(call)                                                                        \
+    do {                                                                                      \
+        cudaError_t _e = (call);                                                              \
+        if (_e != cudaSuccess)                                                                \
+            throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(_e) +    \
+                                     " at " __FILE__ ":" + std::to_string(__LINE__) + ": " #call); \
+    } while (0)
+
+// Device buffer with RAII.
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        if (count) MBG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void ensure(size_t count) { if (count > n) alloc(count); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+struct Comm;  // comm.cu
+
+}  // namespace mbg
+
+// ---- ABI objects ------------------------------------------------------------
+struct mbg_ctx {
+    int device = 0;
+    int num_sms = 0;
+    cudaStream_t stream = nullptr;   // main stream: all hot-path kernels
+    cudaStream_t side = nullptr;     // side stream: overlapped reductions / halo
+    mbg::Comm* comm = nullptr;       // multi-GPU communicator (nullptr: single GPU)
+    // scratch for the API-level execute_group (reduction buffers)
+    mbg::DevBuf<int64_t> scratch_i64;
+    mbg::DevBuf<double> scratch_f64;
+    mbg::DevBuf<int> scratch_ctl;
+    int64_t launches = 0;            // kernels launched by this context
+    // pool of large work vectors reused across solves (no cudaMalloc per solve)
+    std::vector<mbg::DevBuf<double>> pool;
+};
+
+namespace mbg {
+inline DevBuf<double> pool_take(mbg_ctx* ctx, size_t n) {
+    for (size_t i = 0; i < ctx->pool.size(); ++i) {
+        if (ctx->pool[i].n >= n && ctx->pool[i].n <= 2 * n + (1u << 20)) {
+            DevBuf<double> b = std::move(ctx->pool[i]);
+            ctx->pool.erase(ctx->pool.begin() + static_cast<long>(i));
+            return b;
+        }
+    }
+    return DevBuf<double>(n);
+}
+inline void pool_give(mbg_ctx* ctx, DevBuf<double>&& b) {
+    if (b.p) ctx->pool.push_back(std::move(b));
+}
+}  // namespace mbg
+
+// Device CSR.  Offsets are stored int32 when nnz < 2^31 (the byte model's
+// 4-byte offsets, Eq. (3)); cols int32, vals fp64.  For a row partition the
+// local matrix has n_local rows and its columns are renumbered into the local
+// x layout [owned rows | halo rows] (see halo.cu).
+struct mbg_csr {
+    mbg_ctx* ctx = nullptr;
+    int64_t n_global = 0;
+    int64_t n = 0;            // local rows
+    int64_t nnz = 0;          // local nnz
+    int64_t row_begin = 0;    // first owned global row
+    mbg::DevBuf<int32_t> off;
+    mbg::DevBuf<int32_t> col;
+    mbg::DevBuf<double> val;
+    // multi-GPU halo plan (empty for a single GPU)
+    int64_t n_halo = 0;                       // halo rows appended after the owned rows
+    mbg::DevBuf<int32_t> interior_rows;       // rows whose columns are all owned
+    mbg::DevBuf<int32_t> boundary_rows;       // rows touching halo columns
+    int64_t n_interior = 0, n_boundary = 0;
+    struct Peer {
+        int rank;
+        int64_t send_count, recv_count;
+        int64_t recv_offset;                  // first halo slot for this peer
+        mbg::DevBuf<int32_t> send_rows;       // local rows packed for this peer
+    };
+    std::vector<Peer> peers;
+};
+
+struct mbg_mv {
+    mbg_ctx* ctx = nullptr;
+    int64_t n = 0;        // rows (owned)
+    int64_t n_alloc = 0;  // rows allocated (owned + halo capacity)
+    int m = 0;
+    mbg::DevBuf<double> data;
+};

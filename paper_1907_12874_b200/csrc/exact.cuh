@@ -1,0 +1,216 @@
+// exact.cuh -- exact (correctly rounded, order-independent) dot products.
+//
+// Replaces the reference's thread-blocked naive dot (execute.cpp:112-117,
+// 141-157), whose result depends on the thread count (execute.hpp:23-24).
+// An exact dot gives the same bits on 1 GPU, N GPUs and the CPU oracle
+// (DESIGN.md "Parity").
+//
+// Representation
+//   * per thread: a K-term floating-point expansion grown with TwoSum
+//     (error-free); a residual that does not fit after K levels is deposited
+//     exactly into the slot's long accumulator with integer atomics.
+//   * long accumulator ("digits"): NDIG int64 words, word j counts units of
+//     2^(32 j - 1074); three trailing counters record +inf / -inf / NaN
+//     products.  Integer addition is associative, so digits from any number of
+//     blocks or ranks (ncclInt64 sum) combine exactly.
+//   * rounding: carry-normalise, take the top 64 bits plus a sticky bit and
+//     round to nearest even, building the IEEE bits directly.
+#pragma once
+
+#include <cstdint>
+
+#ifndef __CUDACC__
+#define __host__
+#define __device__
+#define __forceinline__ inline
+#endif
+
+namespace mbg {
+
+constexpr int NDIG = 68;          // 68*32 bits >= 2098-bit double range + carry room
+constexpr int NSLOT = 72;         // digits + 3 non-finite counters + pad (int64 words)
+constexpr int IDX_PINF = NDIG, IDX_NINF = NDIG + 1, IDX_NAN = NDIG + 2;
+constexpr int KEXP = 3;           // expansion length per thread accumulator
+
+__host__ __device__ __forceinline__ uint64_t dbits(double x) {
+#ifdef __CUDA_ARCH__
+    return static_cast<uint64_t>(__double_as_longlong(x));
+#else
+    uint64_t b;
+    __builtin_memcpy(&b, &x, 8);
+    return b;
+#endif
+}
+
+__host__ __device__ __forceinline__ double bitsd(uint64_t b) {
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double(static_cast<long long>(b));
+#else
+    double x;
+    __builtin_memcpy(&x, &b, 8);
+    return x;
+#endif
+}
+
+// Decompose a finite nonzero double into (word index j, three 32-bit chunks).
+struct Chunks {
+    int j;
+    int64_t c0, c1, c2;
+    bool neg;
+};
+
+__host__ __device__ __forceinline__ bool decompose(double x, Chunks& out, int& nonfinite_idx) {
+    const uint64_t b = dbits(x);
+    const int ex = static_cast<int>((b >> 52) & 0x7ff);
+    uint64_t mant = b & ((1ull << 52) - 1);
+    out.neg = (b >> 63) != 0;
+    nonfinite_idx = -1;
+    if (ex == 0x7ff) {
+        nonfinite_idx = mant ? IDX_NAN : (out.neg ? IDX_NINF : IDX_PINF);
+        return false;
+    }
+    int pos;
+    if (ex == 0) {
+        pos = 0;
+    } else {
+        mant |= 1ull << 52;
+        pos = ex - 1;
+    }
+    if (!mant) return false;
+    out.j = pos >> 5;
+    const int sh = pos & 31;
+    // mant << sh spans at most 85 bits: split into three 32-bit chunks
+    const uint64_t lo = mant << sh;                         // low 64 bits
+    const uint64_t hi = sh ? (mant >> (64 - sh)) : 0ull;    // bits 64..84
+    out.c0 = static_cast<int64_t>(lo & 0xffffffffull);
+    out.c1 = static_cast<int64_t>(lo >> 32);
+    out.c2 = static_cast<int64_t>(hi);
+    return true;
+}
+
+// Non-atomic deposit (fold kernels, host).
+__host__ __device__ __forceinline__ void digits_add(int64_t* d, double x) {
+    Chunks c;
+    int nf;
+    if (!decompose(x, c, nf)) {
+        if (nf >= 0) d[nf] += 1;
+        return;
+    }
+    if (c.neg) {
+        d[c.j] -= c.c0; d[c.j + 1] -= c.c1; d[c.j + 2] -= c.c2;
+    } else {
+        d[c.j] += c.c0; d[c.j + 1] += c.c1; d[c.j + 2] += c.c2;
+    }
+}
+
+#ifdef __CUDACC__
+// Atomic deposit into a global slot (rare overflow path of the expansions).
+__device__ __forceinline__ void digits_add_atomic(int64_t* d, double x) {
+    Chunks c;
+    int nf;
+    auto* u = reinterpret_cast<unsigned long long*>(d);
+    if (!decompose(x, c, nf)) {
+        if (nf >= 0) atomicAdd(u + nf, 1ull);
+        return;
+    }
+    const unsigned long long s0 = static_cast<unsigned long long>(c.neg ? -c.c0 : c.c0);
+    const unsigned long long s1 = static_cast<unsigned long long>(c.neg ? -c.c1 : c.c1);
+    const unsigned long long s2 = static_cast<unsigned long long>(c.neg ? -c.c2 : c.c2);
+    if (s0) atomicAdd(u + c.j, s0);
+    if (s1) atomicAdd(u + c.j + 1, s1);
+    if (s2) atomicAdd(u + c.j + 2, s2);
+}
+
+// TwoSum-grow x into the expansion a[0..K-1]; the residual (if any) and any
+// non-finite value go to the slot's long accumulator.
+__device__ __forceinline__ void grow(double (&a)[KEXP], double x, int64_t* slot) {
+    if (x == 0.0) return;
+    if (!isfinite(x)) { digits_add_atomic(slot, x); return; }
+#pragma unroll
+    for (int i = 0; i < KEXP; ++i) {
+        const double s = __dadd_rn(a[i], x);
+        if (!isfinite(s)) { digits_add_atomic(slot, x); return; }
+        const double bv = __dsub_rn(s, a[i]);
+        const double av = __dsub_rn(s, bv);
+        const double err = __dadd_rn(__dsub_rn(a[i], av), __dsub_rn(x, bv));
+        a[i] = s;
+        x = err;
+        if (x == 0.0) return;
+    }
+    digits_add_atomic(slot, x);
+}
+#endif
+
+// Carry-normalise in place: words 0..NDIG-2 in [0, 2^32), top word signed.
+__host__ __device__ __forceinline__ void digits_normalize(int64_t* d) {
+    int64_t carry = 0;
+    for (int j = 0; j < NDIG - 1; ++j) {
+        const int64_t v = d[j] + carry;
+        carry = v >> 32;  // arithmetic shift = floor division
+        d[j] = v & 0xffffffffll;
+    }
+    d[NDIG - 1] += carry;
+}
+
+__host__ __device__ __forceinline__ int bitlen32(uint64_t v) {
+#ifdef __CUDA_ARCH__
+    return 64 - __clzll(static_cast<long long>(v));
+#else
+    return v ? 64 - __builtin_clzll(v) : 0;
+#endif
+}
+
+// Correctly rounded value of a slot (round to nearest, ties to even).
+__host__ __device__ inline double digits_round(const int64_t* src) {
+    const int64_t pinf = src[IDX_PINF], ninf = src[IDX_NINF], nan = src[IDX_NAN];
+    if (nan || (pinf && ninf)) return bitsd(0x7ff8000000000000ull);
+    if (pinf) return bitsd(0x7ff0000000000000ull);
+    if (ninf) return bitsd(0xfff0000000000000ull);
+    int64_t d[NDIG];
+    for (int j = 0; j < NDIG; ++j) d[j] = src[j];
+    digits_normalize(d);
+    const bool neg = d[NDIG - 1] < 0;
+    if (neg) {
+        for (int j = 0; j < NDIG; ++j) d[j] = -d[j];
+        digits_normalize(d);
+    }
+    int h = NDIG - 1;
+    while (h >= 0 && d[h] == 0) --h;
+    if (h < 0) return 0.0;
+    const int L = bitlen32(static_cast<uint64_t>(d[h]));  // 1..32
+    const int bitlen = 32 * h + L;
+    uint64_t out;
+    if (bitlen <= 53) {
+        // exact: the bit pattern of mag * 2^-1074 is mag itself
+        const uint64_t mag = (h >= 1 ? (static_cast<uint64_t>(d[1]) << 32) : 0ull) | static_cast<uint64_t>(d[0]);
+        out = mag;
+    } else {
+        uint64_t top;      // top 64 bits of the magnitude, MSB set
+        bool sticky;
+        if (bitlen <= 64) {
+            const uint64_t mag = (static_cast<uint64_t>(d[1]) << 32) | static_cast<uint64_t>(d[0]);
+            top = mag << (64 - bitlen);
+            sticky = false;
+        } else {
+            const uint64_t whi = (static_cast<uint64_t>(d[h]) << 32) | static_cast<uint64_t>(d[h - 1]);
+            const uint64_t wlo = static_cast<uint64_t>(d[h - 2]);
+            top = (whi << (32 - L)) | (wlo >> L);
+            sticky = (wlo & ((1ull << L) - 1)) != 0;
+            for (int j = 0; j < h - 2 && !sticky; ++j) sticky = d[j] != 0;
+        }
+        uint64_t keep = top >> 11;
+        const bool rbit = (top >> 10) & 1;
+        sticky = sticky || (top & 0x3ff) != 0;
+        int shift = bitlen - 53;
+        if (rbit && (sticky || (keep & 1))) ++keep;
+        if (keep == (1ull << 53)) { keep >>= 1; ++shift; }
+        const int biased = shift + 1;
+        if (biased >= 2047)
+            out = 0x7ff0000000000000ull;
+        else
+            out = (static_cast<uint64_t>(biased) << 52) | (keep & ((1ull << 52) - 1));
+    }
+    return bitsd(out | (neg ? 0x8000000000000000ull : 0ull));
+}
+
+}  // namespace mbg

@@ -1,0 +1,328 @@
+// group.cuh -- single-pass fused vector-update + exact-dot kernels.
+//
+// B200 replacement of kernels::execute_group (execute.cpp:123-172): one pass
+// over the n x m interleaved elements, every statement of a merged line
+// evaluated per element in order with produced values kept in registers
+// (the reference's register-reuse rule, statement.hpp:34-38), and all dots of
+// the line accumulated exactly in the same pass.
+//
+// Layout: element e = i*m + c.  The grid is persistent (SM count x resident
+// blocks) and walks the elements with a stride that is a multiple of m, so a
+// thread always sees the same column c: its coefficients are loaded once and
+// its dot accumulators are per-column by construction.  Loads and stores are
+// fully coalesced 8-byte accesses (a warp touches 256 contiguous bytes).
+//
+// Arithmetic: each update is acc = 0.0; acc = acc + coef*v ... in statement
+// term order with separately rounded multiply and add (__dmul_rn/__dadd_rn),
+// exactly as execute.cpp:104-110 compiled without contraction.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "exact.cuh"
+
+namespace mbg {
+
+constexpr int GMAX_IN = 8, GMAX_OUT = 6, GMAX_CO = 8, GMAX_DOT = 4;
+
+struct GroupArgs {
+    int64_t len;                 // n*m
+    int m;
+    const double* in[GMAX_IN];
+    double* out[GMAX_OUT];
+    const double* coef[GMAX_CO]; // device arrays of m doubles
+    int64_t* slot[GMAX_DOT];     // long accumulators: m * NSLOT words each
+    double* part[GMAX_DOT];      // block partial expansions: m * nblocks * KEXP
+    const int* ctl;              // ctl[0] != 0: solve stopped -> no-op
+};
+
+__device__ __forceinline__ double fmadd_rn(double acc, double c, double v) {
+    return __dadd_rn(acc, __dmul_rn(c, v));
+}
+
+// ---------------------------------------------------------------------------
+// Programs: one struct per merged line of SURVEY.md Appendix C (and the
+// singleton statements of the basic formulation).  in/out/co index the
+// GroupArgs arrays; prod[] are the dot-product terms of this element.
+// ---------------------------------------------------------------------------
+
+// Dot (a, b)                                   e.g. delta = (v, r0)
+struct PDot2 {
+    static constexpr const char* NAME = "dot2";
+    static constexpr int NIN = 2, NOUT = 0, NCO = 0, NDOT = 1;
+    __device__ static void run(const double* in, double*, double* prod, const double*) {
+        prod[0] = __dmul_rn(in[0], in[1]);
+    }
+};
+// Dot (a, a)                                   e.g. psi = (t, t)
+struct PDot1 {
+    static constexpr const char* NAME = "dot1";
+    static constexpr int NIN = 1, NOUT = 0, NCO = 0, NDOT = 1;
+    __device__ static void run(const double* in, double*, double* prod, const double*) {
+        prod[0] = __dmul_rn(in[0], in[0]);
+    }
+};
+// out = c0*a
+struct PUpd1 {
+    static constexpr const char* NAME = "upd1";
+    static constexpr int NIN = 1, NOUT = 1, NCO = 1, NDOT = 0;
+    __device__ static void run(const double* in, double* out, double*, const double* co) {
+        out[0] = fmadd_rn(0.0, co[0], in[0]);
+    }
+};
+// out = c0*a + c1*b
+struct PUpd2 {
+    static constexpr const char* NAME = "upd2";
+    static constexpr int NIN = 2, NOUT = 1, NCO = 2, NDOT = 0;
+    __device__ static void run(const double* in, double* out, double*, const double* co) {
+        out[0] = fmadd_rn(fmadd_rn(0.0, co[0], in[0]), co[1], in[1]);
+    }
+};
+// out = c0*a + c1*b + c2*d
+struct PUpd3 {
+    static constexpr const char* NAME = "upd3";
+    static constexpr int NIN = 3, NOUT = 1, NCO = 3, NDOT = 0;
+    __device__ static void run(const double* in, double* out, double*, const double* co) {
+        out[0] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, co[0], in[0]), co[1], in[1]), co[2], in[2]);
+    }
+};
+
+// Classical, Alg. 2 line 9: phi=(t,s), psi=(t,t), theta=(s,s)
+struct PClassicOmega {
+    static constexpr const char* NAME = "classic_omega";
+    static constexpr int NIN = 2, NOUT = 0, NCO = 0, NDOT = 3;   // in: t s
+    __device__ static void run(const double* in, double*, double* prod, const double*) {
+        prod[0] = __dmul_rn(in[0], in[1]);
+        prod[1] = __dmul_rn(in[0], in[0]);
+        prod[2] = __dmul_rn(in[1], in[1]);
+    }
+};
+// Classical, Alg. 2 line 15:
+//   x = 1*x + alpha*p + omega*s ; r = 1*s + (-omega)*t ; rho' = (r, r0)
+struct PClassicXR {
+    static constexpr const char* NAME = "classic_xr";
+    static constexpr int NIN = 5, NOUT = 2, NCO = 3, NDOT = 1;   // in: x p s t r0; co: alpha omega -omega
+    __device__ static void run(const double* in, double* out, double* prod, const double* co) {
+        out[0] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, in[0]), co[0], in[1]), co[1], in[2]);
+        const double r = fmadd_rn(fmadd_rn(0.0, 1.0, in[2]), co[2], in[3]);
+        out[1] = r;
+        prod[0] = __dmul_rn(r, in[4]);
+    }
+};
+
+// Reordered, Alg. 6 line 11:
+//   rt = 1*r + (-alpha)*v ; theta=(t,rt), phi=(t,t), psi=(t,r0), eta=(rt,rt)
+struct PReordG7 {
+    static constexpr const char* NAME = "reord_g7";
+    static constexpr int NIN = 4, NOUT = 1, NCO = 1, NDOT = 4;   // in: r v t r0; co: -alpha
+    __device__ static void run(const double* in, double* out, double* prod, const double* co) {
+        const double rt = fmadd_rn(fmadd_rn(0.0, 1.0, in[0]), co[0], in[1]);
+        out[0] = rt;
+        prod[0] = __dmul_rn(in[2], rt);
+        prod[1] = __dmul_rn(in[2], in[2]);
+        prod[2] = __dmul_rn(in[2], in[3]);
+        prod[3] = __dmul_rn(rt, rt);
+    }
+};
+// Reordered, Alg. 6 lines 20-22 (footnote-5 form):
+//   x = 1*x + alpha*vh + omega*th ; z = 1*th + (-omega)*q ;
+//   vh = 1*z + beta*vh + (-(beta*omega))*s
+struct PReordG12 {
+    static constexpr const char* NAME = "reord_g12";
+    static constexpr int NIN = 5, NOUT = 3, NCO = 5, NDOT = 0;   // in: x vh th q s; co: alpha omega -omega beta -(beta*omega)
+    __device__ static void run(const double* in, double* out, double*, const double* co) {
+        out[0] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, in[0]), co[0], in[1]), co[1], in[2]);
+        const double z = fmadd_rn(fmadd_rn(0.0, 1.0, in[2]), co[2], in[3]);
+        out[1] = z;
+        out[2] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, z), co[3], in[1]), co[4], in[4]);
+    }
+};
+
+// Pipelined, Alg. 4 line 4:
+//   p = 1*r + beta*p + nbo*s ; s = 1*w + beta*s + nbo*z ; z = 1*t + beta*z + nbo*v ;
+//   q = 1*r + (-alpha)*s ; y = 1*w + (-alpha)*z ; theta=(q,y), phi=(y,y), pi=(q,q)
+struct PPipeG1 {
+    static constexpr const char* NAME = "pipe_g1";
+    static constexpr int NIN = 7, NOUT = 5, NCO = 3, NDOT = 3;   // in: r p s w z t v; out: p s z q y; co: beta nbo -alpha
+    __device__ static void run(const double* in, double* out, double* prod, const double* co) {
+        const double r = in[0], p = in[1], s = in[2], w = in[3], z = in[4], t = in[5], v = in[6];
+        const double pn = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, r), co[0], p), co[1], s);
+        const double sn = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, w), co[0], s), co[1], z);
+        const double zn = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, t), co[0], z), co[1], v);
+        const double q = fmadd_rn(fmadd_rn(0.0, 1.0, r), co[2], sn);
+        const double y = fmadd_rn(fmadd_rn(0.0, 1.0, w), co[2], zn);
+        out[0] = pn; out[1] = sn; out[2] = zn; out[3] = q; out[4] = y;
+        prod[0] = __dmul_rn(q, y);
+        prod[1] = __dmul_rn(y, y);
+        prod[2] = __dmul_rn(q, q);
+    }
+};
+// Pipelined, Alg. 4 line 7: x = 1*x + alpha*p + omega*q ; r = 1*q + (-omega)*y
+struct PPipeG4 {
+    static constexpr const char* NAME = "pipe_g4";
+    static constexpr int NIN = 4, NOUT = 2, NCO = 3, NDOT = 0;   // in: x p q y; co: alpha omega -omega
+    __device__ static void run(const double* in, double* out, double*, const double* co) {
+        out[0] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, in[0]), co[0], in[1]), co[1], in[2]);
+        out[1] = fmadd_rn(fmadd_rn(0.0, 1.0, in[2]), co[2], in[3]);
+    }
+};
+// Pipelined, Alg. 4 line 12:
+//   w = 1*y + (-omega)*t + (omega*alpha)*v ; rho'=(r0,r), psi=(r0,z), sigma=(r0,w), delta=(r0,s)
+struct PPipeG5 {
+    static constexpr const char* NAME = "pipe_g5";
+    static constexpr int NIN = 7, NOUT = 1, NCO = 2, NDOT = 4;   // in: y t v r0 r z s; co: -omega omega*alpha
+    __device__ static void run(const double* in, double* out, double* prod, const double* co) {
+        const double w = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, in[0]), co[0], in[1]), co[1], in[2]);
+        out[0] = w;
+        const double r0 = in[3];
+        prod[0] = __dmul_rn(r0, in[4]);
+        prod[1] = __dmul_rn(r0, in[5]);
+        prod[2] = __dmul_rn(r0, w);
+        prod[3] = __dmul_rn(r0, in[6]);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Block-level exact combine of the per-thread expansions; thread t of the
+// block owns column t % m.  Result: one expansion per (dot, column) written
+// to part[d][(c * nblocks + block) * KEXP + i].  Residuals go to the slot.
+// ---------------------------------------------------------------------------
+template <int ND>
+__device__ __forceinline__ void block_combine(double (&acc)[ND][KEXP], const GroupArgs& a, int c,
+                                              double* sh /* blockDim * KEXP doubles */) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int m = a.m;
+    const int nb = gridDim.x;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+        double (&mine)[KEXP] = acc[d];
+        int64_t* slot = a.slot[d] + static_cast<int64_t>(c) * NSLOT;
+        if (m <= 32 && (32 % m) == 0) {
+            // intra-warp: lanes L and L+off share a column when off % m == 0
+            for (int off = 16; off >= m; off >>= 1) {
+                double t[KEXP];
+#pragma unroll
+                for (int i = 0; i < KEXP; ++i) t[i] = __shfl_down_sync(0xffffffffu, mine[i], off);
+                if (lane < off) {
+#pragma unroll
+                    for (int i = 0; i < KEXP; ++i) grow(mine, t[i], slot);
+                }
+            }
+            const int nw = blockDim.x >> 5;
+            if (lane < m) {
+#pragma unroll
+                for (int i = 0; i < KEXP; ++i) sh[(warp * 32 + lane) * KEXP + i] = mine[i];
+            }
+            __syncthreads();
+            for (int s = nw >> 1; s >= 1; s >>= 1) {
+                if (warp < s && lane < m) {
+#pragma unroll
+                    for (int i = 0; i < KEXP; ++i) grow(mine, sh[((warp + s) * 32 + lane) * KEXP + i], slot);
+#pragma unroll
+                    for (int i = 0; i < KEXP; ++i) sh[(warp * 32 + lane) * KEXP + i] = mine[i];
+                }
+                __syncthreads();
+            }
+        } else {
+            // generic: blockDim = m * 2^q, tree over the rows of the block
+#pragma unroll
+            for (int i = 0; i < KEXP; ++i) sh[tid * KEXP + i] = mine[i];
+            __syncthreads();
+            for (int s = (blockDim.x / m) >> 1; s >= 1; s >>= 1) {
+                if (tid < s * m) {
+#pragma unroll
+                    for (int i = 0; i < KEXP; ++i) grow(mine, sh[(tid + s * m) * KEXP + i], slot);
+#pragma unroll
+                    for (int i = 0; i < KEXP; ++i) sh[tid * KEXP + i] = mine[i];
+                }
+                __syncthreads();
+            }
+        }
+        if (tid < m) {
+            double* p = a.part[d] + (static_cast<int64_t>(tid) * nb + blockIdx.x) * KEXP;
+#pragma unroll
+            for (int i = 0; i < KEXP; ++i) p[i] = mine[i];
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// The fused group kernel.  Two elements per thread per trip for memory-level
+// parallelism (all loads of both elements are issued before any store, so an
+// in-place update such as x = x + ... stays correct).
+// ---------------------------------------------------------------------------
+template <class P>
+__global__ void __launch_bounds__(256) group_kernel(GroupArgs a) {
+    if (a.ctl && a.ctl[0]) return;
+    extern __shared__ double sh_dyn[];
+    const int m = a.m;
+    const int c = threadIdx.x % m;
+    constexpr int NCO = P::NCO > 0 ? P::NCO : 1;
+    constexpr int ND = P::NDOT > 0 ? P::NDOT : 1;
+    constexpr int NO = P::NOUT > 0 ? P::NOUT : 1;
+    double co[NCO];
+#pragma unroll
+    for (int i = 0; i < P::NCO; ++i) co[i] = a.coef[i][c];
+    double acc[ND][KEXP];
+#pragma unroll
+    for (int d = 0; d < ND; ++d)
+#pragma unroll
+        for (int i = 0; i < KEXP; ++i) acc[d][i] = 0.0;
+
+    int64_t* slot[ND];
+#pragma unroll
+    for (int d = 0; d < P::NDOT; ++d) slot[d] = a.slot[d] + static_cast<int64_t>(c) * NSLOT;
+
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (; e + stride < a.len; e += 2 * stride) {
+        double in0[P::NIN], in1[P::NIN];
+#pragma unroll
+        for (int i = 0; i < P::NIN; ++i) { in0[i] = a.in[i][e]; in1[i] = a.in[i][e + stride]; }
+        double out0[NO], out1[NO], pr0[ND], pr1[ND];
+        P::run(in0, out0, pr0, co);
+        P::run(in1, out1, pr1, co);
+#pragma unroll
+        for (int i = 0; i < P::NOUT; ++i) { a.out[i][e] = out0[i]; a.out[i][e + stride] = out1[i]; }
+#pragma unroll
+        for (int d = 0; d < P::NDOT; ++d) { grow(acc[d], pr0[d], slot[d]); grow(acc[d], pr1[d], slot[d]); }
+    }
+    if (e < a.len) {
+        double in0[P::NIN];
+#pragma unroll
+        for (int i = 0; i < P::NIN; ++i) in0[i] = a.in[i][e];
+        double out0[NO], pr0[ND];
+        P::run(in0, out0, pr0, co);
+#pragma unroll
+        for (int i = 0; i < P::NOUT; ++i) a.out[i][e] = out0[i];
+#pragma unroll
+        for (int d = 0; d < P::NDOT; ++d) grow(acc[d], pr0[d], slot[d]);
+    }
+    if constexpr (P::NDOT > 0) block_combine<P::NDOT>(acc, a, c, sh_dyn);
+}
+
+// Block size for m columns: m * 2^q <= 256 (m <= 256), else m.
+inline int group_block(int m) {
+    if (m > 256) return m;
+    int b = m;
+    while (b * 2 <= 256) b *= 2;
+    return b;
+}
+
+// ---------------------------------------------------------------------------
+// Fold: combine all block partials and the long accumulator of each
+// (slot, column) into D (long-accumulator form, one carry step applied so
+// words stay below 2^33), and clear the slot for its next use.
+// grid = (m, nslots), block = 32.
+// ---------------------------------------------------------------------------
+struct FoldArgs {
+    int m;
+    int nblocks;
+    int64_t* slot[GMAX_DOT];
+    const double* part[GMAX_DOT];
+    int64_t* D[GMAX_DOT];
+    const int* ctl;
+};
+
+}  // namespace mbg

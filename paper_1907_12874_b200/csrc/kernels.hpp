@@ -1,0 +1,55 @@
+// kernels.hpp -- host-side launchers of the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "group.cuh"
+
+namespace mbg {
+
+// CSR SpMM over the interleaved block (spmm.cu).  rows[] optional: a list of
+// local rows to compute (interior / boundary pass of a partitioned matrix);
+// nullptr = rows [0, n).
+void launch_spmm(cudaStream_t st, int64_t nrows, const int32_t* rows, const int32_t* off,
+                 const int32_t* col, const double* val, int m, const double* x, double* y,
+                 const int* ctl);
+
+// Fold block partials (kernels.cu).
+void launch_fold(cudaStream_t st, const FoldArgs& f, int nslots);
+
+// Generic statement-group interpreter (API-level execute_group).
+constexpr int GEN_MAX_VEC = 16, GEN_MAX_STMT = 16, GEN_MAX_SLOT = 8;
+struct GenericGroup {
+    int64_t len;
+    int m;
+    int nstmt;
+    double* vec[GEN_MAX_VEC];
+    // statement s: kind, out, nterms, first term index; dot: left, right, slot
+    int kind[GEN_MAX_STMT], out[GEN_MAX_STMT], nterms[GEN_MAX_STMT], tfirst[GEN_MAX_STMT];
+    int left[GEN_MAX_STMT], right[GEN_MAX_STMT], dslot[GEN_MAX_STMT];
+    int term_vec[GEN_MAX_STMT * MBG_MAX_TERMS];
+    const double* coef;   // device: term t, column c at coef[t*m + c]
+    int nslots;
+    int64_t* slot;        // nslots * m * NSLOT
+    double* part;         // nslots * m * nblocks * KEXP
+};
+void launch_generic_group(cudaStream_t st, const GenericGroup& g, int num_sms, int* nblocks_out);
+
+// Round D (long accumulators) into doubles: out[s*m + c] (kernels.cu).
+void launch_round(cudaStream_t st, const int64_t* D, int nslots, int m, double* out);
+
+// Occupancy-sized persistent grid for a group kernel instantiation.
+int group_grid(const void* kernel, int block, size_t smem, int num_sms, int64_t len);
+
+template <class P>
+inline int launch_group(cudaStream_t st, const GroupArgs& a, int num_sms) {
+    const int block = group_block(a.m);
+    const size_t smem = P::NDOT > 0 ? static_cast<size_t>(block) * KEXP * sizeof(double) : 0;
+    const int grid = group_grid(reinterpret_cast<const void*>(&group_kernel<P>), block, smem, num_sms, a.len);
+    group_kernel<P><<<grid, block, smem, st>>>(a);
+    return grid;
+}
+
+}  // namespace mbg

@@ -1,0 +1,90 @@
+// plan.cpp -- row partition and halo plan for the distributed SpMM.
+//
+// The paper distributes contiguous row blocks across processes (Fig. 1,
+// PAPER.md:60-78) and exchanges the boundary rows of the vector before each
+// SpMV; the reference only models this analytically
+// (SPEC.md:112).  This is the executable plan: local CSR renumbered to
+// [owned rows | halo rows], per-peer send lists and receive windows, and the
+// interior / boundary row split used to overlap the exchange.
+#include <algorithm>
+#include <limits>
+
+#include "comm.hpp"
+
+namespace mbg {
+
+HaloPlan build_halo_plan(int64_t n, const int64_t* off, const int32_t* col, const double* val,
+                         int nparts, const int64_t* begin, int my) {
+    if (nparts < 1 || my < 0 || my >= nparts) throw Invalid("partition: bad part index");
+    if (begin[0] != 0 || begin[nparts] != n) throw Invalid("partition: bounds must cover [0, n)");
+    for (int p = 0; p < nparts; ++p)
+        if (begin[p] > begin[p + 1]) throw Invalid("partition: bounds must be non-decreasing");
+    const int64_t rb = begin[my], re = begin[my + 1];
+    HaloPlan pl;
+    pl.n_own = re - rb;
+    const int64_t nnz = off[re] - off[rb];
+    if (nnz > std::numeric_limits<int32_t>::max()) throw Invalid("partition: local nnz exceeds int32");
+
+    std::vector<int64_t> halo;
+    for (int64_t i = rb; i < re; ++i)
+        for (int64_t k = off[i]; k < off[i + 1]; ++k) {
+            const int64_t g = col[k];
+            if (g < rb || g >= re) halo.push_back(g);
+        }
+    std::sort(halo.begin(), halo.end());
+    halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
+    pl.n_halo = static_cast<int64_t>(halo.size());
+    pl.halo_global = halo;
+    if (pl.n_own + pl.n_halo > std::numeric_limits<int32_t>::max())
+        throw Invalid("partition: local rows exceed int32");
+
+    pl.nnz = nnz;
+    pl.off.resize(pl.n_own + 1);
+    pl.col.resize(nnz);
+    pl.val.assign(val + off[rb], val + off[re]);
+    pl.off[0] = 0;
+    for (int64_t i = rb; i < re; ++i) {
+        bool bnd = false;
+        for (int64_t k = off[i]; k < off[i + 1]; ++k) {
+            const int64_t g = col[k];
+            int64_t l;
+            if (g >= rb && g < re) {
+                l = g - rb;
+            } else {
+                l = pl.n_own + (std::lower_bound(halo.begin(), halo.end(), g) - halo.begin());
+                bnd = true;
+            }
+            pl.col[k - off[rb]] = static_cast<int32_t>(l);
+        }
+        pl.off[i - rb + 1] = static_cast<int32_t>(off[i + 1] - off[rb]);
+        (bnd ? pl.boundary : pl.interior).push_back(static_cast<int32_t>(i - rb));
+    }
+
+    // Local numbering note: owned columns keep their relative order and halo
+    // columns are appended, so a row's column list may no longer be sorted in
+    // local numbering -- the nonzeros keep their global CSR order, which is
+    // what fixes the summation order (spmv.cpp:40-46).
+    for (int q = 0; q < nparts; ++q) {
+        if (q == my) continue;
+        HaloPlan::Peer peer;
+        peer.part = q;
+        const int64_t qb = begin[q], qe = begin[q + 1];
+        auto lo = std::lower_bound(halo.begin(), halo.end(), qb);
+        auto hi = std::lower_bound(halo.begin(), halo.end(), qe);
+        peer.recv_offset = lo - halo.begin();
+        peer.recv_count = hi - lo;
+        std::vector<int64_t> need;
+        for (int64_t i = qb; i < qe; ++i)
+            for (int64_t k = off[i]; k < off[i + 1]; ++k) {
+                const int64_t g = col[k];
+                if (g >= rb && g < re) need.push_back(g);
+            }
+        std::sort(need.begin(), need.end());
+        need.erase(std::unique(need.begin(), need.end()), need.end());
+        for (int64_t g : need) peer.send_rows.push_back(static_cast<int32_t>(g - rb));
+        if (peer.recv_count || !peer.send_rows.empty()) pl.peers.push_back(std::move(peer));
+    }
+    return pl;
+}
+
+}  // namespace mbg

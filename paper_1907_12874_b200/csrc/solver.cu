@@ -1,0 +1,605 @@
+// solver.cu -- device-resident multi-RHS BiCGStab drivers (classical, Reordered,
+// Pipelined; merged and basic formulations).
+//
+// The reference's solver layer is missing (proj/CMakeLists.txt:22-32); the
+// recurrences are the paper's merged listings -- Alg. 2 PAPER.md:1407-1438,
+// Alg. 6 PAPER.md:1562-1598 (identity M^-1), Alg. 4 PAPER.md:1488-1525 --
+// with the schedules and term expansions of SURVEY.md Appendix C and the
+// solve() contract of SPEC.md:227-235,262-268.
+//
+// Everything stays on the device: per-column scalars (ColumnScalars,
+// types.hpp:39-83) live in a small scalar bank updated by one-block "scalar"
+// kernels after each reduction point; convergence, breakdown and iteration
+// count live in a control word array that every kernel checks first, so an
+// iteration captured once as a CUDA graph can be replayed blindly and becomes
+// a no-op after the solve stops.  The host only polls the control words once
+// per chunk of iterations (lagged by one chunk).
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <map>
+#include <tuple>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "comm.hpp"
+#include "kernels.hpp"
+#include "solver.hpp"
+
+namespace mbg {
+
+// ---- scalar bank / control words ------------------------------------------
+enum Scal : int {
+    S_ONE, S_MONE, S_BB, S_EPS2, S_RHO, S_ALPHA, S_NALPHA, S_OMEGA, S_NOMEGA,
+    S_BETA, S_NBO, S_OA, S_RES2, NSCAL
+};
+enum Ctl : int {
+    C_STOP, C_CONV, C_ITER, C_ITERS, C_BD, C_BDITER, C_BDCOL, C_CONVERGED, NCTL = 16
+};
+enum Point : int {
+    P_SETUP, P_C_ALPHA, P_C_OMEGA, P_C_BETA, P_R_OMEGA, P_R_END, P_P_OMEGA, P_P_BETA
+};
+
+struct ScalArgs {
+    int m, point, method, fixed, maxit;
+    double tol2;
+    double* sc;          // NSCAL * m
+    int* ctl;
+    double* hist;        // (maxit+1) * m
+    const int64_t* D[4]; // rounded here (after any cross-GPU allreduce)
+    int nd;
+};
+
+__device__ __forceinline__ bool finite_d(double x) { return isfinite(x); }
+
+__device__ __forceinline__ double hist_entry(double res2, double bb) {
+    const double r = res2 > 0.0 ? res2 : 0.0;
+    return __dsqrt_rn(__ddiv_rn(r, bb));
+}
+
+// One block, thread c <-> column c.  Expressions follow oracle.c operation by
+// operation (separately rounded, no contraction).
+__global__ void scalar_kernel(ScalArgs a) {
+    __shared__ int s_bad1, s_bad2, s_all;
+    int* ctl = a.ctl;
+    if (ctl[C_STOP]) return;
+    const int m = a.m;
+    const int c = threadIdx.x;
+    const bool on = c < m;
+    if (c == 0) { s_bad1 = INT_MAX; s_bad2 = INT_MAX; s_all = 1; }
+    __syncthreads();
+    double* sc = a.sc;
+#define SC(i) sc[(i) * m + c]
+    double d[4] = {0.0, 0.0, 0.0, 0.0};
+    if (on)
+        for (int i = 0; i < a.nd; ++i) d[i] = digits_round(a.D[i] + static_cast<int64_t>(c) * NSLOT);
+    const int j = ctl[C_ITER];
+    int code1 = 0, code2 = 0;  // breakdown codes for s_bad1 / s_bad2
+    switch (a.point) {
+        case P_SETUP: {
+            // d0 = (r0,r0), d1 = (b,b), d2 = (r0,w) for Pipelined
+            if (on) {
+                SC(S_ONE) = 1.0; SC(S_MONE) = -1.0;
+                SC(S_RHO) = d[0]; SC(S_BB) = d[1];
+                SC(S_EPS2) = __dmul_rn(a.tol2, d[1]);
+                a.hist[c] = hist_entry(d[0], d[1]);
+                if (!(d[0] < SC(S_EPS2))) s_all = 0;
+            }
+            __syncthreads();
+            if (!a.fixed && s_all) {
+                if (c == 0) { ctl[C_STOP] = 1; ctl[C_CONVERGED] = 1; ctl[C_ITERS] = 0; }
+                return;
+            }
+            if (a.method == MBG_PIPEBICGSTAB && on) {
+                const double alpha = __ddiv_rn(d[0], d[2]);
+                SC(S_ALPHA) = alpha; SC(S_NALPHA) = -alpha;
+                SC(S_BETA) = 0.0; SC(S_OMEGA) = 0.0;
+                SC(S_NBO) = -__dmul_rn(0.0, 0.0);
+                if (d[2] == 0.0 || !finite_d(alpha)) atomicMin(&s_bad1, c);
+            }
+            code1 = 1;
+            break;
+        }
+        case P_C_ALPHA: {
+            if (on) {
+                const double alpha = __ddiv_rn(SC(S_RHO), d[0]);
+                SC(S_ALPHA) = alpha; SC(S_NALPHA) = -alpha;
+                if (d[0] == 0.0 || !finite_d(alpha)) atomicMin(&s_bad1, c);
+            }
+            code1 = 1;
+            break;
+        }
+        case P_C_OMEGA:    // d = phi psi theta
+        case P_R_OMEGA:    // d = theta phi psi eta
+        case P_P_OMEGA: {  // d = theta phi pi
+            double num, den, sq;
+            if (a.point == P_C_OMEGA) { num = d[0]; den = d[1]; sq = d[2]; }
+            else if (a.point == P_R_OMEGA) { num = d[0]; den = d[1]; sq = d[3]; }
+            else { num = d[0]; den = d[1]; sq = d[2]; }
+            double omega = 0.0, res2 = 0.0;
+            if (on) {
+                // lucky exact convergence (den == 0 because the residual is exactly 0): omega = 0
+                const bool lucky = den == 0.0 && sq == 0.0;
+                omega = lucky ? 0.0 : __ddiv_rn(num, den);
+                SC(S_OMEGA) = omega; SC(S_NOMEGA) = -omega;
+                if (a.point == P_P_OMEGA) SC(S_OA) = __dmul_rn(omega, SC(S_ALPHA));
+                res2 = __dsub_rn(sq, __dmul_rn(omega, num));
+                SC(S_RES2) = res2;
+                if ((den == 0.0 && !lucky) || !finite_d(omega)) atomicMin(&s_bad2, c);
+            }
+            __syncthreads();
+            if (s_bad2 != INT_MAX) { code2 = 2; break; }
+            if (on) {
+                a.hist[static_cast<int64_t>(j + 1) * m + c] = hist_entry(res2, SC(S_BB));
+                if (!(res2 < SC(S_EPS2))) s_all = 0;
+            }
+            __syncthreads();
+            const bool conv = !a.fixed && s_all;
+            if (c == 0 && conv) ctl[C_CONV] = 1;
+            if (a.point == P_R_OMEGA && !conv && on) {
+                // rho' = -(omega*psi), beta = (rho'/rho)*(alpha/omega)
+                const double rhon = -__dmul_rn(omega, d[2]);
+                const double beta = __dmul_rn(__ddiv_rn(rhon, SC(S_RHO)), __ddiv_rn(SC(S_ALPHA), omega));
+                SC(S_BETA) = beta; SC(S_NBO) = -__dmul_rn(beta, omega); SC(S_RHO) = rhon;
+                if (!finite_d(beta)) atomicMin(&s_bad1, c);
+            }
+            code1 = 3;
+            break;
+        }
+        case P_C_BETA: {
+            if (ctl[C_CONV]) {
+                if (c == 0) { ctl[C_STOP] = 1; ctl[C_CONVERGED] = 1; ctl[C_ITERS] = j + 1; }
+                return;
+            }
+            if (on) {
+                const double rhon = d[0];
+                const double beta = __dmul_rn(__ddiv_rn(rhon, SC(S_RHO)), __ddiv_rn(SC(S_ALPHA), SC(S_OMEGA)));
+                SC(S_BETA) = beta; SC(S_NBO) = -__dmul_rn(beta, SC(S_OMEGA)); SC(S_RHO) = rhon;
+                if (!finite_d(beta)) atomicMin(&s_bad1, c);
+            }
+            code1 = 3;
+            break;
+        }
+        case P_R_END: {
+            if (c == 0) {
+                if (ctl[C_CONV]) { ctl[C_STOP] = 1; ctl[C_CONVERGED] = 1; ctl[C_ITERS] = j + 1; }
+            }
+            break;
+        }
+        case P_P_BETA: {
+            if (ctl[C_CONV]) {
+                if (c == 0) { ctl[C_STOP] = 1; ctl[C_CONVERGED] = 1; ctl[C_ITERS] = j + 1; }
+                return;
+            }
+            if (on) {
+                // d = rho' psi sigma delta
+                const double omega = SC(S_OMEGA), alpha = SC(S_ALPHA);
+                const double beta = __dmul_rn(__ddiv_rn(alpha, omega), __ddiv_rn(d[0], SC(S_RHO)));
+                const double den = __dsub_rn(__dadd_rn(d[2], __dmul_rn(beta, d[3])),
+                                             __dmul_rn(__dmul_rn(beta, omega), d[1]));
+                const double an = __ddiv_rn(d[0], den);
+                SC(S_BETA) = beta; SC(S_ALPHA) = an; SC(S_RHO) = d[0];
+                SC(S_NBO) = -__dmul_rn(beta, omega); SC(S_NALPHA) = -an;
+                if (!finite_d(beta)) atomicMin(&s_bad2, c);
+                if (den == 0.0 || !finite_d(an)) atomicMin(&s_bad1, c);
+            }
+            __syncthreads();
+            if (s_bad2 != INT_MAX) { code2 = 3; break; }
+            code1 = 1;
+            break;
+        }
+    }
+#undef SC
+    __syncthreads();
+    if (c != 0) return;
+    // breakdown bookkeeping (first column)
+    if (code2 && s_bad2 != INT_MAX) {
+        ctl[C_BD] = code2; ctl[C_BDITER] = j; ctl[C_BDCOL] = s_bad2; ctl[C_ITERS] = j; ctl[C_STOP] = 1;
+        return;
+    }
+    if (code1 && s_bad1 != INT_MAX) {
+        // Pipelined's alpha_{j+1} belongs to the next iteration (oracle.c)
+        const int it = (a.point == P_P_BETA) ? j + 1 : j;
+        ctl[C_BD] = code1; ctl[C_BDITER] = it; ctl[C_BDCOL] = s_bad1; ctl[C_ITERS] = it; ctl[C_STOP] = 1;
+        return;
+    }
+    // end of iteration
+    if (a.point == P_C_BETA || a.point == P_R_END || a.point == P_P_BETA) {
+        ctl[C_ITER] = j + 1;
+        ctl[C_ITERS] = j + 1;
+        if (j + 1 >= a.maxit) ctl[C_STOP] = 1;
+    }
+    if (a.point == P_SETUP && a.maxit <= 0) ctl[C_STOP] = 1;
+}
+
+// ===========================================================================
+// Solver
+// ===========================================================================
+Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulation, double tol,
+               int fixed, int maxit)
+    : ctx_(ctx), a_(a), m_(m), method_(method), form_(formulation), tol_(tol), fixed_(fixed),
+      maxit_(maxit) {
+    if (method < 0 || method > 2) throw Invalid("solve: unknown method");
+    if (formulation < 0 || formulation > 1) throw Invalid("solve: unknown formulation");
+    if (m < 1 || m > 1024) throw Invalid("solve: m must be in [1, 1024]");
+    if (maxit < 0) throw Invalid("solve: negative iteration count");
+    if (!fixed && !(tol > 0.0)) throw Invalid("solve: tol must be > 0 in converge mode");
+    n_ = a->n;
+    len_ = n_ * m;
+    rows_alloc_ = a->n + a->n_halo;
+    // only the vectors the method uses (C4 at m=32 is 8.4 GB per vector)
+    static const std::vector<int> need[3] = {
+        {0, 1, 2, 3, 4, 5},                        // r r0 p v s t
+        {0, 1, 3, 4, 5, 6, 7, 8, 9, 10},           // r r0 v s t z vh th rt q
+        {0, 1, 2, 3, 4, 5, 6, 10, 11, 12, 13}};    // r r0 p v s t z q w y tmp
+    work_.resize(15);
+    const size_t vlen = static_cast<size_t>(rows_alloc_) * m;
+    for (int i : need[method]) work_[i] = pool_take(ctx, vlen);
+    if (a->n_halo) work_[14] = pool_take(ctx, vlen);  // x0 staging with halo room
+    scal_.alloc(static_cast<size_t>(NSCAL) * m);
+    ctl_.alloc(NCTL);
+    hist_.alloc(static_cast<size_t>(maxit + 1) * m);
+    max_blocks_ = ctx->num_sms * 8;
+    slots_.alloc(static_cast<size_t>(4) * m * NSLOT);
+    D_.alloc(static_cast<size_t>(4) * m * NSLOT);
+    part_.alloc(static_cast<size_t>(4) * m * max_blocks_ * KEXP);
+    MBG_CUDA(cudaMemsetAsync(slots_.p, 0, slots_.n * sizeof(int64_t), ctx->stream));
+    MBG_CUDA(cudaMemsetAsync(ctl_.p, 0, ctl_.n * sizeof(int), ctx->stream));
+    MBG_CUDA(cudaMallocHost(&ctl_host_, 2 * NCTL * sizeof(int)));
+    for (auto& e : ev_) MBG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    MBG_CUDA(cudaEventCreate(&t0_));
+    MBG_CUDA(cudaEventCreate(&t1_));
+}
+
+Solver::~Solver() {
+    cudaStreamSynchronize(ctx_->stream);
+    for (auto& w : work_) pool_give(ctx_, std::move(w));
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    if (ctl_host_) cudaFreeHost(ctl_host_);
+    for (auto& e : ev_) if (e) cudaEventDestroy(e);
+    if (t0_) cudaEventDestroy(t0_);
+    if (t1_) cudaEventDestroy(t1_);
+}
+
+double* Solver::sc(int i) { return scal_.p + static_cast<int64_t>(i) * m_; }
+int64_t* Solver::slot(int i) { return slots_.p + static_cast<int64_t>(i) * m_ * NSLOT; }
+int64_t* Solver::dsl(int i) { return D_.p + static_cast<int64_t>(i) * m_ * NSLOT; }
+double* Solver::part(int i) { return part_.p + static_cast<int64_t>(i) * m_ * max_blocks_ * KEXP; }
+
+void Solver::mark_begin(const std::string& label, double bytes) {
+    if (!profile_) return;
+    Mark mk{label, bytes, nullptr, nullptr};
+    MBG_CUDA(cudaEventCreate(&mk.a));
+    MBG_CUDA(cudaEventCreate(&mk.b));
+    MBG_CUDA(cudaEventRecord(mk.a, ctx_->stream));
+    marks_.push_back(mk);
+}
+
+void Solver::mark_end() {
+    if (!profile_) return;
+    MBG_CUDA(cudaEventRecord(marks_.back().b, ctx_->stream));
+}
+
+std::string Solver::profile_json() {
+    MBG_CUDA(cudaStreamSynchronize(ctx_->stream));
+    std::map<std::string, std::tuple<int64_t, double, double>> agg;
+    for (auto& mk : marks_) {
+        float ms = 0.f;
+        MBG_CUDA(cudaEventElapsedTime(&ms, mk.a, mk.b));
+        auto& e = agg[mk.label];
+        std::get<0>(e) += 1;
+        std::get<1>(e) += ms;
+        std::get<2>(e) = mk.bytes;
+        cudaEventDestroy(mk.a);
+        cudaEventDestroy(mk.b);
+    }
+    marks_.clear();
+    std::string out = "{";
+    bool first = true;
+    for (auto& [k, v] : agg) {
+        char buf[256];
+        snprintf(buf, sizeof buf, "%s\"%s\": [%lld, %.6f, %.1f]", first ? "" : ", ", k.c_str(),
+                 static_cast<long long>(std::get<0>(v)), std::get<1>(v), std::get<2>(v));
+        out += buf;
+        first = false;
+    }
+    return out + "}";
+}
+
+void Solver::spmm(const double* x, double* y) {
+    mark_begin("spmm", spmv_compulsory_bytes(a_->n, a_->nnz, m_));
+    launches_ += apply_operator(ctx_, a_, m_, const_cast<double*>(x), y, ctl_.p);
+    mark_end();
+}
+
+template <class P>
+void Solver::group(std::initializer_list<const double*> in, std::initializer_list<double*> out,
+                   std::initializer_list<int> co, int first_slot) {
+    GroupArgs g{};
+    g.len = len_;
+    g.m = m_;
+    int i = 0;
+    for (auto p : in) g.in[i++] = p;
+    i = 0;
+    for (auto p : out) g.out[i++] = p;
+    i = 0;
+    for (int s : co) g.coef[i++] = sc(s);
+    for (int d = 0; d < P::NDOT; ++d) {
+        g.slot[d] = slot(first_slot + d);
+        g.part[d] = part(first_slot + d);
+    }
+    g.ctl = ctl_.p;
+    mark_begin(std::string("group:") + P::NAME, static_cast<double>(P::NIN + P::NOUT) * 8.0 * len_);
+    const int grid = launch_group<P>(ctx_->stream, g, ctx_->num_sms);
+    MBG_CUDA(cudaGetLastError());
+    mark_end();
+    launches_++;
+    if (P::NDOT > 0) {
+        // fold immediately (one reduction point per dot group)
+        FoldArgs f{};
+        f.m = m_;
+        f.nblocks = grid;
+        for (int d = 0; d < P::NDOT; ++d) {
+            f.slot[d] = slot(first_slot + d);
+            f.part[d] = part(first_slot + d);
+            f.D[d] = dsl(first_slot + d);
+        }
+        f.ctl = ctl_.p;
+        mark_begin("fold", 0.0);
+        launch_fold(ctx_->stream, f, P::NDOT);
+        mark_end();
+        launches_++;
+        // multi-GPU: one fused allreduce of all dots of this point (int64 limbs)
+        if (ctx_->comm) {
+            comm_allreduce_i64(ctx_, dsl(first_slot), static_cast<size_t>(P::NDOT) * m_ * NSLOT, ctx_->stream);
+        }
+        reductions_++;
+    }
+}
+
+void Solver::copy(double* dst, const double* src) {
+    mark_begin("copy", 16.0 * len_);
+    MBG_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(len_) * sizeof(double), cudaMemcpyDeviceToDevice,
+                             ctx_->stream));
+    mark_end();
+}
+
+void Solver::scalars(int point, int nd) {
+    ScalArgs s{};
+    s.m = m_;
+    s.point = point;
+    s.method = method_;
+    s.fixed = fixed_;
+    s.maxit = maxit_;
+    s.tol2 = tol_ * tol_;
+    s.sc = scal_.p;
+    s.ctl = ctl_.p;
+    s.hist = hist_.p;
+    for (int i = 0; i < nd; ++i) s.D[i] = dsl(i);
+    s.nd = nd;
+    const int threads = ((m_ + 31) / 32) * 32;
+    mark_begin("scalar", 0.0);
+    scalar_kernel<<<1, threads, 0, ctx_->stream>>>(s);
+    MBG_CUDA(cudaGetLastError());
+    mark_end();
+    launches_++;
+}
+
+// Vector roles (indices into work_):
+enum { V_R, V_R0, V_P, V_V, V_S, V_T, V_Z, V_VH, V_TH, V_RT, V_Q, V_W, V_Y, V_TMP };
+
+void Solver::setup(const double* b, double* x) {
+    b_ = b;
+    x_ = x;
+    double* r = w(V_R);
+    double* r0 = w(V_R0);
+    double* tmpv = w(V_V);
+    if (a_->n_halo) {
+        copy(w(14), x);                                  // x0 into a buffer with halo room
+        spmm(w(14), tmpv);                               // z = A x0
+    } else {
+        spmm(x, tmpv);                                   // z = A x0
+    }
+    group<PUpd2>({b, tmpv}, {r}, {S_ONE, S_MONE}, 0);    // r = 1*b + (-1)*z   (needs S_ONE set)
+    group<PUpd1>({r}, {r0}, {S_ONE}, 0);                  // r0 = 1*r
+    group<PDot1>({r0}, {}, {}, 0);                        // rho = (r0, r0)
+    group<PDot1>({b}, {}, {}, 1);                         // bb = (b, b)
+    int nd = 2;
+    if (method_ == MBG_BICGSTAB) {
+        group<PUpd1>({r}, {w(V_P)}, {S_ONE}, 2);          // p = 1*r
+    } else if (method_ == MBG_RBICGSTAB) {
+        copy(w(V_Z), r0);                                 // z0 = M^-1 r0 (identity)
+        copy(w(V_VH), w(V_Z));                            // v^0 = z0
+    } else {
+        spmm(r, w(V_W));                                  // w0 = A r0
+        spmm(w(V_W), w(V_T));                             // t0 = A w0
+        group<PDot2>({r0, w(V_W)}, {}, {}, 2);            // (r0, w0)
+        nd = 3;
+        for (int v : {V_P, V_S, V_Z, V_V})
+            MBG_CUDA(cudaMemsetAsync(w(v), 0, static_cast<size_t>(len_) * sizeof(double), ctx_->stream));
+    }
+    scalars(P_SETUP, nd);
+}
+
+void Solver::iteration() {
+    const bool basic = form_ == MBG_BASIC;
+    double *r = w(V_R), *r0 = w(V_R0), *x = x_;
+    if (method_ == MBG_BICGSTAB) {
+        double *p = w(V_P), *v = w(V_V), *s = w(V_S), *t = w(V_T);
+        spmm(p, v);
+        group<PDot2>({v, r0}, {}, {}, 0);
+        scalars(P_C_ALPHA, 1);
+        group<PUpd2>({r, v}, {s}, {S_ONE, S_NALPHA}, 0);
+        spmm(s, t);
+        if (basic) {
+            group<PDot2>({t, s}, {}, {}, 0);
+            group<PDot1>({t}, {}, {}, 1);
+            group<PDot1>({s}, {}, {}, 2);
+        } else {
+            group<PClassicOmega>({t, s}, {}, {}, 0);
+        }
+        scalars(P_C_OMEGA, 3);
+        if (basic) {
+            group<PUpd3>({x, p, s}, {x}, {S_ONE, S_ALPHA, S_OMEGA}, 0);
+            group<PUpd2>({s, t}, {r}, {S_ONE, S_NOMEGA}, 0);
+            group<PDot2>({r, r0}, {}, {}, 0);
+        } else {
+            group<PClassicXR>({x, p, s, t, r0}, {x, r}, {S_ALPHA, S_OMEGA, S_NOMEGA}, 0);
+        }
+        scalars(P_C_BETA, 1);
+        group<PUpd3>({r, p, v}, {p}, {S_ONE, S_BETA, S_NBO}, 0);
+    } else if (method_ == MBG_RBICGSTAB) {
+        double *z = w(V_Z), *vh = w(V_VH), *v = w(V_V), *s = w(V_S), *th = w(V_TH), *t = w(V_T);
+        double *rt = w(V_RT), *q = w(V_Q);
+        spmm(vh, v);
+        group<PDot2>({v, r0}, {}, {}, 0);
+        copy(s, v);                                               // s = M^-1 v
+        scalars(P_C_ALPHA, 1);
+        group<PUpd2>({z, s}, {th}, {S_ONE, S_NALPHA}, 0);        // th = z - alpha s
+        spmm(th, t);
+        if (basic) {
+            group<PUpd2>({r, v}, {rt}, {S_ONE, S_NALPHA}, 0);
+            group<PDot2>({t, rt}, {}, {}, 0);
+            group<PDot1>({t}, {}, {}, 1);
+            group<PDot2>({t, r0}, {}, {}, 2);
+            group<PDot1>({rt}, {}, {}, 3);
+        } else {
+            group<PReordG7>({r, v, t, r0}, {rt}, {S_NALPHA}, 0);
+        }
+        copy(q, t);                                               // q = M^-1 t
+        scalars(P_R_OMEGA, 4);
+        group<PUpd2>({rt, t}, {r}, {S_ONE, S_NOMEGA}, 0);        // r = rt - omega t
+        if (basic) {
+            group<PUpd3>({x, vh, th}, {x}, {S_ONE, S_ALPHA, S_OMEGA}, 0);
+            group<PUpd2>({th, q}, {z}, {S_ONE, S_NOMEGA}, 0);
+            group<PUpd3>({z, vh, s}, {vh}, {S_ONE, S_BETA, S_NBO}, 0);
+        } else {
+            group<PReordG12>({x, vh, th, q, s}, {x, z, vh}, {S_ALPHA, S_OMEGA, S_NOMEGA, S_BETA, S_NBO}, 0);
+        }
+        scalars(P_R_END, 0);
+    } else {
+        double *p = w(V_P), *s = w(V_S), *wv = w(V_W), *z = w(V_Z), *t = w(V_T), *v = w(V_V);
+        double *q = w(V_Q), *y = w(V_Y), *tmp = w(V_TMP);
+        if (basic) {
+            group<PUpd3>({r, p, s}, {p}, {S_ONE, S_BETA, S_NBO}, 0);
+            group<PUpd3>({wv, s, z}, {s}, {S_ONE, S_BETA, S_NBO}, 0);
+            group<PUpd3>({t, z, v}, {z}, {S_ONE, S_BETA, S_NBO}, 0);
+            group<PUpd2>({r, s}, {q}, {S_ONE, S_NALPHA}, 0);
+            group<PUpd2>({wv, z}, {y}, {S_ONE, S_NALPHA}, 0);
+            group<PDot2>({q, y}, {}, {}, 0);
+            group<PDot1>({y}, {}, {}, 1);
+            group<PDot1>({q}, {}, {}, 2);
+        } else {
+            group<PPipeG1>({r, p, s, wv, z, t, v}, {p, s, z, q, y}, {S_BETA, S_NBO, S_NALPHA}, 0);
+        }
+        spmm(z, v);
+        scalars(P_P_OMEGA, 3);
+        if (basic) {
+            group<PUpd3>({x, p, q}, {x}, {S_ONE, S_ALPHA, S_OMEGA}, 0);
+            group<PUpd2>({q, y}, {r}, {S_ONE, S_NOMEGA}, 0);
+            group<PUpd2>({t, v}, {tmp}, {S_NOMEGA, S_OA}, 0);   // split_basic: trailing pair
+            group<PUpd2>({y, tmp}, {wv}, {S_ONE, S_ONE}, 0);
+            group<PDot2>({r0, r}, {}, {}, 0);
+            group<PDot2>({r0, z}, {}, {}, 1);
+            group<PDot2>({r0, wv}, {}, {}, 2);
+            group<PDot2>({r0, s}, {}, {}, 3);
+        } else {
+            group<PPipeG4>({x, p, q, y}, {x, r}, {S_ALPHA, S_OMEGA, S_NOMEGA}, 0);
+            group<PPipeG5>({y, t, v, r0, r, z, s}, {wv}, {S_NOMEGA, S_OA}, 0);
+        }
+        spmm(wv, t);
+        scalars(P_P_BETA, 4);
+    }
+}
+
+void Solver::run(const double* b, double* x, bool use_graph, int chunk) {
+    if (profile_) use_graph = false;
+    // S_ONE / S_MONE must exist before setup's first group
+    std::vector<double> init(static_cast<size_t>(2) * m_);
+    for (int c = 0; c < m_; ++c) { init[c] = 1.0; init[m_ + c] = -1.0; }
+    MBG_CUDA(cudaMemcpyAsync(sc(S_ONE), init.data(), init.size() * sizeof(double), cudaMemcpyHostToDevice,
+                             ctx_->stream));
+    MBG_CUDA(cudaStreamSynchronize(ctx_->stream));  // init is a stack buffer
+    if (ctx_->comm) comm_barrier(ctx_);
+    MBG_CUDA(cudaEventRecord(t0_, ctx_->stream));
+    setup(b, x);
+    if (profile_) {  // profile the iteration loop only
+        MBG_CUDA(cudaStreamSynchronize(ctx_->stream));
+        for (auto& mk : marks_) { cudaEventDestroy(mk.a); cudaEventDestroy(mk.b); }
+        marks_.clear();
+    }
+    const int64_t setup_launches = launches_;
+    if (maxit_ > 0) {
+        if (use_graph) {
+            cudaGraph_t g;
+            MBG_CUDA(cudaStreamBeginCapture(ctx_->stream, cudaStreamCaptureModeThreadLocal));
+            iteration();
+            MBG_CUDA(cudaStreamEndCapture(ctx_->stream, &g));
+            MBG_CUDA(cudaGraphInstantiate(&graph_exec_, g, 0));
+            MBG_CUDA(cudaGraphDestroy(g));
+        }
+        int64_t per_iter = 0;
+        if (use_graph) {
+            per_iter = launches_ - setup_launches;
+            launches_ = setup_launches;
+        }
+        int launched = 0, k = 0;
+        bool have_prev = false;
+        while (launched < maxit_) {
+            const int n = std::min(chunk, maxit_ - launched);
+            for (int i = 0; i < n; ++i) {
+                if (use_graph) {
+                    MBG_CUDA(cudaGraphLaunch(graph_exec_, ctx_->stream));
+                    launches_ += per_iter;
+                } else {
+                    iteration();
+                }
+            }
+            launched += n;
+            int* snap = ctl_host_ + (k & 1) * NCTL;
+            MBG_CUDA(cudaMemcpyAsync(snap, ctl_.p, NCTL * sizeof(int), cudaMemcpyDeviceToHost, ctx_->stream));
+            MBG_CUDA(cudaEventRecord(ev_[k & 1], ctx_->stream));
+            if (have_prev) {
+                int* prev = ctl_host_ + ((k - 1) & 1) * NCTL;
+                MBG_CUDA(cudaEventSynchronize(ev_[(k - 1) & 1]));
+                if (prev[C_STOP]) break;
+            }
+            have_prev = true;
+            ++k;
+        }
+    }
+    MBG_CUDA(cudaEventRecord(t1_, ctx_->stream));
+    MBG_CUDA(cudaStreamSynchronize(ctx_->stream));
+    float ms = 0.f;
+    MBG_CUDA(cudaEventElapsedTime(&ms, t0_, t1_));
+    loop_ms_ = ms;
+    MBG_CUDA(cudaMemcpy(ctl_host_, ctl_.p, NCTL * sizeof(int), cudaMemcpyDeviceToHost));
+}
+
+void Solver::report(double* hist_host, mbg_report* rep) {
+    const int* c = ctl_host_;
+    std::memset(rep, 0, sizeof(*rep));
+    rep->iterations = c[C_ITERS];
+    rep->converged = c[C_CONVERGED];
+    rep->breakdown = c[C_BD];
+    rep->breakdown_iter = c[C_BDITER];
+    rep->breakdown_col = c[C_BDCOL];
+    if (hist_host) {
+        const size_t cnt = static_cast<size_t>(rep->iterations + 1) * m_;
+        MBG_CUDA(cudaMemcpy(hist_host, hist_.p, cnt * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    int reads = 0, writes = 0, spmvs = 0, nred = 0, dots[8];
+    method_schedule(method_, form_, &reads, &writes, &spmvs, &nred, dots);
+    const int its = rep->iterations;
+    rep->vector_reads = static_cast<int64_t>(reads) * its;
+    rep->vector_writes = static_cast<int64_t>(writes) * its;
+    rep->spmv_bytes = static_cast<double>(spmvs) * its * spmv_traffic_bytes(a_->n, a_->nnz, m_);
+    rep->compulsory_bytes = iteration_bytes(method_, form_, a_->n, a_->nnz, m_) * its;
+    rep->reductions = static_cast<int64_t>(nred) * its;
+    rep->gpu_launches = launches_;
+    rep->loop_ms = loop_ms_;
+}
+
+}  // namespace mbg

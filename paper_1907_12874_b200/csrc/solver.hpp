@@ -1,0 +1,80 @@
+// solver.hpp -- device-resident BiCGStab drivers and the byte model.
+#pragma once
+
+#include <initializer_list>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+
+namespace mbg {
+
+// Byte model.
+double spmv_traffic_bytes(int64_t n, int64_t nnz, int m);      // Eq. (3), spmv.cpp:10-16
+double spmv_compulsory_bytes(int64_t n, int64_t nnz, int m);   // x read once
+// Per-iteration schedule totals (Table 2 + identity M^-1 copies for Reordered).
+void method_schedule(int method, int formulation, int* reads, int* writes, int* spmvs, int* nred,
+                     int* dots_per_reduction);
+double iteration_bytes(int method, int formulation, int64_t n, int64_t nnz, int m);
+
+class Solver {
+public:
+    Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulation, double tol, int fixed,
+           int maxit);
+    ~Solver();
+    Solver(const Solver&) = delete;
+    Solver& operator=(const Solver&) = delete;
+
+    // b, x: device arrays (n*m, owned rows); x holds x0 and receives the solution.
+    void run(const double* b, double* x, bool use_graph = true, int chunk = 8);
+    void report(double* hist_host, mbg_report* rep);
+    // Profiling mode: no graph; every launch bracketed by CUDA events on the
+    // main stream.  profile_json() returns {label: [launches, ms, bytes/launch]}.
+    void enable_profile() { profile_ = true; }
+    std::string profile_json();
+
+private:
+    double* w(int i) { return work_[i].p; }
+    double* sc(int i);
+    int64_t* slot(int i);
+    int64_t* dsl(int i);
+    double* part(int i);
+    void spmm(const double* x, double* y);
+    template <class P>
+    void group(std::initializer_list<const double*> in, std::initializer_list<double*> out,
+               std::initializer_list<int> co, int first_slot);
+    void copy(double* dst, const double* src);
+    void scalars(int point, int nd);
+    void setup(const double* b, double* x);
+    void iteration();
+
+    mbg_ctx* ctx_;
+    const mbg_csr* a_;
+    int m_, method_, form_;
+    double tol_;
+    int fixed_, maxit_;
+    int64_t n_ = 0, len_ = 0, rows_alloc_ = 0;
+    int max_blocks_ = 0;
+    std::vector<DevBuf<double>> work_;
+    DevBuf<double> scal_, hist_, part_;
+    DevBuf<int> ctl_;
+    DevBuf<int64_t> slots_, D_;
+    int* ctl_host_ = nullptr;
+    cudaEvent_t ev_[2] = {nullptr, nullptr};
+    cudaEvent_t t0_ = nullptr, t1_ = nullptr;
+    cudaGraphExec_t graph_exec_ = nullptr;
+    const double* b_ = nullptr;
+    double* x_ = nullptr;
+    int64_t launches_ = 0;
+    int64_t reductions_ = 0;
+    float loop_ms_ = 0.f;
+    // profiling
+    bool profile_ = false;
+    struct Mark { std::string label; double bytes; cudaEvent_t a, b; };
+    std::vector<Mark> marks_;
+    void mark_begin(const std::string& label, double bytes);
+    void mark_end();
+};
+
+}  // namespace mbg
