@@ -115,18 +115,38 @@ extern "C" int mbg_csr_validate(int64_t n, const int64_t* off, const int32_t* co
     return guarded([&] { validate_csr(n, off, col, nnz); });
 }
 
+// Upload a (local) CSR with int32 offsets.  Arrays are padded by 8 entries so
+// the SpMM's 16-byte-aligned TMA bulk copies may round a tile's range up.
+static void csr_arrays_to_device(mbg_ctx* ctx, mbg_csr* a, int64_t n, const std::vector<int32_t>& off32,
+                                 const int32_t* col, const double* val, int64_t nnz) {
+    constexpr int PAD = 8;
+    std::vector<int32_t> o(off32);
+    o.resize(off32.size() + PAD, off32.back());
+    upload(a->off, o.data(), o.size(), ctx->stream);
+    a->col.alloc(static_cast<size_t>(nnz) + PAD);
+    a->val.alloc(static_cast<size_t>(nnz) + PAD);
+    MBG_CUDA(cudaMemsetAsync(a->col.p, 0, (nnz + PAD) * sizeof(int32_t), ctx->stream));
+    MBG_CUDA(cudaMemsetAsync(a->val.p, 0, (nnz + PAD) * sizeof(double), ctx->stream));
+    if (nnz) {
+        MBG_CUDA(cudaMemcpyAsync(a->col.p, col, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+        MBG_CUDA(cudaMemcpyAsync(a->val.p, val, nnz * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    a->n = n;
+    a->nnz = nnz;
+    std::vector<int32_t> all(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) all[i] = static_cast<int32_t>(i);
+    auto t = build_spmm_tiles(off32, all);
+    upload(a->tiles_all, t.data(), t.size(), ctx->stream);
+    MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
 static void csr_to_device(mbg_ctx* ctx, mbg_csr* a, int64_t n, const int64_t* off, const int32_t* col,
                           const double* val) {
     const int64_t nnz = off[n];
-    if (nnz > INT32_MAX) throw Invalid("csr: nnz >= 2^31 needs 64-bit offsets (not supported)");
+    if (nnz > INT32_MAX - 64) throw Invalid("csr: nnz >= 2^31 needs 64-bit offsets (not supported)");
     std::vector<int32_t> off32(n + 1);
     for (int64_t i = 0; i <= n; ++i) off32[i] = static_cast<int32_t>(off[i]);
-    upload(a->off, off32.data(), off32.size(), ctx->stream);
-    upload(a->col, col, nnz, ctx->stream);
-    upload(a->val, val, nnz, ctx->stream);
-    MBG_CUDA(cudaStreamSynchronize(ctx->stream));
-    a->n = n;
-    a->nnz = nnz;
+    csr_arrays_to_device(ctx, a, n, off32, col, val, nnz);
 }
 
 extern "C" int mbg_csr_upload(mbg_ctx* ctx, int64_t n, const int64_t* off, const int32_t* col,
@@ -166,10 +186,13 @@ extern "C" int mbg_csr_upload_partitioned(mbg_ctx* ctx, int64_t n, const int64_t
             a->n = pl.n_own;
             a->nnz = pl.nnz;
             a->n_halo = pl.n_halo;
-            upload(a->off, pl.off.data(), pl.off.size(), ctx->stream);
-            upload(a->col, pl.col.data(), pl.col.size(), ctx->stream);
-            upload(a->val, pl.val.data(), pl.val.size(), ctx->stream);
+            csr_arrays_to_device(ctx, a, pl.n_own, pl.off, pl.col.data(), pl.val.data(), pl.nnz);
+            a->nnz = pl.nnz;
             if (nparts > 1) {
+                auto ti = build_spmm_tiles(pl.off, pl.interior);
+                auto tb = build_spmm_tiles(pl.off, pl.boundary);
+                upload(a->tiles_interior, ti.data(), ti.size(), ctx->stream);
+                upload(a->tiles_boundary, tb.data(), tb.size(), ctx->stream);
                 upload(a->interior_rows, pl.interior.data(), pl.interior.size(), ctx->stream);
                 upload(a->boundary_rows, pl.boundary.data(), pl.boundary.size(), ctx->stream);
                 a->n_interior = static_cast<int64_t>(pl.interior.size());

@@ -52,9 +52,10 @@ static void side_to_main(mbg_ctx* ctx) {
 }
 
 int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, const int* ctl) {
+    auto tiles = [](const mbg::DevBuf<int4>& t) { return SpmmTiles{t.p, static_cast<int64_t>(t.n)}; };
     if (a->peers.empty()) {
-        launch_spmm(ctx->stream, a->n, nullptr, a->off.p, a->col.p, a->val.p, m, x, y, ctl);
-        return 1;
+        return launch_spmm(ctx->stream, tiles(a->tiles_all), a->n, nullptr, a->off.p, a->col.p, a->val.p, m, x,
+                           y, ctl, ctx->num_sms);
     }
     Comm* cm = ctx->comm;
     if (!cm) throw Invalid("spmv: partitioned matrix needs a communicator (mbg_ctx_init_comm)");
@@ -87,11 +88,11 @@ int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, 
     }
     MBG_NCCL(ncclGroupEnd());
     // interior rows overlap the exchange; boundary rows wait for the halo
-    launch_spmm(ctx->stream, a->n_interior, a->interior_rows.p, a->off.p, a->col.p, a->val.p, m, x, y, ctl);
-    ++launches;
+    launches += launch_spmm(ctx->stream, tiles(a->tiles_interior), a->n_interior, a->interior_rows.p, a->off.p,
+                            a->col.p, a->val.p, m, x, y, ctl, ctx->num_sms);
     side_to_main(ctx);
-    launch_spmm(ctx->stream, a->n_boundary, a->boundary_rows.p, a->off.p, a->col.p, a->val.p, m, x, y, ctl);
-    ++launches;
+    launches += launch_spmm(ctx->stream, tiles(a->tiles_boundary), a->n_boundary, a->boundary_rows.p, a->off.p,
+                            a->col.p, a->val.p, m, x, y, ctl, ctx->num_sms);
     return launches;
 }
 

@@ -114,6 +114,8 @@ struct mbg_csr {
     mbg::DevBuf<int32_t> interior_rows;       // rows whose columns are all owned
     mbg::DevBuf<int32_t> boundary_rows;       // rows touching halo columns
     int64_t n_interior = 0, n_boundary = 0;
+    // SpMM tile plans (spmm.cu): all rows, interior rows, boundary rows
+    mbg::DevBuf<int4> tiles_all, tiles_interior, tiles_boundary;
     struct Peer {
         int rank;
         int64_t send_count, recv_count;

@@ -9,102 +9,6 @@
 namespace mbg {
 
 // ===========================================================================
-// SpMM  y = A x  over the row-interleaved n x m block.
-//
-// Restates spmv_rows (spmv.cpp:27-50): for each (row, column) the products
-// val[k]*x(col[k], c) are added to acc = 0.0 sequentially in CSR order, with
-// separately rounded multiply and add.  Mapping (m | 32): a warp covers
-// 32/m consecutive rows, lane = column, so the x-gather of one nonzero is m*8
-// contiguous bytes and the y store of a warp is 256 contiguous bytes.  col/val
-// are read with the no-allocate streaming hint (used once) and x through the
-// read-only path (reused across neighbouring rows from L1/L2).  Nonzeros are
-// processed in batches of 8: all index/value loads, then all gathers, then the
-// ordered adds, to keep 16+ loads in flight per thread.
-// ===========================================================================
-template <int M>
-__global__ void __launch_bounds__(256) spmm_kernel(int64_t nrows, const int32_t* __restrict__ rows,
-                                                   const int32_t* __restrict__ off,
-                                                   const int32_t* __restrict__ col,
-                                                   const double* __restrict__ val,
-                                                   const double* __restrict__ x, double* __restrict__ y,
-                                                   const int* __restrict__ ctl) {
-    if (ctl && ctl[0]) return;
-    constexpr int RPW = 32 / M;
-    const int lane = threadIdx.x & 31;
-    const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t ri = w * RPW + lane / M;
-    const int c = lane % M;
-    if (ri >= nrows) return;
-    const int64_t row = rows ? rows[ri] : ri;
-    const int k0 = __ldg(off + row), k1 = __ldg(off + row + 1);
-    double acc = 0.0;
-    for (int k = k0; k < k1; k += 8) {
-        const int cnt = min(8, k1 - k);
-        int j[8];
-        double a[8], xv[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-            if (i < cnt) {
-                j[i] = __ldcs(col + k + i);
-                a[i] = __ldcs(val + k + i);
-            }
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-            if (i < cnt) xv[i] = __ldg(x + static_cast<int64_t>(j[i]) * M + c);
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-            if (i < cnt) acc = __dadd_rn(acc, __dmul_rn(a[i], xv[i]));
-    }
-    y[row * M + c] = acc;
-}
-
-// Any m: one thread per (row, column) element.
-__global__ void __launch_bounds__(256) spmm_generic_kernel(int64_t nrows, const int32_t* __restrict__ rows,
-                                                           const int32_t* __restrict__ off,
-                                                           const int32_t* __restrict__ col,
-                                                           const double* __restrict__ val, int m,
-                                                           const double* __restrict__ x,
-                                                           double* __restrict__ y,
-                                                           const int* __restrict__ ctl) {
-    if (ctl && ctl[0]) return;
-    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (e >= nrows * m) return;
-    const int64_t ri = e / m;
-    const int c = static_cast<int>(e - ri * m);
-    const int64_t row = rows ? rows[ri] : ri;
-    const int k0 = off[row], k1 = off[row + 1];
-    double acc = 0.0;
-    for (int k = k0; k < k1; ++k)
-        acc = __dadd_rn(acc, __dmul_rn(val[k], x[static_cast<int64_t>(col[k]) * m + c]));
-    y[row * m + c] = acc;
-}
-
-void launch_spmm(cudaStream_t st, int64_t nrows, const int32_t* rows, const int32_t* off,
-                 const int32_t* col, const double* val, int m, const double* x, double* y,
-                 const int* ctl) {
-    if (nrows <= 0) return;
-    const int block = 256;
-    auto grid_for = [&](int M) {
-        const int64_t warps = (nrows + (32 / M) - 1) / (32 / M);
-        return static_cast<unsigned>((warps * 32 + block - 1) / block);
-    };
-    switch (m) {
-        case 1: spmm_kernel<1><<<grid_for(1), block, 0, st>>>(nrows, rows, off, col, val, x, y, ctl); break;
-        case 2: spmm_kernel<2><<<grid_for(2), block, 0, st>>>(nrows, rows, off, col, val, x, y, ctl); break;
-        case 4: spmm_kernel<4><<<grid_for(4), block, 0, st>>>(nrows, rows, off, col, val, x, y, ctl); break;
-        case 8: spmm_kernel<8><<<grid_for(8), block, 0, st>>>(nrows, rows, off, col, val, x, y, ctl); break;
-        case 16: spmm_kernel<16><<<grid_for(16), block, 0, st>>>(nrows, rows, off, col, val, x, y, ctl); break;
-        case 32: spmm_kernel<32><<<grid_for(32), block, 0, st>>>(nrows, rows, off, col, val, x, y, ctl); break;
-        default: {
-            const int64_t total = nrows * m;
-            spmm_generic_kernel<<<static_cast<unsigned>((total + block - 1) / block), block, 0, st>>>(
-                nrows, rows, off, col, val, m, x, y, ctl);
-        }
-    }
-    MBG_CUDA(cudaGetLastError());
-}
-
-// ===========================================================================
 // Fold: block partials + long accumulator -> D, then clear the slot.
 // ===========================================================================
 __global__ void fold_kernel(FoldArgs f) {

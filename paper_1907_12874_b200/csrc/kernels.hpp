@@ -4,17 +4,25 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "group.cuh"
 
 namespace mbg {
 
-// CSR SpMM over the interleaved block (spmm.cu).  rows[] optional: a list of
-// local rows to compute (interior / boundary pass of a partitioned matrix);
-// nullptr = rows [0, n).
-void launch_spmm(cudaStream_t st, int64_t nrows, const int32_t* rows, const int32_t* off,
-                 const int32_t* col, const double* val, int m, const double* x, double* y,
-                 const int* ctl);
+// CSR SpMM over the interleaved block (spmm.cu).  The row set to compute is
+// given twice: as a tile list (TMA-pipelined kernels, m in {1,2,4,8,16,32})
+// and as an explicit row list (nullptr = rows [0, nrows)) for other m.
+constexpr int SPMM_TILE_ROWS = 256;
+constexpr int SPMM_TILE_NNZ = 2560;
+struct SpmmTiles {
+    const int4* tiles = nullptr;   // (r0, r1, k0, k1) per tile
+    int64_t count = 0;
+};
+int launch_spmm(cudaStream_t st, const SpmmTiles& tl, int64_t nrows, const int32_t* rows, const int32_t* off,
+                const int32_t* col, const double* val, int m, const double* x, double* y, const int* ctl,
+                int num_sms);
+std::vector<int4> build_spmm_tiles(const std::vector<int32_t>& off, const std::vector<int32_t>& rows);
 
 // Fold block partials (kernels.cu).
 void launch_fold(cudaStream_t st, const FoldArgs& f, int nslots);

@@ -1,0 +1,264 @@
+// spmm.cu -- CSR SpMM  Y = A X  over the row-interleaved n x m fp64 block.
+//
+// Restates spmv_rows (spmv.cpp:27-50): for every (row, column) the products
+// val[k]*x(col[k], c) are added to acc = 0.0 sequentially in CSR order with
+// separately rounded multiply and add -- bitwise the reference's arithmetic.
+//
+// B200 design (m in {1,2,4,8,16,32}):
+//   * the matrix is cut at upload into row tiles of <= 256 rows and <= 2560
+//     nonzeros (tile list in HBM, see build_spmm_tiles);
+//   * a persistent grid walks the tiles; per block a single thread streams the
+//     next tiles' row offsets, column indices and values into shared memory
+//     with TMA bulk copies (cp.async.bulk, mbarrier complete_tx), double
+//     buffered, so the CSR stream (12 B/nnz + 4 B/row) is fetched
+//     asynchronously while the current tile computes;
+//   * each lane owns one row and two adjacent columns: the x gather of one
+//     nonzero is a 16-byte read-only load (x rows are reused across
+//     neighbouring rows from L1/L2) and a warp's y store is 512 contiguous
+//     bytes;
+//   * gathers are issued in batches of 8 nonzeros before the ordered adds.
+// Any other m uses a thread-per-(row, column) kernel with the same arithmetic.
+#include <cstdint>
+
+#include "common.hpp"
+#include "kernels.hpp"
+
+namespace mbg {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+}  // namespace
+
+// smem layout per buffer: offsets | cols | vals (each 16-byte aligned)
+constexpr int OFF_CAP = SPMM_TILE_ROWS + 8;
+constexpr int NNZ_PAD = SPMM_TILE_NNZ + 8;
+constexpr int BUF_BYTES = OFF_CAP * 4 + NNZ_PAD * 4 + NNZ_PAD * 8;
+constexpr int SMEM_HEAD = 128;  // 2 mbarriers + 2 tile metas
+constexpr int SPMM_SMEM = SMEM_HEAD + 2 * BUF_BYTES;
+static_assert(BUF_BYTES % 16 == 0, "buffer alignment");
+static_assert((OFF_CAP * 4) % 16 == 0 && (NNZ_PAD * 4) % 16 == 0, "region alignment");
+
+template <int M>
+__global__ void __launch_bounds__(256) spmm_tma_kernel(const int4* __restrict__ tiles, int ntiles,
+                                                       const int32_t* __restrict__ off,
+                                                       const int32_t* __restrict__ col,
+                                                       const double* __restrict__ val,
+                                                       const double* __restrict__ x, double* __restrict__ y,
+                                                       const int* __restrict__ ctl) {
+    if (ctl && ctl[0]) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+    int4* meta = reinterpret_cast<int4*>(smem + 32);
+    unsigned char* bufs = smem + SMEM_HEAD;
+    const int tid = threadIdx.x;
+
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    auto issue = [&](int i, int b) {
+        const int t = blockIdx.x + i * gridDim.x;
+        if (t >= ntiles) return;
+        const int4 tl = tiles[t];
+        const int r0a = tl.x & ~3, r1a = (tl.y + 1 + 3) & ~3;
+        const int k0a = tl.z & ~3, k1a = (tl.w + 3) & ~3;
+        const bool lng = tl.w - tl.z > SPMM_TILE_NNZ;
+        meta[b] = make_int4(tl.x, tl.y, r0a, k0a);
+        unsigned char* buf = bufs + b * BUF_BYTES;
+        const uint32_t boff = static_cast<uint32_t>(r1a - r0a) * 4u;
+        const uint32_t bnnz = lng ? 0u : static_cast<uint32_t>(k1a - k0a);
+        mbar_expect_tx(&bars[b], boff + bnnz * 12u);
+        bulk_g2s(buf, off + r0a, boff, &bars[b]);
+        if (bnnz) {
+            bulk_g2s(buf + OFF_CAP * 4, col + k0a, bnnz * 4u, &bars[b]);
+            bulk_g2s(buf + OFF_CAP * 4 + NNZ_PAD * 4, val + k0a, bnnz * 8u, &bars[b]);
+        }
+    };
+    if (tid == 0) {
+        issue(0, 0);
+        issue(1, 1);
+    }
+
+    constexpr int VW = M >= 2 ? 2 : 1;        // columns per lane
+    constexpr int LPR = M / VW;               // lanes per row
+    constexpr int RPP = 256 / LPR;            // rows per pass of the block
+    const int cp = (tid % LPR) * VW;
+
+    for (int i = 0;; ++i) {
+        const int t = blockIdx.x + i * gridDim.x;
+        if (t >= ntiles) break;
+        const int b = i & 1;
+        while (!mbar_try_wait(&bars[b], static_cast<uint32_t>((i >> 1) & 1))) {
+        }
+        const int4 mt = meta[b];
+        const int r0 = mt.x, r1 = mt.y, r0a = mt.z, k0a = mt.w;
+        const unsigned char* buf = bufs + b * BUF_BYTES;
+        const int32_t* s_off = reinterpret_cast<const int32_t*>(buf);
+        const int32_t* s_col = reinterpret_cast<const int32_t*>(buf + OFF_CAP * 4);
+        const double* s_val = reinterpret_cast<const double*>(buf + OFF_CAP * 4 + NNZ_PAD * 4);
+        const int k_first = s_off[r0 - r0a];
+        const bool lng = s_off[r1 - r0a] - k_first > SPMM_TILE_NNZ;
+        for (int rr = tid / LPR; rr < r1 - r0; rr += RPP) {
+            const int row = r0 + rr;
+            const int k0 = s_off[row - r0a], k1 = s_off[row + 1 - r0a];
+            double acc0 = 0.0, acc1 = 0.0;
+            for (int k = k0; k < k1; k += 8) {
+                const int cnt = min(8, k1 - k);
+                int j[8];
+                double a[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (q < cnt) {
+                        if (!lng) {
+                            j[q] = s_col[k - k0a + q];
+                            a[q] = s_val[k - k0a + q];
+                        } else {
+                            j[q] = __ldg(col + k + q);
+                            a[q] = __ldg(val + k + q);
+                        }
+                    }
+                if constexpr (VW == 2) {
+                    double2 xv[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        if (q < cnt) xv[q] = __ldg(reinterpret_cast<const double2*>(x + static_cast<int64_t>(j[q]) * M + cp));
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        if (q < cnt) {
+                            acc0 = __dadd_rn(acc0, __dmul_rn(a[q], xv[q].x));
+                            acc1 = __dadd_rn(acc1, __dmul_rn(a[q], xv[q].y));
+                        }
+                } else {
+                    double xv[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        if (q < cnt) xv[q] = __ldg(x + j[q]);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        if (q < cnt) acc0 = __dadd_rn(acc0, __dmul_rn(a[q], xv[q]));
+                }
+            }
+            if constexpr (VW == 2)
+                *reinterpret_cast<double2*>(y + static_cast<int64_t>(row) * M + cp) = make_double2(acc0, acc1);
+            else
+                y[row] = acc0;
+        }
+        __syncthreads();  // every thread is done with buffer b
+        if (tid == 0) issue(i + 2, b);
+    }
+}
+
+// Any m: one thread per (row, column) element over an explicit row list.
+__global__ void __launch_bounds__(256) spmm_generic_kernel(int64_t nrows, const int32_t* __restrict__ rows,
+                                                           const int32_t* __restrict__ off,
+                                                           const int32_t* __restrict__ col,
+                                                           const double* __restrict__ val, int m,
+                                                           const double* __restrict__ x,
+                                                           double* __restrict__ y,
+                                                           const int* __restrict__ ctl) {
+    if (ctl && ctl[0]) return;
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= nrows * m) return;
+    const int64_t ri = e / m;
+    const int c = static_cast<int>(e - ri * m);
+    const int64_t row = rows ? rows[ri] : ri;
+    const int k0 = off[row], k1 = off[row + 1];
+    double acc = 0.0;
+    for (int k = k0; k < k1; ++k)
+        acc = __dadd_rn(acc, __dmul_rn(val[k], x[static_cast<int64_t>(col[k]) * m + c]));
+    y[row * m + c] = acc;
+}
+
+template <int M>
+static void launch_tma(cudaStream_t st, const SpmmTiles& tl, const int32_t* off, const int32_t* col,
+                       const double* val, const double* x, double* y, const int* ctl, int num_sms) {
+    static int occ = -1;
+    if (occ < 0) {
+        MBG_CUDA(cudaFuncSetAttribute(spmm_tma_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, SPMM_SMEM));
+        MBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmm_tma_kernel<M>, 256, SPMM_SMEM));
+        if (occ < 1) occ = 1;
+    }
+    const int grid = static_cast<int>(std::min<int64_t>(tl.count, static_cast<int64_t>(num_sms) * occ));
+    spmm_tma_kernel<M><<<grid, 256, SPMM_SMEM, st>>>(tl.tiles, static_cast<int>(tl.count), off, col, val, x, y, ctl);
+}
+
+int launch_spmm(cudaStream_t st, const SpmmTiles& tl, int64_t nrows, const int32_t* rows, const int32_t* off,
+                const int32_t* col, const double* val, int m, const double* x, double* y, const int* ctl,
+                int num_sms) {
+    if (nrows <= 0) return 0;
+    switch (m) {
+        case 1: launch_tma<1>(st, tl, off, col, val, x, y, ctl, num_sms); break;
+        case 2: launch_tma<2>(st, tl, off, col, val, x, y, ctl, num_sms); break;
+        case 4: launch_tma<4>(st, tl, off, col, val, x, y, ctl, num_sms); break;
+        case 8: launch_tma<8>(st, tl, off, col, val, x, y, ctl, num_sms); break;
+        case 16: launch_tma<16>(st, tl, off, col, val, x, y, ctl, num_sms); break;
+        case 32: launch_tma<32>(st, tl, off, col, val, x, y, ctl, num_sms); break;
+        default: {
+            const int64_t total = nrows * m;
+            spmm_generic_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(nrows, rows, off, col,
+                                                                                            val, m, x, y, ctl);
+        }
+    }
+    MBG_CUDA(cudaGetLastError());
+    return 1;
+}
+
+// Host: cut row segments into tiles of <= SPMM_TILE_ROWS rows and
+// <= SPMM_TILE_NNZ nonzeros; a longer row gets a tile of its own (read from
+// global memory by the kernel).  rows: sorted local row ids of one class
+// (all rows, interior or boundary); tiles never span a gap.
+std::vector<int4> build_spmm_tiles(const std::vector<int32_t>& off, const std::vector<int32_t>& rows) {
+    std::vector<int4> out;
+    size_t i = 0;
+    while (i < rows.size()) {
+        const int r0 = rows[i];
+        int r1 = r0;
+        size_t j = i;
+        while (j < rows.size() && rows[j] == r1 && r1 - r0 < SPMM_TILE_ROWS &&
+               (off[r1 + 1] - off[r0] <= SPMM_TILE_NNZ || r1 == r0)) {
+            ++r1;
+            ++j;
+        }
+        out.push_back(make_int4(r0, r1, off[r0], off[r1]));
+        i = j;
+    }
+    return out;
+}
+
+}  // namespace mbg
