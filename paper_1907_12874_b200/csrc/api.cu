@@ -413,15 +413,11 @@ extern "C" int mbg_execute_group(mbg_ctx* ctx, const mbg_statement* st, int ns, 
         g.m = m;
         for (int i = 0; i < nvec; ++i) g.vec[i] = vectors[i] ? vectors[i]->data.p : nullptr;
         g.nslots = used_slots;
-        const int max_blocks = ctx->num_sms * 8;
         const size_t slot_words = static_cast<size_t>(used_slots) * m * NSLOT;
-        const size_t part_words = static_cast<size_t>(used_slots) * m * max_blocks * KEXP;
-        ctx->scratch_i64.ensure(2 * slot_words + 1);
-        ctx->scratch_f64.ensure(part_words + coef.size() + static_cast<size_t>(used_slots) * m + 1);
+        ctx->scratch_i64.ensure(slot_words + 1);
+        ctx->scratch_f64.ensure(coef.size() + static_cast<size_t>(used_slots) * m + 1);
         int64_t* slots = ctx->scratch_i64.p;
-        int64_t* D = slots + slot_words;
-        double* part = ctx->scratch_f64.p;
-        double* dcoef = part + part_words;
+        double* dcoef = ctx->scratch_f64.p;
         double* rounded = dcoef + coef.size();
         if (slot_words) MBG_CUDA(cudaMemsetAsync(slots, 0, slot_words * sizeof(int64_t), ctx->stream));
         if (!coef.empty())
@@ -429,26 +425,12 @@ extern "C" int mbg_execute_group(mbg_ctx* ctx, const mbg_statement* st, int ns, 
                                      ctx->stream));
         g.coef = dcoef;
         g.slot = slots;
-        g.part = part;
         int nblocks = 0;
         launch_generic_group(ctx->stream, g, ctx->num_sms, &nblocks);
         ctx->launches++;
         if (used_slots) {
-            for (int s0 = 0; s0 < used_slots; s0 += GMAX_DOT) {
-                FoldArgs f{};
-                f.m = m;
-                f.nblocks = nblocks;
-                const int cnt = std::min(GMAX_DOT, used_slots - s0);
-                for (int s = 0; s < cnt; ++s) {
-                    f.slot[s] = slots + static_cast<size_t>(s0 + s) * m * NSLOT;
-                    f.part[s] = part + static_cast<size_t>(s0 + s) * m * nblocks * KEXP;
-                    f.D[s] = D + static_cast<size_t>(s0 + s) * m * NSLOT;
-                }
-                launch_fold(ctx->stream, f, cnt);
-                ctx->launches++;
-            }
-            if (ctx->comm) comm_allreduce_i64(ctx, D, slot_words, ctx->stream);
-            launch_round(ctx->stream, D, used_slots, m, rounded);
+            if (ctx->comm) comm_allreduce_i64(ctx, slots, slot_words, ctx->stream);
+            launch_round(ctx->stream, slots, used_slots, m, rounded);
             ctx->launches++;
             std::vector<double> h(static_cast<size_t>(used_slots) * m);
             MBG_CUDA(cudaMemcpyAsync(h.data(), rounded, h.size() * sizeof(double), cudaMemcpyDeviceToHost,

@@ -32,7 +32,6 @@ struct GroupArgs {
     double* out[GMAX_OUT];
     const double* coef[GMAX_CO]; // device arrays of m doubles
     int64_t* slot[GMAX_DOT];     // long accumulators: m * NSLOT words each
-    double* part[GMAX_DOT];      // block partial expansions: m * nblocks * KEXP
     const int* ctl;              // ctl[0] != 0: solve stopped -> no-op
 };
 
@@ -183,23 +182,26 @@ struct PPipeG5 {
 };
 
 // ---------------------------------------------------------------------------
-// Block-level exact combine of the per-thread expansions; thread t of the
-// block owns column t % m.  Result: one expansion per (dot, column) written
-// to part[d][(c * nblocks + block) * KEXP + i].  Residuals go to the slot.
+// Block-level exact combine.  Threads of a block fall into `classes` column
+// classes (thread t is in class t % classes; the block size is classes * 2^q).
+// Each thread holds NX expansions; expansion x of class k belongs to the
+// long-accumulator slot slot_of(x, k).  The expansions of one class are
+// merged exactly (warp shuffles, then a shared-memory tree) and the class
+// leader deposits the K terms of each merged expansion into its slot with
+// integer atomics -- so no partial buffer and no fold kernel are needed; the
+// scalar kernel rounds the slot directly.
 // ---------------------------------------------------------------------------
-template <int ND>
-__device__ __forceinline__ void block_combine(double (&acc)[ND][KEXP], const GroupArgs& a, int c,
+template <int NX, class SlotOf>
+__device__ __forceinline__ void block_combine(double (&acc)[NX][KEXP], int classes, SlotOf slot_of,
                                               double* sh /* blockDim * KEXP doubles */) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int m = a.m;
-    const int nb = gridDim.x;
+    const int k = tid % classes;
 #pragma unroll
-    for (int d = 0; d < ND; ++d) {
-        double (&mine)[KEXP] = acc[d];
-        int64_t* slot = a.slot[d] + static_cast<int64_t>(c) * NSLOT;
-        if (m <= 32 && (32 % m) == 0) {
-            // intra-warp: lanes L and L+off share a column when off % m == 0
-            for (int off = 16; off >= m; off >>= 1) {
+    for (int x = 0; x < NX; ++x) {
+        double (&mine)[KEXP] = acc[x];
+        int64_t* slot = slot_of(x, k);
+        if (classes <= 32 && (32 % classes) == 0 && (blockDim.x & 31) == 0) {
+            for (int off = 16; off >= classes; off >>= 1) {
                 double t[KEXP];
 #pragma unroll
                 for (int i = 0; i < KEXP; ++i) t[i] = __shfl_down_sync(0xffffffffu, mine[i], off);
@@ -209,13 +211,13 @@ __device__ __forceinline__ void block_combine(double (&acc)[ND][KEXP], const Gro
                 }
             }
             const int nw = blockDim.x >> 5;
-            if (lane < m) {
+            if (lane < classes) {
 #pragma unroll
                 for (int i = 0; i < KEXP; ++i) sh[(warp * 32 + lane) * KEXP + i] = mine[i];
             }
             __syncthreads();
             for (int s = nw >> 1; s >= 1; s >>= 1) {
-                if (warp < s && lane < m) {
+                if (warp < s && lane < classes) {
 #pragma unroll
                     for (int i = 0; i < KEXP; ++i) grow(mine, sh[((warp + s) * 32 + lane) * KEXP + i], slot);
 #pragma unroll
@@ -224,82 +226,170 @@ __device__ __forceinline__ void block_combine(double (&acc)[ND][KEXP], const Gro
                 __syncthreads();
             }
         } else {
-            // generic: blockDim = m * 2^q, tree over the rows of the block
 #pragma unroll
             for (int i = 0; i < KEXP; ++i) sh[tid * KEXP + i] = mine[i];
             __syncthreads();
-            for (int s = (blockDim.x / m) >> 1; s >= 1; s >>= 1) {
-                if (tid < s * m) {
+            for (int s = (blockDim.x / classes) >> 1; s >= 1; s >>= 1) {
+                if (tid < s * classes) {
 #pragma unroll
-                    for (int i = 0; i < KEXP; ++i) grow(mine, sh[(tid + s * m) * KEXP + i], slot);
+                    for (int i = 0; i < KEXP; ++i) grow(mine, sh[(tid + s * classes) * KEXP + i], slot);
 #pragma unroll
                     for (int i = 0; i < KEXP; ++i) sh[tid * KEXP + i] = mine[i];
                 }
                 __syncthreads();
             }
         }
-        if (tid < m) {
-            double* p = a.part[d] + (static_cast<int64_t>(tid) * nb + blockIdx.x) * KEXP;
+        if (tid < classes) {
 #pragma unroll
-            for (int i = 0; i < KEXP; ++i) p[i] = mine[i];
+            for (int i = 0; i < KEXP; ++i) digits_add_atomic(slot, mine[i]);
         }
         __syncthreads();
     }
 }
 
 // ---------------------------------------------------------------------------
-// The fused group kernel.  Two elements per thread per trip for memory-level
-// parallelism (all loads of both elements are issued before any store, so an
-// in-place update such as x = x + ... stays correct).
+// The fused group kernel.  VEC = 2: each thread streams 16-byte pairs of
+// elements (e, e+1) -- columns c0 = e % m and c0 + 1 (both 0 when m == 1) --
+// and keeps one expansion per (dot, column of the pair).  Two pairs per trip
+// are loaded before any store (in-place updates such as x = x + ... stay
+// correct) for memory-level parallelism.  VEC = 1 covers odd m.
 // ---------------------------------------------------------------------------
-template <class P>
+template <class P, int VEC>
 __global__ void __launch_bounds__(256) group_kernel(GroupArgs a) {
     if (a.ctl && a.ctl[0]) return;
     extern __shared__ double sh_dyn[];
     const int m = a.m;
-    const int c = threadIdx.x % m;
     constexpr int NCO = P::NCO > 0 ? P::NCO : 1;
     constexpr int ND = P::NDOT > 0 ? P::NDOT : 1;
     constexpr int NO = P::NOUT > 0 ? P::NOUT : 1;
-    double co[NCO];
+    // columns handled by this thread (fixed: the grid stride is a multiple of m)
+    const int c0 = (threadIdx.x * VEC) % m;
+    const int c1 = VEC == 2 ? (m == 1 ? 0 : c0 + 1) : c0;
+    double co0[NCO], co1[NCO];
 #pragma unroll
-    for (int i = 0; i < P::NCO; ++i) co[i] = a.coef[i][c];
-    double acc[ND][KEXP];
+    for (int i = 0; i < P::NCO; ++i) {
+        co0[i] = a.coef[i][c0];
+        co1[i] = a.coef[i][c1];
+    }
+    double acc[ND * VEC][KEXP];
 #pragma unroll
-    for (int d = 0; d < ND; ++d)
+    for (int d = 0; d < ND * VEC; ++d)
 #pragma unroll
         for (int i = 0; i < KEXP; ++i) acc[d][i] = 0.0;
-
-    int64_t* slot[ND];
+    int64_t* slot0[ND];
+    int64_t* slot1[ND];
 #pragma unroll
-    for (int d = 0; d < P::NDOT; ++d) slot[d] = a.slot[d] + static_cast<int64_t>(c) * NSLOT;
+    for (int d = 0; d < P::NDOT; ++d) {
+        slot0[d] = a.slot[d] + static_cast<int64_t>(c0) * NSLOT;
+        slot1[d] = a.slot[d] + static_cast<int64_t>(c1) * NSLOT;
+    }
 
+    const int64_t npk = a.len / VEC;  // packets of VEC elements
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    for (; e + stride < a.len; e += 2 * stride) {
-        double in0[P::NIN], in1[P::NIN];
+    int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if constexpr (VEC == 2) {
+        for (; q + stride < npk; q += 2 * stride) {
+            double2 u0[P::NIN], u1[P::NIN];
 #pragma unroll
-        for (int i = 0; i < P::NIN; ++i) { in0[i] = a.in[i][e]; in1[i] = a.in[i][e + stride]; }
-        double out0[NO], out1[NO], pr0[ND], pr1[ND];
-        P::run(in0, out0, pr0, co);
-        P::run(in1, out1, pr1, co);
+            for (int i = 0; i < P::NIN; ++i) {
+                u0[i] = reinterpret_cast<const double2*>(a.in[i])[q];
+                u1[i] = reinterpret_cast<const double2*>(a.in[i])[q + stride];
+            }
+            double in[P::NIN], o0[NO], o1[NO], o2[NO], o3[NO], p0[ND], p1[ND], p2[ND], p3[ND];
 #pragma unroll
-        for (int i = 0; i < P::NOUT; ++i) { a.out[i][e] = out0[i]; a.out[i][e + stride] = out1[i]; }
+            for (int i = 0; i < P::NIN; ++i) in[i] = u0[i].x;
+            P::run(in, o0, p0, co0);
 #pragma unroll
-        for (int d = 0; d < P::NDOT; ++d) { grow(acc[d], pr0[d], slot[d]); grow(acc[d], pr1[d], slot[d]); }
+            for (int i = 0; i < P::NIN; ++i) in[i] = u0[i].y;
+            P::run(in, o1, p1, co1);
+#pragma unroll
+            for (int i = 0; i < P::NIN; ++i) in[i] = u1[i].x;
+            P::run(in, o2, p2, co0);
+#pragma unroll
+            for (int i = 0; i < P::NIN; ++i) in[i] = u1[i].y;
+            P::run(in, o3, p3, co1);
+#pragma unroll
+            for (int i = 0; i < P::NOUT; ++i) {
+                reinterpret_cast<double2*>(a.out[i])[q] = make_double2(o0[i], o1[i]);
+                reinterpret_cast<double2*>(a.out[i])[q + stride] = make_double2(o2[i], o3[i]);
+            }
+#pragma unroll
+            for (int d = 0; d < P::NDOT; ++d) {
+                grow(acc[2 * d], p0[d], slot0[d]);
+                grow(acc[2 * d + 1], p1[d], slot1[d]);
+                grow(acc[2 * d], p2[d], slot0[d]);
+                grow(acc[2 * d + 1], p3[d], slot1[d]);
+            }
+        }
+        if (q < npk) {
+            double2 u0[P::NIN];
+#pragma unroll
+            for (int i = 0; i < P::NIN; ++i) u0[i] = reinterpret_cast<const double2*>(a.in[i])[q];
+            double in[P::NIN], o0[NO], o1[NO], p0[ND], p1[ND];
+#pragma unroll
+            for (int i = 0; i < P::NIN; ++i) in[i] = u0[i].x;
+            P::run(in, o0, p0, co0);
+#pragma unroll
+            for (int i = 0; i < P::NIN; ++i) in[i] = u0[i].y;
+            P::run(in, o1, p1, co1);
+#pragma unroll
+            for (int i = 0; i < P::NOUT; ++i) reinterpret_cast<double2*>(a.out[i])[q] = make_double2(o0[i], o1[i]);
+#pragma unroll
+            for (int d = 0; d < P::NDOT; ++d) {
+                grow(acc[2 * d], p0[d], slot0[d]);
+                grow(acc[2 * d + 1], p1[d], slot1[d]);
+            }
+        }
+    } else {
+        for (; q + stride < npk; q += 2 * stride) {
+            double in0[P::NIN], in1[P::NIN];
+#pragma unroll
+            for (int i = 0; i < P::NIN; ++i) { in0[i] = a.in[i][q]; in1[i] = a.in[i][q + stride]; }
+            double o0[NO], o1[NO], p0[ND], p1[ND];
+            P::run(in0, o0, p0, co0);
+            P::run(in1, o1, p1, co0);
+#pragma unroll
+            for (int i = 0; i < P::NOUT; ++i) { a.out[i][q] = o0[i]; a.out[i][q + stride] = o1[i]; }
+#pragma unroll
+            for (int d = 0; d < P::NDOT; ++d) { grow(acc[d], p0[d], slot0[d]); grow(acc[d], p1[d], slot0[d]); }
+        }
+        if (q < npk) {
+            double in0[P::NIN];
+#pragma unroll
+            for (int i = 0; i < P::NIN; ++i) in0[i] = a.in[i][q];
+            double o0[NO], p0[ND];
+            P::run(in0, o0, p0, co0);
+#pragma unroll
+            for (int i = 0; i < P::NOUT; ++i) a.out[i][q] = o0[i];
+#pragma unroll
+            for (int d = 0; d < P::NDOT; ++d) grow(acc[d], p0[d], slot0[d]);
+        }
     }
-    if (e < a.len) {
-        double in0[P::NIN];
+    if constexpr (P::NDOT > 0) {
+        int classes;
+        if constexpr (VEC == 2) {
+            if (m == 1) {
+                // both lanes of the pair are column 0: merge the second expansion set
 #pragma unroll
-        for (int i = 0; i < P::NIN; ++i) in0[i] = a.in[i][e];
-        double out0[NO], pr0[ND];
-        P::run(in0, out0, pr0, co);
+                for (int d = 0; d < P::NDOT; ++d)
 #pragma unroll
-        for (int i = 0; i < P::NOUT; ++i) a.out[i][e] = out0[i];
-#pragma unroll
-        for (int d = 0; d < P::NDOT; ++d) grow(acc[d], pr0[d], slot[d]);
+                    for (int i = 0; i < KEXP; ++i) grow(acc[2 * d], acc[2 * d + 1][i], slot0[d]), acc[2 * d + 1][i] = 0.0;
+                classes = 1;
+            } else {
+                classes = m / 2;
+            }
+        } else {
+            classes = m;
+        }
+        // expansion x = d*VEC + v of class k -> column k*VEC + v (or 0 for m == 1)
+        block_combine<ND * VEC>(acc, classes,
+                                [&](int x, int k) {
+                                    const int d = x / VEC, v = x % VEC;
+                                    const int col = m == 1 ? 0 : k * VEC + v;
+                                    return a.slot[d] + static_cast<int64_t>(col) * NSLOT;
+                                },
+                                sh_dyn);
     }
-    if constexpr (P::NDOT > 0) block_combine<P::NDOT>(acc, a, c, sh_dyn);
 }
 
 // Block size for m columns: m * 2^q <= 256 (m <= 256), else m.
@@ -309,20 +399,5 @@ inline int group_block(int m) {
     while (b * 2 <= 256) b *= 2;
     return b;
 }
-
-// ---------------------------------------------------------------------------
-// Fold: combine all block partials and the long accumulator of each
-// (slot, column) into D (long-accumulator form, one carry step applied so
-// words stay below 2^33), and clear the slot for its next use.
-// grid = (m, nslots), block = 32.
-// ---------------------------------------------------------------------------
-struct FoldArgs {
-    int m;
-    int nblocks;
-    int64_t* slot[GMAX_DOT];
-    const double* part[GMAX_DOT];
-    int64_t* D[GMAX_DOT];
-    const int* ctl;
-};
 
 }  // namespace mbg

@@ -8,64 +8,16 @@
 
 namespace mbg {
 
-// ===========================================================================
-// Fold: block partials + long accumulator -> D, then clear the slot.
-// ===========================================================================
-__global__ void fold_kernel(FoldArgs f) {
-    if (f.ctl && f.ctl[0]) return;
-    const int c = blockIdx.x, s = blockIdx.y, lane = threadIdx.x;
-    int64_t* slot = f.slot[s] + static_cast<int64_t>(c) * NSLOT;
-    int64_t* D = f.D[s] + static_cast<int64_t>(c) * NSLOT;
-    const double* part = f.part[s] + static_cast<int64_t>(c) * f.nblocks * KEXP;
-    double acc[KEXP] = {0.0, 0.0, 0.0};
-    for (int b = lane; b < f.nblocks; b += 32)
-#pragma unroll
-        for (int i = 0; i < KEXP; ++i) grow(acc, part[b * KEXP + i], slot);
-    for (int o = 16; o >= 1; o >>= 1) {
-        double t[KEXP];
-#pragma unroll
-        for (int i = 0; i < KEXP; ++i) t[i] = __shfl_down_sync(0xffffffffu, acc[i], o);
-        if (lane < o)
-#pragma unroll
-            for (int i = 0; i < KEXP; ++i) grow(acc, t[i], slot);
-    }
-    __shared__ int64_t sd[NSLOT];
-    __syncwarp();
-    __threadfence_block();
-    for (int j = lane; j < NSLOT; j += 32) {
-        sd[j] = atomicExch(reinterpret_cast<unsigned long long*>(slot + j), 0ull);
-    }
-    __syncwarp();
-    if (lane == 0)
-#pragma unroll
-        for (int i = 0; i < KEXP; ++i) digits_add(sd, acc[i]);
-    __syncwarp();
-    // one parallel carry step: words stay below 2^33 in magnitude
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-        const int j = lane + 32 * q;
-        if (j < NDIG) {
-            const int64_t v = sd[j];
-            const int64_t low = (j < NDIG - 1) ? (v & 0xffffffffll) : v;
-            const int64_t cin = j > 0 ? (sd[j - 1] >> 32) : 0;
-            D[j] = low + cin;
-        } else if (j < NSLOT) {
-            D[j] = sd[j];
-        }
-    }
-}
-
-void launch_fold(cudaStream_t st, const FoldArgs& f, int nslots) {
-    fold_kernel<<<dim3(f.m, nslots), 32, 0, st>>>(f);
-    MBG_CUDA(cudaGetLastError());
-}
-
-__global__ void round_kernel(const int64_t* D, int nslots, int m, double* out) {
+__global__ void round_kernel(int64_t* D, int nslots, int m, double* out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < nslots * m) out[i] = digits_round(D + static_cast<int64_t>(i) * NSLOT);
+    if (i < nslots * m) {
+        int64_t* d = D + static_cast<int64_t>(i) * NSLOT;
+        out[i] = digits_round(d);
+        for (int j = 0; j < NSLOT; ++j) d[j] = 0;
+    }
 }
 
-void launch_round(cudaStream_t st, const int64_t* D, int nslots, int m, double* out) {
+void launch_round(cudaStream_t st, int64_t* D, int nslots, int m, double* out) {
     const int n = nslots * m;
     round_kernel<<<(n + 127) / 128, 128, 0, st>>>(D, nslots, m, out);
     MBG_CUDA(cudaGetLastError());
@@ -102,6 +54,7 @@ __global__ void __launch_bounds__(256) generic_group_kernel(GenericGroup g) {
     const int m = g.m;
     const int c = threadIdx.x % m;
     double acc[GEN_MAX_SLOT][KEXP];
+    (void)c;
 #pragma unroll
     for (int s = 0; s < GEN_MAX_SLOT; ++s)
 #pragma unroll
@@ -137,11 +90,8 @@ __global__ void __launch_bounds__(256) generic_group_kernel(GenericGroup g) {
                 if (q == s) v = acc[q][i];
             one[0][i] = v;
         }
-        GroupArgs a{};
-        a.m = m;
-        a.slot[0] = g.slot + static_cast<int64_t>(s) * m * NSLOT;
-        a.part[0] = g.part + static_cast<int64_t>(s) * m * gridDim.x * KEXP;
-        block_combine<1>(one, a, c, sh_dyn);
+        block_combine<1>(one, m,
+                         [&](int, int k) { return g.slot + (static_cast<int64_t>(s) * m + k) * NSLOT; }, sh_dyn);
     }
 }
 

@@ -24,9 +24,6 @@ int launch_spmm(cudaStream_t st, const SpmmTiles& tl, int64_t nrows, const int32
                 int num_sms);
 std::vector<int4> build_spmm_tiles(const std::vector<int32_t>& off, const std::vector<int32_t>& rows);
 
-// Fold block partials (kernels.cu).
-void launch_fold(cudaStream_t st, const FoldArgs& f, int nslots);
-
 // Generic statement-group interpreter (API-level execute_group).
 constexpr int GEN_MAX_VEC = 16, GEN_MAX_STMT = 16, GEN_MAX_SLOT = 8;
 struct GenericGroup {
@@ -41,12 +38,11 @@ struct GenericGroup {
     const double* coef;   // device: term t, column c at coef[t*m + c]
     int nslots;
     int64_t* slot;        // nslots * m * NSLOT
-    double* part;         // nslots * m * nblocks * KEXP
 };
 void launch_generic_group(cudaStream_t st, const GenericGroup& g, int num_sms, int* nblocks_out);
 
-// Round D (long accumulators) into doubles: out[s*m + c] (kernels.cu).
-void launch_round(cudaStream_t st, const int64_t* D, int nslots, int m, double* out);
+// Round long accumulators into doubles out[s*m + c] and clear them (kernels.cu).
+void launch_round(cudaStream_t st, int64_t* D, int nslots, int m, double* out);
 
 // Occupancy-sized persistent grid for a group kernel instantiation.
 int group_grid(const void* kernel, int block, size_t smem, int num_sms, int64_t len);
@@ -55,8 +51,15 @@ template <class P>
 inline int launch_group(cudaStream_t st, const GroupArgs& a, int num_sms) {
     const int block = group_block(a.m);
     const size_t smem = P::NDOT > 0 ? static_cast<size_t>(block) * KEXP * sizeof(double) : 0;
-    const int grid = group_grid(reinterpret_cast<const void*>(&group_kernel<P>), block, smem, num_sms, a.len);
-    group_kernel<P><<<grid, block, smem, st>>>(a);
+    const bool vec2 = (a.m % 2 == 0 || a.m == 1) && a.len % 2 == 0;
+    if (vec2) {
+        const int grid =
+            group_grid(reinterpret_cast<const void*>(&group_kernel<P, 2>), block, smem, num_sms, a.len / 2);
+        group_kernel<P, 2><<<grid, block, smem, st>>>(a);
+        return grid;
+    }
+    const int grid = group_grid(reinterpret_cast<const void*>(&group_kernel<P, 1>), block, smem, num_sms, a.len);
+    group_kernel<P, 1><<<grid, block, smem, st>>>(a);
     return grid;
 }
 

@@ -48,7 +48,7 @@ struct ScalArgs {
     double* sc;          // NSCAL * m
     int* ctl;
     double* hist;        // (maxit+1) * m
-    const int64_t* D[4]; // rounded here (after any cross-GPU allreduce)
+    int64_t* D[4];       // long accumulators: rounded here (after any cross-GPU allreduce), then cleared
     int nd;
 };
 
@@ -74,7 +74,11 @@ __global__ void scalar_kernel(ScalArgs a) {
 #define SC(i) sc[(i) * m + c]
     double d[4] = {0.0, 0.0, 0.0, 0.0};
     if (on)
-        for (int i = 0; i < a.nd; ++i) d[i] = digits_round(a.D[i] + static_cast<int64_t>(c) * NSLOT);
+        for (int i = 0; i < a.nd; ++i) {
+            int64_t* sl = a.D[i] + static_cast<int64_t>(c) * NSLOT;
+            d[i] = digits_round(sl);
+            for (int w = 0; w < NSLOT; ++w) sl[w] = 0;
+        }
     const int j = ctl[C_ITER];
     int code1 = 0, code2 = 0;  // breakdown codes for s_bad1 / s_bad2
     switch (a.point) {
@@ -241,10 +245,7 @@ Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulatio
     scal_.alloc(static_cast<size_t>(NSCAL) * m);
     ctl_.alloc(NCTL);
     hist_.alloc(static_cast<size_t>(maxit + 1) * m);
-    max_blocks_ = ctx->num_sms * 8;
     slots_.alloc(static_cast<size_t>(4) * m * NSLOT);
-    D_.alloc(static_cast<size_t>(4) * m * NSLOT);
-    part_.alloc(static_cast<size_t>(4) * m * max_blocks_ * KEXP);
     MBG_CUDA(cudaMemsetAsync(slots_.p, 0, slots_.n * sizeof(int64_t), ctx->stream));
     MBG_CUDA(cudaMemsetAsync(ctl_.p, 0, ctl_.n * sizeof(int), ctx->stream));
     MBG_CUDA(cudaMallocHost(&ctl_host_, 2 * NCTL * sizeof(int)));
@@ -265,8 +266,6 @@ Solver::~Solver() {
 
 double* Solver::sc(int i) { return scal_.p + static_cast<int64_t>(i) * m_; }
 int64_t* Solver::slot(int i) { return slots_.p + static_cast<int64_t>(i) * m_ * NSLOT; }
-int64_t* Solver::dsl(int i) { return D_.p + static_cast<int64_t>(i) * m_ * NSLOT; }
-double* Solver::part(int i) { return part_.p + static_cast<int64_t>(i) * m_ * max_blocks_ * KEXP; }
 
 void Solver::mark_begin(const std::string& label, double bytes) {
     if (!profile_) return;
@@ -326,34 +325,17 @@ void Solver::group(std::initializer_list<const double*> in, std::initializer_lis
     for (auto p : out) g.out[i++] = p;
     i = 0;
     for (int s : co) g.coef[i++] = sc(s);
-    for (int d = 0; d < P::NDOT; ++d) {
-        g.slot[d] = slot(first_slot + d);
-        g.part[d] = part(first_slot + d);
-    }
+    for (int d = 0; d < P::NDOT; ++d) g.slot[d] = slot(first_slot + d);
     g.ctl = ctl_.p;
     mark_begin(std::string("group:") + P::NAME, static_cast<double>(P::NIN + P::NOUT) * 8.0 * len_);
-    const int grid = launch_group<P>(ctx_->stream, g, ctx_->num_sms);
+    launch_group<P>(ctx_->stream, g, ctx_->num_sms);
     MBG_CUDA(cudaGetLastError());
     mark_end();
     launches_++;
     if (P::NDOT > 0) {
-        // fold immediately (one reduction point per dot group)
-        FoldArgs f{};
-        f.m = m_;
-        f.nblocks = grid;
-        for (int d = 0; d < P::NDOT; ++d) {
-            f.slot[d] = slot(first_slot + d);
-            f.part[d] = part(first_slot + d);
-            f.D[d] = dsl(first_slot + d);
-        }
-        f.ctl = ctl_.p;
-        mark_begin("fold", 0.0);
-        launch_fold(ctx_->stream, f, P::NDOT);
-        mark_end();
-        launches_++;
         // multi-GPU: one fused allreduce of all dots of this point (int64 limbs)
         if (ctx_->comm) {
-            comm_allreduce_i64(ctx_, dsl(first_slot), static_cast<size_t>(P::NDOT) * m_ * NSLOT, ctx_->stream);
+            comm_allreduce_i64(ctx_, slot(first_slot), static_cast<size_t>(P::NDOT) * m_ * NSLOT, ctx_->stream);
         }
         reductions_++;
     }
@@ -377,7 +359,7 @@ void Solver::scalars(int point, int nd) {
     s.sc = scal_.p;
     s.ctl = ctl_.p;
     s.hist = hist_.p;
-    for (int i = 0; i < nd; ++i) s.D[i] = dsl(i);
+    for (int i = 0; i < nd; ++i) s.D[i] = slot(i);
     s.nd = nd;
     const int threads = ((m_ + 31) / 32) * 32;
     mark_begin("scalar", 0.0);

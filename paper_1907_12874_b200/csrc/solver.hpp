@@ -38,8 +38,6 @@ private:
     double* w(int i) { return work_[i].p; }
     double* sc(int i);
     int64_t* slot(int i);
-    int64_t* dsl(int i);
-    double* part(int i);
     void spmm(const double* x, double* y);
     template <class P>
     void group(std::initializer_list<const double*> in, std::initializer_list<double*> out,
@@ -55,11 +53,10 @@ private:
     double tol_;
     int fixed_, maxit_;
     int64_t n_ = 0, len_ = 0, rows_alloc_ = 0;
-    int max_blocks_ = 0;
     std::vector<DevBuf<double>> work_;
-    DevBuf<double> scal_, hist_, part_;
+    DevBuf<double> scal_, hist_;
     DevBuf<int> ctl_;
-    DevBuf<int64_t> slots_, D_;
+    DevBuf<int64_t> slots_;
     int* ctl_host_ = nullptr;
     cudaEvent_t ev_[2] = {nullptr, nullptr};
     cudaEvent_t t0_ = nullptr, t1_ = nullptr;
