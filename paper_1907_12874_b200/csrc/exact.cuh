@@ -213,4 +213,86 @@ __host__ __device__ inline double digits_round(const int64_t* src) {
     return bitsd(out | (neg ? 0x8000000000000000ull : 0ull));
 }
 
+#ifdef __CUDACC__
+// Device rounding with every word in registers (fully unrolled; no local
+// memory).  Same result as digits_round.
+__device__ __forceinline__ double digits_round_regs(const int64_t* __restrict__ src) {
+    const int64_t pinf = src[IDX_PINF], ninf = src[IDX_NINF], nan = src[IDX_NAN];
+    int64_t d[NDIG];
+#pragma unroll
+    for (int j = 0; j < NDIG; ++j) d[j] = src[j];
+    if (nan || (pinf && ninf)) return bitsd(0x7ff8000000000000ull);
+    if (pinf) return bitsd(0x7ff0000000000000ull);
+    if (ninf) return bitsd(0xfff0000000000000ull);
+    int64_t carry = 0;
+#pragma unroll
+    for (int j = 0; j < NDIG - 1; ++j) {
+        const int64_t v = d[j] + carry;
+        carry = v >> 32;
+        d[j] = v & 0xffffffffll;
+    }
+    d[NDIG - 1] += carry;
+    const bool neg = d[NDIG - 1] < 0;
+    if (neg) {
+        carry = 0;
+#pragma unroll
+        for (int j = 0; j < NDIG - 1; ++j) {
+            const int64_t v = -d[j] + carry;
+            carry = v >> 32;
+            d[j] = v & 0xffffffffll;
+        }
+        d[NDIG - 1] = -d[NDIG - 1] + carry;
+    }
+    // top nonzero word h and the two below it, plus a sticky flag for the rest
+    int h = -1;
+    uint64_t t0 = 0, t1 = 0, t2 = 0;
+    bool below = false;   // any nonzero word strictly below h-2
+    bool acc2 = false;    // OR of words 0..j-3 while scanning
+#pragma unroll
+    for (int j = 0; j < NDIG; ++j) {
+        if (j >= 3) acc2 = acc2 || (d[j - 3] != 0);
+        if (d[j] != 0) {
+            h = j;
+            t0 = static_cast<uint64_t>(d[j]);
+            t1 = j >= 1 ? static_cast<uint64_t>(d[j - 1]) : 0ull;
+            t2 = j >= 2 ? static_cast<uint64_t>(d[j - 2]) : 0ull;
+            below = acc2;
+        }
+    }
+    if (h < 0) return 0.0;
+    const int L = bitlen32(t0);
+    const int bitlen = 32 * h + L;
+    uint64_t out;
+    if (bitlen <= 64) {
+        const uint64_t mag = h >= 1 ? ((t0 << 32) | t1) : t0;
+        if (bitlen <= 53) {
+            out = mag;
+        } else {
+            const int shift = bitlen - 53;
+            uint64_t keep = mag >> shift;
+            const bool rbit = (mag >> (shift - 1)) & 1;
+            const bool sticky = (mag & ((1ull << (shift - 1)) - 1)) != 0;
+            if (rbit && (sticky || (keep & 1))) ++keep;
+            int sh = shift;
+            if (keep == (1ull << 53)) { keep >>= 1; ++sh; }
+            out = (static_cast<uint64_t>(sh + 1) << 52) | (keep & ((1ull << 52) - 1));
+        }
+    } else {
+        const uint64_t whi = (t0 << 32) | t1;
+        const uint64_t top = (whi << (32 - L)) | (t2 >> L);
+        bool sticky = below || (t2 & ((1ull << L) - 1)) != 0;
+        uint64_t keep = top >> 11;
+        const bool rbit = (top >> 10) & 1;
+        sticky = sticky || (top & 0x3ff) != 0;
+        int shift = bitlen - 53;
+        if (rbit && (sticky || (keep & 1))) ++keep;
+        if (keep == (1ull << 53)) { keep >>= 1; ++shift; }
+        const int biased = shift + 1;
+        out = biased >= 2047 ? 0x7ff0000000000000ull
+                             : (static_cast<uint64_t>(biased) << 52) | (keep & ((1ull << 52) - 1));
+    }
+    return bitsd(out | (neg ? 0x8000000000000000ull : 0ull));
+}
+#endif
+
 }  // namespace mbg

@@ -10,11 +10,7 @@ namespace mbg {
 
 __global__ void round_kernel(int64_t* D, int nslots, int m, double* out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < nslots * m) {
-        int64_t* d = D + static_cast<int64_t>(i) * NSLOT;
-        out[i] = digits_round(d);
-        for (int j = 0; j < NSLOT; ++j) d[j] = 0;
-    }
+    if (i < nslots * m) out[i] = digits_round_regs(D + static_cast<int64_t>(i) * NSLOT);
 }
 
 void launch_round(cudaStream_t st, int64_t* D, int nslots, int m, double* out) {

@@ -63,22 +63,28 @@ __device__ __forceinline__ double hist_entry(double res2, double bb) {
 // operation (separately rounded, no contraction).
 __global__ void scalar_kernel(ScalArgs a) {
     __shared__ int s_bad1, s_bad2, s_all;
+    extern __shared__ double s_dots[];  // nd * m rounded dots
     int* ctl = a.ctl;
     if (ctl[C_STOP]) return;
     const int m = a.m;
     const int c = threadIdx.x;
     const bool on = c < m;
     if (c == 0) { s_bad1 = INT_MAX; s_bad2 = INT_MAX; s_all = 1; }
+    // round every (dot, column) long accumulator (one thread each), then clear
+    // the (contiguous) slots for their next use
+    const int nslot = a.nd * m;
+    for (int i = threadIdx.x; i < nslot; i += blockDim.x)
+        s_dots[i] = digits_round_regs(a.D[i / m] + static_cast<int64_t>(i % m) * NSLOT);
     __syncthreads();
+    if (nslot) {
+        int64_t* base = a.D[0];
+        for (int w = threadIdx.x; w < nslot * NSLOT; w += blockDim.x) base[w] = 0;
+    }
     double* sc = a.sc;
 #define SC(i) sc[(i) * m + c]
     double d[4] = {0.0, 0.0, 0.0, 0.0};
     if (on)
-        for (int i = 0; i < a.nd; ++i) {
-            int64_t* sl = a.D[i] + static_cast<int64_t>(c) * NSLOT;
-            d[i] = digits_round(sl);
-            for (int w = 0; w < NSLOT; ++w) sl[w] = 0;
-        }
+        for (int i = 0; i < a.nd; ++i) d[i] = s_dots[i * m + c];
     const int j = ctl[C_ITER];
     int code1 = 0, code2 = 0;  // breakdown codes for s_bad1 / s_bad2
     switch (a.point) {
@@ -361,9 +367,9 @@ void Solver::scalars(int point, int nd) {
     s.hist = hist_.p;
     for (int i = 0; i < nd; ++i) s.D[i] = slot(i);
     s.nd = nd;
-    const int threads = ((m_ + 31) / 32) * 32;
+    const int threads = std::min(1024, std::max(((m_ + 31) / 32) * 32, ((nd * m_ + 31) / 32) * 32));
     mark_begin("scalar", 0.0);
-    scalar_kernel<<<1, threads, 0, ctx_->stream>>>(s);
+    scalar_kernel<<<1, threads, static_cast<size_t>(nd > 0 ? nd : 1) * m_ * sizeof(double), ctx_->stream>>>(s);
     MBG_CUDA(cudaGetLastError());
     mark_end();
     launches_++;

@@ -1,0 +1,215 @@
+"""Host-side logic of the product library (no GPU): generators, traffic
+analyzer / schedules (Table 2), byte model, CSR validation, exact-dot limb
+format and the halo plan."""
+import json
+from fractions import Fraction
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle_ctypes as O
+import paper_1907_12874_b200 as P
+
+GOLD = json.loads((Path(__file__).parent / "golden" / "reference_fixtures.json").read_text())
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.int64)
+
+
+@pytest.mark.parametrize("kind,dims,seed", [("poisson7", (32, 32, 32), 0), ("convdiff7", (17, 9, 5), 1),
+                                            ("stencil27", (12, 7, 9), 2), ("stencil27", (1, 1, 1), 2),
+                                            ("convdiff7", (1, 5, 1), 3)])
+def test_product_generators_equal_oracle(kind, dims, seed):
+    a = P.gen_stencil(kind, *dims, seed=seed)
+    o = O.gen_stencil(kind, *dims, seed=seed)
+    assert np.array_equal(a.row_offsets, o.off) and np.array_equal(a.col_indices, o.col)
+    assert np.array_equal(bits(a.values), bits(o.val))
+    a.validate()
+
+
+def test_product_banded_equals_oracle():
+    a = P.gen_banded(150_000, 65536, 16, 32, 4)
+    o = O.gen_banded(150_000, 65536, 16, 32, 4)
+    assert np.array_equal(a.row_offsets, o.off) and np.array_equal(a.col_indices, o.col)
+    assert np.array_equal(bits(a.values), bits(o.val))
+    counts = np.diff(a.row_offsets)
+    assert counts.min() >= 16 and counts.max() <= 32
+    a.validate()
+    # diagonal dominance 1.1 * sum |offdiag|
+    i = 777
+    cols = a.col_indices[a.row_offsets[i]:a.row_offsets[i + 1]]
+    vals = a.values[a.row_offsets[i]:a.row_offsets[i + 1]]
+    assert np.isclose(vals[cols == i][0], 1.1 * np.abs(vals[cols != i]).sum())
+    # tiny n: band clipped, counts capped by available columns
+    t = P.gen_banded(5, 65536, 16, 32, 4)
+    assert np.all(np.diff(t.row_offsets) == 5)
+
+
+def test_product_rhs_equals_oracle():
+    assert np.array_equal(bits(P.gen_rhs(1000, 8, 3)), bits(O.rhs(1000, 8, 3)))
+    b = P.gen_rhs(100_000, 2, 1)
+    assert -1.0 <= b.min() < -0.99 and 0.99 < b.max() < 1.0
+
+
+TABLE2 = {  # PAPER.md:343-363 (merged / basic) + 2 identity-M^-1 copies for Reordered
+    ("bicgstab", "merged"): (14, 4), ("bicgstab", "basic"): (18, 4),
+    ("rbicgstab", "merged"): (15 + 2, 6 + 2), ("rbicgstab", "basic"): (22 + 2, 6 + 2),
+    ("pipebicgstab", "merged"): (18, 8), ("pipebicgstab", "basic"): (34, 9),
+}
+
+
+@pytest.mark.parametrize("key", list(TABLE2))
+def test_method_schedule_table2(key):
+    s = P.method_schedule(*key)
+    assert (s["reads"], s["writes"]) == TABLE2[key]
+    assert s["spmvs"] == 2
+
+
+def test_method_schedule_reductions():
+    # Eq. (14) / (16) / (18): message layout of the reductions
+    assert P.method_schedule("bicgstab")["reductions"] == [1, 3, 1]
+    assert P.method_schedule("rbicgstab")["reductions"] == [1, 4]
+    assert P.method_schedule("pipebicgstab")["reductions"] == [3, 4]
+    assert P.method_schedule("bicgstab", "basic")["reductions"] == [1] * 5
+
+
+# merged lines as (kind, ...) tuples with symbolic vector ids
+X, P_, R, R0, V, S, T, Z, VH, TH, RT, Q, W, Y = range(14)
+GROUPS = {
+    "bicgstab": [[("d", V, R0, 0)], [("u", S, [R, V])], [("d", T, S, 0), ("d", T, T, 1), ("d", S, S, 2)],
+                 [("u", X, [X, P_, S]), ("u", R, [S, T]), ("d", R, R0, 0)], [("u", P_, [R, P_, V])]],
+    "rbicgstab": [[("d", V, R0, 0)], [("u", TH, [Z, S])],
+                  [("u", RT, [R, V]), ("d", T, RT, 0), ("d", T, T, 1), ("d", T, R0, 2), ("d", RT, RT, 3)],
+                  [("u", R, [RT, T])], [("u", X, [X, VH, TH]), ("u", Z, [TH, Q]), ("u", VH, [Z, VH, S])]],
+    "pipebicgstab": [[("u", P_, [R, P_, S]), ("u", S, [W, S, Z]), ("u", Z, [T, Z, V]), ("u", Q, [R, S]),
+                      ("u", Y, [W, Z]), ("d", Q, Y, 0), ("d", Y, Y, 1), ("d", Q, Q, 2)],
+                     [("u", X, [X, P_, Q]), ("u", R, [Q, Y])],
+                     [("u", W, [Y, T, V]), ("d", R0, R, 0), ("d", R0, Z, 1), ("d", R0, W, 2), ("d", R0, S, 3)]],
+}
+
+
+def to_group(g):
+    one = np.ones(1)
+    out = []
+    for st in g:
+        if st[0] == "u":
+            out.append(P.UpdateStatement(st[1], [(one, v) for v in st[2]]))
+        else:
+            out.append(P.DotStatement(st[1], st[2], st[3]))
+    return out
+
+
+@pytest.mark.parametrize("method", list(GROUPS))
+def test_analyzer_matches_reference_analyzer(method):
+    """Per merged line, analyze_traffic / split_basic equal the reference's
+    (statement.cpp:25-85, golden fixture generated from the reference)."""
+    for g, want in zip(GROUPS[method], GOLD["traffic"][method]):
+        grp = to_group(g)
+        assert list(P.analyze_traffic(grp)) == want["merged"]
+        r, w, n = P.split_basic_traffic(grp, 100)
+        assert [r, w] == want["basic"] and n == want["pieces"]
+
+
+def test_analyzer_spec_examples():
+    one = np.ones(2)
+    # y = a x + b y -> (2, 1)
+    assert P.analyze_traffic([P.UpdateStatement(1, [(one, 0), (one, 1)])]) == (2, 1)
+    # w = y - omega (t - alpha v) splits through one temporary: 2x(2,1)
+    r, w, n = P.split_basic_traffic([P.UpdateStatement(0, [(one, 1), (one, 2), (one, 3)])], 100)
+    assert (r, w, n) == (4, 2, 2)
+    # dot (v, v) counts v once; empty group
+    assert P.analyze_traffic([P.DotStatement(3, 3, 0)]) == (1, 0)
+    assert P.analyze_traffic([]) == (0, 0)
+    with pytest.raises(ValueError, match="dangling"):
+        P.analyze_traffic([P.DotStatement(-1, 0, 0)])
+
+
+def test_byte_models():
+    assert P.spmv_traffic_bytes(8_000_000, 56_000_000, 1) == GOLD["spmv_traffic_bytes_8e6_m1_C7"]
+    if O.ref_available():
+        for n, nnz, m in [(1000, 6000, 1), (8000, 55000, 4), (33, 200, 16)]:
+            assert P.spmv_traffic_bytes(n, nnz, m) == O.ref().ref_spmv_traffic_bytes(n, nnz, m)
+    n, nnz, m = 2_097_152, 14_581_760, 8
+    assert P.spmv_compulsory_bytes(n, nnz, m) == 16 * m * n + 12 * nnz + 4 * (n + 1)
+
+
+def test_csr_validate_messages_match_reference():
+    good = O.gen_stencil("poisson7", 3, 3, 3)
+    P.CsrMatrix(good.n, good.off, good.col, good.val).validate()
+    bad_cols = good.col.copy()
+    bad_cols[5], bad_cols[6] = bad_cols[6], bad_cols[5]
+    cases = [
+        (P.CsrMatrix(good.n, good.off, bad_cols, good.val), "not strictly increasing in row"),
+        (P.CsrMatrix(good.n, good.off, np.where(good.col == 4, 99, good.col), good.val), "out of range"),
+        (P.CsrMatrix(good.n, np.concatenate([[1], good.off[1:]]), good.col, good.val), "row_offsets\\[0\\]"),
+    ]
+    for a, msg in cases:
+        with pytest.raises(ValueError, match=msg) as ei:
+            a.validate()
+        if O.ref_available():
+            lib = O.ref()
+            assert lib.ref_validate(a.n_rows, a.row_offsets, a.col_indices, a.values) == 1
+            assert lib.ref_last_error().decode() == str(ei.value)
+
+
+# --------------------------------------------------------------------------
+# exact-dot limb format (host hooks share exact.cuh with the device)
+# --------------------------------------------------------------------------
+def test_exact_limbs_vs_fraction_and_partition_independent():
+    rng = np.random.default_rng(11)
+    n, m = 6000, 3
+    a = rng.standard_normal(n * m) * np.exp2(rng.integers(-300, 300, n * m))
+    b = rng.standard_normal(n * m)
+    whole = P.exact_round(P.exact_accumulate(a, b, m), m)
+    for c in range(m):
+        want = float(sum((Fraction(float(p)) for p in a[c::m] * b[c::m]), Fraction(0)))
+        assert whole[c] == want
+    # any split of the rows, limbs summed as int64: identical result
+    cuts = np.sort(rng.choice(np.arange(1, n), 5, replace=False))
+    parts = np.split(np.arange(n), cuts)
+    acc = np.zeros(m * P.exact_slot_words(), np.int64)
+    for rows in parts:
+        idx = (rows[:, None] * m + np.arange(m)).reshape(-1)
+        acc += P.exact_accumulate(a[idx], b[idx], m)
+    assert np.array_equal(bits(P.exact_round(acc, m)), bits(whole))
+    assert np.array_equal(bits(whole), bits(O.dot_exact(a, b, m)))
+
+
+def test_exact_round_edge_cases():
+    w = P.exact_slot_words()
+    cases = [np.array([2.0 ** 53, 1.0]), np.array([2.0 ** 53, 1.0, 2.0 ** -60]), np.array([5e-324, 5e-324]),
+             np.array([1e308, 1e308, -1e308]), np.array([1.7e308, 1.7e308]), np.array([-3.0, 3.0]),
+             np.array([-1e-300, 1e-310]), np.array([np.inf, 2.0]), np.array([np.inf, -np.inf])]
+    for v in cases:
+        got = P.exact_round(P.exact_accumulate(v, np.ones_like(v), 1), 1)[0]
+        want = O.sum_exact(v)
+        assert (np.isnan(got) and np.isnan(want)) or bits(got) == bits(want), (v, got, want)
+    assert w == 72
+
+
+# --------------------------------------------------------------------------
+# halo plan (single process view of every part)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("nparts", [1, 2, 3, 5])
+def test_halo_plan_consistent(nparts):
+    a = P.gen_banded(3000, 400, 4, 12, 9)
+    n = a.n_rows
+    bounds = [n * p // nparts for p in range(nparts + 1)]
+    plans = [P.halo_plan(a, bounds, p) for p in range(nparts)]
+    for p, pl in enumerate(plans):
+        r0, r1 = bounds[p], bounds[p + 1]
+        assert pl["n_own"] == r1 - r0
+        # local column -> global column reproduces the CSR, order preserved
+        glob = np.concatenate([np.arange(r0, r1), pl["halo_global"]])
+        sl = slice(a.row_offsets[r0], a.row_offsets[r1])
+        assert np.array_equal(glob[pl["col"]], a.col_indices[sl])
+        assert np.array_equal(bits(pl["val"]), bits(a.values[sl]))
+        # my receive window from q == q's send list to me
+        for peer in pl["peers"]:
+            q = peer["part"]
+            mine = pl["halo_global"][peer["recv_offset"]:peer["recv_offset"] + peer["recv_count"]]
+            theirs = [x for x in plans[q]["peers"] if x["part"] == p]
+            sent = theirs[0]["send_rows"] + bounds[q] if theirs else np.zeros(0, np.int64)
+            assert np.array_equal(mine, sent)
