@@ -46,7 +46,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--method", default="bicgstab", choices=["bicgstab", "rbicgstab", "pipebicgstab"])
-    p.add_argument("--formulation", default="merged", choices=["merged", "basic"])
+    p.add_argument("--formulation", default="merged", choices=["merged", "basic", "fused"])
     p.add_argument("--grid", type=int, default=128, help="per-GPU grid edge (config C2: 128)")
     p.add_argument("--m", type=int, default=8)
     p.add_argument("--tol", type=float, default=1e-8)

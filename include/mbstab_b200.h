@@ -137,6 +137,10 @@ int mbg_execute_group(mbg_ctx* ctx, const mbg_statement* stmts, int nstmts, mbg_
 #define MBG_PIPEBICGSTAB 2
 #define MBG_MERGED 0
 #define MBG_BASIC 1
+/* Merged + beyond-paper fusions: dots fused
+ * into the SpMM epilogue, identity-M^-1 copies elided (Reordered), Alg. 4
+ * lines 7+12 in one pass (Pipelined).  Bitwise the same results as merged. */
+#define MBG_FUSED 2
 
 typedef struct mbg_report {
     int iterations;

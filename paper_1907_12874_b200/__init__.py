@@ -37,7 +37,7 @@ import numpy as np
 from ._lib import BreakdownError, MbgReport, MbgStatement, build, check, lib  # noqa: F401
 
 METHODS = {"bicgstab": 0, "rbicgstab": 1, "pipebicgstab": 2}
-FORMULATIONS = {"merged": 0, "basic": 1}
+FORMULATIONS = {"merged": 0, "basic": 1, "fused": 2}
 
 
 def _ptr(a: np.ndarray) -> int:

@@ -51,11 +51,12 @@ static void side_to_main(mbg_ctx* ctx) {
     MBG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->comm->ev_side, 0));
 }
 
-int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, const int* ctl) {
+int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, const int* ctl,
+                   const SpmmEpi* epi) {
     auto tiles = [](const mbg::DevBuf<int4>& t) { return SpmmTiles{t.p, static_cast<int64_t>(t.n)}; };
     if (a->peers.empty()) {
         return launch_spmm(ctx->stream, tiles(a->tiles_all), a->n, nullptr, a->off.p, a->col.p, a->val.p, m, x,
-                           y, ctl, ctx->num_sms);
+                           y, ctl, ctx->num_sms, epi);
     }
     Comm* cm = ctx->comm;
     if (!cm) throw Invalid("spmv: partitioned matrix needs a communicator (mbg_ctx_init_comm)");
@@ -89,10 +90,10 @@ int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, 
     MBG_NCCL(ncclGroupEnd());
     // interior rows overlap the exchange; boundary rows wait for the halo
     launches += launch_spmm(ctx->stream, tiles(a->tiles_interior), a->n_interior, a->interior_rows.p, a->off.p,
-                            a->col.p, a->val.p, m, x, y, ctl, ctx->num_sms);
+                            a->col.p, a->val.p, m, x, y, ctl, ctx->num_sms, epi);
     side_to_main(ctx);
     launches += launch_spmm(ctx->stream, tiles(a->tiles_boundary), a->n_boundary, a->boundary_rows.p, a->off.p,
-                            a->col.p, a->val.p, m, x, y, ctl, ctx->num_sms);
+                            a->col.p, a->val.p, m, x, y, ctl, ctx->num_sms, epi);
     return launches;
 }
 

@@ -14,7 +14,9 @@ namespace mbg {
 // send/recv of the boundary rows on the side stream while the interior rows
 // are multiplied on the main stream, then the boundary rows.  Returns the
 // number of kernels launched.
-int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, const int* ctl);
+struct SpmmEpi;
+int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, const int* ctl,
+                   const SpmmEpi* epi = nullptr);
 
 // Sum int64 limbs over all ranks (exact, order-independent).
 void comm_allreduce_i64(mbg_ctx* ctx, int64_t* buf, size_t count, cudaStream_t st);

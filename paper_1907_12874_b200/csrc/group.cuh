@@ -23,7 +23,7 @@
 
 namespace mbg {
 
-constexpr int GMAX_IN = 8, GMAX_OUT = 6, GMAX_CO = 8, GMAX_DOT = 4;
+constexpr int GMAX_IN = 10, GMAX_OUT = 6, GMAX_CO = 8, GMAX_DOT = 4;
 
 struct GroupArgs {
     int64_t len;                 // n*m
@@ -181,6 +181,34 @@ struct PPipeG5 {
     }
 };
 
+// Pipelined, fused formulation: Alg. 4 lines 7 and 12 in ONE pass (the
+// convergence break between them only skips w, which the GPU may compute and
+// discard): x = 1*x + alpha*p + omega*q ; r = 1*q + (-omega)*y ;
+// w = 1*y + (-omega)*t + (omega*alpha)*v ; rho'=(r0,r), psi=(r0,z), sigma=(r0,w), delta=(r0,s)
+struct PPipeG45 {
+    static constexpr const char* NAME = "pipe_g45";
+    static constexpr int NIN = 9, NOUT = 3, NCO = 4, NDOT = 4, UNROLL = 1;
+    // in: x p q y t v r0 z s ; out: x r w ; co: alpha omega -omega omega*alpha
+    __device__ static void run(const double* in, double* out, double* prod, const double* co) {
+        out[0] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, in[0]), co[0], in[1]), co[1], in[2]);
+        const double r = fmadd_rn(fmadd_rn(0.0, 1.0, in[2]), co[2], in[3]);
+        out[1] = r;
+        const double w = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, in[3]), co[2], in[4]), co[3], in[5]);
+        out[2] = w;
+        const double r0 = in[6];
+        prod[0] = __dmul_rn(r0, r);
+        prod[1] = __dmul_rn(r0, in[7]);
+        prod[2] = __dmul_rn(r0, w);
+        prod[3] = __dmul_rn(r0, in[8]);
+    }
+};
+
+// Unroll (pairs of packets per trip) unless a program declares UNROLL = 1.
+template <class P, class = void>
+struct unroll_of { static constexpr int value = 2; };
+template <class P>
+struct unroll_of<P, decltype(void(P::UNROLL))> { static constexpr int value = P::UNROLL; };
+
 // ---------------------------------------------------------------------------
 // Block-level exact combine.  Threads of a block fall into `classes` column
 // classes (thread t is in class t % classes; the block size is classes * 2^q).
@@ -287,8 +315,9 @@ __global__ void __launch_bounds__(256) group_kernel(GroupArgs a) {
     const int64_t npk = a.len / VEC;  // packets of VEC elements
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    constexpr int UNR = unroll_of<P>::value;
     if constexpr (VEC == 2) {
-        for (; q + stride < npk; q += 2 * stride) {
+        for (; UNR == 2 && q + stride < npk; q += 2 * stride) {
             double2 u0[P::NIN], u1[P::NIN];
 #pragma unroll
             for (int i = 0; i < P::NIN; ++i) {
@@ -321,7 +350,7 @@ __global__ void __launch_bounds__(256) group_kernel(GroupArgs a) {
                 grow(acc[2 * d + 1], p3[d], slot1[d]);
             }
         }
-        if (q < npk) {
+        for (; q < npk; q += stride) {
             double2 u0[P::NIN];
 #pragma unroll
             for (int i = 0; i < P::NIN; ++i) u0[i] = reinterpret_cast<const double2*>(a.in[i])[q];
@@ -341,7 +370,7 @@ __global__ void __launch_bounds__(256) group_kernel(GroupArgs a) {
             }
         }
     } else {
-        for (; q + stride < npk; q += 2 * stride) {
+        for (; UNR == 2 && q + stride < npk; q += 2 * stride) {
             double in0[P::NIN], in1[P::NIN];
 #pragma unroll
             for (int i = 0; i < P::NIN; ++i) { in0[i] = a.in[i][q]; in1[i] = a.in[i][q + stride]; }
@@ -353,7 +382,7 @@ __global__ void __launch_bounds__(256) group_kernel(GroupArgs a) {
 #pragma unroll
             for (int d = 0; d < P::NDOT; ++d) { grow(acc[d], p0[d], slot0[d]); grow(acc[d], p1[d], slot0[d]); }
         }
-        if (q < npk) {
+        for (; q < npk; q += stride) {
             double in0[P::NIN];
 #pragma unroll
             for (int i = 0; i < P::NIN; ++i) in0[i] = a.in[i][q];

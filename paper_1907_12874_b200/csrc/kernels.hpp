@@ -13,15 +13,23 @@ namespace mbg {
 // CSR SpMM over the interleaved block (spmm.cu).  The row set to compute is
 // given twice: as a tile list (TMA-pipelined kernels, m in {1,2,4,8,16,32})
 // and as an explicit row list (nullptr = rows [0, nrows)) for other m.
-constexpr int SPMM_TILE_ROWS = 256;
-constexpr int SPMM_TILE_NNZ = 2560;
+constexpr int SPMM_TILE_ROWS = 128;
+constexpr int SPMM_TILE_NNZ = 1280;
 struct SpmmTiles {
     const int4* tiles = nullptr;   // (r0, r1, k0, k1) per tile
     int64_t count = 0;
 };
+// Optional fused epilogue of the SpMM y = A x (beyond-paper merge):
+//   kind 1: slot[0] += exact (y, aux)                    e.g. delta = (v, r0)
+//   kind 2: slot[0..2] += exact (y, x), (y, y), (x, x)    phi, psi, theta of Alg. 2
+struct SpmmEpi {
+    int kind = 0;
+    const double* aux = nullptr;
+    int64_t* slot[3] = {nullptr, nullptr, nullptr};
+};
 int launch_spmm(cudaStream_t st, const SpmmTiles& tl, int64_t nrows, const int32_t* rows, const int32_t* off,
                 const int32_t* col, const double* val, int m, const double* x, double* y, const int* ctl,
-                int num_sms);
+                int num_sms, const SpmmEpi* epi = nullptr);
 std::vector<int4> build_spmm_tiles(const std::vector<int32_t>& off, const std::vector<int32_t>& rows);
 
 // Generic statement-group interpreter (API-level execute_group).

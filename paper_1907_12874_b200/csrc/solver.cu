@@ -232,7 +232,7 @@ Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulatio
     : ctx_(ctx), a_(a), m_(m), method_(method), form_(formulation), tol_(tol), fixed_(fixed),
       maxit_(maxit) {
     if (method < 0 || method > 2) throw Invalid("solve: unknown method");
-    if (formulation < 0 || formulation > 1) throw Invalid("solve: unknown formulation");
+    if (formulation < 0 || formulation > 2) throw Invalid("solve: unknown formulation");
     if (m < 1 || m > 1024) throw Invalid("solve: m must be in [1, 1024]");
     if (maxit < 0) throw Invalid("solve: negative iteration count");
     if (!fixed && !(tol > 0.0)) throw Invalid("solve: tol must be > 0 in converge mode");
@@ -242,7 +242,7 @@ Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulatio
     // only the vectors the method uses (C4 at m=32 is 8.4 GB per vector)
     static const std::vector<int> need[3] = {
         {0, 1, 2, 3, 4, 5},                        // r r0 p v s t
-        {0, 1, 3, 4, 5, 6, 7, 8, 9, 10},           // r r0 v s t z vh th rt q
+        {0, 1, 3, 4, 5, 6, 7, 8, 9, 10},           // r r0 v s t z vh th rt q (s, q unused when fused)
         {0, 1, 2, 3, 4, 5, 6, 10, 11, 12, 13}};    // r r0 p v s t z q w y tmp
     work_.resize(15);
     const size_t vlen = static_cast<size_t>(rows_alloc_) * m;
@@ -313,10 +313,20 @@ std::string Solver::profile_json() {
     return out + "}";
 }
 
-void Solver::spmm(const double* x, double* y) {
-    mark_begin("spmm", spmv_compulsory_bytes(a_->n, a_->nnz, m_));
-    launches_ += apply_operator(ctx_, a_, m_, const_cast<double*>(x), y, ctl_.p);
+void Solver::spmm(const double* x, double* y, int epi_kind, const double* aux) {
+    SpmmEpi e;
+    e.kind = epi_kind;
+    e.aux = aux;
+    for (int d = 0; d < 3; ++d) e.slot[d] = slot(d);
+    const double extra = epi_kind == 1 ? 8.0 * len_ : 0.0;   // aux vector read
+    mark_begin(epi_kind ? "spmm+dots" : "spmm", spmv_compulsory_bytes(a_->n, a_->nnz, m_) + extra);
+    launches_ += apply_operator(ctx_, a_, m_, const_cast<double*>(x), y, ctl_.p, epi_kind ? &e : nullptr);
     mark_end();
+    if (epi_kind) {
+        if (ctx_->comm)
+            comm_allreduce_i64(ctx_, slot(0), static_cast<size_t>(epi_kind == 2 ? 3 : 1) * m_ * NSLOT, ctx_->stream);
+        reductions_++;
+    }
 }
 
 template <class P>
@@ -413,20 +423,29 @@ void Solver::setup(const double* b, double* x) {
 
 void Solver::iteration() {
     const bool basic = form_ == MBG_BASIC;
+    const bool fused = form_ == MBG_FUSED;
     double *r = w(V_R), *r0 = w(V_R0), *x = x_;
     if (method_ == MBG_BICGSTAB) {
         double *p = w(V_P), *v = w(V_V), *s = w(V_S), *t = w(V_T);
-        spmm(p, v);
-        group<PDot2>({v, r0}, {}, {}, 0);
+        if (fused) {
+            spmm(p, v, 1, r0);                                    // v = A p ; delta = (v, r0)
+        } else {
+            spmm(p, v);
+            group<PDot2>({v, r0}, {}, {}, 0);
+        }
         scalars(P_C_ALPHA, 1);
         group<PUpd2>({r, v}, {s}, {S_ONE, S_NALPHA}, 0);
-        spmm(s, t);
-        if (basic) {
-            group<PDot2>({t, s}, {}, {}, 0);
-            group<PDot1>({t}, {}, {}, 1);
-            group<PDot1>({s}, {}, {}, 2);
+        if (fused) {
+            spmm(s, t, 2);                                        // t = A s ; phi psi theta
         } else {
-            group<PClassicOmega>({t, s}, {}, {}, 0);
+            spmm(s, t);
+            if (basic) {
+                group<PDot2>({t, s}, {}, {}, 0);
+                group<PDot1>({t}, {}, {}, 1);
+                group<PDot1>({s}, {}, {}, 2);
+            } else {
+                group<PClassicOmega>({t, s}, {}, {}, 0);
+            }
         }
         scalars(P_C_OMEGA, 3);
         if (basic) {
@@ -439,11 +458,18 @@ void Solver::iteration() {
         scalars(P_C_BETA, 1);
         group<PUpd3>({r, p, v}, {p}, {S_ONE, S_BETA, S_NBO}, 0);
     } else if (method_ == MBG_RBICGSTAB) {
-        double *z = w(V_Z), *vh = w(V_VH), *v = w(V_V), *s = w(V_S), *th = w(V_TH), *t = w(V_T);
-        double *rt = w(V_RT), *q = w(V_Q);
-        spmm(vh, v);
-        group<PDot2>({v, r0}, {}, {}, 0);
-        copy(s, v);                                               // s = M^-1 v
+        double *z = w(V_Z), *vh = w(V_VH), *v = w(V_V), *th = w(V_TH), *t = w(V_T);
+        double *rt = w(V_RT);
+        // identity M^-1: the fused formulation aliases s = v and q = t instead of copying
+        double* s = fused ? v : w(V_S);
+        double* q = fused ? t : w(V_Q);
+        if (fused) {
+            spmm(vh, v, 1, r0);                                   // v = A vh ; delta = (v, r0)
+        } else {
+            spmm(vh, v);
+            group<PDot2>({v, r0}, {}, {}, 0);
+            copy(s, v);                                           // s = M^-1 v
+        }
         scalars(P_C_ALPHA, 1);
         group<PUpd2>({z, s}, {th}, {S_ONE, S_NALPHA}, 0);        // th = z - alpha s
         spmm(th, t);
@@ -456,7 +482,7 @@ void Solver::iteration() {
         } else {
             group<PReordG7>({r, v, t, r0}, {rt}, {S_NALPHA}, 0);
         }
-        copy(q, t);                                               // q = M^-1 t
+        if (!fused) copy(q, t);                                   // q = M^-1 t
         scalars(P_R_OMEGA, 4);
         group<PUpd2>({rt, t}, {r}, {S_ONE, S_NOMEGA}, 0);        // r = rt - omega t
         if (basic) {
@@ -493,6 +519,8 @@ void Solver::iteration() {
             group<PDot2>({r0, z}, {}, {}, 1);
             group<PDot2>({r0, wv}, {}, {}, 2);
             group<PDot2>({r0, s}, {}, {}, 3);
+        } else if (fused) {
+            group<PPipeG45>({x, p, q, y, t, v, r0, z, s}, {x, r, wv}, {S_ALPHA, S_OMEGA, S_NOMEGA, S_OA}, 0);
         } else {
             group<PPipeG4>({x, p, q, y}, {x, r}, {S_ALPHA, S_OMEGA, S_NOMEGA}, 0);
             group<PPipeG5>({y, t, v, r0, r, z, s}, {wv}, {S_NOMEGA, S_OA}, 0);

@@ -38,7 +38,7 @@ private:
     double* w(int i) { return work_[i].p; }
     double* sc(int i);
     int64_t* slot(int i);
-    void spmm(const double* x, double* y);
+    void spmm(const double* x, double* y, int epi_kind = 0, const double* aux = nullptr);
     template <class P>
     void group(std::initializer_list<const double*> in, std::initializer_list<double*> out,
                std::initializer_list<int> co, int first_slot);

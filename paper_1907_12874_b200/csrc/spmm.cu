@@ -19,6 +19,7 @@
 //   * gathers are issued in batches of 8 nonzeros before the ordered adds.
 // Any other m uses a thread-per-(row, column) kernel with the same arithmetic.
 #include <cstdint>
+#include <type_traits>
 
 #include "common.hpp"
 #include "kernels.hpp"
@@ -62,22 +63,25 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 }  // namespace
 
-// smem layout per buffer: offsets | cols | vals (each 16-byte aligned)
+// smem layout per stage: offsets | cols | vals (each 16-byte aligned)
+constexpr int STAGES = 3;
 constexpr int OFF_CAP = SPMM_TILE_ROWS + 8;
 constexpr int NNZ_PAD = SPMM_TILE_NNZ + 8;
 constexpr int BUF_BYTES = OFF_CAP * 4 + NNZ_PAD * 4 + NNZ_PAD * 8;
-constexpr int SMEM_HEAD = 128;  // 2 mbarriers + 2 tile metas
-constexpr int SPMM_SMEM = SMEM_HEAD + 2 * BUF_BYTES;
+constexpr int SMEM_HEAD = 128;  // STAGES mbarriers + STAGES tile metas
+constexpr int SPMM_SMEM = SMEM_HEAD + STAGES * BUF_BYTES;
 static_assert(BUF_BYTES % 16 == 0, "buffer alignment");
 static_assert((OFF_CAP * 4) % 16 == 0 && (NNZ_PAD * 4) % 16 == 0, "region alignment");
+static_assert(STAGES * BUF_BYTES >= 256 * KEXP * 8, "combine scratch aliases the stages");
+static_assert(8 * STAGES <= 32 && 32 + 16 * STAGES <= SMEM_HEAD, "head layout");
 
-template <int M>
-__global__ void __launch_bounds__(256) spmm_tma_kernel(const int4* __restrict__ tiles, int ntiles,
+template <int M, int EPI>
+__global__ void __launch_bounds__(256, 2) spmm_tma_kernel(const int4* __restrict__ tiles, int ntiles,
                                                        const int32_t* __restrict__ off,
                                                        const int32_t* __restrict__ col,
                                                        const double* __restrict__ val,
                                                        const double* __restrict__ x, double* __restrict__ y,
-                                                       const int* __restrict__ ctl) {
+                                                       const int* __restrict__ ctl, SpmmEpi epi) {
     if (ctl && ctl[0]) return;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
@@ -86,8 +90,7 @@ __global__ void __launch_bounds__(256) spmm_tma_kernel(const int4* __restrict__ 
     const int tid = threadIdx.x;
 
     if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        for (int b = 0; b < STAGES; ++b) mbar_init(&bars[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -110,21 +113,51 @@ __global__ void __launch_bounds__(256) spmm_tma_kernel(const int4* __restrict__ 
             bulk_g2s(buf + OFF_CAP * 4 + NNZ_PAD * 4, val + k0a, bnnz * 8u, &bars[b]);
         }
     };
-    if (tid == 0) {
-        issue(0, 0);
-        issue(1, 1);
-    }
+    if (tid == 0)
+        for (int b = 0; b < STAGES; ++b) issue(b, b);
 
     constexpr int VW = M >= 2 ? 2 : 1;        // columns per lane
     constexpr int LPR = M / VW;               // lanes per row
     constexpr int RPP = 256 / LPR;            // rows per pass of the block
+    constexpr int ND = EPI == 2 ? 3 : 1;      // dots of the fused epilogue
     const int cp = (tid % LPR) * VW;
+    double ex[ND * VW][KEXP];
+#pragma unroll
+    for (int q = 0; q < ND * VW; ++q)
+#pragma unroll
+        for (int i = 0; i < KEXP; ++i) ex[q][i] = 0.0;
+
+    // fused epilogue: exact dot terms of one finished row
+    auto epilogue = [&](int row, double t0, double t1) {
+        if constexpr (EPI == 1) {
+            const double* au = epi.aux + static_cast<int64_t>(row) * M + cp;
+            grow(ex[0], __dmul_rn(t0, au[0]), epi.slot[0] + static_cast<int64_t>(cp) * NSLOT);
+            if constexpr (VW == 2) grow(ex[1], __dmul_rn(t1, au[1]), epi.slot[0] + static_cast<int64_t>(cp + 1) * NSLOT);
+        } else if constexpr (EPI == 2) {
+            double s0, s1 = 0.0;
+            if constexpr (VW == 2) {
+                const double2 sv = __ldg(reinterpret_cast<const double2*>(x + static_cast<int64_t>(row) * M + cp));
+                s0 = sv.x;
+                s1 = sv.y;
+            } else {
+                s0 = __ldg(x + row);
+            }
+#pragma unroll
+            for (int v = 0; v < VW; ++v) {
+                const double t = v ? t1 : t0, sv = v ? s1 : s0;
+                const int64_t so = static_cast<int64_t>(cp + v) * NSLOT;
+                grow(ex[0 * VW + v], __dmul_rn(t, sv), epi.slot[0] + so);
+                grow(ex[1 * VW + v], __dmul_rn(t, t), epi.slot[1] + so);
+                grow(ex[2 * VW + v], __dmul_rn(sv, sv), epi.slot[2] + so);
+            }
+        }
+    };
 
     for (int i = 0;; ++i) {
         const int t = blockIdx.x + i * gridDim.x;
         if (t >= ntiles) break;
-        const int b = i & 1;
-        while (!mbar_try_wait(&bars[b], static_cast<uint32_t>((i >> 1) & 1))) {
+        const int b = i % STAGES;
+        while (!mbar_try_wait(&bars[b], static_cast<uint32_t>((i / STAGES) & 1))) {
         }
         const int4 mt = meta[b];
         const int r0 = mt.x, r1 = mt.y, r0a = mt.z, k0a = mt.w;
@@ -132,55 +165,86 @@ __global__ void __launch_bounds__(256) spmm_tma_kernel(const int4* __restrict__ 
         const int32_t* s_off = reinterpret_cast<const int32_t*>(buf);
         const int32_t* s_col = reinterpret_cast<const int32_t*>(buf + OFF_CAP * 4);
         const double* s_val = reinterpret_cast<const double*>(buf + OFF_CAP * 4 + NNZ_PAD * 4);
-        const int k_first = s_off[r0 - r0a];
-        const bool lng = s_off[r1 - r0a] - k_first > SPMM_TILE_NNZ;
-        for (int rr = tid / LPR; rr < r1 - r0; rr += RPP) {
-            const int row = r0 + rr;
-            const int k0 = s_off[row - r0a], k1 = s_off[row + 1 - r0a];
-            double acc0 = 0.0, acc1 = 0.0;
-            for (int k = k0; k < k1; k += 8) {
-                const int cnt = min(8, k1 - k);
-                int j[8];
-                double a[8];
+        const bool lng = s_off[r1 - r0a] - s_off[r0 - r0a] > SPMM_TILE_NNZ;
+        // a long row (single-row tile beyond the stage capacity) reads global memory
+        const int32_t* colp = lng ? col : s_col - k0a;
+        const double* valp = lng ? val : s_val - k0a;
+        // two rows per lane at a time (rows rr and rr + RPP of the tile): twice
+        // the gathers in flight and two independent ordered add chains
+        for (int rr = tid / LPR; rr < r1 - r0; rr += 2 * RPP) {
+            const int rowA = r0 + rr, rowB = rowA + RPP;
+            const bool hasB = rr + RPP < r1 - r0;
+            const int kA = s_off[rowA - r0a], lenA = s_off[rowA + 1 - r0a] - kA;
+            const int kB = hasB ? s_off[rowB - r0a] : 0;
+            const int lenB = hasB ? s_off[rowB + 1 - r0a] - kB : 0;
+            const int len = lenA > lenB ? lenA : lenB;
+            double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+            for (int kk = 0; kk < len; kk += 4) {
+                int ja[4], jb[4];
+                double va[4], vb[4];
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    if (q < cnt) {
-                        if (!lng) {
-                            j[q] = s_col[k - k0a + q];
-                            a[q] = s_val[k - k0a + q];
-                        } else {
-                            j[q] = __ldg(col + k + q);
-                            a[q] = __ldg(val + k + q);
+                for (int q = 0; q < 4; ++q) {
+                    if (kk + q < lenA) { ja[q] = colp[kA + kk + q]; va[q] = valp[kA + kk + q]; }
+                    if (kk + q < lenB) { jb[q] = colp[kB + kk + q]; vb[q] = valp[kB + kk + q]; }
+                }
+                if constexpr (VW == 2) {
+                    double2 xa[4], xb[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (kk + q < lenA)
+                            xa[q] = __ldg(reinterpret_cast<const double2*>(x + static_cast<int64_t>(ja[q]) * M + cp));
+                        if (kk + q < lenB)
+                            xb[q] = __ldg(reinterpret_cast<const double2*>(x + static_cast<int64_t>(jb[q]) * M + cp));
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (kk + q < lenA) {
+                            a0 = __dadd_rn(a0, __dmul_rn(va[q], xa[q].x));
+                            a1 = __dadd_rn(a1, __dmul_rn(va[q], xa[q].y));
+                        }
+                        if (kk + q < lenB) {
+                            b0 = __dadd_rn(b0, __dmul_rn(vb[q], xb[q].x));
+                            b1 = __dadd_rn(b1, __dmul_rn(vb[q], xb[q].y));
                         }
                     }
-                if constexpr (VW == 2) {
-                    double2 xv[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        if (q < cnt) xv[q] = __ldg(reinterpret_cast<const double2*>(x + static_cast<int64_t>(j[q]) * M + cp));
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        if (q < cnt) {
-                            acc0 = __dadd_rn(acc0, __dmul_rn(a[q], xv[q].x));
-                            acc1 = __dadd_rn(acc1, __dmul_rn(a[q], xv[q].y));
-                        }
                 } else {
-                    double xv[8];
+                    double xa[4], xb[4];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        if (q < cnt) xv[q] = __ldg(x + j[q]);
+                    for (int q = 0; q < 4; ++q) {
+                        if (kk + q < lenA) xa[q] = __ldg(x + ja[q]);
+                        if (kk + q < lenB) xb[q] = __ldg(x + jb[q]);
+                    }
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        if (q < cnt) acc0 = __dadd_rn(acc0, __dmul_rn(a[q], xv[q]));
+                    for (int q = 0; q < 4; ++q) {
+                        if (kk + q < lenA) a0 = __dadd_rn(a0, __dmul_rn(va[q], xa[q]));
+                        if (kk + q < lenB) b0 = __dadd_rn(b0, __dmul_rn(vb[q], xb[q]));
+                    }
                 }
             }
-            if constexpr (VW == 2)
-                *reinterpret_cast<double2*>(y + static_cast<int64_t>(row) * M + cp) = make_double2(acc0, acc1);
-            else
-                y[row] = acc0;
+            if constexpr (VW == 2) {
+                *reinterpret_cast<double2*>(y + static_cast<int64_t>(rowA) * M + cp) = make_double2(a0, a1);
+                if (hasB) *reinterpret_cast<double2*>(y + static_cast<int64_t>(rowB) * M + cp) = make_double2(b0, b1);
+            } else {
+                y[rowA] = a0;
+                if (hasB) y[rowB] = b0;
+            }
+            if constexpr (EPI != 0) {
+                epilogue(rowA, a0, a1);
+                if (hasB) epilogue(rowB, b0, b1);
+            }
         }
-        __syncthreads();  // every thread is done with buffer b
-        if (tid == 0) issue(i + 2, b);
+        __syncthreads();  // every thread is done with stage b
+        if (tid == 0) issue(i + STAGES, b);
+    }
+    if constexpr (EPI != 0) {
+        // no bulk copy is in flight any more: the stage memory is free scratch
+        double* sh = reinterpret_cast<double*>(bufs);
+        block_combine<ND * VW>(ex, M >= 2 ? LPR : 1,
+                               [&](int q, int k) {
+                                   const int c_ = M >= 2 ? k * VW + q % VW : 0;
+                                   return epi.slot[q / VW] + static_cast<int64_t>(c_) * NSLOT;
+                               },
+                               sh);
     }
 }
 
@@ -205,31 +269,47 @@ __global__ void __launch_bounds__(256) spmm_generic_kernel(int64_t nrows, const 
     y[row * m + c] = acc;
 }
 
-template <int M>
+template <int M, int EPI>
 static void launch_tma(cudaStream_t st, const SpmmTiles& tl, const int32_t* off, const int32_t* col,
-                       const double* val, const double* x, double* y, const int* ctl, int num_sms) {
+                       const double* val, const double* x, double* y, const int* ctl, int num_sms,
+                       const SpmmEpi& epi) {
     static int occ = -1;
     if (occ < 0) {
-        MBG_CUDA(cudaFuncSetAttribute(spmm_tma_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, SPMM_SMEM));
-        MBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmm_tma_kernel<M>, 256, SPMM_SMEM));
+        MBG_CUDA(cudaFuncSetAttribute(spmm_tma_kernel<M, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SPMM_SMEM));
+        MBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmm_tma_kernel<M, EPI>, 256, SPMM_SMEM));
         if (occ < 1) occ = 1;
     }
     const int grid = static_cast<int>(std::min<int64_t>(tl.count, static_cast<int64_t>(num_sms) * occ));
-    spmm_tma_kernel<M><<<grid, 256, SPMM_SMEM, st>>>(tl.tiles, static_cast<int>(tl.count), off, col, val, x, y, ctl);
+    spmm_tma_kernel<M, EPI><<<grid, 256, SPMM_SMEM, st>>>(tl.tiles, static_cast<int>(tl.count), off, col, val, x,
+                                                          y, ctl, epi);
+}
+
+template <int M>
+static void launch_tma_epi(cudaStream_t st, const SpmmTiles& tl, const int32_t* off, const int32_t* col,
+                           const double* val, const double* x, double* y, const int* ctl, int num_sms,
+                           const SpmmEpi* epi) {
+    if (!epi || epi->kind == 0)
+        launch_tma<M, 0>(st, tl, off, col, val, x, y, ctl, num_sms, SpmmEpi{});
+    else if (epi->kind == 1)
+        launch_tma<M, 1>(st, tl, off, col, val, x, y, ctl, num_sms, *epi);
+    else
+        launch_tma<M, 2>(st, tl, off, col, val, x, y, ctl, num_sms, *epi);
 }
 
 int launch_spmm(cudaStream_t st, const SpmmTiles& tl, int64_t nrows, const int32_t* rows, const int32_t* off,
                 const int32_t* col, const double* val, int m, const double* x, double* y, const int* ctl,
-                int num_sms) {
+                int num_sms, const SpmmEpi* epi) {
     if (nrows <= 0) return 0;
     switch (m) {
-        case 1: launch_tma<1>(st, tl, off, col, val, x, y, ctl, num_sms); break;
-        case 2: launch_tma<2>(st, tl, off, col, val, x, y, ctl, num_sms); break;
-        case 4: launch_tma<4>(st, tl, off, col, val, x, y, ctl, num_sms); break;
-        case 8: launch_tma<8>(st, tl, off, col, val, x, y, ctl, num_sms); break;
-        case 16: launch_tma<16>(st, tl, off, col, val, x, y, ctl, num_sms); break;
-        case 32: launch_tma<32>(st, tl, off, col, val, x, y, ctl, num_sms); break;
+        case 1: launch_tma_epi<1>(st, tl, off, col, val, x, y, ctl, num_sms, epi); break;
+        case 2: launch_tma_epi<2>(st, tl, off, col, val, x, y, ctl, num_sms, epi); break;
+        case 4: launch_tma_epi<4>(st, tl, off, col, val, x, y, ctl, num_sms, epi); break;
+        case 8: launch_tma_epi<8>(st, tl, off, col, val, x, y, ctl, num_sms, epi); break;
+        case 16: launch_tma_epi<16>(st, tl, off, col, val, x, y, ctl, num_sms, epi); break;
+        case 32: launch_tma_epi<32>(st, tl, off, col, val, x, y, ctl, num_sms, epi); break;
         default: {
+            if (epi && epi->kind != 0) throw Invalid("spmv: fused epilogue needs m in {1,2,4,8,16,32}");
             const int64_t total = nrows * m;
             spmm_generic_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(nrows, rows, off, col,
                                                                                             val, m, x, y, ctl);

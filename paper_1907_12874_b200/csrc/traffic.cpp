@@ -132,6 +132,37 @@ std::vector<Group> schedule(int method) {
     throw Invalid("unknown method");
 }
 
+// Fused formulation: dots fused into SpMM epilogues read one aux
+// vector there (aux_reads); identity M^-1 copies are elided (s = v, q = t);
+// Alg. 4 lines 7 + 12 run as one pass.
+std::vector<Group> schedule_fused(int method, int* aux_reads, int* spmm_dots) {
+    switch (method) {
+        case MBG_BICGSTAB:
+            *aux_reads = 1;                 // r0 in v = A p
+            spmm_dots[0] = 1;                // delta
+            spmm_dots[1] = 3;                // phi psi theta
+            return {{U(S, {R, V})},
+                    {U(X, {X, P, S}), U(R, {S, T}), Dt(R, R0, 0)},
+                    {U(P, {R, P, V})}};
+        case MBG_RBICGSTAB:
+            *aux_reads = 1;                 // r0 in v = A vh
+            spmm_dots[0] = 1;
+            spmm_dots[1] = 0;
+            return {{U(TH, {Z, V})},
+                    {U(RT, {R, V}), Dt(T, RT, 0), Dt(T, T, 1), Dt(T, R0, 2), Dt(RT, RT, 3)},
+                    {U(R, {RT, T})},
+                    {U(X, {X, VH, TH}), U(Z, {TH, T}), U(VH, {Z, VH, V})}};
+        case MBG_PIPEBICGSTAB:
+            *aux_reads = 0;
+            spmm_dots[0] = spmm_dots[1] = 0;
+            return {{U(P, {R, P, S}), U(S, {W, S, Z}), U(Z, {T, Z, V}), U(Q, {R, S}), U(Y, {W, Z}),
+                     Dt(Q, Y, 0), Dt(Y, Y, 1), Dt(Q, Q, 2)},
+                    {U(X, {X, P, Q}), U(R, {Q, Y}), U(W, {Y, T, V}), Dt(R0, R, 0), Dt(R0, Z, 1), Dt(R0, W, 2),
+                     Dt(R0, S, 3)}};
+    }
+    throw Invalid("unknown method");
+}
+
 }  // namespace
 
 double spmv_traffic_bytes(int64_t n, int64_t nnz, int m) {
@@ -147,6 +178,28 @@ double spmv_compulsory_bytes(int64_t n, int64_t nnz, int m) {
 void method_schedule(int method, int formulation, int* reads, int* writes, int* spmvs, int* nred,
                      int* dots) {
     int r = 0, w = 0, k = 0;
+    if (formulation == MBG_FUSED) {
+        int aux = 0, sd[2] = {0, 0};
+        for (const auto& g : schedule_fused(method, &aux, sd)) {
+            int gr, gw;
+            analyze(g.data(), static_cast<int>(g.size()), &gr, &gw);
+            r += gr;
+            w += gw;
+        }
+        r += aux;
+        // reductions in iteration order
+        std::vector<int> red;
+        if (method == MBG_BICGSTAB) red = {1, 3, 1};
+        else if (method == MBG_RBICGSTAB) red = {1, 4};
+        else red = {3, 4};
+        for (size_t i = 0; i < red.size(); ++i)
+            if (dots && i < 8) dots[i] = red[i];
+        *reads = r;
+        *writes = w;
+        *spmvs = 2;
+        *nred = static_cast<int>(red.size());
+        return;
+    }
     for (const auto& g : schedule(method)) {
         if (formulation == MBG_BASIC) {
             for (const auto& s : split(g.data(), static_cast<int>(g.size()), TEMP)) {
@@ -227,7 +280,8 @@ extern "C" int mbg_split_basic_traffic(const mbg_statement* st, int ns, int firs
 extern "C" int mbg_method_schedule(int method, int formulation, int* reads, int* writes, int* spmvs,
                                    int* nreductions, int* dots_per_reduction) {
     try {
-        if (formulation != MBG_MERGED && formulation != MBG_BASIC) throw mbg::Invalid("unknown formulation");
+        if (formulation != MBG_MERGED && formulation != MBG_BASIC && formulation != MBG_FUSED)
+            throw mbg::Invalid("unknown formulation");
         mbg::method_schedule(method, formulation, reads, writes, spmvs, nreductions, dots_per_reduction);
         return MBG_OK;
     } catch (const mbg::Invalid& e) {

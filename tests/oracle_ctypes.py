@@ -32,7 +32,7 @@ class OrcReport(C.Structure):
 
 
 METHODS = {"bicgstab": 0, "rbicgstab": 1, "pipebicgstab": 2}
-FORMULATIONS = {"merged": 0, "basic": 1}
+FORMULATIONS = {"merged": 0, "basic": 1, "fused": 0}  # fused rounds exactly like merged
 
 
 def build_oracle() -> None:

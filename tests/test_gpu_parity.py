@@ -161,8 +161,7 @@ def assert_same_solve(want, rep, X, what):
     assert_bitwise(X.download(), want["x"], f"{what} x")
 
 
-METHODS = [("bicgstab", "merged"), ("bicgstab", "basic"), ("rbicgstab", "merged"), ("rbicgstab", "basic"),
-           ("pipebicgstab", "merged"), ("pipebicgstab", "basic")]
+METHODS = [(m, f) for m in ("bicgstab", "rbicgstab", "pipebicgstab") for f in ("merged", "basic", "fused")]
 
 
 @pytest.mark.parametrize("method,form", METHODS)
@@ -185,33 +184,54 @@ def test_solve_convdiff_m8(ctx, method, form):
     assert_same_solve(want, rep, X, f"convdiff {method}/{form}")
 
 
+@pytest.mark.parametrize("form", ["merged", "fused"])
 @pytest.mark.parametrize("method", ["bicgstab", "rbicgstab", "pipebicgstab"])
-def test_solve_stencil27_m16(ctx, method):
+def test_solve_stencil27_m16(ctx, method, form):
     """Config-3 shape at 24^3 (27-pt perturbed, m=16, seed 2)."""
     a = O.gen_stencil("stencil27", 24, 24, 24, seed=2)
     b = O.rhs(a.n, 16, 2)
-    want, rep, X = run_both(ctx, a, b, 16, method)
-    assert_same_solve(want, rep, X, f"27pt {method}")
+    want, rep, X = run_both(ctx, a, b, 16, method, form)
+    assert_same_solve(want, rep, X, f"27pt {method}/{form}")
 
 
+@pytest.mark.parametrize("form", ["merged", "fused"])
 @pytest.mark.parametrize("method", ["bicgstab", "rbicgstab", "pipebicgstab"])
-def test_solve_fixed_m32(ctx, method):
+def test_solve_fixed_m32(ctx, method, form):
     """Config-4 shape at 32^3: conv-diff, m=32, fixed 40 iterations."""
     a = O.gen_stencil("convdiff7", 32, 32, 32)
     b = O.rhs(a.n, 32, 3)
-    want, rep, X = run_both(ctx, a, b, 32, method, fixed=True, maxit=40)
+    want, rep, X = run_both(ctx, a, b, 32, method, form, fixed=True, maxit=40)
     assert want["iterations"] == 40
-    assert_same_solve(want, rep, X, f"fixed m32 {method}")
+    assert_same_solve(want, rep, X, f"fixed m32 {method}/{form}")
 
 
-@pytest.mark.parametrize("m", [1, 3, 8])
+@pytest.mark.parametrize("form", ["merged", "fused"])
+@pytest.mark.parametrize("m", [1, 2, 3, 8])
 @pytest.mark.parametrize("method", ["bicgstab", "rbicgstab", "pipebicgstab"])
-def test_solve_banded(ctx, method, m):
+def test_solve_banded(ctx, method, m, form):
     """Config-5 shape at n=100k (random banded, seed 4), fixed 30 iterations."""
+    if form == "fused" and m == 3:
+        pytest.skip("fused SpMM epilogue needs m in {1,2,4,8,16,32}")
     a = O.gen_banded(100_000, 65536, 16, 32, 4)
     b = O.rhs(a.n, m, 4)
-    want, rep, X = run_both(ctx, a, b, m, method, fixed=True, maxit=30)
-    assert_same_solve(want, rep, X, f"banded {method} m={m}")
+    want, rep, X = run_both(ctx, a, b, m, method, form, fixed=True, maxit=30)
+    assert_same_solve(want, rep, X, f"banded {method}/{form} m={m}")
+
+
+def test_spmv_long_rows(ctx):
+    """Rows longer than a SpMM tile's shared-memory capacity (read from global)."""
+    n = 3000
+    rng = np.random.default_rng(5)
+    lens = np.where(np.arange(n) % 500 == 7, 2000, 5)
+    off = np.concatenate([[0], np.cumsum(lens)])
+    cols = np.concatenate([np.sort(rng.choice(n, size=k, replace=False)) for k in lens]).astype(np.int32)
+    a = O.Csr(n, off, cols, rng.standard_normal(off[-1]))
+    for m in (1, 2, 8, 32):
+        x = rng.standard_normal(n * m)
+        d = ctx.upload(to_prod(a))
+        X, Y = ctx.multivector(n, m, x), ctx.multivector(n, m)
+        P.spmv(ctx, d, X, Y)
+        assert_bitwise(Y.download(), O.spmv(a, x, m), f"long rows m={m}")
 
 
 def test_solve_breakdown_zero_rhs_column(ctx):
