@@ -293,6 +293,104 @@ __device__ __forceinline__ double digits_round_regs(const int64_t* __restrict__ 
     }
     return bitsd(out | (neg ? 0x8000000000000000ull : 0ull));
 }
+
+// Warp-cooperative rounding of one slot (all 32 lanes call it; all return the
+// same value).  Only the window of nonzero words is walked: lanes hold the
+// words, a ballot finds the window [lo, hi], and the carry pass runs
+// sequentially over it (typically < 12 words) with the words delivered by
+// shuffles.  A negative sum is detected by the signed top word of the first
+// pass and the pass repeats on the negated words.  Same result as digits_round.
+__device__ __forceinline__ double warp_round_slot(const int64_t* __restrict__ src) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = src[lane];
+    const int64_t w1 = src[lane + 32];
+    const int64_t w2 = lane + 64 < NDIG ? src[lane + 64] : 0;
+    const int64_t pinf = src[IDX_PINF], ninf = src[IDX_NINF], nan = src[IDX_NAN];
+    if (nan || (pinf && ninf)) return bitsd(0x7ff8000000000000ull);
+    if (pinf) return bitsd(0x7ff0000000000000ull);
+    if (ninf) return bitsd(0xfff0000000000000ull);
+    const unsigned m0 = __ballot_sync(0xffffffffu, w0 != 0);
+    const unsigned m1 = __ballot_sync(0xffffffffu, w1 != 0);
+    const unsigned m2 = __ballot_sync(0xffffffffu, w2 != 0);
+    if (!(m0 | m1 | m2)) return 0.0;
+    const int lo = m0 ? __ffs(m0) - 1 : (m1 ? 32 + __ffs(m1) - 1 : 64 + __ffs(m2) - 1);
+    const int hi = m2 ? 64 + 31 - __clz(m2) : (m1 ? 32 + 31 - __clz(m1) : 31 - __clz(m0));
+    const int top = hi + 2 < NDIG - 1 ? hi + 2 : NDIG - 1;  // |word| < 2^44: carries reach <= 2 words up
+
+    int h = -1;
+    uint64_t t0 = 0, t1 = 0, t2 = 0;
+    bool below = false;
+    int64_t wtop = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+        const int64_t sgn = pass ? -1 : 1;
+        int64_t carry = 0;
+        uint64_t p1 = 0, p2 = 0;   // the two previous normalised words
+        bool acc = false;          // OR of words at least three below the current one
+        h = -1;
+        for (int j = lo; j <= top; ++j) {
+            const int g = j >> 5;
+            const int64_t mine = g == 0 ? w0 : (g == 1 ? w1 : w2);
+            const int64_t dj = __shfl_sync(0xffffffffu, mine, j & 31) * sgn;
+            const int64_t v = dj + carry;
+            uint64_t word;
+            if (j < top) {
+                carry = v >> 32;
+                word = static_cast<uint64_t>(v & 0xffffffffll);
+            } else {
+                wtop = v;
+                word = static_cast<uint64_t>(v);
+            }
+            if (word != 0) {
+                h = j;
+                t0 = word;
+                t1 = p1;
+                t2 = p2;
+                below = acc;
+            }
+            acc = acc || (p2 != 0);
+            p2 = p1;
+            p1 = word;
+        }
+        if (wtop >= 0) {
+            const bool neg = pass == 1;
+            if (h < 0) return 0.0;
+            const int L = bitlen32(t0);
+            const int bitlen = 32 * h + L;
+            uint64_t out;
+            if (bitlen <= 64) {
+                // h <= 1: the window started at word 0 or 1 and t1 is word h-1
+                const uint64_t mag = h >= 1 ? ((t0 << 32) | t1) : t0;
+                if (bitlen <= 53) {
+                    out = mag;
+                } else {
+                    const int shift = bitlen - 53;
+                    uint64_t keep = mag >> shift;
+                    const bool rbit = (mag >> (shift - 1)) & 1;
+                    const bool sticky = (mag & ((1ull << (shift - 1)) - 1)) != 0;
+                    if (rbit && (sticky || (keep & 1))) ++keep;
+                    int sh = shift;
+                    if (keep == (1ull << 53)) { keep >>= 1; ++sh; }
+                    out = (static_cast<uint64_t>(sh + 1) << 52) | (keep & ((1ull << 52) - 1));
+                }
+            } else {
+                const uint64_t whi = (t0 << 32) | t1;
+                const uint64_t topbits = (whi << (32 - L)) | (t2 >> L);
+                bool sticky = below || (t2 & ((1ull << L) - 1)) != 0;
+                uint64_t keep = topbits >> 11;
+                const bool rbit = (topbits >> 10) & 1;
+                sticky = sticky || (topbits & 0x3ff) != 0;
+                int shift = bitlen - 53;
+                if (rbit && (sticky || (keep & 1))) ++keep;
+                if (keep == (1ull << 53)) { keep >>= 1; ++shift; }
+                const int biased = shift + 1;
+                out = biased >= 2047 ? 0x7ff0000000000000ull
+                                     : (static_cast<uint64_t>(biased) << 52) | (keep & ((1ull << 52) - 1));
+            }
+            return bitsd(out | (neg ? 0x8000000000000000ull : 0ull));
+        }
+    }
+    return bitsd(0x7ff8000000000000ull);  // unreachable: the negated pass has a non-negative top
+}
 #endif
 
 }  // namespace mbg

@@ -88,6 +88,7 @@ struct PUpd3 {
 
 // Classical, Alg. 2 line 9: phi=(t,s), psi=(t,t), theta=(s,s)
 struct PClassicOmega {
+    static constexpr int UNROLL = 1;  // register budget: 3+ dot expansions per column pair
     static constexpr const char* NAME = "classic_omega";
     static constexpr int NIN = 2, NOUT = 0, NCO = 0, NDOT = 3;   // in: t s
     __device__ static void run(const double* in, double*, double* prod, const double*) {
@@ -112,6 +113,7 @@ struct PClassicXR {
 // Reordered, Alg. 6 line 11:
 //   rt = 1*r + (-alpha)*v ; theta=(t,rt), phi=(t,t), psi=(t,r0), eta=(rt,rt)
 struct PReordG7 {
+    static constexpr int UNROLL = 1;  // register budget: 3+ dot expansions per column pair
     static constexpr const char* NAME = "reord_g7";
     static constexpr int NIN = 4, NOUT = 1, NCO = 1, NDOT = 4;   // in: r v t r0; co: -alpha
     __device__ static void run(const double* in, double* out, double* prod, const double* co) {
@@ -141,6 +143,7 @@ struct PReordG12 {
 //   p = 1*r + beta*p + nbo*s ; s = 1*w + beta*s + nbo*z ; z = 1*t + beta*z + nbo*v ;
 //   q = 1*r + (-alpha)*s ; y = 1*w + (-alpha)*z ; theta=(q,y), phi=(y,y), pi=(q,q)
 struct PPipeG1 {
+    static constexpr int UNROLL = 1;  // register budget: 3+ dot expansions per column pair
     static constexpr const char* NAME = "pipe_g1";
     static constexpr int NIN = 7, NOUT = 5, NCO = 3, NDOT = 3;   // in: r p s w z t v; out: p s z q y; co: beta nbo -alpha
     __device__ static void run(const double* in, double* out, double* prod, const double* co) {
@@ -168,6 +171,7 @@ struct PPipeG4 {
 // Pipelined, Alg. 4 line 12:
 //   w = 1*y + (-omega)*t + (omega*alpha)*v ; rho'=(r0,r), psi=(r0,z), sigma=(r0,w), delta=(r0,s)
 struct PPipeG5 {
+    static constexpr int UNROLL = 1;  // register budget: 3+ dot expansions per column pair
     static constexpr const char* NAME = "pipe_g5";
     static constexpr int NIN = 7, NOUT = 1, NCO = 2, NDOT = 4;   // in: y t v r0 r z s; co: -omega omega*alpha
     __device__ static void run(const double* in, double* out, double* prod, const double* co) {

@@ -9,13 +9,16 @@
 namespace mbg {
 
 __global__ void round_kernel(int64_t* D, int nslots, int m, double* out) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < nslots * m) out[i] = digits_round_regs(D + static_cast<int64_t>(i) * NSLOT);
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);   // one warp per slot
+    if (i < nslots * m) {
+        const double r = warp_round_slot(D + static_cast<int64_t>(i) * NSLOT);
+        if ((threadIdx.x & 31) == 0) out[i] = r;
+    }
 }
 
 void launch_round(cudaStream_t st, int64_t* D, int nslots, int m, double* out) {
     const int n = nslots * m;
-    round_kernel<<<(n + 127) / 128, 128, 0, st>>>(D, nslots, m, out);
+    round_kernel<<<(n + 3) / 4, 128, 0, st>>>(D, nslots, m, out);
     MBG_CUDA(cudaGetLastError());
 }
 

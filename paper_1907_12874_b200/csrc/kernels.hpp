@@ -13,8 +13,8 @@ namespace mbg {
 // CSR SpMM over the interleaved block (spmm.cu).  The row set to compute is
 // given twice: as a tile list (TMA-pipelined kernels, m in {1,2,4,8,16,32})
 // and as an explicit row list (nullptr = rows [0, nrows)) for other m.
-constexpr int SPMM_TILE_ROWS = 128;
-constexpr int SPMM_TILE_NNZ = 1280;
+constexpr int SPMM_TILE_ROWS = 192;
+constexpr int SPMM_TILE_NNZ = 1920;
 struct SpmmTiles {
     const int4* tiles = nullptr;   // (r0, r1, k0, k1) per tile
     int64_t count = 0;

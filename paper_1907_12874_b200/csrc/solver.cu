@@ -73,8 +73,10 @@ __global__ void scalar_kernel(ScalArgs a) {
     // round every (dot, column) long accumulator (one thread each), then clear
     // the (contiguous) slots for their next use
     const int nslot = a.nd * m;
-    for (int i = threadIdx.x; i < nslot; i += blockDim.x)
-        s_dots[i] = digits_round_regs(a.D[i / m] + static_cast<int64_t>(i % m) * NSLOT);
+    for (int i = threadIdx.x >> 5; i < nslot; i += blockDim.x >> 5) {
+        const double r = warp_round_slot(a.D[i / m] + static_cast<int64_t>(i % m) * NSLOT);
+        if ((threadIdx.x & 31) == 0) s_dots[i] = r;
+    }
     __syncthreads();
     if (nslot) {
         int64_t* base = a.D[0];
@@ -377,7 +379,7 @@ void Solver::scalars(int point, int nd) {
     s.hist = hist_.p;
     for (int i = 0; i < nd; ++i) s.D[i] = slot(i);
     s.nd = nd;
-    const int threads = std::min(1024, std::max(((m_ + 31) / 32) * 32, ((nd * m_ + 31) / 32) * 32));
+    const int threads = std::min(1024, std::max(((m_ + 31) / 32) * 32, 32 * nd * m_));
     mark_begin("scalar", 0.0);
     scalar_kernel<<<1, threads, static_cast<size_t>(nd > 0 ? nd : 1) * m_ * sizeof(double), ctx_->stream>>>(s);
     MBG_CUDA(cudaGetLastError());

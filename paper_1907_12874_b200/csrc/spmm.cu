@@ -5,18 +5,21 @@
 // separately rounded multiply and add -- bitwise the reference's arithmetic.
 //
 // B200 design (m in {1,2,4,8,16,32}):
-//   * the matrix is cut at upload into row tiles of <= 256 rows and <= 2560
+//   * the matrix is cut at upload into row tiles of <= 192 rows and <= 1920
 //     nonzeros (tile list in HBM, see build_spmm_tiles);
 //   * a persistent grid walks the tiles; per block a single thread streams the
-//     next tiles' row offsets, column indices and values into shared memory
+//     next tile's row offsets, column indices and values into shared memory
 //     with TMA bulk copies (cp.async.bulk, mbarrier complete_tx), double
 //     buffered, so the CSR stream (12 B/nnz + 4 B/row) is fetched
 //     asynchronously while the current tile computes;
 //   * each lane owns one row and two adjacent columns: the x gather of one
 //     nonzero is a 16-byte read-only load (x rows are reused across
-//     neighbouring rows from L1/L2) and a warp's y store is 512 contiguous
-//     bytes;
-//   * gathers are issued in batches of 8 nonzeros before the ordered adds.
+//     neighbouring rows from L1/L2) and a warp's y store is contiguous;
+//   * gathers are issued in batches of 4 nonzeros before the ordered adds.
+//   Sizing (tools/spmm_lab.cu sweep on B200, C2 shape): 4 resident blocks of
+//   256 threads (<= 64 registers, 2 x 24 KB stages) beat deeper pipelines,
+//   larger tiles, wider gather batches and two rows per lane, all of which
+//   trade occupancy for in-flight bytes and lose.
 // Any other m uses a thread-per-(row, column) kernel with the same arithmetic.
 #include <cstdint>
 #include <type_traits>
@@ -64,7 +67,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }  // namespace
 
 // smem layout per stage: offsets | cols | vals (each 16-byte aligned)
-constexpr int STAGES = 3;
+constexpr int STAGES = 2;
 constexpr int OFF_CAP = SPMM_TILE_ROWS + 8;
 constexpr int NNZ_PAD = SPMM_TILE_NNZ + 8;
 constexpr int BUF_BYTES = OFF_CAP * 4 + NNZ_PAD * 4 + NNZ_PAD * 8;
@@ -76,7 +79,7 @@ static_assert(STAGES * BUF_BYTES >= 256 * KEXP * 8, "combine scratch aliases the
 static_assert(8 * STAGES <= 32 && 32 + 16 * STAGES <= SMEM_HEAD, "head layout");
 
 template <int M, int EPI>
-__global__ void __launch_bounds__(256, 2) spmm_tma_kernel(const int4* __restrict__ tiles, int ntiles,
+__global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 1 ? 3 : 2)) spmm_tma_kernel(const int4* __restrict__ tiles, int ntiles,
                                                        const int32_t* __restrict__ off,
                                                        const int32_t* __restrict__ col,
                                                        const double* __restrict__ val,
@@ -169,69 +172,45 @@ __global__ void __launch_bounds__(256, 2) spmm_tma_kernel(const int4* __restrict
         // a long row (single-row tile beyond the stage capacity) reads global memory
         const int32_t* colp = lng ? col : s_col - k0a;
         const double* valp = lng ? val : s_val - k0a;
-        // two rows per lane at a time (rows rr and rr + RPP of the tile): twice
-        // the gathers in flight and two independent ordered add chains
-        for (int rr = tid / LPR; rr < r1 - r0; rr += 2 * RPP) {
-            const int rowA = r0 + rr, rowB = rowA + RPP;
-            const bool hasB = rr + RPP < r1 - r0;
-            const int kA = s_off[rowA - r0a], lenA = s_off[rowA + 1 - r0a] - kA;
-            const int kB = hasB ? s_off[rowB - r0a] : 0;
-            const int lenB = hasB ? s_off[rowB + 1 - r0a] - kB : 0;
-            const int len = lenA > lenB ? lenA : lenB;
-            double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-            for (int kk = 0; kk < len; kk += 4) {
-                int ja[4], jb[4];
-                double va[4], vb[4];
+        for (int rr = tid / LPR; rr < r1 - r0; rr += RPP) {
+            const int row = r0 + rr;
+            const int k0 = s_off[row - r0a], k1 = s_off[row + 1 - r0a];
+            double a0 = 0.0, a1 = 0.0;
+            // batches of 4 nonzeros: index/value loads, then the gathers, then
+            // the ordered adds (4 gathers in flight per lane; more costs occupancy)
+            for (int k = k0; k < k1; k += 4) {
+                int j[4];
+                double va[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    if (kk + q < lenA) { ja[q] = colp[kA + kk + q]; va[q] = valp[kA + kk + q]; }
-                    if (kk + q < lenB) { jb[q] = colp[kB + kk + q]; vb[q] = valp[kB + kk + q]; }
-                }
+                for (int q = 0; q < 4; ++q)
+                    if (k + q < k1) { j[q] = colp[k + q]; va[q] = valp[k + q]; }
                 if constexpr (VW == 2) {
-                    double2 xa[4], xb[4];
+                    double2 xa[4];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        if (kk + q < lenA)
-                            xa[q] = __ldg(reinterpret_cast<const double2*>(x + static_cast<int64_t>(ja[q]) * M + cp));
-                        if (kk + q < lenB)
-                            xb[q] = __ldg(reinterpret_cast<const double2*>(x + static_cast<int64_t>(jb[q]) * M + cp));
-                    }
+                    for (int q = 0; q < 4; ++q)
+                        if (k + q < k1)
+                            xa[q] = __ldg(reinterpret_cast<const double2*>(x + static_cast<int64_t>(j[q]) * M + cp));
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        if (kk + q < lenA) {
+                    for (int q = 0; q < 4; ++q)
+                        if (k + q < k1) {
                             a0 = __dadd_rn(a0, __dmul_rn(va[q], xa[q].x));
                             a1 = __dadd_rn(a1, __dmul_rn(va[q], xa[q].y));
                         }
-                        if (kk + q < lenB) {
-                            b0 = __dadd_rn(b0, __dmul_rn(vb[q], xb[q].x));
-                            b1 = __dadd_rn(b1, __dmul_rn(vb[q], xb[q].y));
-                        }
-                    }
                 } else {
-                    double xa[4], xb[4];
+                    double xa[4];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        if (kk + q < lenA) xa[q] = __ldg(x + ja[q]);
-                        if (kk + q < lenB) xb[q] = __ldg(x + jb[q]);
-                    }
+                    for (int q = 0; q < 4; ++q)
+                        if (k + q < k1) xa[q] = __ldg(x + j[q]);
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        if (kk + q < lenA) a0 = __dadd_rn(a0, __dmul_rn(va[q], xa[q]));
-                        if (kk + q < lenB) b0 = __dadd_rn(b0, __dmul_rn(vb[q], xb[q]));
-                    }
+                    for (int q = 0; q < 4; ++q)
+                        if (k + q < k1) a0 = __dadd_rn(a0, __dmul_rn(va[q], xa[q]));
                 }
             }
-            if constexpr (VW == 2) {
-                *reinterpret_cast<double2*>(y + static_cast<int64_t>(rowA) * M + cp) = make_double2(a0, a1);
-                if (hasB) *reinterpret_cast<double2*>(y + static_cast<int64_t>(rowB) * M + cp) = make_double2(b0, b1);
-            } else {
-                y[rowA] = a0;
-                if (hasB) y[rowB] = b0;
-            }
-            if constexpr (EPI != 0) {
-                epilogue(rowA, a0, a1);
-                if (hasB) epilogue(rowB, b0, b1);
-            }
+            if constexpr (VW == 2)
+                *reinterpret_cast<double2*>(y + static_cast<int64_t>(row) * M + cp) = make_double2(a0, a1);
+            else
+                y[row] = a0;
+            if constexpr (EPI != 0) epilogue(row, a0, a1);
         }
         __syncthreads();  // every thread is done with stage b
         if (tid == 0) issue(i + STAGES, b);
