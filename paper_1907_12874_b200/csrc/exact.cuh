@@ -302,10 +302,11 @@ __device__ __forceinline__ double digits_round_regs(const int64_t* __restrict__ 
 // pass and the pass repeats on the negated words.  Same result as digits_round.
 __device__ __forceinline__ double warp_round_slot(const int64_t* __restrict__ src) {
     const int lane = threadIdx.x & 31;
-    const int64_t w0 = src[lane];
-    const int64_t w1 = src[lane + 32];
-    const int64_t w2 = lane + 64 < NDIG ? src[lane + 64] : 0;
-    const int64_t pinf = src[IDX_PINF], ninf = src[IDX_NINF], nan = src[IDX_NAN];
+    // L2 loads: the slot was filled by other blocks' atomics
+    const int64_t w0 = __ldcg(src + lane);
+    const int64_t w1 = __ldcg(src + lane + 32);
+    const int64_t w2 = lane + 64 < NDIG ? __ldcg(src + lane + 64) : 0;
+    const int64_t pinf = __ldcg(src + IDX_PINF), ninf = __ldcg(src + IDX_NINF), nan = __ldcg(src + IDX_NAN);
     if (nan || (pinf && ninf)) return bitsd(0x7ff8000000000000ull);
     if (pinf) return bitsd(0x7ff0000000000000ull);
     if (ninf) return bitsd(0xfff0000000000000ull);

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include "exact.cuh"
+#include "scalar.cuh"
 
 namespace mbg {
 
@@ -33,6 +34,7 @@ struct GroupArgs {
     const double* coef[GMAX_CO]; // device arrays of m doubles
     int64_t* slot[GMAX_DOT];     // long accumulators: m * NSLOT words each
     const int* ctl;              // ctl[0] != 0: solve stopped -> no-op
+    PostArgs post;               // scalar step run by the last block (scalar.cuh)
 };
 
 __device__ __forceinline__ double fmadd_rn(double acc, double c, double v) {
@@ -287,7 +289,7 @@ __device__ __forceinline__ void block_combine(double (&acc)[NX][KEXP], int class
 // correct) for memory-level parallelism.  VEC = 1 covers odd m.
 // ---------------------------------------------------------------------------
 template <class P, int VEC>
-__global__ void __launch_bounds__(256) group_kernel(GroupArgs a) {
+__global__ void __launch_bounds__(256, 2) group_kernel(GroupArgs a) {
     if (a.ctl && a.ctl[0]) return;
     extern __shared__ double sh_dyn[];
     const int m = a.m;
@@ -423,6 +425,7 @@ __global__ void __launch_bounds__(256) group_kernel(GroupArgs a) {
                                 },
                                 sh_dyn);
     }
+    if (a.post.enabled) post_step(a.post, sh_dyn);
 }
 
 // Block size for m columns: m * 2^q <= 256 (m <= 256), else m.

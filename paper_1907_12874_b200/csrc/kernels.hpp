@@ -26,6 +26,7 @@ struct SpmmEpi {
     int kind = 0;
     const double* aux = nullptr;
     int64_t* slot[3] = {nullptr, nullptr, nullptr};
+    PostArgs post{};     // scalar step run by the last block
 };
 int launch_spmm(cudaStream_t st, const SpmmTiles& tl, int64_t nrows, const int32_t* rows, const int32_t* off,
                 const int32_t* col, const double* val, int m, const double* x, double* y, const int* ctl,
@@ -58,7 +59,11 @@ int group_grid(const void* kernel, int block, size_t smem, int num_sms, int64_t 
 template <class P>
 inline int launch_group(cudaStream_t st, const GroupArgs& a, int num_sms) {
     const int block = group_block(a.m);
-    const size_t smem = P::NDOT > 0 ? static_cast<size_t>(block) * KEXP * sizeof(double) : 0;
+    size_t smem = P::NDOT > 0 ? static_cast<size_t>(block) * KEXP * sizeof(double) : 0;
+    if (a.post.enabled) {
+        const size_t need = static_cast<size_t>(a.post.s.nd > 0 ? a.post.s.nd : 1) * a.m * sizeof(double);
+        if (need > smem) smem = need;
+    }
     const bool vec2 = (a.m % 2 == 0 || a.m == 1) && a.len % 2 == 0;
     if (vec2) {
         const int grid =

@@ -1,0 +1,236 @@
+// scalar.cuh -- per-column scalar recurrences of the three BiCGStab variants
+// (ColumnScalars arithmetic, types.hpp:39-83, on the device), convergence,
+// breakdown and iteration control.  Runs either as its own one-block kernel
+// or as the "post" step of the kernel that produced the dots: the last block
+// of that kernel to finish (atomic ticket) performs it, saving a launch per
+// reduction point.
+#pragma once
+
+#include <climits>
+
+#include "exact.cuh"
+
+namespace mbg {
+
+// ---- scalar bank / control words ------------------------------------------
+enum Scal : int {
+    S_ONE, S_MONE, S_BB, S_EPS2, S_RHO, S_ALPHA, S_NALPHA, S_OMEGA, S_NOMEGA,
+    S_BETA, S_NBO, S_OA, S_RES2, NSCAL
+};
+enum Ctl : int {
+    C_STOP, C_CONV, C_ITER, C_ITERS, C_BD, C_BDITER, C_BDCOL, C_CONVERGED, NCTL = 16
+};
+enum Point : int {
+    P_SETUP, P_C_ALPHA, P_C_OMEGA, P_C_BETA, P_R_OMEGA, P_R_END, P_P_OMEGA, P_P_BETA
+};
+
+struct ScalArgs {
+    int m, point, method, fixed, maxit;
+    double tol2;
+    double* sc;          // NSCAL * m
+    int* ctl;
+    double* hist;        // (maxit+1) * m
+    int64_t* D[4];       // long accumulators: rounded here (after any cross-GPU allreduce), then cleared
+    int nd;
+};
+
+__device__ __forceinline__ bool finite_d(double x) { return isfinite(x); }
+
+__device__ __forceinline__ double hist_entry(double res2, double bb) {
+    const double r = res2 > 0.0 ? res2 : 0.0;
+    return __dsqrt_rn(__ddiv_rn(r, bb));
+}
+
+// One block, thread c <-> column c (blockDim >= m).  Expressions follow
+// oracle.c operation by operation (separately rounded, no contraction).
+// s_dots: shared scratch of nd * m doubles.
+static __device__ __forceinline__ void scalar_block(const ScalArgs& a, double* s_dots) {
+    __shared__ int s_bad1, s_bad2, s_all;
+    int* ctl = a.ctl;
+    if (ctl[C_STOP]) return;
+    const int m = a.m;
+    const int c = threadIdx.x;
+    const bool on = c < m;
+    if (c == 0) { s_bad1 = INT_MAX; s_bad2 = INT_MAX; s_all = 1; }
+    // round every (dot, column) long accumulator (one thread each), then clear
+    // the (contiguous) slots for their next use
+    const int nslot = a.nd * m;
+    for (int i = threadIdx.x >> 5; i < nslot; i += blockDim.x >> 5) {
+        const double r = warp_round_slot(a.D[i / m] + static_cast<int64_t>(i % m) * NSLOT);
+        if ((threadIdx.x & 31) == 0) s_dots[i] = r;
+    }
+    __syncthreads();
+    if (nslot) {
+        int64_t* base = a.D[0];
+        for (int w = threadIdx.x; w < nslot * NSLOT; w += blockDim.x) base[w] = 0;
+    }
+    double* sc = a.sc;
+#define SC(i) sc[(i) * m + c]
+    double d[4] = {0.0, 0.0, 0.0, 0.0};
+    if (on)
+        for (int i = 0; i < a.nd; ++i) d[i] = s_dots[i * m + c];
+    const int j = ctl[C_ITER];
+    int code1 = 0, code2 = 0;  // breakdown codes for s_bad1 / s_bad2
+    switch (a.point) {
+        case P_SETUP: {
+            // d0 = (r0,r0), d1 = (b,b), d2 = (r0,w) for Pipelined
+            if (on) {
+                SC(S_ONE) = 1.0; SC(S_MONE) = -1.0;
+                SC(S_RHO) = d[0]; SC(S_BB) = d[1];
+                SC(S_EPS2) = __dmul_rn(a.tol2, d[1]);
+                a.hist[c] = hist_entry(d[0], d[1]);
+                if (!(d[0] < SC(S_EPS2))) s_all = 0;
+            }
+            __syncthreads();
+            if (!a.fixed && s_all) {
+                if (c == 0) { ctl[C_STOP] = 1; ctl[C_CONVERGED] = 1; ctl[C_ITERS] = 0; }
+                return;
+            }
+            if (a.method == MBG_PIPEBICGSTAB && on) {
+                const double alpha = __ddiv_rn(d[0], d[2]);
+                SC(S_ALPHA) = alpha; SC(S_NALPHA) = -alpha;
+                SC(S_BETA) = 0.0; SC(S_OMEGA) = 0.0;
+                SC(S_NBO) = -__dmul_rn(0.0, 0.0);
+                if (d[2] == 0.0 || !finite_d(alpha)) atomicMin(&s_bad1, c);
+            }
+            code1 = 1;
+            break;
+        }
+        case P_C_ALPHA: {
+            if (on) {
+                const double alpha = __ddiv_rn(SC(S_RHO), d[0]);
+                SC(S_ALPHA) = alpha; SC(S_NALPHA) = -alpha;
+                if (d[0] == 0.0 || !finite_d(alpha)) atomicMin(&s_bad1, c);
+            }
+            code1 = 1;
+            break;
+        }
+        case P_C_OMEGA:    // d = phi psi theta
+        case P_R_OMEGA:    // d = theta phi psi eta
+        case P_P_OMEGA: {  // d = theta phi pi
+            double num, den, sq;
+            if (a.point == P_C_OMEGA) { num = d[0]; den = d[1]; sq = d[2]; }
+            else if (a.point == P_R_OMEGA) { num = d[0]; den = d[1]; sq = d[3]; }
+            else { num = d[0]; den = d[1]; sq = d[2]; }
+            double omega = 0.0, res2 = 0.0;
+            if (on) {
+                // lucky exact convergence (den == 0 because the residual is exactly 0): omega = 0
+                const bool lucky = den == 0.0 && sq == 0.0;
+                omega = lucky ? 0.0 : __ddiv_rn(num, den);
+                SC(S_OMEGA) = omega; SC(S_NOMEGA) = -omega;
+                if (a.point == P_P_OMEGA) SC(S_OA) = __dmul_rn(omega, SC(S_ALPHA));
+                res2 = __dsub_rn(sq, __dmul_rn(omega, num));
+                SC(S_RES2) = res2;
+                if ((den == 0.0 && !lucky) || !finite_d(omega)) atomicMin(&s_bad2, c);
+            }
+            __syncthreads();
+            if (s_bad2 != INT_MAX) { code2 = 2; break; }
+            if (on) {
+                a.hist[static_cast<int64_t>(j + 1) * m + c] = hist_entry(res2, SC(S_BB));
+                if (!(res2 < SC(S_EPS2))) s_all = 0;
+            }
+            __syncthreads();
+            const bool conv = !a.fixed && s_all;
+            if (c == 0 && conv) ctl[C_CONV] = 1;
+            if (a.point == P_R_OMEGA && !conv && on) {
+                // rho' = -(omega*psi), beta = (rho'/rho)*(alpha/omega)
+                const double rhon = -__dmul_rn(omega, d[2]);
+                const double beta = __dmul_rn(__ddiv_rn(rhon, SC(S_RHO)), __ddiv_rn(SC(S_ALPHA), omega));
+                SC(S_BETA) = beta; SC(S_NBO) = -__dmul_rn(beta, omega); SC(S_RHO) = rhon;
+                if (!finite_d(beta)) atomicMin(&s_bad1, c);
+            }
+            code1 = 3;
+            break;
+        }
+        case P_C_BETA: {
+            if (ctl[C_CONV]) {
+                if (c == 0) { ctl[C_STOP] = 1; ctl[C_CONVERGED] = 1; ctl[C_ITERS] = j + 1; }
+                return;
+            }
+            if (on) {
+                const double rhon = d[0];
+                const double beta = __dmul_rn(__ddiv_rn(rhon, SC(S_RHO)), __ddiv_rn(SC(S_ALPHA), SC(S_OMEGA)));
+                SC(S_BETA) = beta; SC(S_NBO) = -__dmul_rn(beta, SC(S_OMEGA)); SC(S_RHO) = rhon;
+                if (!finite_d(beta)) atomicMin(&s_bad1, c);
+            }
+            code1 = 3;
+            break;
+        }
+        case P_R_END: {
+            if (c == 0) {
+                if (ctl[C_CONV]) { ctl[C_STOP] = 1; ctl[C_CONVERGED] = 1; ctl[C_ITERS] = j + 1; }
+            }
+            break;
+        }
+        case P_P_BETA: {
+            if (ctl[C_CONV]) {
+                if (c == 0) { ctl[C_STOP] = 1; ctl[C_CONVERGED] = 1; ctl[C_ITERS] = j + 1; }
+                return;
+            }
+            if (on) {
+                // d = rho' psi sigma delta
+                const double omega = SC(S_OMEGA), alpha = SC(S_ALPHA);
+                const double beta = __dmul_rn(__ddiv_rn(alpha, omega), __ddiv_rn(d[0], SC(S_RHO)));
+                const double den = __dsub_rn(__dadd_rn(d[2], __dmul_rn(beta, d[3])),
+                                             __dmul_rn(__dmul_rn(beta, omega), d[1]));
+                const double an = __ddiv_rn(d[0], den);
+                SC(S_BETA) = beta; SC(S_ALPHA) = an; SC(S_RHO) = d[0];
+                SC(S_NBO) = -__dmul_rn(beta, omega); SC(S_NALPHA) = -an;
+                if (!finite_d(beta)) atomicMin(&s_bad2, c);
+                if (den == 0.0 || !finite_d(an)) atomicMin(&s_bad1, c);
+            }
+            __syncthreads();
+            if (s_bad2 != INT_MAX) { code2 = 3; break; }
+            code1 = 1;
+            break;
+        }
+    }
+#undef SC
+    __syncthreads();
+    if (c != 0) return;
+    // breakdown bookkeeping (first column)
+    if (code2 && s_bad2 != INT_MAX) {
+        ctl[C_BD] = code2; ctl[C_BDITER] = j; ctl[C_BDCOL] = s_bad2; ctl[C_ITERS] = j; ctl[C_STOP] = 1;
+        return;
+    }
+    if (code1 && s_bad1 != INT_MAX) {
+        // Pipelined's alpha_{j+1} belongs to the next iteration (oracle.c)
+        const int it = (a.point == P_P_BETA) ? j + 1 : j;
+        ctl[C_BD] = code1; ctl[C_BDITER] = it; ctl[C_BDCOL] = s_bad1; ctl[C_ITERS] = it; ctl[C_STOP] = 1;
+        return;
+    }
+    // end of iteration
+    if (a.point == P_C_BETA || a.point == P_R_END || a.point == P_P_BETA) {
+        ctl[C_ITER] = j + 1;
+        ctl[C_ITERS] = j + 1;
+        if (j + 1 >= a.maxit) ctl[C_STOP] = 1;
+    }
+    if (a.point == P_SETUP && a.maxit <= 0) ctl[C_STOP] = 1;
+}
+
+
+// Post step appended to a dot-producing kernel: the last block to finish runs
+// scalar_block.  Every thread fences its slot atomics before the block takes
+// its ticket; the last block fences again before reading the slots.
+struct PostArgs {
+    int enabled;
+    unsigned int* counter;
+    ScalArgs s;
+};
+
+__device__ __forceinline__ void post_step(const PostArgs& p, double* s_dots) {
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned t = atomicAdd(p.counter, 1u);
+        s_last = t == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    scalar_block(p.s, s_dots);
+    if (threadIdx.x == 0) *p.counter = 0u;
+}
+
+}  // namespace mbg

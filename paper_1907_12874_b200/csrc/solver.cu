@@ -26,204 +26,14 @@
 #include "common.hpp"
 #include "comm.hpp"
 #include "kernels.hpp"
+#include "scalar.cuh"
 #include "solver.hpp"
 
 namespace mbg {
 
-// ---- scalar bank / control words ------------------------------------------
-enum Scal : int {
-    S_ONE, S_MONE, S_BB, S_EPS2, S_RHO, S_ALPHA, S_NALPHA, S_OMEGA, S_NOMEGA,
-    S_BETA, S_NBO, S_OA, S_RES2, NSCAL
-};
-enum Ctl : int {
-    C_STOP, C_CONV, C_ITER, C_ITERS, C_BD, C_BDITER, C_BDCOL, C_CONVERGED, NCTL = 16
-};
-enum Point : int {
-    P_SETUP, P_C_ALPHA, P_C_OMEGA, P_C_BETA, P_R_OMEGA, P_R_END, P_P_OMEGA, P_P_BETA
-};
-
-struct ScalArgs {
-    int m, point, method, fixed, maxit;
-    double tol2;
-    double* sc;          // NSCAL * m
-    int* ctl;
-    double* hist;        // (maxit+1) * m
-    int64_t* D[4];       // long accumulators: rounded here (after any cross-GPU allreduce), then cleared
-    int nd;
-};
-
-__device__ __forceinline__ bool finite_d(double x) { return isfinite(x); }
-
-__device__ __forceinline__ double hist_entry(double res2, double bb) {
-    const double r = res2 > 0.0 ? res2 : 0.0;
-    return __dsqrt_rn(__ddiv_rn(r, bb));
-}
-
-// One block, thread c <-> column c.  Expressions follow oracle.c operation by
-// operation (separately rounded, no contraction).
 __global__ void scalar_kernel(ScalArgs a) {
-    __shared__ int s_bad1, s_bad2, s_all;
     extern __shared__ double s_dots[];  // nd * m rounded dots
-    int* ctl = a.ctl;
-    if (ctl[C_STOP]) return;
-    const int m = a.m;
-    const int c = threadIdx.x;
-    const bool on = c < m;
-    if (c == 0) { s_bad1 = INT_MAX; s_bad2 = INT_MAX; s_all = 1; }
-    // round every (dot, column) long accumulator (one thread each), then clear
-    // the (contiguous) slots for their next use
-    const int nslot = a.nd * m;
-    for (int i = threadIdx.x >> 5; i < nslot; i += blockDim.x >> 5) {
-        const double r = warp_round_slot(a.D[i / m] + static_cast<int64_t>(i % m) * NSLOT);
-        if ((threadIdx.x & 31) == 0) s_dots[i] = r;
-    }
-    __syncthreads();
-    if (nslot) {
-        int64_t* base = a.D[0];
-        for (int w = threadIdx.x; w < nslot * NSLOT; w += blockDim.x) base[w] = 0;
-    }
-    double* sc = a.sc;
-#define SC(i) sc[(i) * m + c]
-    double d[4] = {0.0, 0.0, 0.0, 0.0};
-    if (on)
-        for (int i = 0; i < a.nd; ++i) d[i] = s_dots[i * m + c];
-    const int j = ctl[C_ITER];
-    int code1 = 0, code2 = 0;  // breakdown codes for s_bad1 / s_bad2
-    switch (a.point) {
-        case P_SETUP: {
-            // d0 = (r0,r0), d1 = (b,b), d2 = (r0,w) for Pipelined
-            if (on) {
-                SC(S_ONE) = 1.0; SC(S_MONE) = -1.0;
-                SC(S_RHO) = d[0]; SC(S_BB) = d[1];
-                SC(S_EPS2) = __dmul_rn(a.tol2, d[1]);
-                a.hist[c] = hist_entry(d[0], d[1]);
-                if (!(d[0] < SC(S_EPS2))) s_all = 0;
-            }
-            __syncthreads();
-            if (!a.fixed && s_all) {
-                if (c == 0) { ctl[C_STOP] = 1; ctl[C_CONVERGED] = 1; ctl[C_ITERS] = 0; }
-                return;
-            }
-            if (a.method == MBG_PIPEBICGSTAB && on) {
-                const double alpha = __ddiv_rn(d[0], d[2]);
-                SC(S_ALPHA) = alpha; SC(S_NALPHA) = -alpha;
-                SC(S_BETA) = 0.0; SC(S_OMEGA) = 0.0;
-                SC(S_NBO) = -__dmul_rn(0.0, 0.0);
-                if (d[2] == 0.0 || !finite_d(alpha)) atomicMin(&s_bad1, c);
-            }
-            code1 = 1;
-            break;
-        }
-        case P_C_ALPHA: {
-            if (on) {
-                const double alpha = __ddiv_rn(SC(S_RHO), d[0]);
-                SC(S_ALPHA) = alpha; SC(S_NALPHA) = -alpha;
-                if (d[0] == 0.0 || !finite_d(alpha)) atomicMin(&s_bad1, c);
-            }
-            code1 = 1;
-            break;
-        }
-        case P_C_OMEGA:    // d = phi psi theta
-        case P_R_OMEGA:    // d = theta phi psi eta
-        case P_P_OMEGA: {  // d = theta phi pi
-            double num, den, sq;
-            if (a.point == P_C_OMEGA) { num = d[0]; den = d[1]; sq = d[2]; }
-            else if (a.point == P_R_OMEGA) { num = d[0]; den = d[1]; sq = d[3]; }
-            else { num = d[0]; den = d[1]; sq = d[2]; }
-            double omega = 0.0, res2 = 0.0;
-            if (on) {
-                // lucky exact convergence (den == 0 because the residual is exactly 0): omega = 0
-                const bool lucky = den == 0.0 && sq == 0.0;
-                omega = lucky ? 0.0 : __ddiv_rn(num, den);
-                SC(S_OMEGA) = omega; SC(S_NOMEGA) = -omega;
-                if (a.point == P_P_OMEGA) SC(S_OA) = __dmul_rn(omega, SC(S_ALPHA));
-                res2 = __dsub_rn(sq, __dmul_rn(omega, num));
-                SC(S_RES2) = res2;
-                if ((den == 0.0 && !lucky) || !finite_d(omega)) atomicMin(&s_bad2, c);
-            }
-            __syncthreads();
-            if (s_bad2 != INT_MAX) { code2 = 2; break; }
-            if (on) {
-                a.hist[static_cast<int64_t>(j + 1) * m + c] = hist_entry(res2, SC(S_BB));
-                if (!(res2 < SC(S_EPS2))) s_all = 0;
-            }
-            __syncthreads();
-            const bool conv = !a.fixed && s_all;
-            if (c == 0 && conv) ctl[C_CONV] = 1;
-            if (a.point == P_R_OMEGA && !conv && on) {
-                // rho' = -(omega*psi), beta = (rho'/rho)*(alpha/omega)
-                const double rhon = -__dmul_rn(omega, d[2]);
-                const double beta = __dmul_rn(__ddiv_rn(rhon, SC(S_RHO)), __ddiv_rn(SC(S_ALPHA), omega));
-                SC(S_BETA) = beta; SC(S_NBO) = -__dmul_rn(beta, omega); SC(S_RHO) = rhon;
-                if (!finite_d(beta)) atomicMin(&s_bad1, c);
-            }
-            code1 = 3;
-            break;
-        }
-        case P_C_BETA: {
-            if (ctl[C_CONV]) {
-                if (c == 0) { ctl[C_STOP] = 1; ctl[C_CONVERGED] = 1; ctl[C_ITERS] = j + 1; }
-                return;
-            }
-            if (on) {
-                const double rhon = d[0];
-                const double beta = __dmul_rn(__ddiv_rn(rhon, SC(S_RHO)), __ddiv_rn(SC(S_ALPHA), SC(S_OMEGA)));
-                SC(S_BETA) = beta; SC(S_NBO) = -__dmul_rn(beta, SC(S_OMEGA)); SC(S_RHO) = rhon;
-                if (!finite_d(beta)) atomicMin(&s_bad1, c);
-            }
-            code1 = 3;
-            break;
-        }
-        case P_R_END: {
-            if (c == 0) {
-                if (ctl[C_CONV]) { ctl[C_STOP] = 1; ctl[C_CONVERGED] = 1; ctl[C_ITERS] = j + 1; }
-            }
-            break;
-        }
-        case P_P_BETA: {
-            if (ctl[C_CONV]) {
-                if (c == 0) { ctl[C_STOP] = 1; ctl[C_CONVERGED] = 1; ctl[C_ITERS] = j + 1; }
-                return;
-            }
-            if (on) {
-                // d = rho' psi sigma delta
-                const double omega = SC(S_OMEGA), alpha = SC(S_ALPHA);
-                const double beta = __dmul_rn(__ddiv_rn(alpha, omega), __ddiv_rn(d[0], SC(S_RHO)));
-                const double den = __dsub_rn(__dadd_rn(d[2], __dmul_rn(beta, d[3])),
-                                             __dmul_rn(__dmul_rn(beta, omega), d[1]));
-                const double an = __ddiv_rn(d[0], den);
-                SC(S_BETA) = beta; SC(S_ALPHA) = an; SC(S_RHO) = d[0];
-                SC(S_NBO) = -__dmul_rn(beta, omega); SC(S_NALPHA) = -an;
-                if (!finite_d(beta)) atomicMin(&s_bad2, c);
-                if (den == 0.0 || !finite_d(an)) atomicMin(&s_bad1, c);
-            }
-            __syncthreads();
-            if (s_bad2 != INT_MAX) { code2 = 3; break; }
-            code1 = 1;
-            break;
-        }
-    }
-#undef SC
-    __syncthreads();
-    if (c != 0) return;
-    // breakdown bookkeeping (first column)
-    if (code2 && s_bad2 != INT_MAX) {
-        ctl[C_BD] = code2; ctl[C_BDITER] = j; ctl[C_BDCOL] = s_bad2; ctl[C_ITERS] = j; ctl[C_STOP] = 1;
-        return;
-    }
-    if (code1 && s_bad1 != INT_MAX) {
-        // Pipelined's alpha_{j+1} belongs to the next iteration (oracle.c)
-        const int it = (a.point == P_P_BETA) ? j + 1 : j;
-        ctl[C_BD] = code1; ctl[C_BDITER] = it; ctl[C_BDCOL] = s_bad1; ctl[C_ITERS] = it; ctl[C_STOP] = 1;
-        return;
-    }
-    // end of iteration
-    if (a.point == P_C_BETA || a.point == P_R_END || a.point == P_P_BETA) {
-        ctl[C_ITER] = j + 1;
-        ctl[C_ITERS] = j + 1;
-        if (j + 1 >= a.maxit) ctl[C_STOP] = 1;
-    }
-    if (a.point == P_SETUP && a.maxit <= 0) ctl[C_STOP] = 1;
+    scalar_block(a, s_dots);
 }
 
 // ===========================================================================
@@ -254,6 +64,8 @@ Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulatio
     ctl_.alloc(NCTL);
     hist_.alloc(static_cast<size_t>(maxit + 1) * m);
     slots_.alloc(static_cast<size_t>(4) * m * NSLOT);
+    ticket_.alloc(1);
+    MBG_CUDA(cudaMemsetAsync(ticket_.p, 0, sizeof(unsigned), ctx->stream));
     MBG_CUDA(cudaMemsetAsync(slots_.p, 0, slots_.n * sizeof(int64_t), ctx->stream));
     MBG_CUDA(cudaMemsetAsync(ctl_.p, 0, ctl_.n * sizeof(int), ctx->stream));
     MBG_CUDA(cudaMallocHost(&ctl_host_, 2 * NCTL * sizeof(int)));
@@ -315,11 +127,19 @@ std::string Solver::profile_json() {
     return out + "}";
 }
 
-void Solver::spmm(const double* x, double* y, int epi_kind, const double* aux) {
+void Solver::spmm(const double* x, double* y, int epi_kind, const double* aux, int post_point, int post_nd) {
     SpmmEpi e;
     e.kind = epi_kind;
     e.aux = aux;
     for (int d = 0; d < 3; ++d) e.slot[d] = slot(d);
+    // the scalar step can ride on a single fused-epilogue SpMM launch
+    const bool post = post_point >= 0 && epi_kind != 0 && can_post() && a_->peers.empty() &&
+                      (m_ == 1 || m_ == 2 || m_ == 4 || m_ == 8 || m_ == 16 || m_ == 32);
+    if (post) {
+        e.post.enabled = 1;
+        e.post.counter = ticket_.p;
+        e.post.s = scal_args(post_point, post_nd);
+    }
     const double extra = epi_kind == 1 ? 8.0 * len_ : 0.0;   // aux vector read
     mark_begin(epi_kind ? "spmm+dots" : "spmm", spmv_compulsory_bytes(a_->n, a_->nnz, m_) + extra);
     launches_ += apply_operator(ctx_, a_, m_, const_cast<double*>(x), y, ctl_.p, epi_kind ? &e : nullptr);
@@ -329,11 +149,12 @@ void Solver::spmm(const double* x, double* y, int epi_kind, const double* aux) {
             comm_allreduce_i64(ctx_, slot(0), static_cast<size_t>(epi_kind == 2 ? 3 : 1) * m_ * NSLOT, ctx_->stream);
         reductions_++;
     }
+    if (post_point >= 0 && !post) scalars(post_point, post_nd);
 }
 
 template <class P>
 void Solver::group(std::initializer_list<const double*> in, std::initializer_list<double*> out,
-                   std::initializer_list<int> co, int first_slot) {
+                   std::initializer_list<int> co, int first_slot, int post_point, int post_nd) {
     GroupArgs g{};
     g.len = len_;
     g.m = m_;
@@ -345,6 +166,12 @@ void Solver::group(std::initializer_list<const double*> in, std::initializer_lis
     for (int s : co) g.coef[i++] = sc(s);
     for (int d = 0; d < P::NDOT; ++d) g.slot[d] = slot(first_slot + d);
     g.ctl = ctl_.p;
+    const bool post = post_point >= 0 && can_post();
+    if (post) {
+        g.post.enabled = 1;
+        g.post.counter = ticket_.p;
+        g.post.s = scal_args(post_point, post_nd);
+    }
     mark_begin(std::string("group:") + P::NAME, static_cast<double>(P::NIN + P::NOUT) * 8.0 * len_);
     launch_group<P>(ctx_->stream, g, ctx_->num_sms);
     MBG_CUDA(cudaGetLastError());
@@ -357,6 +184,7 @@ void Solver::group(std::initializer_list<const double*> in, std::initializer_lis
         }
         reductions_++;
     }
+    if (post_point >= 0 && !post) scalars(post_point, post_nd);
 }
 
 void Solver::copy(double* dst, const double* src) {
@@ -366,7 +194,7 @@ void Solver::copy(double* dst, const double* src) {
     mark_end();
 }
 
-void Solver::scalars(int point, int nd) {
+ScalArgs Solver::scal_args(int point, int nd) {
     ScalArgs s{};
     s.m = m_;
     s.point = point;
@@ -379,6 +207,17 @@ void Solver::scalars(int point, int nd) {
     s.hist = hist_.p;
     for (int i = 0; i < nd; ++i) s.D[i] = slot(i);
     s.nd = nd;
+    return s;
+}
+
+bool Solver::can_post() const {
+    // the fused scalar step needs every dot of the point locally (no pending
+    // cross-GPU allreduce) and whole warps
+    return ctx_->comm == nullptr && group_block(m_) % 32 == 0;
+}
+
+void Solver::scalars(int point, int nd) {
+    ScalArgs s = scal_args(point, nd);
     const int threads = std::min(1024, std::max(((m_ + 31) / 32) * 32, 32 * nd * m_));
     mark_begin("scalar", 0.0);
     scalar_kernel<<<1, threads, static_cast<size_t>(nd > 0 ? nd : 1) * m_ * sizeof(double), ctx_->stream>>>(s);
@@ -405,22 +244,22 @@ void Solver::setup(const double* b, double* x) {
     group<PUpd2>({b, tmpv}, {r}, {S_ONE, S_MONE}, 0);    // r = 1*b + (-1)*z   (needs S_ONE set)
     group<PUpd1>({r}, {r0}, {S_ONE}, 0);                  // r0 = 1*r
     group<PDot1>({r0}, {}, {}, 0);                        // rho = (r0, r0)
-    group<PDot1>({b}, {}, {}, 1);                         // bb = (b, b)
-    int nd = 2;
     if (method_ == MBG_BICGSTAB) {
         group<PUpd1>({r}, {w(V_P)}, {S_ONE}, 2);          // p = 1*r
+        group<PDot1>({b}, {}, {}, 1, P_SETUP, 2);         // bb = (b, b)
     } else if (method_ == MBG_RBICGSTAB) {
         copy(w(V_Z), r0);                                 // z0 = M^-1 r0 (identity)
         copy(w(V_VH), w(V_Z));                            // v^0 = z0
+        group<PDot1>({b}, {}, {}, 1, P_SETUP, 2);         // bb = (b, b)
     } else {
+        group<PDot1>({b}, {}, {}, 1);                     // bb = (b, b)
+        for (int v : {V_P, V_S, V_Z, V_V})
+            if (v != V_V) MBG_CUDA(cudaMemsetAsync(w(v), 0, static_cast<size_t>(len_) * sizeof(double), ctx_->stream));
         spmm(r, w(V_W));                                  // w0 = A r0
         spmm(w(V_W), w(V_T));                             // t0 = A w0
-        group<PDot2>({r0, w(V_W)}, {}, {}, 2);            // (r0, w0)
-        nd = 3;
-        for (int v : {V_P, V_S, V_Z, V_V})
-            MBG_CUDA(cudaMemsetAsync(w(v), 0, static_cast<size_t>(len_) * sizeof(double), ctx_->stream));
+        MBG_CUDA(cudaMemsetAsync(w(V_V), 0, static_cast<size_t>(len_) * sizeof(double), ctx_->stream));
+        group<PDot2>({r0, w(V_W)}, {}, {}, 2, P_SETUP, 3); // (r0, w0) ; alpha0
     }
-    scalars(P_SETUP, nd);
 }
 
 void Solver::iteration() {
@@ -430,34 +269,31 @@ void Solver::iteration() {
     if (method_ == MBG_BICGSTAB) {
         double *p = w(V_P), *v = w(V_V), *s = w(V_S), *t = w(V_T);
         if (fused) {
-            spmm(p, v, 1, r0);                                    // v = A p ; delta = (v, r0)
+            spmm(p, v, 1, r0, P_C_ALPHA, 1);                      // v = A p ; delta = (v, r0) ; alpha
         } else {
             spmm(p, v);
-            group<PDot2>({v, r0}, {}, {}, 0);
+            group<PDot2>({v, r0}, {}, {}, 0, P_C_ALPHA, 1);
         }
-        scalars(P_C_ALPHA, 1);
         group<PUpd2>({r, v}, {s}, {S_ONE, S_NALPHA}, 0);
         if (fused) {
-            spmm(s, t, 2);                                        // t = A s ; phi psi theta
+            spmm(s, t, 2, nullptr, P_C_OMEGA, 3);                 // t = A s ; phi psi theta ; omega
         } else {
             spmm(s, t);
             if (basic) {
                 group<PDot2>({t, s}, {}, {}, 0);
                 group<PDot1>({t}, {}, {}, 1);
-                group<PDot1>({s}, {}, {}, 2);
+                group<PDot1>({s}, {}, {}, 2, P_C_OMEGA, 3);
             } else {
-                group<PClassicOmega>({t, s}, {}, {}, 0);
+                group<PClassicOmega>({t, s}, {}, {}, 0, P_C_OMEGA, 3);
             }
         }
-        scalars(P_C_OMEGA, 3);
         if (basic) {
             group<PUpd3>({x, p, s}, {x}, {S_ONE, S_ALPHA, S_OMEGA}, 0);
             group<PUpd2>({s, t}, {r}, {S_ONE, S_NOMEGA}, 0);
-            group<PDot2>({r, r0}, {}, {}, 0);
+            group<PDot2>({r, r0}, {}, {}, 0, P_C_BETA, 1);
         } else {
-            group<PClassicXR>({x, p, s, t, r0}, {x, r}, {S_ALPHA, S_OMEGA, S_NOMEGA}, 0);
+            group<PClassicXR>({x, p, s, t, r0}, {x, r}, {S_ALPHA, S_OMEGA, S_NOMEGA}, 0, P_C_BETA, 1);
         }
-        scalars(P_C_BETA, 1);
         group<PUpd3>({r, p, v}, {p}, {S_ONE, S_BETA, S_NBO}, 0);
     } else if (method_ == MBG_RBICGSTAB) {
         double *z = w(V_Z), *vh = w(V_VH), *v = w(V_V), *th = w(V_TH), *t = w(V_T);
@@ -466,38 +302,40 @@ void Solver::iteration() {
         double* s = fused ? v : w(V_S);
         double* q = fused ? t : w(V_Q);
         if (fused) {
-            spmm(vh, v, 1, r0);                                   // v = A vh ; delta = (v, r0)
+            spmm(vh, v, 1, r0, P_C_ALPHA, 1);                     // v = A vh ; delta = (v, r0) ; alpha
         } else {
             spmm(vh, v);
-            group<PDot2>({v, r0}, {}, {}, 0);
             copy(s, v);                                           // s = M^-1 v
+            group<PDot2>({v, r0}, {}, {}, 0, P_C_ALPHA, 1);
         }
-        scalars(P_C_ALPHA, 1);
         group<PUpd2>({z, s}, {th}, {S_ONE, S_NALPHA}, 0);        // th = z - alpha s
         spmm(th, t);
+        if (!fused) copy(q, t);                                   // q = M^-1 t
         if (basic) {
             group<PUpd2>({r, v}, {rt}, {S_ONE, S_NALPHA}, 0);
             group<PDot2>({t, rt}, {}, {}, 0);
             group<PDot1>({t}, {}, {}, 1);
             group<PDot2>({t, r0}, {}, {}, 2);
-            group<PDot1>({rt}, {}, {}, 3);
+            group<PDot1>({rt}, {}, {}, 3, P_R_OMEGA, 4);
         } else {
-            group<PReordG7>({r, v, t, r0}, {rt}, {S_NALPHA}, 0);
+            group<PReordG7>({r, v, t, r0}, {rt}, {S_NALPHA}, 0, P_R_OMEGA, 4);
         }
-        if (!fused) copy(q, t);                                   // q = M^-1 t
-        scalars(P_R_OMEGA, 4);
         group<PUpd2>({rt, t}, {r}, {S_ONE, S_NOMEGA}, 0);        // r = rt - omega t
         if (basic) {
             group<PUpd3>({x, vh, th}, {x}, {S_ONE, S_ALPHA, S_OMEGA}, 0);
             group<PUpd2>({th, q}, {z}, {S_ONE, S_NOMEGA}, 0);
-            group<PUpd3>({z, vh, s}, {vh}, {S_ONE, S_BETA, S_NBO}, 0);
+            group<PUpd3>({z, vh, s}, {vh}, {S_ONE, S_BETA, S_NBO}, 0, P_R_END, 0);
         } else {
-            group<PReordG12>({x, vh, th, q, s}, {x, z, vh}, {S_ALPHA, S_OMEGA, S_NOMEGA, S_BETA, S_NBO}, 0);
+            group<PReordG12>({x, vh, th, q, s}, {x, z, vh}, {S_ALPHA, S_OMEGA, S_NOMEGA, S_BETA, S_NBO}, 0,
+                             P_R_END, 0);
         }
-        scalars(P_R_END, 0);
     } else {
         double *p = w(V_P), *s = w(V_S), *wv = w(V_W), *z = w(V_Z), *t = w(V_T), *v = w(V_V);
         double *q = w(V_Q), *y = w(V_Y), *tmp = w(V_TMP);
+        // On one GPU the scalar steps ride on the dot kernels (omega needs only
+        // G1's dots, alpha/beta only G5's); with a communicator they wait for the
+        // allreduce, which overlaps the following SpMM on the side stream.
+        const bool early = can_post();
         if (basic) {
             group<PUpd3>({r, p, s}, {p}, {S_ONE, S_BETA, S_NBO}, 0);
             group<PUpd3>({wv, s, z}, {s}, {S_ONE, S_BETA, S_NBO}, 0);
@@ -506,12 +344,13 @@ void Solver::iteration() {
             group<PUpd2>({wv, z}, {y}, {S_ONE, S_NALPHA}, 0);
             group<PDot2>({q, y}, {}, {}, 0);
             group<PDot1>({y}, {}, {}, 1);
-            group<PDot1>({q}, {}, {}, 2);
+            group<PDot1>({q}, {}, {}, 2, early ? P_P_OMEGA : -1, 3);
         } else {
-            group<PPipeG1>({r, p, s, wv, z, t, v}, {p, s, z, q, y}, {S_BETA, S_NBO, S_NALPHA}, 0);
+            group<PPipeG1>({r, p, s, wv, z, t, v}, {p, s, z, q, y}, {S_BETA, S_NBO, S_NALPHA}, 0,
+                           early ? P_P_OMEGA : -1, 3);
         }
         spmm(z, v);
-        scalars(P_P_OMEGA, 3);
+        if (!early) scalars(P_P_OMEGA, 3);
         if (basic) {
             group<PUpd3>({x, p, q}, {x}, {S_ONE, S_ALPHA, S_OMEGA}, 0);
             group<PUpd2>({q, y}, {r}, {S_ONE, S_NOMEGA}, 0);
@@ -520,15 +359,16 @@ void Solver::iteration() {
             group<PDot2>({r0, r}, {}, {}, 0);
             group<PDot2>({r0, z}, {}, {}, 1);
             group<PDot2>({r0, wv}, {}, {}, 2);
-            group<PDot2>({r0, s}, {}, {}, 3);
+            group<PDot2>({r0, s}, {}, {}, 3, early ? P_P_BETA : -1, 4);
         } else if (fused) {
-            group<PPipeG45>({x, p, q, y, t, v, r0, z, s}, {x, r, wv}, {S_ALPHA, S_OMEGA, S_NOMEGA, S_OA}, 0);
+            group<PPipeG45>({x, p, q, y, t, v, r0, z, s}, {x, r, wv}, {S_ALPHA, S_OMEGA, S_NOMEGA, S_OA}, 0,
+                            early ? P_P_BETA : -1, 4);
         } else {
             group<PPipeG4>({x, p, q, y}, {x, r}, {S_ALPHA, S_OMEGA, S_NOMEGA}, 0);
-            group<PPipeG5>({y, t, v, r0, r, z, s}, {wv}, {S_NOMEGA, S_OA}, 0);
+            group<PPipeG5>({y, t, v, r0, r, z, s}, {wv}, {S_NOMEGA, S_OA}, 0, early ? P_P_BETA : -1, 4);
         }
         spmm(wv, t);
-        scalars(P_P_BETA, 4);
+        if (!early) scalars(P_P_BETA, 4);
     }
 }
 

@@ -38,10 +38,15 @@ private:
     double* w(int i) { return work_[i].p; }
     double* sc(int i);
     int64_t* slot(int i);
-    void spmm(const double* x, double* y, int epi_kind = 0, const double* aux = nullptr);
+    // post_point >= 0: run the scalar step `post_point` over `post_nd` dots
+    // after this kernel -- fused into its last block when possible.
+    void spmm(const double* x, double* y, int epi_kind = 0, const double* aux = nullptr, int post_point = -1,
+              int post_nd = 0);
     template <class P>
     void group(std::initializer_list<const double*> in, std::initializer_list<double*> out,
-               std::initializer_list<int> co, int first_slot);
+               std::initializer_list<int> co, int first_slot, int post_point = -1, int post_nd = 0);
+    struct ScalArgs scal_args(int point, int nd);
+    bool can_post() const;
     void copy(double* dst, const double* src);
     void scalars(int point, int nd);
     void setup(const double* b, double* x);
@@ -57,6 +62,7 @@ private:
     DevBuf<double> scal_, hist_;
     DevBuf<int> ctl_;
     DevBuf<int64_t> slots_;
+    DevBuf<unsigned> ticket_;
     int* ctl_host_ = nullptr;
     cudaEvent_t ev_[2] = {nullptr, nullptr};
     cudaEvent_t t0_ = nullptr, t1_ = nullptr;

@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 1 ? 3 : 2)) spmm_t
                                },
                                sh);
     }
+    if (epi.post.enabled) post_step(epi.post, reinterpret_cast<double*>(bufs));
 }
 
 // Any m: one thread per (row, column) element over an explicit row list.
