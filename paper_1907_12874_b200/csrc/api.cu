@@ -137,6 +137,8 @@ static void csr_arrays_to_device(mbg_ctx* ctx, mbg_csr* a, int64_t n, const std:
     for (int64_t i = 0; i < n; ++i) all[i] = static_cast<int32_t>(i);
     auto t = build_spmm_tiles(off32, all);
     upload(a->tiles_all, t.data(), t.size(), ctx->stream);
+    auto lr = long_rows_of(t);
+    upload(a->long_all, lr.data(), lr.size(), ctx->stream);
     MBG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
@@ -193,6 +195,9 @@ extern "C" int mbg_csr_upload_partitioned(mbg_ctx* ctx, int64_t n, const int64_t
                 auto tb = build_spmm_tiles(pl.off, pl.boundary);
                 upload(a->tiles_interior, ti.data(), ti.size(), ctx->stream);
                 upload(a->tiles_boundary, tb.data(), tb.size(), ctx->stream);
+                auto li = long_rows_of(ti), lb = long_rows_of(tb);
+                upload(a->long_interior, li.data(), li.size(), ctx->stream);
+                upload(a->long_boundary, lb.data(), lb.size(), ctx->stream);
                 upload(a->interior_rows, pl.interior.data(), pl.interior.size(), ctx->stream);
                 upload(a->boundary_rows, pl.boundary.data(), pl.boundary.size(), ctx->stream);
                 a->n_interior = static_cast<int64_t>(pl.interior.size());

@@ -53,9 +53,11 @@ static void side_to_main(mbg_ctx* ctx) {
 
 int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, const int* ctl,
                    const SpmmEpi* epi) {
-    auto tiles = [](const mbg::DevBuf<int4>& t) { return SpmmTiles{t.p, static_cast<int64_t>(t.n)}; };
+    auto tiles = [](const mbg::DevBuf<int4>& t, const mbg::DevBuf<int32_t>& l) {
+        return SpmmTiles{t.p, static_cast<int64_t>(t.n), l.p, static_cast<int64_t>(l.n)};
+    };
     if (a->peers.empty()) {
-        return launch_spmm(ctx->stream, tiles(a->tiles_all), a->n, nullptr, a->off.p, a->col.p, a->val.p, m, x,
+        return launch_spmm(ctx->stream, tiles(a->tiles_all, a->long_all), a->n, nullptr, a->off.p, a->col.p, a->val.p, m, x,
                            y, ctl, ctx->num_sms, epi);
     }
     Comm* cm = ctx->comm;
@@ -89,10 +91,10 @@ int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, 
     }
     MBG_NCCL(ncclGroupEnd());
     // interior rows overlap the exchange; boundary rows wait for the halo
-    launches += launch_spmm(ctx->stream, tiles(a->tiles_interior), a->n_interior, a->interior_rows.p, a->off.p,
+    launches += launch_spmm(ctx->stream, tiles(a->tiles_interior, a->long_interior), a->n_interior, a->interior_rows.p, a->off.p,
                             a->col.p, a->val.p, m, x, y, ctl, ctx->num_sms, epi);
     side_to_main(ctx);
-    launches += launch_spmm(ctx->stream, tiles(a->tiles_boundary), a->n_boundary, a->boundary_rows.p, a->off.p,
+    launches += launch_spmm(ctx->stream, tiles(a->tiles_boundary, a->long_boundary), a->n_boundary, a->boundary_rows.p, a->off.p,
                             a->col.p, a->val.p, m, x, y, ctl, ctx->num_sms, epi);
     return launches;
 }

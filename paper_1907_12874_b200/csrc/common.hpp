@@ -116,6 +116,7 @@ struct mbg_csr {
     int64_t n_interior = 0, n_boundary = 0;
     // SpMM tile plans (spmm.cu): all rows, interior rows, boundary rows
     mbg::DevBuf<int4> tiles_all, tiles_interior, tiles_boundary;
+    mbg::DevBuf<int32_t> long_all, long_interior, long_boundary;   // rows beyond a tile's capacity
     struct Peer {
         int rank;
         int64_t send_count, recv_count;

@@ -18,6 +18,8 @@ constexpr int SPMM_TILE_NNZ = 1920;
 struct SpmmTiles {
     const int4* tiles = nullptr;   // (r0, r1, k0, k1) per tile
     int64_t count = 0;
+    const int32_t* long_rows = nullptr;  // rows of the single-row tiles beyond SPMM_TILE_NNZ
+    int64_t nlong = 0;
 };
 // Optional fused epilogue of the SpMM y = A x (beyond-paper merge):
 //   kind 1: slot[0] += exact (y, aux)                    e.g. delta = (v, r0)
@@ -32,6 +34,7 @@ int launch_spmm(cudaStream_t st, const SpmmTiles& tl, int64_t nrows, const int32
                 const int32_t* col, const double* val, int m, const double* x, double* y, const int* ctl,
                 int num_sms, const SpmmEpi* epi = nullptr);
 std::vector<int4> build_spmm_tiles(const std::vector<int32_t>& off, const std::vector<int32_t>& rows);
+std::vector<int32_t> long_rows_of(const std::vector<int4>& tiles);
 
 // Generic statement-group interpreter (API-level execute_group).
 constexpr int GEN_MAX_VEC = 16, GEN_MAX_STMT = 16, GEN_MAX_SLOT = 8;

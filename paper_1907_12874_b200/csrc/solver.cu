@@ -15,6 +15,7 @@
 // a no-op after the solve stops.  The host only polls the control words once
 // per chunk of iterations (lagged by one chunk).
 #include <algorithm>
+#include <cstdlib>
 #include <climits>
 #include <cstdio>
 #include <map>
@@ -212,8 +213,9 @@ ScalArgs Solver::scal_args(int point, int nd) {
 
 bool Solver::can_post() const {
     // the fused scalar step needs every dot of the point locally (no pending
-    // cross-GPU allreduce) and whole warps
-    return ctx_->comm == nullptr && group_block(m_) % 32 == 0;
+    // cross-GPU allreduce) and whole warps.  MBG_NO_POST=1 disables it (A/B).
+    static const bool disabled = std::getenv("MBG_NO_POST") != nullptr;
+    return !disabled && ctx_->comm == nullptr && group_block(m_) % 32 == 0;
 }
 
 void Solver::scalars(int point, int nd) {

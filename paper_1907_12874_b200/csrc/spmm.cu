@@ -169,48 +169,65 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 1 ? 3 : 2)) spmm_t
         const int32_t* s_col = reinterpret_cast<const int32_t*>(buf + OFF_CAP * 4);
         const double* s_val = reinterpret_cast<const double*>(buf + OFF_CAP * 4 + NNZ_PAD * 4);
         const bool lng = s_off[r1 - r0a] - s_off[r0 - r0a] > SPMM_TILE_NNZ;
-        // a long row (single-row tile beyond the stage capacity) reads global memory
-        const int32_t* colp = lng ? col : s_col - k0a;
-        const double* valp = lng ? val : s_val - k0a;
-        for (int rr = tid / LPR; rr < r1 - r0; rr += RPP) {
-            const int row = r0 + rr;
-            const int k0 = s_off[row - r0a], k1 = s_off[row + 1 - r0a];
-            double a0 = 0.0, a1 = 0.0;
-            // batches of 4 nonzeros: index/value loads, then the gathers, then
-            // the ordered adds (4 gathers in flight per lane; more costs occupancy)
-            for (int k = k0; k < k1; k += 4) {
-                int j[4];
-                double va[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (k + q < k1) { j[q] = colp[k + q]; va[q] = valp[k + q]; }
-                if constexpr (VW == 2) {
-                    double2 xa[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if (k + q < k1)
-                            xa[q] = __ldg(reinterpret_cast<const double2*>(x + static_cast<int64_t>(j[q]) * M + cp));
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if (k + q < k1) {
-                            a0 = __dadd_rn(a0, __dmul_rn(va[q], xa[q].x));
-                            a1 = __dadd_rn(a1, __dmul_rn(va[q], xa[q].y));
-                        }
-                } else {
-                    double xa[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if (k + q < k1) xa[q] = __ldg(x + j[q]);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if (k + q < k1) a0 = __dadd_rn(a0, __dmul_rn(va[q], xa[q]));
+        if (lng) {
+            // a row longer than the stage capacity was multiplied beforehand by
+            // spmm_long_rows_kernel; only its fused epilogue runs here
+            if constexpr (EPI != 0) {
+                if (tid < LPR) {
+                    double a0, a1 = 0.0;
+                    if constexpr (VW == 2) {
+                        const double2 yv = *reinterpret_cast<const double2*>(y + static_cast<int64_t>(r0) * M + cp);
+                        a0 = yv.x;
+                        a1 = yv.y;
+                    } else {
+                        a0 = y[r0];
+                    }
+                    epilogue(r0, a0, a1);
                 }
             }
-            if constexpr (VW == 2)
-                *reinterpret_cast<double2*>(y + static_cast<int64_t>(row) * M + cp) = make_double2(a0, a1);
-            else
-                y[row] = a0;
-            if constexpr (EPI != 0) epilogue(row, a0, a1);
+        } else {
+            const int32_t* cs = s_col - k0a;   // index with the global k
+            const double* vs = s_val - k0a;
+            for (int rr = tid / LPR; rr < r1 - r0; rr += RPP) {
+                const int row = r0 + rr;
+                const int k0 = s_off[row - r0a], k1 = s_off[row + 1 - r0a];
+                double a0 = 0.0, a1 = 0.0;
+                // batches of 4 nonzeros: index/value loads, then the gathers, then
+                // the ordered adds (4 gathers in flight per lane; more costs occupancy)
+                for (int k = k0; k < k1; k += 4) {
+                    int j[4];
+                    double va[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (k + q < k1) { j[q] = cs[k + q]; va[q] = vs[k + q]; }
+                    if constexpr (VW == 2) {
+                        double2 xa[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (k + q < k1)
+                                xa[q] = __ldg(reinterpret_cast<const double2*>(x + static_cast<int64_t>(j[q]) * M + cp));
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (k + q < k1) {
+                                a0 = __dadd_rn(a0, __dmul_rn(va[q], xa[q].x));
+                                a1 = __dadd_rn(a1, __dmul_rn(va[q], xa[q].y));
+                            }
+                    } else {
+                        double xa[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (k + q < k1) xa[q] = __ldg(x + j[q]);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (k + q < k1) a0 = __dadd_rn(a0, __dmul_rn(va[q], xa[q]));
+                    }
+                }
+                if constexpr (VW == 2)
+                    *reinterpret_cast<double2*>(y + static_cast<int64_t>(row) * M + cp) = make_double2(a0, a1);
+                else
+                    y[row] = a0;
+                if constexpr (EPI != 0) epilogue(row, a0, a1);
+            }
         }
         __syncthreads();  // every thread is done with stage b
         if (tid == 0) issue(i + STAGES, b);
@@ -226,6 +243,24 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 1 ? 3 : 2)) spmm_t
                                sh);
     }
     if (epi.post.enabled) post_step(epi.post, reinterpret_cast<double*>(bufs));
+}
+
+// Rows longer than a tile's shared-memory capacity: one thread per (row,
+// column), nonzeros read from global memory in CSR order (rare; runs before
+// the tile kernel, which then only applies the fused epilogue to them).
+__global__ void spmm_long_rows_kernel(int nlong, const int32_t* __restrict__ rows, const int32_t* __restrict__ off,
+                                      const int32_t* __restrict__ col, const double* __restrict__ val, int m,
+                                      const double* __restrict__ x, double* __restrict__ y,
+                                      const int* __restrict__ ctl) {
+    if (ctl && ctl[0]) return;
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= static_cast<int64_t>(nlong) * m) return;
+    const int row = rows[e / m];
+    const int c = static_cast<int>(e % m);
+    double acc = 0.0;
+    for (int k = off[row]; k < off[row + 1]; ++k)
+        acc = __dadd_rn(acc, __dmul_rn(val[k], x[static_cast<int64_t>(col[k]) * m + c]));
+    y[static_cast<int64_t>(row) * m + c] = acc;
 }
 
 // Any m: one thread per (row, column) element over an explicit row list.
@@ -281,6 +316,13 @@ int launch_spmm(cudaStream_t st, const SpmmTiles& tl, int64_t nrows, const int32
                 const int32_t* col, const double* val, int m, const double* x, double* y, const int* ctl,
                 int num_sms, const SpmmEpi* epi) {
     if (nrows <= 0) return 0;
+    int launched = 0;
+    if (tl.nlong > 0 && (m == 1 || m == 2 || m == 4 || m == 8 || m == 16 || m == 32)) {
+        const int64_t tot = tl.nlong * m;
+        spmm_long_rows_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(
+            static_cast<int>(tl.nlong), tl.long_rows, off, col, val, m, x, y, ctl);
+        ++launched;
+    }
     switch (m) {
         case 1: launch_tma_epi<1>(st, tl, off, col, val, x, y, ctl, num_sms, epi); break;
         case 2: launch_tma_epi<2>(st, tl, off, col, val, x, y, ctl, num_sms, epi); break;
@@ -296,13 +338,20 @@ int launch_spmm(cudaStream_t st, const SpmmTiles& tl, int64_t nrows, const int32
         }
     }
     MBG_CUDA(cudaGetLastError());
-    return 1;
+    return launched + 1;
 }
 
 // Host: cut row segments into tiles of <= SPMM_TILE_ROWS rows and
 // <= SPMM_TILE_NNZ nonzeros; a longer row gets a tile of its own (read from
 // global memory by the kernel).  rows: sorted local row ids of one class
 // (all rows, interior or boundary); tiles never span a gap.
+std::vector<int32_t> long_rows_of(const std::vector<int4>& tiles) {
+    std::vector<int32_t> out;
+    for (const auto& t : tiles)
+        if (t.w - t.z > SPMM_TILE_NNZ) out.push_back(t.x);
+    return out;
+}
+
 std::vector<int4> build_spmm_tiles(const std::vector<int32_t>& off, const std::vector<int32_t>& rows) {
     std::vector<int4> out;
     size_t i = 0;
