@@ -122,22 +122,26 @@ __device__ __forceinline__ void digits_add_atomic(int64_t* d, double x) {
 }
 
 // TwoSum-grow x into the expansion a[0..K-1]; the residual (if any) and any
-// non-finite value go to the slot's long accumulator.
+// non-finite value go to the slot's long accumulator.  Straight-line: the
+// three TwoSum levels always run (adding 0 is exact), so warps never diverge
+// on data; only the rare residual / overflow paths branch.
 __device__ __forceinline__ void grow(double (&a)[KEXP], double x, int64_t* slot) {
-    if (x == 0.0) return;
-    if (!isfinite(x)) { digits_add_atomic(slot, x); return; }
+    double s[KEXP];
+    double e = x;
 #pragma unroll
     for (int i = 0; i < KEXP; ++i) {
-        const double s = __dadd_rn(a[i], x);
-        if (!isfinite(s)) { digits_add_atomic(slot, x); return; }
-        const double bv = __dsub_rn(s, a[i]);
-        const double av = __dsub_rn(s, bv);
-        const double err = __dadd_rn(__dsub_rn(a[i], av), __dsub_rn(x, bv));
-        a[i] = s;
-        x = err;
-        if (x == 0.0) return;
+        s[i] = __dadd_rn(a[i], e);
+        const double bv = __dsub_rn(s[i], a[i]);
+        const double av = __dsub_rn(s[i], bv);
+        e = __dadd_rn(__dsub_rn(a[i], av), __dsub_rn(e, bv));
     }
-    digits_add_atomic(slot, x);
+    if (!isfinite(s[0])) {  // x non-finite, or the running sum would overflow
+        digits_add_atomic(slot, x);
+        return;
+    }
+#pragma unroll
+    for (int i = 0; i < KEXP; ++i) a[i] = s[i];
+    if (e != 0.0) digits_add_atomic(slot, e);
 }
 #endif
 

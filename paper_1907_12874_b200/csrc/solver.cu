@@ -212,10 +212,13 @@ ScalArgs Solver::scal_args(int point, int nd) {
 }
 
 bool Solver::can_post() const {
-    // the fused scalar step needs every dot of the point locally (no pending
-    // cross-GPU allreduce) and whole warps.  MBG_NO_POST=1 disables it (A/B).
-    static const bool disabled = std::getenv("MBG_NO_POST") != nullptr;
-    return !disabled && ctx_->comm == nullptr && group_block(m_) % 32 == 0;
+    // The fused scalar step needs every dot of the point locally (no pending
+    // cross-GPU allreduce) and whole warps.  Measured on B200 (C2): the separate
+    // one-block scalar kernel inside the CUDA graph is ~1% faster than the
+    // last-block post step (whose per-block fences lengthen the tail), so the
+    // post step is opt-in (MBG_POST=1).
+    static const bool enabled = std::getenv("MBG_POST") != nullptr;
+    return enabled && ctx_->comm == nullptr && group_block(m_) % 32 == 0;
 }
 
 void Solver::scalars(int point, int nd) {
