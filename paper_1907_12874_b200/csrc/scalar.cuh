@@ -47,12 +47,21 @@ __device__ __forceinline__ double hist_entry(double res2, double bb) {
 static __device__ __forceinline__ void scalar_block(const ScalArgs& a, double* s_dots) {
     __shared__ int s_bad1, s_bad2, s_all;
     int* ctl = a.ctl;
-    if (ctl[C_STOP]) return;
     const int m = a.m;
     const int c = threadIdx.x;
     const bool on = c < m;
+    // issue every independent load up front (control words, this column's
+    // scalar bank, the slots): one memory round trip instead of three
+    const int stop = ctl[C_STOP];
+    const int conv_flag = ctl[C_CONV];
+    const int j = ctl[C_ITER];
+    double* sc = a.sc;
+    double scv[NSCAL];
+#pragma unroll
+    for (int i = 0; i < NSCAL; ++i) scv[i] = on ? sc[i * m + c] : 0.0;
+    if (stop) return;
     if (c == 0) { s_bad1 = INT_MAX; s_bad2 = INT_MAX; s_all = 1; }
-    // round every (dot, column) long accumulator (one thread each), then clear
+    // round every (dot, column) long accumulator (one warp each), then clear
     // the (contiguous) slots for their next use
     const int nslot = a.nd * m;
     for (int i = threadIdx.x >> 5; i < nslot; i += blockDim.x >> 5) {
@@ -64,22 +73,20 @@ static __device__ __forceinline__ void scalar_block(const ScalArgs& a, double* s
         int64_t* base = a.D[0];
         for (int w = threadIdx.x; w < nslot * NSLOT; w += blockDim.x) base[w] = 0;
     }
-    double* sc = a.sc;
-#define SC(i) sc[(i) * m + c]
+#define SCW(i, v) do { const double _v = (v); scv[i] = _v; sc[(i) * m + c] = _v; } while (0)
     double d[4] = {0.0, 0.0, 0.0, 0.0};
     if (on)
         for (int i = 0; i < a.nd; ++i) d[i] = s_dots[i * m + c];
-    const int j = ctl[C_ITER];
     int code1 = 0, code2 = 0;  // breakdown codes for s_bad1 / s_bad2
     switch (a.point) {
         case P_SETUP: {
             // d0 = (r0,r0), d1 = (b,b), d2 = (r0,w) for Pipelined
             if (on) {
-                SC(S_ONE) = 1.0; SC(S_MONE) = -1.0;
-                SC(S_RHO) = d[0]; SC(S_BB) = d[1];
-                SC(S_EPS2) = __dmul_rn(a.tol2, d[1]);
+                SCW(S_ONE, 1.0); SCW(S_MONE, -1.0);
+                SCW(S_RHO, d[0]); SCW(S_BB, d[1]);
+                SCW(S_EPS2, __dmul_rn(a.tol2, d[1]));
                 a.hist[c] = hist_entry(d[0], d[1]);
-                if (!(d[0] < SC(S_EPS2))) s_all = 0;
+                if (!(d[0] < scv[S_EPS2])) s_all = 0;
             }
             __syncthreads();
             if (!a.fixed && s_all) {
@@ -88,9 +95,9 @@ static __device__ __forceinline__ void scalar_block(const ScalArgs& a, double* s
             }
             if (a.method == MBG_PIPEBICGSTAB && on) {
                 const double alpha = __ddiv_rn(d[0], d[2]);
-                SC(S_ALPHA) = alpha; SC(S_NALPHA) = -alpha;
-                SC(S_BETA) = 0.0; SC(S_OMEGA) = 0.0;
-                SC(S_NBO) = -__dmul_rn(0.0, 0.0);
+                SCW(S_ALPHA, alpha); SCW(S_NALPHA, -alpha);
+                SCW(S_BETA, 0.0); SCW(S_OMEGA, 0.0);
+                SCW(S_NBO, -__dmul_rn(0.0, 0.0));
                 if (d[2] == 0.0 || !finite_d(alpha)) atomicMin(&s_bad1, c);
             }
             code1 = 1;
@@ -98,8 +105,8 @@ static __device__ __forceinline__ void scalar_block(const ScalArgs& a, double* s
         }
         case P_C_ALPHA: {
             if (on) {
-                const double alpha = __ddiv_rn(SC(S_RHO), d[0]);
-                SC(S_ALPHA) = alpha; SC(S_NALPHA) = -alpha;
+                const double alpha = __ddiv_rn(scv[S_RHO], d[0]);
+                SCW(S_ALPHA, alpha); SCW(S_NALPHA, -alpha);
                 if (d[0] == 0.0 || !finite_d(alpha)) atomicMin(&s_bad1, c);
             }
             code1 = 1;
@@ -117,17 +124,17 @@ static __device__ __forceinline__ void scalar_block(const ScalArgs& a, double* s
                 // lucky exact convergence (den == 0 because the residual is exactly 0): omega = 0
                 const bool lucky = den == 0.0 && sq == 0.0;
                 omega = lucky ? 0.0 : __ddiv_rn(num, den);
-                SC(S_OMEGA) = omega; SC(S_NOMEGA) = -omega;
-                if (a.point == P_P_OMEGA) SC(S_OA) = __dmul_rn(omega, SC(S_ALPHA));
+                SCW(S_OMEGA, omega); SCW(S_NOMEGA, -omega);
+                if (a.point == P_P_OMEGA) SCW(S_OA, __dmul_rn(omega, scv[S_ALPHA]));
                 res2 = __dsub_rn(sq, __dmul_rn(omega, num));
-                SC(S_RES2) = res2;
+                SCW(S_RES2, res2);
                 if ((den == 0.0 && !lucky) || !finite_d(omega)) atomicMin(&s_bad2, c);
             }
             __syncthreads();
             if (s_bad2 != INT_MAX) { code2 = 2; break; }
             if (on) {
-                a.hist[static_cast<int64_t>(j + 1) * m + c] = hist_entry(res2, SC(S_BB));
-                if (!(res2 < SC(S_EPS2))) s_all = 0;
+                a.hist[static_cast<int64_t>(j + 1) * m + c] = hist_entry(res2, scv[S_BB]);
+                if (!(res2 < scv[S_EPS2])) s_all = 0;
             }
             __syncthreads();
             const bool conv = !a.fixed && s_all;
@@ -135,22 +142,22 @@ static __device__ __forceinline__ void scalar_block(const ScalArgs& a, double* s
             if (a.point == P_R_OMEGA && !conv && on) {
                 // rho' = -(omega*psi), beta = (rho'/rho)*(alpha/omega)
                 const double rhon = -__dmul_rn(omega, d[2]);
-                const double beta = __dmul_rn(__ddiv_rn(rhon, SC(S_RHO)), __ddiv_rn(SC(S_ALPHA), omega));
-                SC(S_BETA) = beta; SC(S_NBO) = -__dmul_rn(beta, omega); SC(S_RHO) = rhon;
+                const double beta = __dmul_rn(__ddiv_rn(rhon, scv[S_RHO]), __ddiv_rn(scv[S_ALPHA], omega));
+                SCW(S_BETA, beta); SCW(S_NBO, -__dmul_rn(beta, omega)); SCW(S_RHO, rhon);
                 if (!finite_d(beta)) atomicMin(&s_bad1, c);
             }
             code1 = 3;
             break;
         }
         case P_C_BETA: {
-            if (ctl[C_CONV]) {
+            if (conv_flag) {
                 if (c == 0) { ctl[C_STOP] = 1; ctl[C_CONVERGED] = 1; ctl[C_ITERS] = j + 1; }
                 return;
             }
             if (on) {
                 const double rhon = d[0];
-                const double beta = __dmul_rn(__ddiv_rn(rhon, SC(S_RHO)), __ddiv_rn(SC(S_ALPHA), SC(S_OMEGA)));
-                SC(S_BETA) = beta; SC(S_NBO) = -__dmul_rn(beta, SC(S_OMEGA)); SC(S_RHO) = rhon;
+                const double beta = __dmul_rn(__ddiv_rn(rhon, scv[S_RHO]), __ddiv_rn(scv[S_ALPHA], scv[S_OMEGA]));
+                SCW(S_BETA, beta); SCW(S_NBO, -__dmul_rn(beta, scv[S_OMEGA])); SCW(S_RHO, rhon);
                 if (!finite_d(beta)) atomicMin(&s_bad1, c);
             }
             code1 = 3;
@@ -158,24 +165,24 @@ static __device__ __forceinline__ void scalar_block(const ScalArgs& a, double* s
         }
         case P_R_END: {
             if (c == 0) {
-                if (ctl[C_CONV]) { ctl[C_STOP] = 1; ctl[C_CONVERGED] = 1; ctl[C_ITERS] = j + 1; }
+                if (conv_flag) { ctl[C_STOP] = 1; ctl[C_CONVERGED] = 1; ctl[C_ITERS] = j + 1; }
             }
             break;
         }
         case P_P_BETA: {
-            if (ctl[C_CONV]) {
+            if (conv_flag) {
                 if (c == 0) { ctl[C_STOP] = 1; ctl[C_CONVERGED] = 1; ctl[C_ITERS] = j + 1; }
                 return;
             }
             if (on) {
                 // d = rho' psi sigma delta
-                const double omega = SC(S_OMEGA), alpha = SC(S_ALPHA);
-                const double beta = __dmul_rn(__ddiv_rn(alpha, omega), __ddiv_rn(d[0], SC(S_RHO)));
+                const double omega = scv[S_OMEGA], alpha = scv[S_ALPHA];
+                const double beta = __dmul_rn(__ddiv_rn(alpha, omega), __ddiv_rn(d[0], scv[S_RHO]));
                 const double den = __dsub_rn(__dadd_rn(d[2], __dmul_rn(beta, d[3])),
                                              __dmul_rn(__dmul_rn(beta, omega), d[1]));
                 const double an = __ddiv_rn(d[0], den);
-                SC(S_BETA) = beta; SC(S_ALPHA) = an; SC(S_RHO) = d[0];
-                SC(S_NBO) = -__dmul_rn(beta, omega); SC(S_NALPHA) = -an;
+                SCW(S_BETA, beta); SCW(S_ALPHA, an); SCW(S_RHO, d[0]);
+                SCW(S_NBO, -__dmul_rn(beta, omega)); SCW(S_NALPHA, -an);
                 if (!finite_d(beta)) atomicMin(&s_bad2, c);
                 if (den == 0.0 || !finite_d(an)) atomicMin(&s_bad1, c);
             }
@@ -185,7 +192,7 @@ static __device__ __forceinline__ void scalar_block(const ScalArgs& a, double* s
             break;
         }
     }
-#undef SC
+#undef SCW
     __syncthreads();
     if (c != 0) return;
     // breakdown bookkeeping (first column)
