@@ -27,11 +27,25 @@ KEYS = [
 ]
 
 
+SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
 def raw(rep):
+    """Rows of the raw page; byte metrics normalised to MB using the units row."""
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr = rows[0]
-    return [dict(zip(hdr, r)) for r in rows[2:]]
+    hdr, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        for k, u in zip(hdr, units):
+            if u in SCALE and d.get(k):
+                try:
+                    d[k] = str(float(d[k].replace(",", "")) * SCALE[u] / 1e6)
+                except ValueError:
+                    pass
+        res.append(d)
+    return res
 
 
 def launches(path):
@@ -70,8 +84,6 @@ def main():
                 v = d.get(k, "")
                 try:
                     f = float(v.replace(",", ""))
-                    if k.startswith("dram__bytes"):
-                        f /= 1.0  # ncu reports MB for these in raw csv units
                     v = f"{f:.1f}"
                 except ValueError:
                     pass

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <vector>
+#include <algorithm>
 
 #define CK(x)                                                                              \
     do {                                                                                   \
@@ -75,6 +76,55 @@ __global__ void __launch_bounds__(256, MINB) k_direct(int n, const int* __restri
             if (k + q < k1) { a0 = __dadd_rn(a0, __dmul_rn(v[q], xv[q].x)); a1 = __dadd_rn(a1, __dmul_rn(v[q], xv[q].y)); }
     }
     *(double2*)(y + (int64_t)row * M + cp) = make_double2(a0, a1);
+}
+
+__device__ __forceinline__ int ld_na_i(const int* p) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ld_na_d(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+template <int M, int B, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_direct_na(int n, const int* __restrict__ off, const int* __restrict__ col,
+                                                   const double* __restrict__ val, const double* __restrict__ x,
+                                                   double* __restrict__ y) {
+    constexpr int VW = M >= 2 ? 2 : 1;
+    constexpr int LPR = M / VW, RPB = 256 / LPR;
+    const int row = blockIdx.x * RPB + threadIdx.x / LPR;
+    const int cp = (threadIdx.x % LPR) * VW;
+    if (row >= n) return;
+    const int k0 = ld_na_i(off + row), k1 = ld_na_i(off + row + 1);
+    double a0 = 0.0, a1 = 0.0;
+    for (int k = k0; k < k1; k += B) {
+        int j[B];
+        double v[B];
+#pragma unroll
+        for (int q = 0; q < B; ++q)
+            if (k + q < k1) { j[q] = ld_na_i(col + k + q); v[q] = ld_na_d(val + k + q); }
+        if constexpr (VW == 2) {
+            double2 xv[B];
+#pragma unroll
+            for (int q = 0; q < B; ++q)
+                if (k + q < k1) xv[q] = __ldg((const double2*)(x + (int64_t)j[q] * M + cp));
+#pragma unroll
+            for (int q = 0; q < B; ++q)
+                if (k + q < k1) { a0 = __dadd_rn(a0, __dmul_rn(v[q], xv[q].x)); a1 = __dadd_rn(a1, __dmul_rn(v[q], xv[q].y)); }
+        } else {
+            double xv[B];
+#pragma unroll
+            for (int q = 0; q < B; ++q)
+                if (k + q < k1) xv[q] = __ldg(x + j[q]);
+#pragma unroll
+            for (int q = 0; q < B; ++q)
+                if (k + q < k1) a0 = __dadd_rn(a0, __dmul_rn(v[q], xv[q]));
+        }
+    }
+    if constexpr (VW == 2) *(double2*)(y + (int64_t)row * M + cp) = make_double2(a0, a1);
+    else y[row] = a0;
 }
 
 // ---------------------------------------------------------------- V4: warp-cooperative coalesced CSR loads + shuffles
@@ -279,22 +329,47 @@ void run_tma(Ctx& c, const char* name) {
     CK(cudaFree(dt));
 }
 
+static int g_kind = 0;  // 0 conv-diff 7pt, 1 27pt, 2 banded random (n = g^3)
+
 template <int M>
 int run_all(int g) {
     const int n = g * g * g, plane = g * g;
     std::vector<int> off(n + 1 + 8), col;
     std::vector<double> val;
     off[0] = 0;
+    uint64_t st = 12345;
+    auto rnd = [&]() { st = st * 6364136223846793005ull + 1442695040888963407ull; return st >> 33; };
     for (int r = 0; r < n; ++r) {
         int x = r % g, y = (r / g) % g, z = r / plane;
         auto put = [&](int c, double v) { col.push_back(c); val.push_back(v); };
-        if (z > 0) put(r - plane, -1.0);
-        if (y > 0) put(r - g, -1.0);
-        if (x > 0) put(r - 1, -1.3);
-        put(r, 6.0);
-        if (x < g - 1) put(r + 1, -0.7);
-        if (y < g - 1) put(r + g, -1.0);
-        if (z < g - 1) put(r + plane, -1.0);
+        if (g_kind == 0) {
+            if (z > 0) put(r - plane, -1.0);
+            if (y > 0) put(r - g, -1.0);
+            if (x > 0) put(r - 1, -1.3);
+            put(r, 6.0);
+            if (x < g - 1) put(r + 1, -0.7);
+            if (y < g - 1) put(r + g, -1.0);
+            if (z < g - 1) put(r + plane, -1.0);
+        } else if (g_kind == 1) {
+            for (int dz = -1; dz <= 1; ++dz)
+                for (int dy = -1; dy <= 1; ++dy)
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        if (z + dz < 0 || z + dz >= g || y + dy < 0 || y + dy >= g || x + dx < 0 || x + dx >= g) continue;
+                        put(r + dz * plane + dy * g + dx, (dx | dy | dz) ? -1.0 : 26.0);
+                    }
+        } else {
+            const int k = 16 + rnd() % 17;
+            std::vector<int> cs{r};
+            const int lo = std::max(0, r - 65536), hi = std::min(n - 1, r + 65536);
+            while ((int)cs.size() < k) {
+                int c = lo + (int)(rnd() % (uint64_t)(hi - lo + 1));
+                bool dup = false;
+                for (int q : cs) dup |= q == c;
+                if (!dup) cs.push_back(c);
+            }
+            std::sort(cs.begin(), cs.end());
+            for (int c : cs) put(c, c == r ? 20.0 : -0.5);
+        }
         off[r + 1] = (int)col.size();
     }
     for (int i = n + 1; i < n + 9; ++i) off[i] = off[n];
@@ -346,23 +421,26 @@ int run_all(int g) {
     timeit("ref thread/(row,col)", c, [&] {
         k_ref<<<(unsigned)(((int64_t)n * M + 255) / 256), 256>>>(n, c.off, c.col, c.val, M, c.x, c.y);
     });
-    if constexpr (M >= 2) {
-        timeit("direct B4 minb4", c, [&] { k_direct<M, 4, 4><<<(n + 256 / (M / 2) - 1) / (256 / (M / 2)), 256>>>(n, c.off, c.col, c.val, c.x, c.y); });
-    }
-    run_tma<M, 256, 2560, 2, 1, 4, 1>(c, "tma 256r 2st B4");
-    run_tma<M, 192, 1920, 2, 1, 4, 4>(c, "tma 192r 2st B4 minb4");
-    run_tma<M, 160, 1600, 2, 1, 4, 5>(c, "tma 160r 2st B4 minb5");
-    run_tma<M, 128, 1280, 2, 1, 4, 6>(c, "tma 128r 2st B4 minb6");
-    run_tma<M, 192, 1920, 2, 1, 8, 4>(c, "tma 192r 2st B8 minb4");
-    run_tma<M, 192, 1920, 2, 1, 6, 4>(c, "tma 192r 2st B6 minb4");
-    run_tma<M, 96, 960, 3, 1, 4, 5>(c, "tma 96r 3st B4 minb5");
-    run_tma<M, 128, 1280, 3, 1, 4, 4>(c, "tma 128r 3st B4 minb4");
+    timeit("direct-noalloc B4 minb4", c, [&] {
+        constexpr int RPB = 256 / (M >= 2 ? M / 2 : 1);
+        k_direct_na<M, 4, 4><<<(n + RPB - 1) / RPB, 256>>>(n, c.off, c.col, c.val, c.x, c.y);
+    });
+    timeit("direct-noalloc B8 minb2", c, [&] {
+        constexpr int RPB = 256 / (M >= 2 ? M / 2 : 1);
+        k_direct_na<M, 8, 2><<<(n + RPB - 1) / RPB, 256>>>(n, c.off, c.col, c.val, c.x, c.y);
+    });
+    run_tma<M, 192, 1920, 2, 1, 4, 4>(c, "tma 192r/1920 2st B4 minb4");
+    run_tma<M, 96, 960, 2, 1, 4, 4>(c, "tma 96r/960 2st B4 minb4");
+    run_tma<M, 192, 960, 2, 1, 4, 4>(c, "tma 192r/960 2st B4 minb4");
+    run_tma<M, 64, 640, 2, 1, 4, 4>(c, "tma 64r/640 2st B4 minb4");
+    run_tma<M, 192, 1920, 2, 1, 4, 3>(c, "tma 192r/1920 2st B4 minb3");
     return 0;
 }
 
 int main(int argc, char** argv) {
     const int g = argc > 1 ? atoi(argv[1]) : 128;
     const int m = argc > 2 ? atoi(argv[2]) : 8;
+    g_kind = argc > 3 ? atoi(argv[3]) : 0;
     if (m == 1) return run_all<1>(g);
     if (m == 8) return run_all<8>(g);
     if (m == 32) return run_all<32>(g);
