@@ -3,6 +3,7 @@
 // maps to MBG_ERR_INVALID with the reference's message text.
 #include <algorithm>
 #include <climits>
+#include <thread>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -97,6 +98,8 @@ extern "C" int mbg_ctx_destroy(mbg_ctx* ctx) {
         ctx->scratch_f64.release();
         ctx->scratch_ctl.release();
         ctx->pool.clear();
+        if (ctx->ctl_host) cudaFreeHost(ctx->ctl_host);
+        if (ctx->stage) cudaFreeHost(ctx->stage);
         cudaStreamDestroy(ctx->stream);
         cudaStreamDestroy(ctx->side);
         delete ctx;
@@ -485,6 +488,55 @@ extern "C" int mbg_solve(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* b, mbg_mv
     });
 }
 
+// Host <-> device copies of user (pageable) buffers: a multi-threaded memcpy
+// into a context-owned pinned staging buffer, then one DMA.  Pageable
+// cudaMemcpy runs at a few GB/s; this reaches PCIe rates.
+static void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+    const size_t per = 8u << 20;
+    unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    nt = static_cast<unsigned>(std::min<size_t>(nt, (bytes + per - 1) / per));
+    if (nt <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> th;
+    const size_t chunk = (bytes + nt - 1) / nt;
+    for (unsigned t = 0; t < nt; ++t) {
+        const size_t b = std::min(bytes, t * chunk), e = std::min(bytes, b + chunk);
+        if (b < e)
+            th.emplace_back([=] {
+                std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, e - b);
+            });
+    }
+    for (auto& x : th) x.join();
+}
+
+static unsigned char* stage_buffer(mbg_ctx* ctx, size_t bytes) {
+    if (ctx->stage_bytes < bytes) {
+        if (ctx->stage) cudaFreeHost(ctx->stage);
+        ctx->stage = nullptr;
+        ctx->stage_bytes = 0;
+        MBG_CUDA(cudaMallocHost(&ctx->stage, bytes));
+        ctx->stage_bytes = bytes;
+    }
+    return ctx->stage;
+}
+
+static void upload_host(mbg_ctx* ctx, double* dev, const double* host, size_t count) {
+    unsigned char* st = stage_buffer(ctx, count * sizeof(double));
+    MBG_CUDA(cudaStreamSynchronize(ctx->stream));   // staging buffer free
+    parallel_memcpy(st, host, count * sizeof(double));
+    MBG_CUDA(cudaMemcpyAsync(dev, st, count * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+static void download_host(mbg_ctx* ctx, double* host, const double* dev, size_t count) {
+    unsigned char* st = stage_buffer(ctx, count * sizeof(double));
+    MBG_CUDA(cudaMemcpyAsync(st, dev, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+    parallel_memcpy(host, st, count * sizeof(double));
+}
+
 extern "C" int mbg_solve_host(mbg_ctx* ctx, const mbg_csr* a, int m, const double* b_host, double* x_host,
                               int method, int formulation, double tol, int fixed, int max_iters, double* hist,
                               mbg_report* report) {
@@ -492,16 +544,22 @@ extern "C" int mbg_solve_host(mbg_ctx* ctx, const mbg_csr* a, int m, const doubl
         check_solve_args(ctx, a, m, tol, fixed, max_iters);
         if (!b_host || !x_host) throw Invalid("solve: null host buffer");
         const size_t cnt = static_cast<size_t>(a->n) * m;
-        DevBuf<double> db(cnt), dx(cnt);
-        MBG_CUDA(cudaMemcpyAsync(db.p, b_host, cnt * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        MBG_CUDA(cudaMemcpyAsync(dx.p, x_host, cnt * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        DevBuf<double> db = pool_take(ctx, cnt), dx = pool_take(ctx, cnt);
+        struct Give {
+            mbg_ctx* c;
+            DevBuf<double>& a;
+            DevBuf<double>& b;
+            ~Give() { pool_give(c, std::move(a)); pool_give(c, std::move(b)); }
+        } give{ctx, db, dx};
+        upload_host(ctx, db.p, b_host, cnt);
+        upload_host(ctx, dx.p, x_host, cnt);
         try {
             do_solve(ctx, a, m, db.p, dx.p, method, formulation, tol, fixed, max_iters, hist, report);
         } catch (const Breakdown&) {
-            MBG_CUDA(cudaMemcpy(x_host, dx.p, cnt * sizeof(double), cudaMemcpyDeviceToHost));
+            download_host(ctx, x_host, dx.p, cnt);
             throw;
         }
-        MBG_CUDA(cudaMemcpy(x_host, dx.p, cnt * sizeof(double), cudaMemcpyDeviceToHost));
+        download_host(ctx, x_host, dx.p, cnt);
     });
 }
 

@@ -78,6 +78,11 @@ struct mbg_ctx {
     int64_t launches = 0;            // kernels launched by this context
     // pool of large work vectors reused across solves (no cudaMalloc per solve)
     std::vector<mbg::DevBuf<double>> pool;
+    // pinned host memory reused across calls: control-word snapshots and the
+    // staging buffer of the host-buffer entry points
+    int* ctl_host = nullptr;        // 64 ints
+    unsigned char* stage = nullptr;
+    size_t stage_bytes = 0;
 };
 
 namespace mbg {

@@ -69,7 +69,8 @@ Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulatio
     MBG_CUDA(cudaMemsetAsync(ticket_.p, 0, sizeof(unsigned), ctx->stream));
     MBG_CUDA(cudaMemsetAsync(slots_.p, 0, slots_.n * sizeof(int64_t), ctx->stream));
     MBG_CUDA(cudaMemsetAsync(ctl_.p, 0, ctl_.n * sizeof(int), ctx->stream));
-    MBG_CUDA(cudaMallocHost(&ctl_host_, 2 * NCTL * sizeof(int)));
+    if (!ctx->ctl_host) MBG_CUDA(cudaMallocHost(&ctx->ctl_host, 64 * sizeof(int)));
+    ctl_host_ = ctx->ctl_host;
     for (auto& e : ev_) MBG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     MBG_CUDA(cudaEventCreate(&t0_));
     MBG_CUDA(cudaEventCreate(&t1_));
@@ -79,7 +80,6 @@ Solver::~Solver() {
     cudaStreamSynchronize(ctx_->stream);
     for (auto& w : work_) pool_give(ctx_, std::move(w));
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
-    if (ctl_host_) cudaFreeHost(ctl_host_);
     for (auto& e : ev_) if (e) cudaEventDestroy(e);
     if (t0_) cudaEventDestroy(t0_);
     if (t1_) cudaEventDestroy(t1_);
