@@ -65,6 +65,10 @@ int mbg_ctx_synchronize(mbg_ctx* ctx);
  * and broadcast by the caller (e.g. torch.distributed). */
 int mbg_comm_unique_id(unsigned char out_id[128]);
 int mbg_ctx_init_comm(mbg_ctx* ctx, int rank, int world, const unsigned char nccl_id[128]);
+/* Validation only: link `world` contexts on ONE device into an emulated
+ * communicator (device copies + a sum kernel instead of NCCL, host barriers
+ * between rank threads).  Drive each rank from its own host thread. */
+int mbg_local_group_create(mbg_ctx** ctxs, int world);
 
 /* ---- CSR matrix ----------------------------------------------------------
  * Square CSR, offsets int64[n+1], cols int32[nnz] strictly increasing per

@@ -167,6 +167,12 @@ class Context:
         return v
 
 
+def local_group(ctxs: Sequence["Context"]) -> None:
+    """Validation only: emulate a len(ctxs)-rank communicator on one GPU."""
+    arr = (C.c_void_p * len(ctxs))(*[c.h for c in ctxs])
+    check(lib().mbg_local_group_create(arr, len(ctxs)))
+
+
 def comm_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     check(lib().mbg_comm_unique_id(buf))

@@ -79,6 +79,7 @@ def lib() -> C.CDLL:
         "mbg_ctx_synchronize": (i32, [vp]),
         "mbg_comm_unique_id": (i32, [C.c_char_p]),
         "mbg_ctx_init_comm": (i32, [vp, i32, i32, C.c_char_p]),
+        "mbg_local_group_create": (i32, [vp, i32]),
         "mbg_csr_validate": (i32, [i64, vp, vp, i64]),
         "mbg_csr_upload": (i32, [vp, i64, vp, vp, vp, pp]),
         "mbg_csr_upload_partitioned": (i32, [vp, i64, vp, vp, vp, i32, vp, i32, pp]),

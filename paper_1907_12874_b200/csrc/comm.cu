@@ -9,7 +9,11 @@
 // dot allreduce).
 #include <nccl.h>
 
+#include <chrono>
+#include <condition_variable>
 #include <cstring>
+#include <memory>
+#include <mutex>
 
 #include "comm.hpp"
 #include "kernels.hpp"
@@ -24,13 +28,56 @@ namespace mbg {
                                      " at " __FILE__ ":" + std::to_string(__LINE__));          \
     } while (0)
 
+// Single-GPU emulation of a multi-rank communicator (validation only): P
+// contexts on one device, one host thread per rank.  Collectives do the same
+// data movement as the NCCL path with device copies / a sum kernel ordered by
+// cross-stream events; host barriers only publish pointers and events, no
+// kernel ever waits on another (B200_PROFILING.md).
+struct LocalGroup {
+    int P = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    long generation = 0;
+    std::vector<const void*> ptr;          // published buffer per rank
+    std::vector<cudaEvent_t> ev;           // published event per rank
+    std::vector<std::vector<int64_t>> seg; // halo: seg[q][r] = offset (rows) of q's segment for r
+    std::vector<cudaEvent_t> consumed;     // halo: rank r finished copying from its peers
+    explicit LocalGroup(int p) : P(p), ptr(p), ev(p), seg(p), consumed(p, nullptr) {}
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const long g = generation;
+        if (++arrived == P) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+            return;
+        }
+        if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return generation != g; }))
+            throw std::runtime_error("local communicator: barrier timeout (a rank failed)");
+    }
+};
+
 struct Comm {
     ncclComm_t comm = nullptr;
     int rank = 0, world = 1;
     cudaEvent_t ev_main = nullptr, ev_side = nullptr;
     DevBuf<double> sendbuf;
     DevBuf<int> one;
+    // local (single-GPU) emulation
+    std::shared_ptr<LocalGroup> local;
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_consumed = nullptr;
+    DevBuf<int64_t> tmp;
 };
+
+__global__ void local_sum_kernel(const int64_t* const* srcs, int P, int64_t count, int64_t* dst) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int64_t s = 0;
+        for (int q = 0; q < P; ++q) s += srcs[q][i];
+        dst[i] = s;
+    }
+}
 
 __global__ void halo_pack_kernel(const double* __restrict__ x, const int32_t* __restrict__ rows, int64_t count,
                                  int m, double* __restrict__ out) {
@@ -78,6 +125,40 @@ int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, 
         }
         so += p.send_count;
     }
+    if (cm->local) {
+        LocalGroup& g = *cm->local;
+        // my send segments, by destination rank
+        std::vector<int64_t> seg(g.P, -1);
+        int64_t o = 0;
+        for (const auto& p : a->peers) {
+            seg[p.rank] = o;
+            o += p.send_count;
+        }
+        MBG_CUDA(cudaEventRecord(cm->ev_a, ctx->side));
+        {
+            std::lock_guard<std::mutex> lk(g.mu);
+            g.ptr[cm->rank] = cm->sendbuf.p;
+            g.ev[cm->rank] = cm->ev_a;
+            g.seg[cm->rank] = seg;
+        }
+        g.barrier();
+        for (const auto& p : a->peers) {
+            if (!p.recv_count) continue;
+            MBG_CUDA(cudaStreamWaitEvent(ctx->side, g.ev[p.rank], 0));
+            const double* src = static_cast<const double*>(g.ptr[p.rank]) + g.seg[p.rank][cm->rank] * m;
+            MBG_CUDA(cudaMemcpyAsync(x + (a->n + p.recv_offset) * m, src, static_cast<size_t>(p.recv_count) * m * 8,
+                                     cudaMemcpyDeviceToDevice, ctx->side));
+        }
+        MBG_CUDA(cudaEventRecord(cm->ev_consumed, ctx->side));
+        {
+            std::lock_guard<std::mutex> lk(g.mu);
+            g.consumed[cm->rank] = cm->ev_consumed;
+        }
+        g.barrier();
+        // my send buffer may be repacked only after every peer copied from it
+        for (const auto& p : a->peers) MBG_CUDA(cudaStreamWaitEvent(ctx->side, g.consumed[p.rank], 0));
+        g.barrier();
+    } else {
     MBG_NCCL(ncclGroupStart());
     so = 0;
     for (const auto& p : a->peers) {
@@ -90,6 +171,7 @@ int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, 
         so += p.send_count;
     }
     MBG_NCCL(ncclGroupEnd());
+    }
     // interior rows overlap the exchange; boundary rows wait for the halo
     launches += launch_spmm(ctx->stream, tiles(a->tiles_interior, a->long_interior), a->n_interior, a->interior_rows.p, a->off.p,
                             a->col.p, a->val.p, m, x, y, ctl, ctx->num_sms, epi);
@@ -104,22 +186,63 @@ void comm_allreduce_i64(mbg_ctx* ctx, int64_t* buf, size_t count, cudaStream_t s
     if (!cm || cm->world == 1) return;
     (void)st;
     main_to_side(ctx);
-    MBG_NCCL(ncclAllReduce(buf, buf, count, ncclInt64, ncclSum, cm->comm, ctx->side));
+    if (cm->local) {
+        LocalGroup& g = *cm->local;
+        cm->tmp.ensure(count);
+        MBG_CUDA(cudaEventRecord(cm->ev_a, ctx->side));
+        {
+            std::lock_guard<std::mutex> lk(g.mu);
+            g.ptr[cm->rank] = buf;
+            g.ev[cm->rank] = cm->ev_a;
+        }
+        g.barrier();
+        std::vector<const int64_t*> srcs(g.P);
+        for (int q = 0; q < g.P; ++q) {
+            MBG_CUDA(cudaStreamWaitEvent(ctx->side, g.ev[q], 0));
+            srcs[q] = static_cast<const int64_t*>(g.ptr[q]);
+        }
+        DevBuf<const int64_t*> dsrc(g.P);
+        MBG_CUDA(cudaMemcpyAsync(dsrc.p, srcs.data(), g.P * sizeof(void*), cudaMemcpyHostToDevice, ctx->side));
+        local_sum_kernel<<<64, 256, 0, ctx->side>>>(dsrc.p, g.P, static_cast<int64_t>(count), cm->tmp.p);
+        MBG_CUDA(cudaGetLastError());
+        MBG_CUDA(cudaEventRecord(cm->ev_b, ctx->side));
+        {
+            std::lock_guard<std::mutex> lk(g.mu);
+            g.ev[cm->rank] = cm->ev_b;
+        }
+        g.barrier();
+        for (int q = 0; q < g.P; ++q) MBG_CUDA(cudaStreamWaitEvent(ctx->side, g.ev[q], 0));
+        MBG_CUDA(cudaMemcpyAsync(buf, cm->tmp.p, count * sizeof(int64_t), cudaMemcpyDeviceToDevice, ctx->side));
+        MBG_CUDA(cudaStreamSynchronize(ctx->side));   // dsrc / tmp lifetime; validation path only
+        g.barrier();
+    } else {
+        MBG_NCCL(ncclAllReduce(buf, buf, count, ncclInt64, ncclSum, cm->comm, ctx->side));
+    }
     side_to_main(ctx);
 }
 
 void comm_barrier(mbg_ctx* ctx) {
     Comm* cm = ctx->comm;
     if (!cm) return;
+    if (cm->local) {
+        MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+        cm->local->barrier();
+        return;
+    }
     cm->one.ensure(1);
     MBG_NCCL(ncclAllReduce(cm->one.p, cm->one.p, 1, ncclInt32, ncclSum, cm->comm, ctx->side));
     MBG_CUDA(cudaStreamSynchronize(ctx->side));
 }
 
+bool comm_is_local(const mbg_ctx* ctx) { return ctx->comm && ctx->comm->local; }
+
 void comm_destroy(mbg_ctx* ctx) {
     if (!ctx->comm) return;
     Comm* cm = ctx->comm;
     if (cm->comm) ncclCommDestroy(cm->comm);
+    if (cm->ev_a) cudaEventDestroy(cm->ev_a);
+    if (cm->ev_b) cudaEventDestroy(cm->ev_b);
+    if (cm->ev_consumed) cudaEventDestroy(cm->ev_consumed);
     if (cm->ev_main) cudaEventDestroy(cm->ev_main);
     if (cm->ev_side) cudaEventDestroy(cm->ev_side);
     delete cm;
@@ -160,6 +283,34 @@ extern "C" int mbg_ctx_init_comm(mbg_ctx* ctx, int rank, int world, const unsign
         MBG_CUDA(cudaEventCreateWithFlags(&cm->ev_main, cudaEventDisableTiming));
         MBG_CUDA(cudaEventCreateWithFlags(&cm->ev_side, cudaEventDisableTiming));
         ctx->comm = cm;
+        return MBG_OK;
+    } catch (const mbg::Invalid& e) {
+        mbg::set_error(e.what());
+        return MBG_ERR_INVALID;
+    } catch (const std::exception& e) {
+        mbg::set_error(e.what());
+        return MBG_ERR_RUNTIME;
+    }
+}
+
+// Link `world` contexts on one device into an emulated communicator (tests).
+extern "C" int mbg_local_group_create(mbg_ctx** ctxs, int world) {
+    try {
+        if (!ctxs || world < 1) throw mbg::Invalid("local group: bad arguments");
+        auto grp = std::make_shared<mbg::LocalGroup>(world);
+        for (int r = 0; r < world; ++r) {
+            mbg_ctx* ctx = ctxs[r];
+            if (!ctx) throw mbg::Invalid("local group: null context");
+            MBG_CUDA(cudaSetDevice(ctx->device));
+            mbg::comm_destroy(ctx);
+            auto* cm = new mbg::Comm();
+            cm->rank = r;
+            cm->world = world;
+            cm->local = grp;
+            for (cudaEvent_t* e : {&cm->ev_main, &cm->ev_side, &cm->ev_a, &cm->ev_b, &cm->ev_consumed})
+                MBG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+            ctx->comm = cm;
+        }
         return MBG_OK;
     } catch (const mbg::Invalid& e) {
         mbg::set_error(e.what());

@@ -22,6 +22,7 @@ int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, 
 void comm_allreduce_i64(mbg_ctx* ctx, int64_t* buf, size_t count, cudaStream_t st);
 void comm_barrier(mbg_ctx* ctx);
 void comm_destroy(mbg_ctx* ctx);
+bool comm_is_local(const mbg_ctx* ctx);   // single-GPU emulation (no graph capture)
 
 // Host-side partition / halo plan (plan.cpp).  Rows [begin[p], begin[p+1])
 // belong to part p.  Local numbering: owned rows 0..n_own-1, then halo rows

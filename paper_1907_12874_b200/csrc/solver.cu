@@ -378,7 +378,7 @@ void Solver::iteration() {
 }
 
 void Solver::run(const double* b, double* x, bool use_graph, int chunk) {
-    if (profile_) use_graph = false;
+    if (profile_ || comm_is_local(ctx_)) use_graph = false;
     // S_ONE / S_MONE must exist before setup's first group
     std::vector<double> init(static_cast<size_t>(2) * m_);
     for (int c = 0; c < m_; ++c) { init[c] = 1.0; init[m_ + c] = -1.0; }
