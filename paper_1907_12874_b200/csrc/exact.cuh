@@ -121,27 +121,35 @@ __device__ __forceinline__ void digits_add_atomic(int64_t* d, double x) {
     if (s2) atomicAdd(u + c.j + 2, s2);
 }
 
-// TwoSum-grow x into the expansion a[0..K-1]; the residual (if any) and any
-// non-finite value go to the slot's long accumulator.  Straight-line: the
-// three TwoSum levels always run (adding 0 is exact), so warps never diverge
-// on data; only the rare residual / overflow paths branch.
+// TwoSum-grow x into the expansion a[0..2]; the residual (if any) and any
+// non-finite value go to the slot's long accumulator.
+//
+// Levels 1 and 2 always run (adding 0 is exact, so warps never diverge on
+// data).  Level 3 runs only when level 2 leaves an error: for products of a
+// normal dynamic range the bits of a thread's partial sum fit in 106 bits, so
+// the second-level error is almost always exactly zero and the third TwoSum
+// (and the atomic deposit after it) is a rarely taken branch.
 __device__ __forceinline__ void grow(double (&a)[KEXP], double x, int64_t* slot) {
-    double s[KEXP];
-    double e = x;
-#pragma unroll
-    for (int i = 0; i < KEXP; ++i) {
-        s[i] = __dadd_rn(a[i], e);
-        const double bv = __dsub_rn(s[i], a[i]);
-        const double av = __dsub_rn(s[i], bv);
-        e = __dadd_rn(__dsub_rn(a[i], av), __dsub_rn(e, bv));
-    }
-    if (!isfinite(s[0])) {  // x non-finite, or the running sum would overflow
+    static_assert(KEXP == 3, "grow is written for a 3-term expansion");
+    const double s0 = __dadd_rn(a[0], x);
+    if (!isfinite(s0)) {  // x non-finite, or the running sum would overflow
         digits_add_atomic(slot, x);
         return;
     }
-#pragma unroll
-    for (int i = 0; i < KEXP; ++i) a[i] = s[i];
-    if (e != 0.0) digits_add_atomic(slot, e);
+    const double b0 = __dsub_rn(s0, a[0]);
+    const double e0 = __dadd_rn(__dsub_rn(a[0], __dsub_rn(s0, b0)), __dsub_rn(x, b0));
+    const double s1 = __dadd_rn(a[1], e0);
+    const double b1 = __dsub_rn(s1, a[1]);
+    const double e1 = __dadd_rn(__dsub_rn(a[1], __dsub_rn(s1, b1)), __dsub_rn(e0, b1));
+    a[0] = s0;
+    a[1] = s1;
+    if (e1 != 0.0) {
+        const double s2 = __dadd_rn(a[2], e1);
+        const double b2 = __dsub_rn(s2, a[2]);
+        const double e2 = __dadd_rn(__dsub_rn(a[2], __dsub_rn(s2, b2)), __dsub_rn(e1, b2));
+        a[2] = s2;
+        if (e2 != 0.0) digits_add_atomic(slot, e2);
+    }
 }
 #endif
 

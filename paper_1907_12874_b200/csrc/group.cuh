@@ -88,6 +88,30 @@ struct PUpd3 {
     }
 };
 
+// Classical, fused formulation: Alg. 2 line 8 with theta = (s,s) computed where
+// s is produced (it is reduced at the same point as phi and psi, so the
+// message layout and the traffic are unchanged; the fp64 work of the dots is
+// spread over two memory-bound passes instead of one compute-bound one).
+//   s = 1*r + (-alpha)*v ; theta = (s, s)
+struct PUpd2Sq {
+    static constexpr const char* NAME = "upd2_sq";
+    static constexpr int NIN = 2, NOUT = 1, NCO = 2, NDOT = 1;
+    __device__ static void run(const double* in, double* out, double* prod, const double* co) {
+        const double s = fmadd_rn(fmadd_rn(0.0, co[0], in[0]), co[1], in[1]);
+        out[0] = s;
+        prod[0] = __dmul_rn(s, s);
+    }
+};
+// ... and phi = (t,s), psi = (t,t) in the pass after t = A s
+struct PClassicPhiPsi {
+    static constexpr const char* NAME = "classic_phipsi";
+    static constexpr int NIN = 2, NOUT = 0, NCO = 0, NDOT = 2;   // in: t s
+    __device__ static void run(const double* in, double*, double* prod, const double*) {
+        prod[0] = __dmul_rn(in[0], in[1]);
+        prod[1] = __dmul_rn(in[0], in[0]);
+    }
+};
+
 // Classical, Alg. 2 line 9: phi=(t,s), psi=(t,t), theta=(s,s)
 struct PClassicOmega {
     static constexpr int UNROLL = 1;  // register budget: 3+ dot expansions per column pair

@@ -155,7 +155,7 @@ void Solver::spmm(const double* x, double* y, int epi_kind, const double* aux, i
 
 template <class P>
 void Solver::group(std::initializer_list<const double*> in, std::initializer_list<double*> out,
-                   std::initializer_list<int> co, int first_slot, int post_point, int post_nd) {
+                   std::initializer_list<int> co, int first_slot, int post_point, int post_nd, int reduce) {
     GroupArgs g{};
     g.len = len_;
     g.m = m_;
@@ -180,10 +180,13 @@ void Solver::group(std::initializer_list<const double*> in, std::initializer_lis
     launches_++;
     if (P::NDOT > 0) {
         // multi-GPU: one fused allreduce of all dots of this point (int64 limbs)
-        if (ctx_->comm) {
-            comm_allreduce_i64(ctx_, slot(first_slot), static_cast<size_t>(P::NDOT) * m_ * NSLOT, ctx_->stream);
+        // reduce < 0: this point's own slots; 0: deferred to a later group of
+        // the same reduction point; > 0: that many slots from first_slot
+        const int nred = reduce < 0 ? P::NDOT : reduce;
+        if (ctx_->comm && nred > 0) {
+            comm_allreduce_i64(ctx_, slot(first_slot), static_cast<size_t>(nred) * m_ * NSLOT, ctx_->stream);
         }
-        reductions_++;
+        if (nred > 0) reductions_++;
     }
     if (post_point >= 0 && !post) scalars(post_point, post_nd);
 }
@@ -273,16 +276,14 @@ void Solver::iteration() {
     double *r = w(V_R), *r0 = w(V_R0), *x = x_;
     if (method_ == MBG_BICGSTAB) {
         double *p = w(V_P), *v = w(V_V), *s = w(V_S), *t = w(V_T);
+        spmm(p, v);
+        group<PDot2>({v, r0}, {}, {}, 0, P_C_ALPHA, 1);
         if (fused) {
-            spmm(p, v, 1, r0, P_C_ALPHA, 1);                      // v = A p ; delta = (v, r0) ; alpha
+            group<PUpd2Sq>({r, v}, {s}, {S_ONE, S_NALPHA}, 2, -1, 0, 0);   // s ; theta = (s,s) -> slot 2
+            spmm(s, t);
+            group<PClassicPhiPsi>({t, s}, {}, {}, 0, P_C_OMEGA, 3, 3);     // phi psi -> slots 0,1 ; omega
         } else {
-            spmm(p, v);
-            group<PDot2>({v, r0}, {}, {}, 0, P_C_ALPHA, 1);
-        }
-        group<PUpd2>({r, v}, {s}, {S_ONE, S_NALPHA}, 0);
-        if (fused) {
-            spmm(s, t, 2, nullptr, P_C_OMEGA, 3);                 // t = A s ; phi psi theta ; omega
-        } else {
+            group<PUpd2>({r, v}, {s}, {S_ONE, S_NALPHA}, 0);
             spmm(s, t);
             if (basic) {
                 group<PDot2>({t, s}, {}, {}, 0);

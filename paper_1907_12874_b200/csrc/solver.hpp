@@ -44,7 +44,8 @@ private:
               int post_nd = 0);
     template <class P>
     void group(std::initializer_list<const double*> in, std::initializer_list<double*> out,
-               std::initializer_list<int> co, int first_slot, int post_point = -1, int post_nd = 0);
+               std::initializer_list<int> co, int first_slot, int post_point = -1, int post_nd = 0,
+               int reduce = -1);
     struct ScalArgs scal_args(int point, int nd);
     bool can_post() const;
     void copy(double* dst, const double* src);
