@@ -19,6 +19,8 @@
 
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "exact.cuh"
 #include "scalar.cuh"
 
@@ -233,6 +235,13 @@ struct PPipeG45 {
     }
 };
 
+// Register-pipelined loads for dot-heavy, byte-light programs (the dots'
+// TwoSum chains would otherwise serialise with the memory latency).
+template <class P>
+struct prefetch_of {
+    static constexpr bool value = P::NDOT >= 1 && P::NIN + P::NOUT <= 3;
+};
+
 // Unroll (pairs of packets per trip) unless a program declares UNROLL = 1.
 template <class P, class = void>
 struct unroll_of { static constexpr int value = 2; };
@@ -344,84 +353,66 @@ __global__ void __launch_bounds__(256, 2) group_kernel(GroupArgs a) {
 
     const int64_t npk = a.len / VEC;  // packets of VEC elements
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     constexpr int UNR = unroll_of<P>::value;
-    if constexpr (VEC == 2) {
-        for (; UNR == 2 && q + stride < npk; q += 2 * stride) {
-            double2 u0[P::NIN], u1[P::NIN];
+    using Pk = typename std::conditional<VEC == 2, double2, double>::type;
+    // Software pipeline: the next trip's UNR packets are loaded before the
+    // current trip's statements and dot expansions run, so the TwoSum chains
+    // of the exact dots overlap the memory latency instead of adding to it.
+    int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    Pk cur[UNR][P::NIN], nxt[UNR][P::NIN];
+    auto load = [&](Pk (&dst)[UNR][P::NIN], int64_t q0) {
 #pragma unroll
-            for (int i = 0; i < P::NIN; ++i) {
-                u0[i] = reinterpret_cast<const double2*>(a.in[i])[q];
-                u1[i] = reinterpret_cast<const double2*>(a.in[i])[q + stride];
-            }
-            double in[P::NIN], o0[NO], o1[NO], o2[NO], o3[NO], p0[ND], p1[ND], p2[ND], p3[ND];
+        for (int u = 0; u < UNR; ++u)
+            if (q0 + u * stride < npk)
 #pragma unroll
-            for (int i = 0; i < P::NIN; ++i) in[i] = u0[i].x;
-            P::run(in, o0, p0, co0);
+                for (int i = 0; i < P::NIN; ++i) dst[u][i] = reinterpret_cast<const Pk*>(a.in[i])[q0 + u * stride];
+    };
+    // (only kernels with dots pipeline: the plain updates are memory-bound
+    // already and the extra registers would cost occupancy)
+    constexpr bool PF = prefetch_of<P>::value;
+    if constexpr (PF) load(cur, q);
+    for (; q < npk; q += UNR * stride) {
+        const int64_t qn = q + UNR * stride;
+        if constexpr (PF) {
+            if (qn < npk) load(nxt, qn);
+        } else {
+            load(cur, q);
+        }
 #pragma unroll
-            for (int i = 0; i < P::NIN; ++i) in[i] = u0[i].y;
-            P::run(in, o1, p1, co1);
+        for (int u = 0; u < UNR; ++u) {
+            const int64_t qu = q + u * stride;
+            if (qu >= npk) break;
+            double in[P::NIN], o0[NO], p0[ND];
+            if constexpr (VEC == 2) {
+                double o1[NO], p1[ND];
 #pragma unroll
-            for (int i = 0; i < P::NIN; ++i) in[i] = u1[i].x;
-            P::run(in, o2, p2, co0);
+                for (int i = 0; i < P::NIN; ++i) in[i] = cur[u][i].x;
+                P::run(in, o0, p0, co0);
 #pragma unroll
-            for (int i = 0; i < P::NIN; ++i) in[i] = u1[i].y;
-            P::run(in, o3, p3, co1);
+                for (int i = 0; i < P::NIN; ++i) in[i] = cur[u][i].y;
+                P::run(in, o1, p1, co1);
 #pragma unroll
-            for (int i = 0; i < P::NOUT; ++i) {
-                reinterpret_cast<double2*>(a.out[i])[q] = make_double2(o0[i], o1[i]);
-                reinterpret_cast<double2*>(a.out[i])[q + stride] = make_double2(o2[i], o3[i]);
-            }
+                for (int i = 0; i < P::NOUT; ++i) reinterpret_cast<double2*>(a.out[i])[qu] = make_double2(o0[i], o1[i]);
 #pragma unroll
-            for (int d = 0; d < P::NDOT; ++d) {
-                grow(acc[2 * d], p0[d], slot0[d]);
-                grow(acc[2 * d + 1], p1[d], slot1[d]);
-                grow(acc[2 * d], p2[d], slot0[d]);
-                grow(acc[2 * d + 1], p3[d], slot1[d]);
+                for (int d = 0; d < P::NDOT; ++d) {
+                    grow(acc[2 * d], p0[d], slot0[d]);
+                    grow(acc[2 * d + 1], p1[d], slot1[d]);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < P::NIN; ++i) in[i] = cur[u][i];
+                P::run(in, o0, p0, co0);
+#pragma unroll
+                for (int i = 0; i < P::NOUT; ++i) a.out[i][qu] = o0[i];
+#pragma unroll
+                for (int d = 0; d < P::NDOT; ++d) grow(acc[d], p0[d], slot0[d]);
             }
         }
-        for (; q < npk; q += stride) {
-            double2 u0[P::NIN];
+        if constexpr (PF) {
 #pragma unroll
-            for (int i = 0; i < P::NIN; ++i) u0[i] = reinterpret_cast<const double2*>(a.in[i])[q];
-            double in[P::NIN], o0[NO], o1[NO], p0[ND], p1[ND];
+            for (int u = 0; u < UNR; ++u)
 #pragma unroll
-            for (int i = 0; i < P::NIN; ++i) in[i] = u0[i].x;
-            P::run(in, o0, p0, co0);
-#pragma unroll
-            for (int i = 0; i < P::NIN; ++i) in[i] = u0[i].y;
-            P::run(in, o1, p1, co1);
-#pragma unroll
-            for (int i = 0; i < P::NOUT; ++i) reinterpret_cast<double2*>(a.out[i])[q] = make_double2(o0[i], o1[i]);
-#pragma unroll
-            for (int d = 0; d < P::NDOT; ++d) {
-                grow(acc[2 * d], p0[d], slot0[d]);
-                grow(acc[2 * d + 1], p1[d], slot1[d]);
-            }
-        }
-    } else {
-        for (; UNR == 2 && q + stride < npk; q += 2 * stride) {
-            double in0[P::NIN], in1[P::NIN];
-#pragma unroll
-            for (int i = 0; i < P::NIN; ++i) { in0[i] = a.in[i][q]; in1[i] = a.in[i][q + stride]; }
-            double o0[NO], o1[NO], p0[ND], p1[ND];
-            P::run(in0, o0, p0, co0);
-            P::run(in1, o1, p1, co0);
-#pragma unroll
-            for (int i = 0; i < P::NOUT; ++i) { a.out[i][q] = o0[i]; a.out[i][q + stride] = o1[i]; }
-#pragma unroll
-            for (int d = 0; d < P::NDOT; ++d) { grow(acc[d], p0[d], slot0[d]); grow(acc[d], p1[d], slot0[d]); }
-        }
-        for (; q < npk; q += stride) {
-            double in0[P::NIN];
-#pragma unroll
-            for (int i = 0; i < P::NIN; ++i) in0[i] = a.in[i][q];
-            double o0[NO], p0[ND];
-            P::run(in0, o0, p0, co0);
-#pragma unroll
-            for (int i = 0; i < P::NOUT; ++i) a.out[i][q] = o0[i];
-#pragma unroll
-            for (int d = 0; d < P::NDOT; ++d) grow(acc[d], p0[d], slot0[d]);
+                for (int i = 0; i < P::NIN; ++i) cur[u][i] = nxt[u][i];
         }
     }
     if constexpr (P::NDOT > 0) {
