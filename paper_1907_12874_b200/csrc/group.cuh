@@ -242,11 +242,19 @@ struct prefetch_of {
     static constexpr bool value = P::NDOT >= 1 && P::NIN + P::NOUT <= 3;
 };
 
-// Unroll (pairs of packets per trip) unless a program declares UNROLL = 1.
+// Unroll (pairs of packets per trip) unless a program declares UNROLL = 1;
+// pipelined programs get their memory parallelism from the prefetch instead.
 template <class P, class = void>
-struct unroll_of { static constexpr int value = 2; };
+struct unroll_of { static constexpr int value = prefetch_of<P>::value ? 1 : 2; };
 template <class P>
 struct unroll_of<P, decltype(void(P::UNROLL))> { static constexpr int value = P::UNROLL; };
+
+// Resident blocks to budget registers for: pipelined programs are latency
+// bound and need 4 blocks of 256 threads (<= 64 registers); the rest 2.
+template <class P>
+struct minblocks_of {
+    static constexpr int value = prefetch_of<P>::value ? (P::NDOT >= 3 ? 3 : 4) : 2;
+};
 
 // ---------------------------------------------------------------------------
 // Block-level exact combine.  Threads of a block fall into `classes` column
@@ -322,7 +330,7 @@ __device__ __forceinline__ void block_combine(double (&acc)[NX][KEXP], int class
 // correct) for memory-level parallelism.  VEC = 1 covers odd m.
 // ---------------------------------------------------------------------------
 template <class P, int VEC>
-__global__ void __launch_bounds__(256, 2) group_kernel(GroupArgs a) {
+__global__ void __launch_bounds__(256, minblocks_of<P>::value) group_kernel(GroupArgs a) {
     if (a.ctl && a.ctl[0]) return;
     extern __shared__ double sh_dyn[];
     const int m = a.m;
