@@ -24,6 +24,7 @@ struct SpmmTiles {
 // Optional fused epilogue of the SpMM y = A x (beyond-paper merge):
 //   kind 1: slot[0] += exact (y, aux)                    e.g. delta = (v, r0)
 //   kind 2: slot[0..2] += exact (y, x), (y, y), (x, x)    phi, psi, theta of Alg. 2
+//   kind 3: slot[0] += exact (y, y)                       e.g. psi = (t, t)
 struct SpmmEpi {
     int kind = 0;
     const double* aux = nullptr;

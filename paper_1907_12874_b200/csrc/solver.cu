@@ -128,11 +128,12 @@ std::string Solver::profile_json() {
     return out + "}";
 }
 
-void Solver::spmm(const double* x, double* y, int epi_kind, const double* aux, int post_point, int post_nd) {
+void Solver::spmm(const double* x, double* y, int epi_kind, const double* aux, int post_point, int post_nd,
+                  int first_slot, int reduce) {
     SpmmEpi e;
     e.kind = epi_kind;
     e.aux = aux;
-    for (int d = 0; d < 3; ++d) e.slot[d] = slot(d);
+    for (int d = 0; d < 3; ++d) e.slot[d] = slot(first_slot + d);
     // the scalar step can ride on a single fused-epilogue SpMM launch
     const bool post = post_point >= 0 && epi_kind != 0 && can_post() && a_->peers.empty() &&
                       (m_ == 1 || m_ == 2 || m_ == 4 || m_ == 8 || m_ == 16 || m_ == 32);
@@ -146,9 +147,10 @@ void Solver::spmm(const double* x, double* y, int epi_kind, const double* aux, i
     launches_ += apply_operator(ctx_, a_, m_, const_cast<double*>(x), y, ctl_.p, epi_kind ? &e : nullptr);
     mark_end();
     if (epi_kind) {
-        if (ctx_->comm)
-            comm_allreduce_i64(ctx_, slot(0), static_cast<size_t>(epi_kind == 2 ? 3 : 1) * m_ * NSLOT, ctx_->stream);
-        reductions_++;
+        const int nred = reduce < 0 ? (epi_kind == 2 ? 3 : 1) : reduce;
+        if (ctx_->comm && nred > 0)
+            comm_allreduce_i64(ctx_, slot(first_slot), static_cast<size_t>(nred) * m_ * NSLOT, ctx_->stream);
+        if (nred > 0) reductions_++;
     }
     if (post_point >= 0 && !post) scalars(post_point, post_nd);
 }
@@ -276,13 +278,15 @@ void Solver::iteration() {
     double *r = w(V_R), *r0 = w(V_R0), *x = x_;
     if (method_ == MBG_BICGSTAB) {
         double *p = w(V_P), *v = w(V_V), *s = w(V_S), *t = w(V_T);
-        spmm(p, v);
-        group<PDot2>({v, r0}, {}, {}, 0, P_C_ALPHA, 1);
         if (fused) {
+            // dots spread over the passes that produce their operands:
+            spmm(p, v, 1, r0, P_C_ALPHA, 1);                              // v = A p ; delta = (v, r0)
             group<PUpd2Sq>({r, v}, {s}, {S_ONE, S_NALPHA}, 2, -1, 0, 0);   // s ; theta = (s,s) -> slot 2
-            spmm(s, t);
-            group<PClassicPhiPsi>({t, s}, {}, {}, 0, P_C_OMEGA, 3, 3);     // phi psi -> slots 0,1 ; omega
+            spmm(s, t, 3, nullptr, -1, 0, 1, 0);                           // t = A s ; psi = (t,t) -> slot 1
+            group<PDot2>({t, s}, {}, {}, 0, P_C_OMEGA, 3, 3);              // phi = (t,s) -> slot 0 ; omega
         } else {
+            spmm(p, v);
+            group<PDot2>({v, r0}, {}, {}, 0, P_C_ALPHA, 1);
             group<PUpd2>({r, v}, {s}, {S_ONE, S_NALPHA}, 0);
             spmm(s, t);
             if (basic) {

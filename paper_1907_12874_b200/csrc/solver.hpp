@@ -41,7 +41,7 @@ private:
     // post_point >= 0: run the scalar step `post_point` over `post_nd` dots
     // after this kernel -- fused into its last block when possible.
     void spmm(const double* x, double* y, int epi_kind = 0, const double* aux = nullptr, int post_point = -1,
-              int post_nd = 0);
+              int post_nd = 0, int first_slot = 0, int reduce = -1);
     template <class P>
     void group(std::initializer_list<const double*> in, std::initializer_list<double*> out,
                std::initializer_list<int> co, int first_slot, int post_point = -1, int post_nd = 0,

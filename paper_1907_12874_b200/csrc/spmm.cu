@@ -79,7 +79,7 @@ static_assert(STAGES * BUF_BYTES >= 256 * KEXP * 8, "combine scratch aliases the
 static_assert(8 * STAGES <= 32 && 32 + 16 * STAGES <= SMEM_HEAD, "head layout");
 
 template <int M, int EPI>
-__global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 1 ? 3 : 2)) spmm_tma_kernel(const int4* __restrict__ tiles, int ntiles,
+__global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_tma_kernel(const int4* __restrict__ tiles, int ntiles,
                                                        const int32_t* __restrict__ off,
                                                        const int32_t* __restrict__ col,
                                                        const double* __restrict__ val,
@@ -132,7 +132,10 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 1 ? 3 : 2)) spmm_t
 
     // fused epilogue: exact dot terms of one finished row
     auto epilogue = [&](int row, double t0, double t1) {
-        if constexpr (EPI == 1) {
+        if constexpr (EPI == 3) {
+            grow(ex[0], __dmul_rn(t0, t0), epi.slot[0] + static_cast<int64_t>(cp) * NSLOT);
+            if constexpr (VW == 2) grow(ex[1], __dmul_rn(t1, t1), epi.slot[0] + static_cast<int64_t>(cp + 1) * NSLOT);
+        } else if constexpr (EPI == 1) {
             const double* au = epi.aux + static_cast<int64_t>(row) * M + cp;
             grow(ex[0], __dmul_rn(t0, au[0]), epi.slot[0] + static_cast<int64_t>(cp) * NSLOT);
             if constexpr (VW == 2) grow(ex[1], __dmul_rn(t1, au[1]), epi.slot[0] + static_cast<int64_t>(cp + 1) * NSLOT);
@@ -308,6 +311,8 @@ static void launch_tma_epi(cudaStream_t st, const SpmmTiles& tl, const int32_t* 
         launch_tma<M, 0>(st, tl, off, col, val, x, y, ctl, num_sms, SpmmEpi{});
     else if (epi->kind == 1)
         launch_tma<M, 1>(st, tl, off, col, val, x, y, ctl, num_sms, *epi);
+    else if (epi->kind == 3)
+        launch_tma<M, 3>(st, tl, off, col, val, x, y, ctl, num_sms, *epi);
     else
         launch_tma<M, 2>(st, tl, off, col, val, x, y, ctl, num_sms, *epi);
 }
