@@ -191,6 +191,11 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
         } else {
             const int32_t* cs = s_col - k0a;   // index with the global k
             const double* vs = s_val - k0a;
+            // fused epilogue of the previous row, deferred until this row's
+            // gathers are in flight so its TwoSum chain overlaps their latency
+            bool pend = false;
+            int prow = 0;
+            double pa0 = 0.0, pa1 = 0.0;
             for (int rr = tid / LPR; rr < r1 - r0; rr += RPP) {
                 const int row = r0 + rr;
                 const int k0 = s_off[row - r0a], k1 = s_off[row + 1 - r0a];
@@ -209,6 +214,9 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
                         for (int q = 0; q < 4; ++q)
                             if (k + q < k1)
                                 xa[q] = __ldg(reinterpret_cast<const double2*>(x + static_cast<int64_t>(j[q]) * M + cp));
+                        if constexpr (EPI != 0) {
+                            if (pend) { epilogue(prow, pa0, pa1); pend = false; }
+                        }
 #pragma unroll
                         for (int q = 0; q < 4; ++q)
                             if (k + q < k1) {
@@ -220,6 +228,9 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
 #pragma unroll
                         for (int q = 0; q < 4; ++q)
                             if (k + q < k1) xa[q] = __ldg(x + j[q]);
+                        if constexpr (EPI != 0) {
+                            if (pend) { epilogue(prow, pa0, pa1); pend = false; }
+                        }
 #pragma unroll
                         for (int q = 0; q < 4; ++q)
                             if (k + q < k1) a0 = __dadd_rn(a0, __dmul_rn(va[q], xa[q]));
@@ -229,7 +240,16 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
                     *reinterpret_cast<double2*>(y + static_cast<int64_t>(row) * M + cp) = make_double2(a0, a1);
                 else
                     y[row] = a0;
-                if constexpr (EPI != 0) epilogue(row, a0, a1);
+                if constexpr (EPI != 0) {
+                    if (pend) epilogue(prow, pa0, pa1);   // previous row had no gathers to hide behind
+                    pend = true;
+                    prow = row;
+                    pa0 = a0;
+                    pa1 = a1;
+                }
+            }
+            if constexpr (EPI != 0) {
+                if (pend) epilogue(prow, pa0, pa1);
             }
         }
         __syncthreads();  // every thread is done with stage b
