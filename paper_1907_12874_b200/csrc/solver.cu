@@ -279,11 +279,15 @@ void Solver::iteration() {
     if (method_ == MBG_BICGSTAB) {
         double *p = w(V_P), *v = w(V_V), *s = w(V_S), *t = w(V_T);
         if (fused) {
-            // dots spread over the passes that produce their operands:
-            spmm(p, v, 1, r0, P_C_ALPHA, 1);                              // v = A p ; delta = (v, r0)
+            // theta computed where s is produced (spreads the exact-dot work over
+            // two passes); delta and phi/psi stay in their own passes: fusing
+            // them into the SpMM epilogue costs the SpMM more than it saves
+            // (measured on B200)
+            spmm(p, v);
+            group<PDot2>({v, r0}, {}, {}, 0, P_C_ALPHA, 1);
             group<PUpd2Sq>({r, v}, {s}, {S_ONE, S_NALPHA}, 2, -1, 0, 0);   // s ; theta = (s,s) -> slot 2
-            spmm(s, t, 3, nullptr, -1, 0, 1, 0);                           // t = A s ; psi = (t,t) -> slot 1
-            group<PDot2>({t, s}, {}, {}, 0, P_C_OMEGA, 3, 3);              // phi = (t,s) -> slot 0 ; omega
+            spmm(s, t);
+            group<PClassicPhiPsi>({t, s}, {}, {}, 0, P_C_OMEGA, 3, 3);     // phi psi -> slots 0,1 ; omega
         } else {
             spmm(p, v);
             group<PDot2>({v, r0}, {}, {}, 0, P_C_ALPHA, 1);

@@ -131,14 +131,14 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
         for (int i = 0; i < KEXP; ++i) ex[q][i] = 0.0;
 
     // fused epilogue: exact dot terms of one finished row
-    auto epilogue = [&](int row, double t0, double t1, double u0, double u1) {
+    auto epilogue = [&](int row, double t0, double t1) {
         if constexpr (EPI == 3) {
             grow(ex[0], __dmul_rn(t0, t0), epi.slot[0] + static_cast<int64_t>(cp) * NSLOT);
             if constexpr (VW == 2) grow(ex[1], __dmul_rn(t1, t1), epi.slot[0] + static_cast<int64_t>(cp + 1) * NSLOT);
         } else if constexpr (EPI == 1) {
-            // u0/u1: aux(row, cp..cp+1), loaded when the row started
-            grow(ex[0], __dmul_rn(t0, u0), epi.slot[0] + static_cast<int64_t>(cp) * NSLOT);
-            if constexpr (VW == 2) grow(ex[1], __dmul_rn(t1, u1), epi.slot[0] + static_cast<int64_t>(cp + 1) * NSLOT);
+            const double* au = epi.aux + static_cast<int64_t>(row) * M + cp;
+            grow(ex[0], __dmul_rn(t0, au[0]), epi.slot[0] + static_cast<int64_t>(cp) * NSLOT);
+            if constexpr (VW == 2) grow(ex[1], __dmul_rn(t1, au[1]), epi.slot[0] + static_cast<int64_t>(cp + 1) * NSLOT);
         } else if constexpr (EPI == 2) {
             double s0, s1 = 0.0;
             if constexpr (VW == 2) {
@@ -185,35 +185,16 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
                     } else {
                         a0 = y[r0];
                     }
-                    double u0 = 0.0, u1 = 0.0;
-                    if constexpr (EPI == 1) {
-                        u0 = epi.aux[static_cast<int64_t>(r0) * M + cp];
-                        if constexpr (VW == 2) u1 = epi.aux[static_cast<int64_t>(r0) * M + cp + 1];
-                    }
-                    epilogue(r0, a0, a1, u0, u1);
+                    epilogue(r0, a0, a1);
                 }
             }
         } else {
             const int32_t* cs = s_col - k0a;   // index with the global k
             const double* vs = s_val - k0a;
-            // fused epilogue of the previous row, deferred until this row's
-            // gathers are in flight so its TwoSum chain overlaps their latency
-            bool pend = false;
-            int prow = 0;
-            double pa0 = 0.0, pa1 = 0.0, pu0 = 0.0, pu1 = 0.0;
             for (int rr = tid / LPR; rr < r1 - r0; rr += RPP) {
                 const int row = r0 + rr;
                 const int k0 = s_off[row - r0a], k1 = s_off[row + 1 - r0a];
-                double a0 = 0.0, a1 = 0.0, u0 = 0.0, u1 = 0.0;
-                if constexpr (EPI == 1) {   // aux row issued with the row, consumed one row later
-                    if constexpr (VW == 2) {
-                        const double2 uv = __ldg(reinterpret_cast<const double2*>(epi.aux + static_cast<int64_t>(row) * M + cp));
-                        u0 = uv.x;
-                        u1 = uv.y;
-                    } else {
-                        u0 = __ldg(epi.aux + row);
-                    }
-                }
+                double a0 = 0.0, a1 = 0.0;
                 // batches of 4 nonzeros: index/value loads, then the gathers, then
                 // the ordered adds (4 gathers in flight per lane; more costs occupancy)
                 for (int k = k0; k < k1; k += 4) {
@@ -228,9 +209,6 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
                         for (int q = 0; q < 4; ++q)
                             if (k + q < k1)
                                 xa[q] = __ldg(reinterpret_cast<const double2*>(x + static_cast<int64_t>(j[q]) * M + cp));
-                        if constexpr (EPI != 0) {
-                            if (pend) { epilogue(prow, pa0, pa1, pu0, pu1); pend = false; }
-                        }
 #pragma unroll
                         for (int q = 0; q < 4; ++q)
                             if (k + q < k1) {
@@ -242,9 +220,6 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
 #pragma unroll
                         for (int q = 0; q < 4; ++q)
                             if (k + q < k1) xa[q] = __ldg(x + j[q]);
-                        if constexpr (EPI != 0) {
-                            if (pend) { epilogue(prow, pa0, pa1, pu0, pu1); pend = false; }
-                        }
 #pragma unroll
                         for (int q = 0; q < 4; ++q)
                             if (k + q < k1) a0 = __dadd_rn(a0, __dmul_rn(va[q], xa[q]));
@@ -254,18 +229,7 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
                     *reinterpret_cast<double2*>(y + static_cast<int64_t>(row) * M + cp) = make_double2(a0, a1);
                 else
                     y[row] = a0;
-                if constexpr (EPI != 0) {
-                    if (pend) epilogue(prow, pa0, pa1, pu0, pu1);   // previous row had no gathers to hide behind
-                    pend = true;
-                    prow = row;
-                    pa0 = a0;
-                    pa1 = a1;
-                    pu0 = u0;
-                    pu1 = u1;
-                }
-            }
-            if constexpr (EPI != 0) {
-                if (pend) epilogue(prow, pa0, pa1, pu0, pu1);
+                if constexpr (EPI != 0) epilogue(row, a0, a1);
             }
         }
         __syncthreads();  // every thread is done with stage b

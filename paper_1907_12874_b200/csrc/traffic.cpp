@@ -138,13 +138,12 @@ std::vector<Group> schedule(int method) {
 std::vector<Group> schedule_fused(int method, int* aux_reads, int* spmm_dots) {
     switch (method) {
         case MBG_BICGSTAB:
-            // delta fused into v = A p (reads r0 there), theta = (s,s) where s
-            // is produced, psi = (t,t) in t = A s, phi = (t,s) alone
-            *aux_reads = 1;
-            spmm_dots[0] = 1;
-            spmm_dots[1] = 1;
-            return {{U(S, {R, V}), Dt(S, S, 2)},
-                    {Dt(T, S, 0)},
+            // theta = (s,s) computed where s is produced; same transfers as merged
+            *aux_reads = 0;
+            spmm_dots[0] = spmm_dots[1] = 0;
+            return {{Dt(V, R0, 0)},
+                    {U(S, {R, V}), Dt(S, S, 2)},
+                    {Dt(T, S, 0), Dt(T, T, 1)},
                     {U(X, {X, P, S}), U(R, {S, T}), Dt(R, R0, 0)},
                     {U(P, {R, P, V})}};
         case MBG_RBICGSTAB:
