@@ -100,8 +100,9 @@ static void side_to_main(mbg_ctx* ctx) {
 
 int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, const int* ctl,
                    const SpmmEpi* epi) {
-    auto tiles = [](const mbg::DevBuf<int4>& t, const mbg::DevBuf<int32_t>& l) {
-        return SpmmTiles{t.p, static_cast<int64_t>(t.n), l.p, static_cast<int64_t>(l.n)};
+    const bool hint = a->n > 0 && a->nnz > 12 * a->n;
+    auto tiles = [hint](const mbg::DevBuf<int4>& t, const mbg::DevBuf<int32_t>& l) {
+        return SpmmTiles{t.p, static_cast<int64_t>(t.n), l.p, static_cast<int64_t>(l.n), hint};
     };
     if (a->peers.empty()) {
         return launch_spmm(ctx->stream, tiles(a->tiles_all, a->long_all), a->n, nullptr, a->off.p, a->col.p, a->val.p, m, x,

@@ -20,6 +20,7 @@ struct SpmmTiles {
     int64_t count = 0;
     const int32_t* long_rows = nullptr;  // rows of the single-row tiles beyond SPMM_TILE_NNZ
     int64_t nlong = 0;
+    bool long_rows_hint = false;         // average row length > 12: use the 3-block variant
 };
 // Optional fused epilogue of the SpMM y = A x (beyond-paper merge):
 //   kind 1: slot[0] += exact (y, aux)                    e.g. delta = (v, r0)

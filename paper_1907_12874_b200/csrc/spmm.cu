@@ -78,6 +78,9 @@ static_assert((OFF_CAP * 4) % 16 == 0 && (NNZ_PAD * 4) % 16 == 0, "region alignm
 static_assert(STAGES * BUF_BYTES >= 256 * KEXP * 8, "combine scratch aliases the stages");
 static_assert(8 * STAGES <= 32 && 32 + 16 * STAGES <= SMEM_HEAD, "head layout");
 
+// EPI: 0 plain; 1/2/3 fused dot epilogues (kernels.hpp SpmmEpi kinds); 4 plain
+// with a 3-block register budget, faster for long rows (>12 nonzeros on
+// average: the 27-point stencil, the random banded matrix -- spmm_lab sweep).
 template <int M, int EPI>
 __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_tma_kernel(const int4* __restrict__ tiles, int ntiles,
                                                        const int32_t* __restrict__ off,
@@ -175,7 +178,7 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
         if (lng) {
             // a row longer than the stage capacity was multiplied beforehand by
             // spmm_long_rows_kernel; only its fused epilogue runs here
-            if constexpr (EPI != 0) {
+            if constexpr (EPI >= 1 && EPI <= 3) {
                 if (tid < LPR) {
                     double a0, a1 = 0.0;
                     if constexpr (VW == 2) {
@@ -229,13 +232,13 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
                     *reinterpret_cast<double2*>(y + static_cast<int64_t>(row) * M + cp) = make_double2(a0, a1);
                 else
                     y[row] = a0;
-                if constexpr (EPI != 0) epilogue(row, a0, a1);
+                if constexpr (EPI >= 1 && EPI <= 3) epilogue(row, a0, a1);
             }
         }
         __syncthreads();  // every thread is done with stage b
         if (tid == 0) issue(i + STAGES, b);
     }
-    if constexpr (EPI != 0) {
+    if constexpr (EPI >= 1 && EPI <= 3) {
         // no bulk copy is in flight any more: the stage memory is free scratch
         double* sh = reinterpret_cast<double*>(bufs);
         block_combine<ND * VW>(ex, M >= 2 ? LPR : 1,
@@ -307,7 +310,9 @@ template <int M>
 static void launch_tma_epi(cudaStream_t st, const SpmmTiles& tl, const int32_t* off, const int32_t* col,
                            const double* val, const double* x, double* y, const int* ctl, int num_sms,
                            const SpmmEpi* epi) {
-    if (!epi || epi->kind == 0)
+    if ((!epi || epi->kind == 0) && tl.long_rows_hint)
+        launch_tma<M, 4>(st, tl, off, col, val, x, y, ctl, num_sms, SpmmEpi{});
+    else if (!epi || epi->kind == 0)
         launch_tma<M, 0>(st, tl, off, col, val, x, y, ctl, num_sms, SpmmEpi{});
     else if (epi->kind == 1)
         launch_tma<M, 1>(st, tl, off, col, val, x, y, ctl, num_sms, *epi);

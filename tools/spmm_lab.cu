@@ -179,7 +179,11 @@ __global__ void __launch_bounds__(256) k_warpshfl(int n, const int* __restrict__
 }
 
 // ---------------------------------------------------------------- TMA tiled (parametrised)
-template <int M, int TR, int TN, int ST, int RPT, int B, int MINB, int NT = 256, bool CONTIG = false>
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <int M, int TR, int TN, int ST, int RPT, int B, int MINB, int NT = 256, bool CONTIG = false, int PFD = 0>
 __global__ void __launch_bounds__(NT, MINB) k_tma(const int4* __restrict__ tiles, int ntiles, const int* __restrict__ off,
                                                    const int* __restrict__ col, const double* __restrict__ val,
                                                    const double* __restrict__ x, double* __restrict__ y) {
@@ -208,6 +212,15 @@ __global__ void __launch_bounds__(NT, MINB) k_tma(const int4* __restrict__ tiles
         bulk_g2s(buf, off + r0a, bo, &bars[b]);
         bulk_g2s(buf + OFFC * 4, col + k0a, bn * 4u, &bars[b]);
         bulk_g2s(buf + OFFC * 4 + NNZP * 4, val + k0a, bn * 8u, &bars[b]);
+        if constexpr (PFD > 0) {   // warm L2 with the tile PFD trips ahead
+            const int tp = tile_of(i + PFD);
+            if (tp < ntiles) {
+                const int4 tq = tiles[tp];
+                const int q0 = tq.z & ~3, q1 = (tq.w + 3) & ~3;
+                l2_prefetch(col + q0, (q1 - q0) * 4u);
+                l2_prefetch(val + q0, (q1 - q0) * 8u);
+            }
+        }
     };
     if (tid == 0)
         for (int b = 0; b < ST; ++b) issue(b, b);
@@ -308,7 +321,7 @@ void timeit(const char* name, Ctx& c, F launch) {
     printf("%-34s %8.1f us  %7.1f GB/s  %s\n", name, us, c.bytes / us / 1e3, ok ? "bitwise-ok" : "MISMATCH");
 }
 
-template <int M, int TR, int TN, int ST, int RPT, int B, int MINB, int NT = 256, bool CONTIG = false>
+template <int M, int TR, int TN, int ST, int RPT, int B, int MINB, int NT = 256, bool CONTIG = false, int PFD = 0>
 void run_tma(Ctx& c, const char* name) {
     auto tiles = make_tiles(c.hoff, c.n, TR, TN);
     int4* dt;
@@ -316,7 +329,7 @@ void run_tma(Ctx& c, const char* name) {
     CK(cudaMemcpy(dt, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice));
     constexpr int BUF = (TR + 8) * 4 + (TN + 8) * 12;
     const int smem = 192 + ST * BUF;
-    auto kern = k_tma<M, TR, TN, ST, RPT, B, MINB, NT, CONTIG>;
+    auto kern = k_tma<M, TR, TN, ST, RPT, B, MINB, NT, CONTIG, PFD>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int occ;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem));
@@ -421,19 +434,12 @@ int run_all(int g) {
     timeit("ref thread/(row,col)", c, [&] {
         k_ref<<<(unsigned)(((int64_t)n * M + 255) / 256), 256>>>(n, c.off, c.col, c.val, M, c.x, c.y);
     });
-    timeit("direct-noalloc B4 minb4", c, [&] {
-        constexpr int RPB = 256 / (M >= 2 ? M / 2 : 1);
-        k_direct_na<M, 4, 4><<<(n + RPB - 1) / RPB, 256>>>(n, c.off, c.col, c.val, c.x, c.y);
-    });
-    timeit("direct-noalloc B8 minb2", c, [&] {
-        constexpr int RPB = 256 / (M >= 2 ? M / 2 : 1);
-        k_direct_na<M, 8, 2><<<(n + RPB - 1) / RPB, 256>>>(n, c.off, c.col, c.val, c.x, c.y);
-    });
-    run_tma<M, 192, 1920, 2, 1, 4, 4>(c, "tma 192r/1920 2st B4 minb4");
-    run_tma<M, 96, 960, 2, 1, 4, 4>(c, "tma 96r/960 2st B4 minb4");
-    run_tma<M, 192, 960, 2, 1, 4, 4>(c, "tma 192r/960 2st B4 minb4");
-    run_tma<M, 64, 640, 2, 1, 4, 4>(c, "tma 64r/640 2st B4 minb4");
-    run_tma<M, 192, 1920, 2, 1, 4, 3>(c, "tma 192r/1920 2st B4 minb3");
+    run_tma<M, 192, 1920, 2, 1, 4, 4>(c, "tma 192r 2st B4 minb4");
+    run_tma<M, 192, 1920, 2, 1, 4, 4, 256, false, 2>(c, "tma 192r 2st B4 minb4 pf2");
+    run_tma<M, 192, 1920, 2, 1, 4, 4, 256, false, 3>(c, "tma 192r 2st B4 minb4 pf3");
+    run_tma<M, 192, 1920, 2, 1, 4, 4, 256, false, 5>(c, "tma 192r 2st B4 minb4 pf5");
+    run_tma<M, 192, 1920, 2, 1, 4, 3, 256, false, 3>(c, "tma 192r 2st B4 minb3 pf3");
+    run_tma<M, 128, 1280, 2, 1, 4, 4, 256, false, 4>(c, "tma 128r 2st B4 minb4 pf4");
     return 0;
 }
 
