@@ -79,8 +79,9 @@ static_assert(STAGES * BUF_BYTES >= 256 * KEXP * 8, "combine scratch aliases the
 static_assert(8 * STAGES <= 32 && 32 + 16 * STAGES <= SMEM_HEAD, "head layout");
 
 // EPI: 0 plain; 1/2/3 fused dot epilogues (kernels.hpp SpmmEpi kinds); 4 plain
-// with a 3-block register budget, faster for long rows (>12 nonzeros on
-// average: the 27-point stencil, the random banded matrix -- spmm_lab sweep).
+// with a 3-block register budget -- measured faster only for long rows (>12
+// nonzeros on average) at m = 32 (C5: 14.2 vs 17.7 ms/iteration), slower at
+// m <= 16 (C3, C5 m=8), so it is used for that case only.
 template <int M, int EPI>
 __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_tma_kernel(const int4* __restrict__ tiles, int ntiles,
                                                        const int32_t* __restrict__ off,
@@ -310,7 +311,7 @@ template <int M>
 static void launch_tma_epi(cudaStream_t st, const SpmmTiles& tl, const int32_t* off, const int32_t* col,
                            const double* val, const double* x, double* y, const int* ctl, int num_sms,
                            const SpmmEpi* epi) {
-    if ((!epi || epi->kind == 0) && tl.long_rows_hint)
+    if ((!epi || epi->kind == 0) && tl.long_rows_hint && M >= 32)
         launch_tma<M, 4>(st, tl, off, col, val, x, y, ctl, num_sms, SpmmEpi{});
     else if (!epi || epi->kind == 0)
         launch_tma<M, 0>(st, tl, off, col, val, x, y, ctl, num_sms, SpmmEpi{});
