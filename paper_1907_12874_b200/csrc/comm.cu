@@ -182,7 +182,7 @@ int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, 
     return launches;
 }
 
-void comm_allreduce_i64(mbg_ctx* ctx, int64_t* buf, size_t count, cudaStream_t st) {
+void comm_allreduce_i64(mbg_ctx* ctx, int64_t* buf, size_t count, cudaStream_t st, bool join) {
     Comm* cm = ctx->comm;
     if (!cm || cm->world == 1) return;
     (void)st;
@@ -219,7 +219,11 @@ void comm_allreduce_i64(mbg_ctx* ctx, int64_t* buf, size_t count, cudaStream_t s
     } else {
         MBG_NCCL(ncclAllReduce(buf, buf, count, ncclInt64, ncclSum, cm->comm, ctx->side));
     }
-    side_to_main(ctx);
+    if (join) side_to_main(ctx);
+}
+
+void comm_join(mbg_ctx* ctx) {
+    if (ctx->comm && ctx->comm->world > 1) side_to_main(ctx);
 }
 
 void comm_barrier(mbg_ctx* ctx) {

@@ -18,8 +18,12 @@ struct SpmmEpi;
 int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, const int* ctl,
                    const SpmmEpi* epi = nullptr);
 
-// Sum int64 limbs over all ranks (exact, order-independent).
-void comm_allreduce_i64(mbg_ctx* ctx, int64_t* buf, size_t count, cudaStream_t st);
+// Sum int64 limbs over all ranks (exact, order-independent).  join=false
+// leaves the allreduce in flight on the side stream so the main stream's next
+// kernels (the Pipelined SpMM, the Reordered copy) overlap it; comm_join()
+// makes the main stream wait for it before the slots are read.
+void comm_allreduce_i64(mbg_ctx* ctx, int64_t* buf, size_t count, cudaStream_t st, bool join = true);
+void comm_join(mbg_ctx* ctx);
 void comm_barrier(mbg_ctx* ctx);
 void comm_destroy(mbg_ctx* ctx);
 bool comm_is_local(const mbg_ctx* ctx);   // single-GPU emulation (no graph capture)

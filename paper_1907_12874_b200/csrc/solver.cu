@@ -148,8 +148,11 @@ void Solver::spmm(const double* x, double* y, int epi_kind, const double* aux, i
     mark_end();
     if (epi_kind) {
         const int nred = reduce < 0 ? (epi_kind == 2 ? 3 : 1) : reduce;
-        if (ctx_->comm && nred > 0)
-            comm_allreduce_i64(ctx_, slot(first_slot), static_cast<size_t>(nred) * m_ * NSLOT, ctx_->stream);
+        if (ctx_->comm && nred > 0) {
+            comm_allreduce_i64(ctx_, slot(first_slot), static_cast<size_t>(nred) * m_ * NSLOT, ctx_->stream,
+                               /*join=*/false);
+            pending_join_ = true;
+        }
         if (nred > 0) reductions_++;
     }
     if (post_point >= 0 && !post) scalars(post_point, post_nd);
@@ -186,7 +189,9 @@ void Solver::group(std::initializer_list<const double*> in, std::initializer_lis
         // the same reduction point; > 0: that many slots from first_slot
         const int nred = reduce < 0 ? P::NDOT : reduce;
         if (ctx_->comm && nred > 0) {
-            comm_allreduce_i64(ctx_, slot(first_slot), static_cast<size_t>(nred) * m_ * NSLOT, ctx_->stream);
+            comm_allreduce_i64(ctx_, slot(first_slot), static_cast<size_t>(nred) * m_ * NSLOT, ctx_->stream,
+                               /*join=*/false);
+            pending_join_ = true;
         }
         if (nred > 0) reductions_++;
     }
@@ -226,7 +231,13 @@ bool Solver::can_post() const {
     return enabled && ctx_->comm == nullptr && group_block(m_) % 32 == 0;
 }
 
+void Solver::join() {
+    if (pending_join_) comm_join(ctx_);
+    pending_join_ = false;
+}
+
 void Solver::scalars(int point, int nd) {
+    join();   // the dots of this point may still be in an allreduce on the side stream
     ScalArgs s = scal_args(point, nd);
     const int threads = std::min(1024, std::max(((m_ + 31) / 32) * 32, 32 * nd * m_));
     mark_begin("scalar", 0.0);
@@ -384,6 +395,7 @@ void Solver::iteration() {
         spmm(wv, t);
         if (!early) scalars(P_P_BETA, 4);
     }
+    join();   // a captured graph must end joined to the origin stream
 }
 
 void Solver::run(const double* b, double* x, bool use_graph, int chunk) {
@@ -397,6 +409,7 @@ void Solver::run(const double* b, double* x, bool use_graph, int chunk) {
     if (ctx_->comm) comm_barrier(ctx_);
     MBG_CUDA(cudaEventRecord(t0_, ctx_->stream));
     setup(b, x);
+    join();
     if (profile_) {  // profile the iteration loop only
         MBG_CUDA(cudaStreamSynchronize(ctx_->stream));
         for (auto& mk : marks_) { cudaEventDestroy(mk.a); cudaEventDestroy(mk.b); }

@@ -50,6 +50,7 @@ private:
     bool can_post() const;
     void copy(double* dst, const double* src);
     void scalars(int point, int nd);
+    void join();   // main stream waits for an in-flight dot allreduce
     void setup(const double* b, double* x);
     void iteration();
 
@@ -72,6 +73,7 @@ private:
     double* x_ = nullptr;
     int64_t launches_ = 0;
     int64_t reductions_ = 0;
+    bool pending_join_ = false;
     float loop_ms_ = 0.f;
     // profiling
     bool profile_ = false;
