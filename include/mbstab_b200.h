@@ -95,6 +95,11 @@ int mbg_halo_plan(int64_t n, const int64_t* offsets, const int32_t* cols, const 
 int mbg_csr_free(mbg_csr* a);
 int64_t mbg_csr_rows(const mbg_csr* a);   /* local rows */
 int64_t mbg_csr_nnz(const mbg_csr* a);    /* local nnz */
+/* SpMM kernel choice made at upload (no reference counterpart; diagnostics):
+ * staged = 1 when the gather-once tiling is in use (x rows reused inside
+ * tiles, e.g. 27-point stencils; MBG_SPMM_STAGE=0/1 forces it off/on),
+ * reuse = nonzeros per distinct column per tile of that tiling (0 if none). */
+int mbg_csr_stage_info(const mbg_csr* a, int* staged, double* reuse);
 
 /* ---- multivector: n x m fp64, row-interleaved (element (i,c) at i*m+c) -- */
 int mbg_mv_alloc(mbg_ctx* ctx, int64_t n, int m, mbg_mv** out);

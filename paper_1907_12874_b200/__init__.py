@@ -197,6 +197,12 @@ class DeviceCsr:
         self.n = int(lib().mbg_csr_rows(h))
         self.nnz = int(lib().mbg_csr_nnz(h))
 
+    def stage_info(self):
+        """(staged, reuse): whether the gather-once SpMM tiling is in use."""
+        st, ru = C.c_int(0), C.c_double(0.0)
+        check(lib().mbg_csr_stage_info(self.h, C.byref(st), C.byref(ru)))
+        return bool(st.value), float(ru.value)
+
     def __del__(self):
         try:
             if self.h:

@@ -118,6 +118,48 @@ extern "C" int mbg_csr_validate(int64_t n, const int64_t* off, const int32_t* co
     return guarded([&] { validate_csr(n, off, col, nnz); });
 }
 
+// Gather-once SpMM tilings (spmm.cu spmm_stage_kernel): built when the tiles
+// reuse x rows (>= 2 nonzeros per distinct column, e.g. 27-point stencils);
+// MBG_SPMM_STAGE=0 / 1 forces them off / on (tests, A/B measurements).
+static int stage_mode() {
+    const char* e = std::getenv("MBG_SPMM_STAGE");
+    return e ? std::atoi(e) : -1;
+}
+
+static void stage_tilings(mbg_ctx* ctx, mbg_csr* a, const std::vector<int32_t>& off32, const int32_t* col,
+                          const std::vector<int32_t>* all, const std::vector<int32_t>* interior,
+                          const std::vector<int32_t>* boundary) {
+    const int mode = stage_mode();
+    if (mode == 0) return;
+    const int64_t ncols = a->n + a->n_halo;
+    std::vector<uint16_t> lcol(static_cast<size_t>(a->nnz) + 16, 0);
+    if (all) {
+        StageTiling st;
+        if (!build_stage_tiles(off32, col, *all, ncols, lcol, st)) return;
+        a->stage_reuse = st.reuse;
+        if (mode != 1) return;
+        upload(a->stiles_all, st.tiles.data(), st.tiles.size(), ctx->stream);
+        upload(a->umeta_all, st.umeta.data(), st.umeta.size(), ctx->stream);
+        upload(a->ucols_all, st.ucols.data(), st.ucols.size(), ctx->stream);
+        upload(a->lcol_all, lcol.data(), lcol.size(), ctx->stream);
+        MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+    } else {
+        StageTiling si, sb;
+        if (!build_stage_tiles(off32, col, *interior, ncols, lcol, si)) return;
+        if (!build_stage_tiles(off32, col, *boundary, ncols, lcol, sb)) return;
+        a->stage_reuse = si.reuse;
+        if (mode != 1) return;
+        upload(a->stiles_interior, si.tiles.data(), si.tiles.size(), ctx->stream);
+        upload(a->umeta_interior, si.umeta.data(), si.umeta.size(), ctx->stream);
+        upload(a->ucols_interior, si.ucols.data(), si.ucols.size(), ctx->stream);
+        upload(a->stiles_boundary, sb.tiles.data(), sb.tiles.size(), ctx->stream);
+        upload(a->umeta_boundary, sb.umeta.data(), sb.umeta.size(), ctx->stream);
+        upload(a->ucols_boundary, sb.ucols.data(), sb.ucols.size(), ctx->stream);
+        upload(a->lcol_split, lcol.data(), lcol.size(), ctx->stream);
+        MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+}
+
 // Upload a (local) CSR with int32 offsets.  Arrays are padded by 8 entries so
 // the SpMM's 16-byte-aligned TMA bulk copies may round a tile's range up.
 static void csr_arrays_to_device(mbg_ctx* ctx, mbg_csr* a, int64_t n, const std::vector<int32_t>& off32,
@@ -142,6 +184,7 @@ static void csr_arrays_to_device(mbg_ctx* ctx, mbg_csr* a, int64_t n, const std:
     upload(a->tiles_all, t.data(), t.size(), ctx->stream);
     auto lr = long_rows_of(t);
     upload(a->long_all, lr.data(), lr.size(), ctx->stream);
+    stage_tilings(ctx, a, off32, col, &all, nullptr, nullptr);
     MBG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
@@ -163,6 +206,7 @@ extern "C" int mbg_csr_upload(mbg_ctx* ctx, int64_t n, const int64_t* off, const
         auto* a = new mbg_csr();
         try {
             a->ctx = ctx;
+            a->device = ctx->device;
             a->n_global = n;
             csr_to_device(ctx, a, n, off, col, val);
         } catch (...) {
@@ -186,6 +230,7 @@ extern "C" int mbg_csr_upload_partitioned(mbg_ctx* ctx, int64_t n, const int64_t
         auto* a = new mbg_csr();
         try {
             a->ctx = ctx;
+            a->device = ctx->device;
             a->n_global = n;
             a->row_begin = bounds[my_part];
             a->n = pl.n_own;
@@ -201,6 +246,7 @@ extern "C" int mbg_csr_upload_partitioned(mbg_ctx* ctx, int64_t n, const int64_t
                 auto li = long_rows_of(ti), lb = long_rows_of(tb);
                 upload(a->long_interior, li.data(), li.size(), ctx->stream);
                 upload(a->long_boundary, lb.data(), lb.size(), ctx->stream);
+                stage_tilings(ctx, a, pl.off, pl.col.data(), nullptr, &pl.interior, &pl.boundary);
                 upload(a->interior_rows, pl.interior.data(), pl.interior.size(), ctx->stream);
                 upload(a->boundary_rows, pl.boundary.data(), pl.boundary.size(), ctx->stream);
                 a->n_interior = static_cast<int64_t>(pl.interior.size());
@@ -257,13 +303,21 @@ extern "C" int mbg_halo_plan(int64_t n, const int64_t* off, const int32_t* col, 
 extern "C" int mbg_csr_free(mbg_csr* a) {
     return guarded([&] {
         if (!a) return;
-        if (a->ctx) cudaSetDevice(a->ctx->device);
+        cudaSetDevice(a->device);
         delete a;
     });
 }
 
 extern "C" int64_t mbg_csr_rows(const mbg_csr* a) { return a ? a->n : -1; }
 extern "C" int64_t mbg_csr_nnz(const mbg_csr* a) { return a ? a->nnz : -1; }
+
+extern "C" int mbg_csr_stage_info(const mbg_csr* a, int* staged, double* reuse) {
+    return guarded([&] {
+        if (!a) throw Invalid("null matrix");
+        if (staged) *staged = (a->stiles_all.n || a->stiles_interior.n || a->stiles_boundary.n) ? 1 : 0;
+        if (reuse) *reuse = a->stage_reuse;
+    });
+}
 
 extern "C" int mbg_mv_alloc(mbg_ctx* ctx, int64_t n, int m, mbg_mv** out) {
     return guarded([&] {
@@ -272,6 +326,7 @@ extern "C" int mbg_mv_alloc(mbg_ctx* ctx, int64_t n, int m, mbg_mv** out) {
         if (n < 0 || m < 1) throw Invalid("multivector: bad shape");
         auto* v = new mbg_mv();
         v->ctx = ctx;
+        v->device = ctx->device;
         v->n = n;
         v->n_alloc = n;
         v->m = m;
@@ -290,7 +345,7 @@ extern "C" int mbg_mv_alloc(mbg_ctx* ctx, int64_t n, int m, mbg_mv** out) {
 extern "C" int mbg_mv_free(mbg_mv* v) {
     return guarded([&] {
         if (!v) return;
-        if (v->ctx) cudaSetDevice(v->ctx->device);
+        cudaSetDevice(v->device);
         delete v;
     });
 }

@@ -101,11 +101,20 @@ static void side_to_main(mbg_ctx* ctx) {
 int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, const int* ctl,
                    const SpmmEpi* epi) {
     const bool hint = a->n > 0 && a->nnz > 12 * a->n;
-    auto tiles = [hint](const mbg::DevBuf<int4>& t, const mbg::DevBuf<int32_t>& l) {
-        return SpmmTiles{t.p, static_cast<int64_t>(t.n), l.p, static_cast<int64_t>(l.n), hint};
+    auto tiles = [hint](const mbg::DevBuf<int4>& t, const mbg::DevBuf<int32_t>& l, const mbg::DevBuf<int4>& st,
+                        const mbg::DevBuf<int2>& um, const mbg::DevBuf<int32_t>& uc, const mbg::DevBuf<uint16_t>& lc) {
+        SpmmTiles r{t.p, static_cast<int64_t>(t.n), l.p, static_cast<int64_t>(l.n), hint};
+        if (st.n && lc.p) {
+            r.stiles = st.p;
+            r.umeta = um.p;
+            r.ucols = uc.p;
+            r.lcol = lc.p;
+            r.scount = static_cast<int64_t>(st.n);
+        }
+        return r;
     };
     if (a->peers.empty()) {
-        return launch_spmm(ctx->stream, tiles(a->tiles_all, a->long_all), a->n, nullptr, a->off.p, a->col.p, a->val.p, m, x,
+        return launch_spmm(ctx->stream, tiles(a->tiles_all, a->long_all, a->stiles_all, a->umeta_all, a->ucols_all, a->lcol_all), a->n, nullptr, a->off.p, a->col.p, a->val.p, m, x,
                            y, ctl, ctx->num_sms, epi);
     }
     Comm* cm = ctx->comm;
@@ -174,10 +183,12 @@ int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, 
     MBG_NCCL(ncclGroupEnd());
     }
     // interior rows overlap the exchange; boundary rows wait for the halo
-    launches += launch_spmm(ctx->stream, tiles(a->tiles_interior, a->long_interior), a->n_interior, a->interior_rows.p, a->off.p,
+    launches += launch_spmm(ctx->stream, tiles(a->tiles_interior, a->long_interior, a->stiles_interior, a->umeta_interior,
+                                                      a->ucols_interior, a->lcol_split), a->n_interior, a->interior_rows.p, a->off.p,
                             a->col.p, a->val.p, m, x, y, ctl, ctx->num_sms, epi);
     side_to_main(ctx);
-    launches += launch_spmm(ctx->stream, tiles(a->tiles_boundary, a->long_boundary), a->n_boundary, a->boundary_rows.p, a->off.p,
+    launches += launch_spmm(ctx->stream, tiles(a->tiles_boundary, a->long_boundary, a->stiles_boundary, a->umeta_boundary,
+                                                      a->ucols_boundary, a->lcol_split), a->n_boundary, a->boundary_rows.p, a->off.p,
                             a->col.p, a->val.p, m, x, y, ctl, ctx->num_sms, epi);
     return launches;
 }

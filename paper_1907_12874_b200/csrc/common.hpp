@@ -28,6 +28,7 @@ void set_error(const std::string& msg);
     do {                                                                                      \
         cudaError_t _e = (call);                                                              \
         if (_e != cudaSuccess)                                                                \
+            (void)cudaGetLastError(), /* do not leak the error into later launches */         \
             throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(_e) +    \
                                      " at " __FILE__ ":" + std::to_string(__LINE__) + ": " #call); \
     } while (0)
@@ -107,6 +108,7 @@ inline void pool_give(mbg_ctx* ctx, DevBuf<double>&& b) {
 // x layout [owned rows | halo rows] (see halo.cu).
 struct mbg_csr {
     mbg_ctx* ctx = nullptr;
+    int device = 0;           // owning device (freeing must not touch ctx)
     int64_t n_global = 0;
     int64_t n = 0;            // local rows
     int64_t nnz = 0;          // local nnz
@@ -122,6 +124,12 @@ struct mbg_csr {
     // SpMM tile plans (spmm.cu): all rows, interior rows, boundary rows
     mbg::DevBuf<int4> tiles_all, tiles_interior, tiles_boundary;
     mbg::DevBuf<int32_t> long_all, long_interior, long_boundary;   // rows beyond a tile's capacity
+    // gather-once tilings (stencil-like matrices; empty when not worth it)
+    mbg::DevBuf<int4> stiles_all, stiles_interior, stiles_boundary;
+    mbg::DevBuf<int2> umeta_all, umeta_interior, umeta_boundary;
+    mbg::DevBuf<int32_t> ucols_all, ucols_interior, ucols_boundary;
+    mbg::DevBuf<uint16_t> lcol_all, lcol_split;    // per nonzero, for the all / interior+boundary tilings
+    double stage_reuse = 0.0;
     struct Peer {
         int rank;
         int64_t send_count, recv_count;
@@ -133,6 +141,7 @@ struct mbg_csr {
 
 struct mbg_mv {
     mbg_ctx* ctx = nullptr;
+    int device = 0;
     int64_t n = 0;        // rows (owned)
     int64_t n_alloc = 0;  // rows allocated (owned + halo capacity)
     int m = 0;

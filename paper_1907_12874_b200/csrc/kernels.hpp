@@ -21,6 +21,14 @@ struct SpmmTiles {
     const int32_t* long_rows = nullptr;  // rows of the single-row tiles beyond SPMM_TILE_NNZ
     int64_t nlong = 0;
     bool long_rows_hint = false;         // average row length > 12: use the 3-block variant
+    // gather-once ("staged") tiling, set when the matrix reuses x rows inside
+    // a tile (stencils): per tile the unique columns, and per nonzero its
+    // 16-bit index into them (spmm.cu spmm_stage_kernel)
+    const int4* stiles = nullptr;        // (r0, r1, k0, k1) per staged tile
+    const int2* umeta = nullptr;         // (u0, U): the tile's columns are ucols[u0 .. u0+U)
+    const int32_t* ucols = nullptr;
+    const uint16_t* lcol = nullptr;      // indexed by the global nonzero k
+    int64_t scount = 0;
 };
 // Optional fused epilogue of the SpMM y = A x (beyond-paper merge):
 //   kind 1: slot[0] += exact (y, aux)                    e.g. delta = (v, r0)
@@ -37,6 +45,20 @@ int launch_spmm(cudaStream_t st, const SpmmTiles& tl, int64_t nrows, const int32
                 int num_sms, const SpmmEpi* epi = nullptr);
 std::vector<int4> build_spmm_tiles(const std::vector<int32_t>& off, const std::vector<int32_t>& rows);
 std::vector<int32_t> long_rows_of(const std::vector<int4>& tiles);
+
+// Gather-once tiling: tiles of <= STAGE_ROWS rows, <= STAGE_NNZ nonzeros and
+// <= STAGE_UCOLS distinct columns.  lcol (size >= nnz, shared by disjoint row
+// classes) receives each nonzero's index into its tile's column list.
+// Returns false (and builds nothing) when a single row exceeds the limits.
+constexpr int STAGE_ROWS = 128, STAGE_NNZ = 1024, STAGE_UCOLS = 256;
+struct StageTiling {
+    std::vector<int4> tiles;
+    std::vector<int2> umeta;
+    std::vector<int32_t> ucols;
+    double reuse = 0.0;   // nonzeros per staged x row
+};
+bool build_stage_tiles(const std::vector<int32_t>& off, const int32_t* col, const std::vector<int32_t>& rows,
+                       int64_t ncols, std::vector<uint16_t>& lcol, StageTiling& out);
 
 // Generic statement-group interpreter (API-level execute_group).
 constexpr int GEN_MAX_VEC = 16, GEN_MAX_STMT = 16, GEN_MAX_SLOT = 8;

@@ -22,6 +22,8 @@
 //   trade occupancy for in-flight bytes and lose.
 // Any other m uses a thread-per-(row, column) kernel with the same arithmetic.
 #include <cstdint>
+#include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.hpp"
@@ -77,6 +79,38 @@ static_assert(BUF_BYTES % 16 == 0, "buffer alignment");
 static_assert((OFF_CAP * 4) % 16 == 0 && (NNZ_PAD * 4) % 16 == 0, "region alignment");
 static_assert(STAGES * BUF_BYTES >= 256 * KEXP * 8, "combine scratch aliases the stages");
 static_assert(8 * STAGES <= 32 && 32 + 16 * STAGES <= SMEM_HEAD, "head layout");
+
+// Fused SpMM epilogue (SpmmEpi kinds 1-3): the exact dot terms of one
+// finished row; lane columns cp, cp+1.
+template <int M, int EPI, int VW, int ND>
+__device__ __forceinline__ void spmm_epi_row(double (&ex)[ND * VW][KEXP], const SpmmEpi& epi, int cp, int row,
+                                             double t0, double t1, const double* __restrict__ x) {
+    if constexpr (EPI == 3) {
+        grow(ex[0], __dmul_rn(t0, t0), epi.slot[0] + static_cast<int64_t>(cp) * NSLOT);
+        if constexpr (VW == 2) grow(ex[1], __dmul_rn(t1, t1), epi.slot[0] + static_cast<int64_t>(cp + 1) * NSLOT);
+    } else if constexpr (EPI == 1) {
+        const double* au = epi.aux + static_cast<int64_t>(row) * M + cp;
+        grow(ex[0], __dmul_rn(t0, au[0]), epi.slot[0] + static_cast<int64_t>(cp) * NSLOT);
+        if constexpr (VW == 2) grow(ex[1], __dmul_rn(t1, au[1]), epi.slot[0] + static_cast<int64_t>(cp + 1) * NSLOT);
+    } else if constexpr (EPI == 2) {
+        double s0, s1 = 0.0;
+        if constexpr (VW == 2) {
+            const double2 sv = __ldg(reinterpret_cast<const double2*>(x + static_cast<int64_t>(row) * M + cp));
+            s0 = sv.x;
+            s1 = sv.y;
+        } else {
+            s0 = __ldg(x + row);
+        }
+#pragma unroll
+        for (int v = 0; v < VW; ++v) {
+            const double t = v ? t1 : t0, sv = v ? s1 : s0;
+            const int64_t so = static_cast<int64_t>(cp + v) * NSLOT;
+            grow(ex[0 * VW + v], __dmul_rn(t, sv), epi.slot[0] + so);
+            grow(ex[1 * VW + v], __dmul_rn(t, t), epi.slot[1] + so);
+            grow(ex[2 * VW + v], __dmul_rn(sv, sv), epi.slot[2] + so);
+        }
+    }
+}
 
 // EPI: 0 plain; 1/2/3 fused dot epilogues (kernels.hpp SpmmEpi kinds); 4 plain
 // with a 3-block register budget -- measured faster only for long rows (>12
@@ -135,33 +169,7 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
         for (int i = 0; i < KEXP; ++i) ex[q][i] = 0.0;
 
     // fused epilogue: exact dot terms of one finished row
-    auto epilogue = [&](int row, double t0, double t1) {
-        if constexpr (EPI == 3) {
-            grow(ex[0], __dmul_rn(t0, t0), epi.slot[0] + static_cast<int64_t>(cp) * NSLOT);
-            if constexpr (VW == 2) grow(ex[1], __dmul_rn(t1, t1), epi.slot[0] + static_cast<int64_t>(cp + 1) * NSLOT);
-        } else if constexpr (EPI == 1) {
-            const double* au = epi.aux + static_cast<int64_t>(row) * M + cp;
-            grow(ex[0], __dmul_rn(t0, au[0]), epi.slot[0] + static_cast<int64_t>(cp) * NSLOT);
-            if constexpr (VW == 2) grow(ex[1], __dmul_rn(t1, au[1]), epi.slot[0] + static_cast<int64_t>(cp + 1) * NSLOT);
-        } else if constexpr (EPI == 2) {
-            double s0, s1 = 0.0;
-            if constexpr (VW == 2) {
-                const double2 sv = __ldg(reinterpret_cast<const double2*>(x + static_cast<int64_t>(row) * M + cp));
-                s0 = sv.x;
-                s1 = sv.y;
-            } else {
-                s0 = __ldg(x + row);
-            }
-#pragma unroll
-            for (int v = 0; v < VW; ++v) {
-                const double t = v ? t1 : t0, sv = v ? s1 : s0;
-                const int64_t so = static_cast<int64_t>(cp + v) * NSLOT;
-                grow(ex[0 * VW + v], __dmul_rn(t, sv), epi.slot[0] + so);
-                grow(ex[1 * VW + v], __dmul_rn(t, t), epi.slot[1] + so);
-                grow(ex[2 * VW + v], __dmul_rn(sv, sv), epi.slot[2] + so);
-            }
-        }
-    };
+    auto epilogue = [&](int row, double t0, double t1) { spmm_epi_row<M, EPI, VW, ND>(ex, epi, cp, row, t0, t1, x); };
 
     for (int i = 0;; ++i) {
         const int t = blockIdx.x + i * gridDim.x;
@@ -236,6 +244,9 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
                 if constexpr (EPI >= 1 && EPI <= 3) epilogue(row, a0, a1);
             }
         }
+        // (a warp-asynchronous release of the stage -- last warp out refills --
+        // measured 6% slower on C3: warps drifting onto different tiles split
+        // the L1 working set that the 27-point gathers depend on)
         __syncthreads();  // every thread is done with stage b
         if (tid == 0) issue(i + STAGES, b);
     }
@@ -246,6 +257,151 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
                                [&](int q, int k) {
                                    const int c_ = M >= 2 ? k * VW + q % VW : 0;
                                    return epi.slot[q / VW] + static_cast<int64_t>(c_) * NSLOT;
+                               },
+                               sh);
+    }
+    if (epi.post.enabled) post_step(epi.post, reinterpret_cast<double*>(bufs));
+}
+
+// ---------------------------------------------------------------------------
+// Gather-once SpMM for matrices whose tiles reuse x rows (stencils: a 27-point
+// row shares most of its columns with its neighbours).  Per tile the distinct
+// columns (<= STAGE_UCOLS) are gathered ONCE into shared memory with 16-byte
+// cp.async, then every nonzero reads its x row from shared memory through a
+// 16-bit local index (2 B/nnz instead of the 4 B column).  Same arithmetic as
+// spmm_tma_kernel: per (row, column) sequential CSR-order adds from 0.0.
+// x traffic from L2 drops from nnz*8m to U*8m bytes per tile (27-point:
+// ~2.8x), which is what bounds the plain kernel on C3.
+// ---------------------------------------------------------------------------
+constexpr int S_STAGES = 2;
+constexpr int S_OFF_CAP = STAGE_ROWS + 8;     // int32
+constexpr int S_LCOL_CAP = STAGE_NNZ + 16;    // uint16 (k0 rounded down to 8)
+constexpr int S_VAL_CAP = STAGE_NNZ + 4;      // double (k0 rounded down to 2)
+constexpr int S_UCOL_CAP = STAGE_UCOLS + 8;   // int32 (u0 rounded down to 4)
+constexpr int S_BUF = S_OFF_CAP * 4 + S_LCOL_CAP * 2 + S_VAL_CAP * 8 + S_UCOL_CAP * 4;
+constexpr int S_HEAD = 128;                   // 2 mbarriers + 2 x 2 int4 metas
+static_assert(S_BUF % 16 == 0 && (S_OFF_CAP * 4) % 16 == 0 && (S_LCOL_CAP * 2) % 16 == 0 &&
+                  (S_VAL_CAP * 8) % 16 == 0, "stage alignment");
+static_assert(S_STAGES * S_BUF >= 256 * KEXP * 8, "combine scratch aliases the stages");
+constexpr int stage_smem(int m) { return S_HEAD + S_STAGES * S_BUF + STAGE_UCOLS * m * 8; }
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+template <int M, int EPI>
+__global__ void __launch_bounds__(256, M >= 32 ? 2 : (EPI == 2 ? 2 : (EPI == 0 ? 4 : 3)))
+    spmm_stage_kernel(const int4* __restrict__ tiles, const int2* __restrict__ umeta, int ntiles,
+                      const int32_t* __restrict__ off, const uint16_t* __restrict__ lcol,
+                      const double* __restrict__ val, const int32_t* __restrict__ ucols,
+                      const double* __restrict__ x, double* __restrict__ y, const int* __restrict__ ctl,
+                      SpmmEpi epi) {
+    static_assert(M >= 4, "x rows of >= 32 bytes");
+    if (ctl && ctl[0]) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+    int4* meta = reinterpret_cast<int4*>(smem + 32);   // [stage][2]
+    unsigned char* bufs = smem + S_HEAD;
+    double* xs = reinterpret_cast<double*>(smem + S_HEAD + S_STAGES * S_BUF);
+    const int tid = threadIdx.x;
+
+    if (tid == 0) {
+        for (int b = 0; b < S_STAGES; ++b) mbar_init(&bars[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    auto issue = [&](int i, int b) {
+        const int t = blockIdx.x + i * gridDim.x;
+        if (t >= ntiles) return;
+        const int4 tl = tiles[t];
+        const int2 um = umeta[t];
+        const int r0a = tl.x & ~3, r1a = (tl.y + 1 + 3) & ~3;
+        const int k0l = tl.z & ~7, k1l = (tl.w + 7) & ~7;
+        const int k0v = tl.z & ~1, k1v = (tl.w + 1) & ~1;
+        const int u0a = um.x & ~3, u1a = (um.x + um.y + 3) & ~3;
+        meta[2 * b] = make_int4(tl.x, tl.y, r0a, k0l);
+        meta[2 * b + 1] = make_int4(k0v, um.x - u0a, um.y, 0);
+        unsigned char* buf = bufs + b * S_BUF;
+        const uint32_t boff = static_cast<uint32_t>(r1a - r0a) * 4u;
+        const uint32_t blc = static_cast<uint32_t>(k1l - k0l) * 2u;
+        const uint32_t bval = static_cast<uint32_t>(k1v - k0v) * 8u;
+        const uint32_t buc = static_cast<uint32_t>(u1a - u0a) * 4u;
+        mbar_expect_tx(&bars[b], boff + blc + bval + buc);
+        bulk_g2s(buf, off + r0a, boff, &bars[b]);
+        if (blc) bulk_g2s(buf + S_OFF_CAP * 4, lcol + k0l, blc, &bars[b]);
+        if (bval) bulk_g2s(buf + S_OFF_CAP * 4 + S_LCOL_CAP * 2, val + k0v, bval, &bars[b]);
+        if (buc) bulk_g2s(buf + S_OFF_CAP * 4 + S_LCOL_CAP * 2 + S_VAL_CAP * 8, ucols + u0a, buc, &bars[b]);
+    };
+    if (tid == 0)
+        for (int b = 0; b < S_STAGES; ++b) issue(b, b);
+
+    constexpr int VW = 2;
+    constexpr int LPR = M / VW;
+    constexpr int RPP = 256 / LPR;
+    constexpr int ND = EPI == 2 ? 3 : 1;
+    constexpr int CPR = M / 2;               // 16-byte chunks per x row
+    const int cp = (tid % LPR) * VW;
+    double ex[ND * VW][KEXP];
+#pragma unroll
+    for (int q = 0; q < ND * VW; ++q)
+#pragma unroll
+        for (int i = 0; i < KEXP; ++i) ex[q][i] = 0.0;
+
+    for (int i = 0;; ++i) {
+        const int t = blockIdx.x + i * gridDim.x;
+        if (t >= ntiles) break;
+        const int b = i % S_STAGES;
+        while (!mbar_try_wait(&bars[b], static_cast<uint32_t>((i / S_STAGES) & 1))) {
+        }
+        const int4 mt = meta[2 * b];
+        const int4 mu = meta[2 * b + 1];
+        const int r0 = mt.x, r1 = mt.y, r0a = mt.z, k0l = mt.w, k0v = mu.x, ush = mu.y, U = mu.z;
+        const unsigned char* buf = bufs + b * S_BUF;
+        const int32_t* s_off = reinterpret_cast<const int32_t*>(buf);
+        const uint16_t* s_lc = reinterpret_cast<const uint16_t*>(buf + S_OFF_CAP * 4) - k0l;   // global k
+        const double* s_val = reinterpret_cast<const double*>(buf + S_OFF_CAP * 4 + S_LCOL_CAP * 2) - k0v;
+        const int32_t* s_uc =
+            reinterpret_cast<const int32_t*>(buf + S_OFF_CAP * 4 + S_LCOL_CAP * 2 + S_VAL_CAP * 8) + ush;
+        // gather the tile's distinct x rows once
+        for (int c = tid; c < U * CPR; c += 256) {
+            const int u = c / CPR, part = c - u * CPR;
+            cp_async16(xs + u * M + part * 2, x + static_cast<int64_t>(s_uc[u]) * M + part * 2);
+        }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        for (int rr = tid / LPR; rr < r1 - r0; rr += RPP) {
+            const int row = r0 + rr;
+            const int k0 = s_off[row - r0a], k1 = s_off[row + 1 - r0a];
+            double a0 = 0.0, a1 = 0.0;
+            for (int k = k0; k < k1; k += 4) {
+                int j[4];
+                double va[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (k + q < k1) { j[q] = s_lc[k + q]; va[q] = s_val[k + q]; }
+                double2 xa[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (k + q < k1) xa[q] = *reinterpret_cast<const double2*>(xs + j[q] * M + cp);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (k + q < k1) {
+                        a0 = __dadd_rn(a0, __dmul_rn(va[q], xa[q].x));
+                        a1 = __dadd_rn(a1, __dmul_rn(va[q], xa[q].y));
+                    }
+            }
+            *reinterpret_cast<double2*>(y + static_cast<int64_t>(row) * M + cp) = make_double2(a0, a1);
+            if constexpr (EPI >= 1 && EPI <= 3) spmm_epi_row<M, EPI, VW, ND>(ex, epi, cp, row, a0, a1, x);
+        }
+        __syncthreads();  // stage b and xs are free
+        if (tid == 0) issue(i + S_STAGES, b);
+    }
+    if constexpr (EPI >= 1 && EPI <= 3) {
+        double* sh = reinterpret_cast<double*>(bufs);
+        block_combine<ND * VW>(ex, LPR,
+                               [&](int q, int k) {
+                                   return epi.slot[q / VW] + static_cast<int64_t>(k * VW + q % VW) * NSLOT;
                                },
                                sh);
     }
@@ -323,10 +479,48 @@ static void launch_tma_epi(cudaStream_t st, const SpmmTiles& tl, const int32_t* 
         launch_tma<M, 2>(st, tl, off, col, val, x, y, ctl, num_sms, *epi);
 }
 
+template <int M, int EPI>
+static void launch_stage(cudaStream_t st, const SpmmTiles& tl, const int32_t* off, const double* val,
+                         const double* x, double* y, const int* ctl, int num_sms, const SpmmEpi& epi) {
+    static int occ = -1;
+    constexpr int smem = stage_smem(M);
+    if (occ < 0) {
+        MBG_CUDA(cudaFuncSetAttribute(spmm_stage_kernel<M, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        MBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmm_stage_kernel<M, EPI>, 256, smem));
+        if (occ < 1) occ = 1;
+    }
+    const int grid = static_cast<int>(std::min<int64_t>(tl.scount, static_cast<int64_t>(num_sms) * occ));
+    spmm_stage_kernel<M, EPI><<<grid, 256, smem, st>>>(tl.stiles, tl.umeta, static_cast<int>(tl.scount), off,
+                                                       tl.lcol, val, tl.ucols, x, y, ctl, epi);
+}
+
+template <int M>
+static void launch_stage_epi(cudaStream_t st, const SpmmTiles& tl, const int32_t* off, const double* val,
+                             const double* x, double* y, const int* ctl, int num_sms, const SpmmEpi* epi) {
+    if (!epi || epi->kind == 0)
+        launch_stage<M, 0>(st, tl, off, val, x, y, ctl, num_sms, SpmmEpi{});
+    else if (epi->kind == 1)
+        launch_stage<M, 1>(st, tl, off, val, x, y, ctl, num_sms, *epi);
+    else if (epi->kind == 3)
+        launch_stage<M, 3>(st, tl, off, val, x, y, ctl, num_sms, *epi);
+    else
+        launch_stage<M, 2>(st, tl, off, val, x, y, ctl, num_sms, *epi);
+}
+
 int launch_spmm(cudaStream_t st, const SpmmTiles& tl, int64_t nrows, const int32_t* rows, const int32_t* off,
                 const int32_t* col, const double* val, int m, const double* x, double* y, const int* ctl,
                 int num_sms, const SpmmEpi* epi) {
     if (nrows <= 0) return 0;
+    if (tl.stiles && tl.scount > 0 && (m == 4 || m == 8 || m == 16 || m == 32)) {
+        switch (m) {
+            case 4: launch_stage_epi<4>(st, tl, off, val, x, y, ctl, num_sms, epi); break;
+            case 8: launch_stage_epi<8>(st, tl, off, val, x, y, ctl, num_sms, epi); break;
+            case 16: launch_stage_epi<16>(st, tl, off, val, x, y, ctl, num_sms, epi); break;
+            default: launch_stage_epi<32>(st, tl, off, val, x, y, ctl, num_sms, epi); break;
+        }
+        MBG_CUDA(cudaGetLastError());
+        return 1;
+    }
     int launched = 0;
     if (tl.nlong > 0 && (m == 1 || m == 2 || m == 4 || m == 8 || m == 16 || m == 32)) {
         const int64_t tot = tl.nlong * m;
@@ -361,6 +555,51 @@ std::vector<int32_t> long_rows_of(const std::vector<int4>& tiles) {
     for (const auto& t : tiles)
         if (t.w - t.z > SPMM_TILE_NNZ) out.push_back(t.x);
     return out;
+}
+
+bool build_stage_tiles(const std::vector<int32_t>& off, const int32_t* col, const std::vector<int32_t>& rows,
+                       int64_t ncols, std::vector<uint16_t>& lcol, StageTiling& out) {
+    out = StageTiling{};
+    std::vector<int32_t> stamp(static_cast<size_t>(ncols), -1), pos(static_cast<size_t>(ncols), 0);
+    std::vector<int32_t> cur;
+    cur.reserve(STAGE_UCOLS);
+    int64_t nnz_total = 0, u_total = 0;
+    int32_t tid = 0;
+    size_t i = 0;
+    while (i < rows.size()) {
+        const int r0 = rows[i];
+        int r1 = r0;
+        size_t j = i;
+        cur.clear();
+        while (j < rows.size() && rows[j] == r1 && r1 - r0 < STAGE_ROWS) {
+            const int k0 = off[r1], k1 = off[r1 + 1];
+            if (k1 - off[r0] > STAGE_NNZ) break;
+            int fresh = 0;
+            for (int k = k0; k < k1; ++k) fresh += stamp[col[k]] != tid;
+            if (static_cast<int>(cur.size()) + fresh > STAGE_UCOLS) break;
+            for (int k = k0; k < k1; ++k)
+                if (stamp[col[k]] != tid) {
+                    stamp[col[k]] = tid;
+                    cur.push_back(col[k]);
+                }
+            ++r1;
+            ++j;
+        }
+        if (r1 == r0) return false;   // one row beyond the limits: keep the plain kernel
+        std::sort(cur.begin(), cur.end());
+        for (size_t u = 0; u < cur.size(); ++u) pos[cur[u]] = static_cast<int32_t>(u);
+        for (int k = off[r0]; k < off[r1]; ++k) lcol[k] = static_cast<uint16_t>(pos[col[k]]);
+        out.tiles.push_back(make_int4(r0, r1, off[r0], off[r1]));
+        out.umeta.push_back(make_int2(static_cast<int>(out.ucols.size()), static_cast<int>(cur.size())));
+        out.ucols.insert(out.ucols.end(), cur.begin(), cur.end());
+        nnz_total += off[r1] - off[r0];
+        u_total += static_cast<int64_t>(cur.size());
+        ++tid;
+        i = j;
+    }
+    out.ucols.resize(out.ucols.size() + 8, 0);   // bulk copies round the last range up
+    out.reuse = u_total ? static_cast<double>(nnz_total) / static_cast<double>(u_total) : 0.0;
+    return true;
 }
 
 std::vector<int4> build_spmm_tiles(const std::vector<int32_t>& off, const std::vector<int32_t>& rows) {
