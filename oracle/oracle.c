@@ -208,6 +208,18 @@ void orc_spmv(const orc_csr* a, int m, const double* x, double* y) {
 }
 
 /* Restates run_rows' update branch (execute.cpp:104-111). */
+void orc_spmv_transpose(const orc_csr* a, int m, const double* x, double* y) {
+    memset(y, 0, sizeof(double) * (size_t)(a->n * m));
+    for (int64_t i = 0; i < a->n; ++i) {
+        const double* xr = x + i * m;
+        for (int64_t k = a->off[i]; k < a->off[i + 1]; ++k) {
+            const double v = a->val[k];
+            double* yr = y + (int64_t)a->col[k] * m;
+            for (int c = 0; c < m; ++c) yr[c] = yr[c] + v * xr[c];
+        }
+    }
+}
+
 void orc_update(int64_t n, int m, int nterms, const double* const* coeff,
                 const double* const* src, double* out) {
     const int64_t len = n * m;
@@ -415,10 +427,39 @@ static int bad_omega(const double* den, const double* sq, const double* om, int 
     return -1;
 }
 
+int orc_method_preconditioned(int method) {
+    return method == ORC_RBICGSTAB || method == ORC_PBICGSTAB || method == ORC_PPIPEBICGSTAB;
+}
+
+/* M^-1: identity = copy; synthetic(alpha) = alpha/2 passes
+ * out = c*in, c = 2.0, 0.5, 2.0, ... and a last factor making the product 1. */
+static void minv(const shape* S, int alpha, const double* c2, const double* ch, const double* c1,
+                 const double* in, double* out) {
+    if (alpha <= 2) {
+        memcpy(out, in, sizeof(double) * (size_t)S->len);
+        return;
+    }
+    const int k = alpha / 2;
+    for (int i = 0; i < k; ++i) {
+        const double* c = i < k - 1 ? ((i & 1) ? ch : c2) : (((k - 1) & 1) ? ch : c1);
+        const double* src = i == 0 ? in : out;
+        orc_update(S->n, S->m, 1, &c, &src, out);
+    }
+}
+
 int orc_solve(const orc_csr* A, int m, const double* b, double* x, int method,
               int formulation, double tol, int fixed, int maxit, double* hist,
               orc_report* rep) {
+    return orc_solve_pc(A, m, b, x, method, formulation, orc_method_preconditioned(method) ? 2 : 0,
+                        tol, fixed, maxit, hist, rep);
+}
+
+int orc_solve_pc(const orc_csr* A, int m, const double* b, double* x, int method,
+                 int formulation, int pa, double tol, int fixed, int maxit, double* hist,
+                 orc_report* rep) {
     shape S = {A->n, m, A->n * m};
+    if (method < 0 || method > 5) return -1;
+    if (orc_method_preconditioned(method) ? (pa < 2 || (pa & 1)) : pa != 0) return -2;
     memset(rep, 0, sizeof *rep);
     double* one = (double*)malloc(sizeof(double) * m);
     double* mone = (double*)malloc(sizeof(double) * m);
@@ -428,10 +469,16 @@ int orc_solve(const orc_csr* A, int m, const double* b, double* x, int method,
     double *beta = calloc(m, 8), *nbo = calloc(m, 8), *oa = calloc(m, 8), *delta = calloc(m, 8);
     double *phi = calloc(m, 8), *psi = calloc(m, 8), *theta = calloc(m, 8), *eta = calloc(m, 8);
     double *pi = calloc(m, 8), *sigma = calloc(m, 8), *res2 = calloc(m, 8), *den = calloc(m, 8);
+    double *two = calloc(m, 8), *half = calloc(m, 8), *sigmap = calloc(m, 8), *tau = calloc(m, 8);
+    double *gam = calloc(m, 8), *kap = calloc(m, 8), *nu = calloc(m, 8), *cz2 = calloc(m, 8);
+    double *cz3 = calloc(m, 8), *ndelta = calloc(m, 8);
+    for (int c = 0; c < m; ++c) { two[c] = 2.0; half[c] = 0.5; }
 
     double* r = vnew(&S); double* r0 = vnew(&S); double* tmp = vnew(&S);
     double *p = NULL, *v = NULL, *s = NULL, *t = NULL, *z = NULL, *vh = NULL, *th = NULL;
     double *rt = NULL, *q = NULL, *w = NULL, *y = NULL, *tmp2 = NULL;
+    double *u = NULL, *f0 = NULL, *ph = NULL, *sh = NULL, *qh = NULL, *rh = NULL, *wh = NULL, *zh = NULL;
+#define MINV(IN, OUT) minv(&S, pa, two, half, one, (IN), (OUT))
 
     /* r0 = b - A x0 (Alg. 2 line 1-2) */
     orc_spmv(A, m, x, tmp);
@@ -487,12 +534,12 @@ int orc_solve(const orc_csr* A, int m, const double* b, double* x, int method,
         /* Alg. 6 (identity M^-1), PAPER.md:1562-1598 with the footnote-5 fix */
         z = vnew(&S); vh = vnew(&S); v = vnew(&S); s = vnew(&S); th = vnew(&S);
         t = vnew(&S); rt = vnew(&S); q = vnew(&S);
-        memcpy(z, r0, sizeof(double) * S.len);   /* z0 = M^-1 r0 */
+        MINV(r0, z);                              /* z0 = M^-1 r0 */
         memcpy(vh, z, sizeof(double) * S.len);   /* v^0 = z0 */
         for (it = 0; it < maxit; ++it) {
             orc_spmv(A, m, vh, v);
             orc_dot_exact(S.n, m, v, r0, delta);
-            memcpy(s, v, sizeof(double) * S.len); /* s = M^-1 v */
+            MINV(v, s);                           /* s = M^-1 v */
             for (int c = 0; c < m; ++c) { alpha[c] = rho[c] / delta[c]; nalpha[c] = -alpha[c]; }
             int bc = bad_col(delta, alpha, m);
             if (bc >= 0) { rep->breakdown = 1; rep->breakdown_col = bc; break; }
@@ -503,7 +550,7 @@ int orc_solve(const orc_csr* A, int m, const double* b, double* x, int method,
             orc_dot_exact(S.n, m, t, t, phi);
             orc_dot_exact(S.n, m, t, r0, psi);
             orc_dot_exact(S.n, m, rt, rt, eta);
-            memcpy(q, t, sizeof(double) * S.len); /* q = M^-1 t */
+            MINV(t, q);                           /* q = M^-1 t */
             for (int c = 0; c < m; ++c) {
                 omega[c] = lucky(phi[c], eta[c]) ? 0.0 : theta[c] / phi[c];
                 nomega[c] = -omega[c];
@@ -587,6 +634,186 @@ int orc_solve(const orc_csr* A, int m, const double* b, double* x, int method,
             bc = bad_col(den, alpha, m);
             if (bc >= 0) { rep->breakdown = 1; rep->breakdown_col = bc; ++it; break; }
         }
+    } else if (method == ORC_IBICGSTAB) {
+        /* Alg. 3 (merged Improved BiCGStab).  Scalar
+         * expression trees (pinned here, mirrored in scalar.cuh):
+         *   rho' = (phi - omega*sigma_{j-1}) + (omega*alpha)*pi
+         *   delta' = (rho'/rho)*alpha ; beta' = delta'/omega
+         *   tau' = (sigma + beta'*tau) - delta'*pi ; alpha' = rho'/tau'
+         *   z: coefficients alpha', beta'*(alpha'/alpha), -(alpha'*delta') */
+        u = vnew(&S); f0 = vnew(&S); q = vnew(&S); v = vnew(&S); z = vnew(&S); s = vnew(&S); t = vnew(&S);
+        orc_spmv(A, m, r, u);                  /* u0 = A r0 */
+        orc_spmv_transpose(A, m, r0, f0);      /* f0 = A^T r0 */
+        orc_dot_exact(S.n, m, r0, u, sigma);   /* sigma_0 = (r0, u0) */
+        for (int c = 0; c < m; ++c) {
+            phi[c] = rho[c];                   /* phi_0 = (r0, r0) */
+            sigmap[c] = 0.0; pi[c] = 0.0; tau[c] = 0.0;
+            rho[c] = 1.0; alpha[c] = 1.0; omega[c] = 1.0;
+        }
+        for (it = 0; it < maxit; ++it) {
+            double* an = den;                  /* alpha_{j+1} */
+            for (int c = 0; c < m; ++c) {
+                rhon[c] = (phi[c] - omega[c] * sigmap[c]) + (omega[c] * alpha[c]) * pi[c];
+                delta[c] = (rhon[c] / rho[c]) * alpha[c];
+                beta[c] = delta[c] / omega[c];
+                tau[c] = (sigma[c] + beta[c] * tau[c]) - delta[c] * pi[c];
+                an[c] = rhon[c] / tau[c];
+            }
+            int bc = bad_col(NULL, beta, m);
+            if (bc >= 0) { rep->breakdown = 3; rep->breakdown_col = bc; break; }
+            bc = bad_col(tau, an, m);
+            if (bc >= 0) { rep->breakdown = 1; rep->breakdown_col = bc; break; }
+            for (int c = 0; c < m; ++c) {
+                cz2[c] = beta[c] * (an[c] / alpha[c]);
+                cz3[c] = -(an[c] * delta[c]);
+                ndelta[c] = -delta[c];
+                alpha[c] = an[c];
+                nalpha[c] = -an[c];
+                rho[c] = rhon[c];
+            }
+            UPD(&S, z, 3, alpha, r, cz2, z, cz3, v);
+            UPD(&S, v, 3, one, u, beta, v, ndelta, q);
+            UPD(&S, s, 2, one, r, nalpha, v);
+            orc_spmv(A, m, v, q);
+            UPD(&S, t, 2, one, u, nalpha, q);
+            orc_dot_exact(S.n, m, r0, s, phi);
+            orc_dot_exact(S.n, m, r0, q, pi);
+            orc_dot_exact(S.n, m, f0, s, gam);
+            orc_dot_exact(S.n, m, f0, t, eta);
+            orc_dot_exact(S.n, m, s, t, theta);
+            orc_dot_exact(S.n, m, t, t, kap);
+            orc_dot_exact(S.n, m, s, s, nu);
+            for (int c = 0; c < m; ++c) {
+                omega[c] = lucky(kap[c], nu[c]) ? 0.0 : theta[c] / kap[c];
+                nomega[c] = -omega[c];
+                res2[c] = nu[c] - omega[c] * theta[c];
+            }
+            bc = bad_omega(kap, nu, omega, m);
+            if (bc >= 0) { rep->breakdown = 2; rep->breakdown_col = bc; break; }
+            for (int c = 0; c < m; ++c) {
+                sigmap[c] = sigma[c];
+                sigma[c] = gam[c] - omega[c] * eta[c];
+                hist[(int64_t)(it + 1) * m + c] = hist_entry(res2[c], bb[c]);
+            }
+            const int conv = !fixed && all_below(res2, eps2, m);
+            UPD(&S, r, 2, one, s, nomega, t);
+            UPD(&S, x, 3, one, x, one, z, omega, s);
+            if (conv) { rep->converged = 1; ++it; break; }
+            orc_spmv(A, m, r, u);
+        }
+    } else if (method == ORC_PBICGSTAB) {
+        /* Alg. 5 (merged preconditioned BiCGStab).  The x
+         * update (independent of beta) runs before beta is formed. */
+        p = vnew(&S); v = vnew(&S); s = vnew(&S); t = vnew(&S); ph = vnew(&S); sh = vnew(&S);
+        UPD(&S, p, 1, one, r);
+        for (it = 0; it < maxit; ++it) {
+            MINV(p, ph);
+            orc_spmv(A, m, ph, v);
+            orc_dot_exact(S.n, m, v, r0, delta);
+            for (int c = 0; c < m; ++c) { alpha[c] = rho[c] / delta[c]; nalpha[c] = -alpha[c]; }
+            int bc = bad_col(delta, alpha, m);
+            if (bc >= 0) { rep->breakdown = 1; rep->breakdown_col = bc; break; }
+            UPD(&S, s, 2, one, r, nalpha, v);
+            MINV(s, sh);
+            orc_spmv(A, m, sh, t);
+            orc_dot_exact(S.n, m, t, s, phi);
+            orc_dot_exact(S.n, m, t, t, psi);
+            orc_dot_exact(S.n, m, s, s, theta);
+            for (int c = 0; c < m; ++c) {
+                omega[c] = lucky(psi[c], theta[c]) ? 0.0 : phi[c] / psi[c];
+                nomega[c] = -omega[c];
+                res2[c] = theta[c] - omega[c] * phi[c];
+            }
+            bc = bad_omega(psi, theta, omega, m);
+            if (bc >= 0) { rep->breakdown = 2; rep->breakdown_col = bc; break; }
+            for (int c = 0; c < m; ++c) hist[(int64_t)(it + 1) * m + c] = hist_entry(res2[c], bb[c]);
+            const int conv = !fixed && all_below(res2, eps2, m);
+            UPD(&S, r, 2, one, s, nomega, t);
+            UPD(&S, x, 3, one, x, alpha, ph, omega, sh);
+            if (conv) { rep->converged = 1; ++it; break; }
+            orc_dot_exact(S.n, m, r, r0, rhon);
+            for (int c = 0; c < m; ++c) {
+                beta[c] = (rhon[c] / rho[c]) * (alpha[c] / omega[c]);
+                nbo[c] = -(beta[c] * omega[c]);
+                rho[c] = rhon[c];
+            }
+            bc = bad_col(NULL, beta, m);
+            if (bc >= 0) { rep->breakdown = 3; rep->breakdown_col = bc; break; }
+            UPD(&S, p, 3, one, r, beta, p, nbo, v);
+        }
+    } else if (method == ORC_PPIPEBICGSTAB) {
+        /* Alg. 7 (merged preconditioned Pipelined BiCGStab)
+         * (line 1: w^_0 = M^-1 w_0).  Expansions as Alg. 4. */
+        rh = vnew(&S); w = vnew(&S); wh = vnew(&S); t = vnew(&S); ph = vnew(&S); sh = vnew(&S);
+        qh = vnew(&S); s = vnew(&S); z = vnew(&S); q = vnew(&S); y = vnew(&S); zh = vnew(&S);
+        v = vnew(&S); tmp2 = vnew(&S);
+        MINV(r, rh);
+        orc_spmv(A, m, rh, w);
+        MINV(w, wh);
+        orc_spmv(A, m, wh, t);
+        orc_dot_exact(S.n, m, r0, w, den);
+        for (int c = 0; c < m; ++c) { alpha[c] = rho[c] / den[c]; beta[c] = 0.0; omega[c] = 0.0; }
+        int bc = bad_col(den, alpha, m);
+        if (bc >= 0) { rep->breakdown = 1; rep->breakdown_col = bc; goto done; }
+        for (it = 0; it < maxit; ++it) {
+            for (int c = 0; c < m; ++c) { nbo[c] = -(beta[c] * omega[c]); nalpha[c] = -alpha[c]; }
+            UPD(&S, ph, 3, one, rh, beta, ph, nbo, sh);
+            UPD(&S, sh, 3, one, wh, beta, sh, nbo, zh);
+            UPD(&S, qh, 2, one, rh, nalpha, sh);
+            UPD(&S, s, 3, one, w, beta, s, nbo, z);
+            UPD(&S, z, 3, one, t, beta, z, nbo, v);
+            UPD(&S, q, 2, one, r, nalpha, s);
+            UPD(&S, y, 2, one, w, nalpha, z);
+            orc_dot_exact(S.n, m, q, y, theta);
+            orc_dot_exact(S.n, m, y, y, phi);
+            orc_dot_exact(S.n, m, q, q, pi);
+            MINV(z, zh);
+            orc_spmv(A, m, zh, v);
+            for (int c = 0; c < m; ++c) {
+                omega[c] = lucky(phi[c], pi[c]) ? 0.0 : theta[c] / phi[c];
+                nomega[c] = -omega[c];
+                oa[c] = omega[c] * alpha[c];
+                res2[c] = pi[c] - omega[c] * theta[c];
+            }
+            bc = bad_omega(phi, pi, omega, m);
+            if (bc >= 0) { rep->breakdown = 2; rep->breakdown_col = bc; break; }
+            for (int c = 0; c < m; ++c) hist[(int64_t)(it + 1) * m + c] = hist_entry(res2[c], bb[c]);
+            const int conv = !fixed && all_below(res2, eps2, m);
+            UPD(&S, x, 3, one, x, alpha, ph, omega, qh);
+            if (conv) {
+                UPD(&S, r, 2, one, q, nomega, y);
+                rep->converged = 1; ++it; break;
+            }
+            if (formulation == ORC_BASIC) {
+                UPD(&S, tmp2, 2, nomega, wh, oa, zh);
+                UPD(&S, rh, 2, one, qh, one, tmp2);
+            } else {
+                UPD(&S, rh, 3, one, qh, nomega, wh, oa, zh);
+            }
+            UPD(&S, r, 2, one, q, nomega, y);
+            if (formulation == ORC_BASIC) {
+                UPD(&S, tmp2, 2, nomega, t, oa, v);
+                UPD(&S, w, 2, one, y, one, tmp2);
+            } else {
+                UPD(&S, w, 3, one, y, nomega, t, oa, v);
+            }
+            orc_dot_exact(S.n, m, r0, r, rhon);
+            orc_dot_exact(S.n, m, r0, z, psi);
+            orc_dot_exact(S.n, m, r0, w, sigma);
+            orc_dot_exact(S.n, m, r0, s, delta);
+            MINV(w, wh);
+            orc_spmv(A, m, wh, t);
+            for (int c = 0; c < m; ++c) {
+                beta[c] = (alpha[c] / omega[c]) * (rhon[c] / rho[c]);
+                den[c] = (sigma[c] + beta[c] * delta[c]) - (beta[c] * omega[c]) * psi[c];
+                alpha[c] = rhon[c] / den[c];
+                rho[c] = rhon[c];
+            }
+            bc = bad_col(NULL, beta, m);
+            if (bc >= 0) { rep->breakdown = 3; rep->breakdown_col = bc; break; }
+            bc = bad_col(den, alpha, m);
+            if (bc >= 0) { rep->breakdown = 1; rep->breakdown_col = bc; ++it; break; }
+        }
     } else {
         it = -1;
     }
@@ -598,5 +825,8 @@ done:
     free(theta); free(eta); free(pi); free(sigma); free(res2); free(den);
     free(r); free(r0); free(tmp); free(p); free(v); free(s); free(t); free(z); free(vh); free(th);
     free(rt); free(q); free(w); free(y); free(tmp2);
-    return method < 0 || method > 2 ? -1 : 0;
+    free(two); free(half); free(sigmap); free(tau); free(gam); free(kap); free(nu); free(cz2); free(cz3);
+    free(ndelta); free(u); free(f0); free(ph); free(sh); free(qh); free(rh); free(wh); free(zh);
+#undef MINV
+    return 0;
 }

@@ -61,6 +61,9 @@ void orc_rhs(int64_t n, int m, uint64_t seed, double* b);
 
 /* ---- kernels ------------------------------------------------------------ */
 void orc_spmv(const orc_csr* a, int m, const double* x, double* y);
+/* y = A^T x: y = 0, then rows i ascending, y(col[k],c) += val[k]*x(i,c)
+ * (spmv_transpose, spmv.cpp:76-90) */
+void orc_spmv_transpose(const orc_csr* a, int m, const double* x, double* y);
 /* out[e] = ((0 + c[0][e%m]*src[0][e]) + c[1][e%m]*src[1][e]) + ... */
 void orc_update(int64_t n, int m, int nterms, const double* const* coeff,
                 const double* const* src, double* out);
@@ -70,7 +73,8 @@ void orc_dot_exact(int64_t n, int m, const double* a, const double* b, double* o
 double orc_sum_exact(int64_t n, const double* v);
 
 /* ---- solver ------------------------------------------------------------- */
-enum { ORC_BICGSTAB = 0, ORC_RBICGSTAB = 1, ORC_PIPEBICGSTAB = 2 };
+enum { ORC_BICGSTAB = 0, ORC_RBICGSTAB = 1, ORC_PIPEBICGSTAB = 2,
+       ORC_IBICGSTAB = 3, ORC_PBICGSTAB = 4, ORC_PPIPEBICGSTAB = 5 };
 enum { ORC_MERGED = 0, ORC_BASIC = 1 };
 
 typedef struct {
@@ -86,6 +90,14 @@ typedef struct {
 int orc_solve(const orc_csr* a, int m, const double* b, double* x, int method,
               int formulation, double tol, int fixed, int maxit, double* hist,
               orc_report* rep);
+/* Same with an explicit preconditioner: precond_alpha 0 =
+ * none (BiCGStab, IBiCGStab, PipeBiCGStab), 2 = identity (one copy), even
+ * alpha >= 4 = synthetic(alpha): alpha/2 scale passes by 2.0 / 0.5 whose
+ * product is exactly 1.  orc_solve uses 2 for the preconditioned methods. */
+int orc_solve_pc(const orc_csr* a, int m, const double* b, double* x, int method,
+                 int formulation, int precond_alpha, double tol, int fixed, int maxit,
+                 double* hist, orc_report* rep);
+int orc_method_preconditioned(int method);
 
 int orc_num_threads(void);
 

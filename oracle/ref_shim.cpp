@@ -109,6 +109,17 @@ extern "C" int ref_spmv(int64_t n, const int64_t* off, const int32_t* col, const
     } catch (const std::exception& e) { g_err = e.what(); return 1; }
 }
 
+extern "C" int ref_spmv_transpose(int64_t n, const int64_t* off, const int32_t* col, const double* val, int m,
+                                  const double* x, double* y) {
+    try {
+        CsrMatrix A = make_csr(n, off, col, val);
+        MultiVector X = make_mv(n, m, x), Y(n, m);
+        core::spmv_transpose(A, X, Y, nullptr);
+        std::memcpy(y, Y.data.data(), sizeof(double) * n * m);
+        return 0;
+    } catch (const std::exception& e) { g_err = e.what(); return 1; }
+}
+
 extern "C" double ref_spmv_traffic_bytes(int64_t n, int64_t nnz, int m) {
     CsrMatrix A;
     A.n_rows = n;

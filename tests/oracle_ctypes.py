@@ -31,7 +31,7 @@ class OrcReport(C.Structure):
                 ("breakdown_iter", C.c_int), ("breakdown_col", C.c_int)]
 
 
-METHODS = {"bicgstab": 0, "rbicgstab": 1, "pipebicgstab": 2}
+METHODS = {"bicgstab": 0, "rbicgstab": 1, "pipebicgstab": 2, "ibicgstab": 3, "pbicgstab": 4, "ppipebicgstab": 5}
 FORMULATIONS = {"merged": 0, "basic": 1, "fused": 0}  # fused rounds exactly like merged
 
 
@@ -67,6 +67,10 @@ def orc() -> C.CDLL:
                                    C.POINTER(C.c_void_p), _f64p]
         lib.orc_solve.argtypes = [C.POINTER(OrcCsr), C.c_int, _f64p, _f64p, C.c_int, C.c_int,
                                   C.c_double, C.c_int, C.c_int, _f64p, C.POINTER(OrcReport)]
+        lib.orc_solve_pc.argtypes = [C.POINTER(OrcCsr), C.c_int, _f64p, _f64p, C.c_int, C.c_int, C.c_int,
+                                     C.c_double, C.c_int, C.c_int, _f64p, C.POINTER(OrcReport)]
+        lib.orc_method_preconditioned.argtypes = [C.c_int]
+        lib.orc_spmv_transpose.argtypes = [C.POINTER(OrcCsr), C.c_int, _f64p, _f64p]
         lib.orc_num_threads.restype = C.c_int
         _orc = lib
     return _orc
@@ -85,6 +89,7 @@ def ref() -> C.CDLL:
                                             C.c_void_p, C.c_void_p, C.c_void_p]
         lib.ref_validate.argtypes = [C.c_int64, _i64p, _i32p, _f64p]
         lib.ref_spmv.argtypes = [C.c_int64, _i64p, _i32p, _f64p, C.c_int, _f64p, _f64p, C.c_int]
+        lib.ref_spmv_transpose.argtypes = [C.c_int64, _i64p, _i32p, _f64p, C.c_int, _f64p, _f64p]
         lib.ref_spmv_traffic_bytes.restype = C.c_double
         lib.ref_spmv_traffic_bytes.argtypes = [C.c_int64, C.c_int64, C.c_int]
         lib.ref_solve.argtypes = [C.c_int, C.c_int64, _i64p, _i32p, _f64p, C.c_int, _f64p, _f64p,
@@ -160,6 +165,13 @@ def spmv(a: Csr, x: np.ndarray, m: int) -> np.ndarray:
     return y
 
 
+def spmv_transpose(a: Csr, x: np.ndarray, m: int) -> np.ndarray:
+    y = np.empty(a.n * m)
+    s = a._orc()
+    orc().orc_spmv_transpose(C.byref(s), m, np.ascontiguousarray(x, dtype=np.float64), y)
+    return y
+
+
 def dot_exact(a: np.ndarray, b: np.ndarray, m: int) -> np.ndarray:
     out = np.empty(m)
     n = a.size // m
@@ -181,15 +193,21 @@ def update(n: int, m: int, terms, out: np.ndarray) -> None:
     orc().orc_update(n, m, nt, cs, vs, out)
 
 
+def preconditioned(method: str) -> bool:
+    return bool(orc().orc_method_preconditioned(METHODS[method]))
+
+
 def solve(a: Csr, b: np.ndarray, m: int, method="bicgstab", formulation="merged", tol=1e-8,
-          fixed=False, maxit=1000, x0=None):
+          fixed=False, maxit=1000, x0=None, precond_alpha=None):
+    """precond_alpha None: identity (2) for the preconditioned methods, else none."""
     x = np.zeros(a.n * m) if x0 is None else np.array(x0, dtype=np.float64)
     hist = np.full((maxit + 1) * m, np.nan)
     rep = OrcReport()
     s = a._orc()
-    rc = orc().orc_solve(C.byref(s), m, np.ascontiguousarray(b), x, METHODS[method],
-                         FORMULATIONS[formulation], tol, int(bool(fixed)), maxit, hist, C.byref(rep))
-    assert rc == 0
+    pa = (2 if preconditioned(method) else 0) if precond_alpha is None else precond_alpha
+    rc = orc().orc_solve_pc(C.byref(s), m, np.ascontiguousarray(b), x, METHODS[method],
+                            FORMULATIONS[formulation], pa, tol, int(bool(fixed)), maxit, hist, C.byref(rep))
+    assert rc == 0, rc
     its = rep.iterations
     return {
         "x": x,
@@ -219,6 +237,13 @@ def ref_gen_poisson_7pt(nx, ny, nz) -> Csr:
 def ref_spmv(a: Csr, x: np.ndarray, m: int, threads: int = 1) -> np.ndarray:
     y = np.empty(a.n * m)
     rc = ref().ref_spmv(a.n, a.off, a.col, a.val, m, np.ascontiguousarray(x), y, threads)
+    assert rc == 0, ref().ref_last_error()
+    return y
+
+
+def ref_spmv_transpose(a: Csr, x: np.ndarray, m: int) -> np.ndarray:
+    y = np.empty(a.n * m)
+    rc = ref().ref_spmv_transpose(a.n, a.off, a.col, a.val, m, np.ascontiguousarray(x), y)
     assert rc == 0, ref().ref_last_error()
     return y
 

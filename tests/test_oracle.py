@@ -154,7 +154,7 @@ def test_exact_dot_thread_independent():
 # --------------------------------------------------------------------------
 # solver contract (SPEC.md:227-278 known answers)
 # --------------------------------------------------------------------------
-METHODS = ["bicgstab", "rbicgstab", "pipebicgstab"]
+METHODS = ["bicgstab", "rbicgstab", "pipebicgstab", "ibicgstab", "pbicgstab", "ppipebicgstab"]
 
 
 @pytest.mark.parametrize("method", METHODS)
@@ -229,7 +229,7 @@ def test_pipelined_basic_vs_merged_close():
 
 
 @pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
-@pytest.mark.parametrize("method", METHODS)
+@pytest.mark.parametrize("method", METHODS[:3])
 def test_oracle_vs_reference_kernel_solver(method):
     """The reference's own kernels (naive, thread-blocked dots) give the same
     solve to rounding: iteration counts within a few, solutions close."""
@@ -259,3 +259,86 @@ def test_configs_converge_small():
     a = O.gen_banded(20_000, 2000, 16, 32, 4)
     r = O.solve(a, O.rhs(a.n, 2, 4), 2, "bicgstab", tol=1e-10)
     assert r["converged"] and r["iterations"] < 40
+
+
+# --------------------------------------------------------------------------
+# IBiCGStab (Alg. 3), PBiCGStab (Alg. 5),
+# PPipeBiCGStab (Alg. 7) and the synthetic(alpha) preconditioner
+# --------------------------------------------------------------------------
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("m", [1, 3, 8])
+def test_spmv_transpose_bitwise_vs_reference(m):
+    """orc_spmv_transpose restates core::spmv_transpose (spmv.cpp:76-90):
+    pinned bit for bit against the reference compiled from its sources."""
+    for a in (O.gen_stencil("stencil27", 9, 8, 7, seed=2), O.gen_banded(5000, 700, 16, 32, 4),
+              O.gen_stencil("convdiff7", 11, 6, 5)):
+        x = np.random.default_rng(m).standard_normal(a.n * m)
+        assert np.array_equal(O.spmv_transpose(a, x, m), O.ref_spmv_transpose(a, x, m))
+
+
+def test_spmv_transpose_is_transpose():
+    a = O.gen_stencil("convdiff7", 7, 6, 5)
+    x = np.random.default_rng(0).standard_normal(a.n * 2)
+    want = (a.to_scipy().T @ x.reshape(a.n, 2)).reshape(-1)
+    assert np.allclose(O.spmv_transpose(a, x, 2), want, rtol=1e-13, atol=1e-13)
+
+
+def test_pbicgstab_identity_equals_bicgstab_bitwise():
+    """Alg. 5 with M^-1 = I is Alg. 2 operation for operation (the x update
+    reads p^ = p and s^ = s)."""
+    a = O.gen_stencil("convdiff7", 14, 12, 10)
+    b = O.rhs(a.n, 3, 1)
+    r1 = O.solve(a, b, 3, "bicgstab")
+    r2 = O.solve(a, b, 3, "pbicgstab")
+    assert r1["iterations"] == r2["iterations"] and r1["converged"]
+    assert np.array_equal(r1["hist"], r2["hist"]) and np.array_equal(r1["x"], r2["x"])
+
+
+@pytest.mark.parametrize("method", ["rbicgstab", "pbicgstab", "ppipebicgstab"])
+@pytest.mark.parametrize("alpha", [4, 6, 8])
+def test_synthetic_preconditioner_is_bitwise_identity(method, alpha):
+    """synthetic(alpha) scales by 2.0 / 0.5 (product exactly 1):
+    the iterates equal the identity preconditioner's bit for bit."""
+    a = O.gen_stencil("poisson7", 12, 11, 10)
+    b = O.rhs(a.n, 2, 0)
+    r1 = O.solve(a, b, 2, method, precond_alpha=2)
+    r2 = O.solve(a, b, 2, method, precond_alpha=alpha)
+    assert r1["iterations"] == r2["iterations"] and r1["converged"]
+    assert np.array_equal(r1["hist"], r2["hist"]) and np.array_equal(r1["x"], r2["x"])
+
+
+def test_preconditioner_presence_mismatch_rejected():
+    """preconditioned ids require a preconditioner, the others reject one."""
+    a = O.gen_stencil("poisson7", 4, 4, 4)
+    b = O.rhs(a.n, 1, 0)
+    s = a._orc()
+    for method, pa in [("bicgstab", 2), ("ibicgstab", 4), ("pbicgstab", 0), ("ppipebicgstab", 3)]:
+        x = np.zeros(a.n)
+        hist = np.zeros(11)
+        rep = O.OrcReport()
+        rc = O.orc().orc_solve_pc(O.C.byref(s), 1, b, x, O.METHODS[method], 0, pa, 1e-8, 0, 10, hist,
+                                  O.C.byref(rep))
+        assert rc == -2, method
+
+
+def test_ibicgstab_residual_identity():
+    """Alg. 3's convergence quantity nu - omega*theta is ||r_{j+1}||^2."""
+    a = O.gen_stencil("convdiff7", 24, 24, 1)
+    b = O.rhs(a.n, 1, 0)
+    sp = a.to_scipy()
+    for its in range(1, 16):
+        r = O.solve(a, b, 1, "ibicgstab", fixed=True, maxit=its)
+        res = b - sp @ r["x"]
+        h = r["hist"][its, 0] ** 2 * np.dot(b, b)
+        assert abs(h - np.dot(res, res)) <= 1e-10 * np.dot(b, b)
+
+
+@pytest.mark.parametrize("method", ["ibicgstab", "pbicgstab", "ppipebicgstab"])
+def test_new_methods_converge_like_classical(method):
+    """Cross-method equivalence: same solution within 1e-6."""
+    a = O.gen_stencil("convdiff7", 16, 16, 16)
+    b = O.rhs(a.n, 2, 1)
+    ref = O.solve(a, b, 2, "bicgstab", tol=1e-10)
+    r = O.solve(a, b, 2, method, tol=1e-10)
+    assert r["converged"] and abs(r["iterations"] - ref["iterations"]) <= 10
+    assert np.max(np.abs(r["x"] - ref["x"])) <= 1e-6 * np.max(np.abs(ref["x"]))
