@@ -142,8 +142,11 @@ int mbg_execute_group(mbg_ctx* ctx, const mbg_statement* stmts, int nstmts, mbg_
 
 /* ---- solver --------------------------------------------- */
 #define MBG_BICGSTAB 0
-#define MBG_RBICGSTAB 1
+#define MBG_RBICGSTAB 1       /* preconditioned (Alg. 6) */
 #define MBG_PIPEBICGSTAB 2
+#define MBG_IBICGSTAB 3       /* Improved, Alg. 3; needs A^T r0 (single GPU) */
+#define MBG_PBICGSTAB 4       /* preconditioned, Alg. 5 */
+#define MBG_PPIPEBICGSTAB 5   /* preconditioned Pipelined, Alg. 7 */
 #define MBG_MERGED 0
 #define MBG_BASIC 1
 /* Merged + beyond-paper fusions: dots fused
@@ -173,6 +176,15 @@ typedef struct mbg_report {
 int mbg_solve(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* b, mbg_mv* x, int method,
               int formulation, double tol, int fixed, int max_iters, double* hist,
               mbg_report* report);
+/* Explicit preconditioner: precond_alpha 0 = none (required
+ * by BiCGStab, IBiCGStab, PipeBiCGStab), 2 = identity M^-1 (one copy per
+ * application), even alpha >= 4 = synthetic(alpha): alpha/2 scale passes by
+ * 2.0 / 0.5 whose product is exactly 1 (alpha transfers per application).
+ * The preconditioned methods (RBiCGStab, PBiCGStab, PPipeBiCGStab) require
+ * alpha >= 2; mbg_solve passes 2 for them and 0 otherwise. */
+int mbg_solve_pc(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* b, mbg_mv* x, int method,
+                 int formulation, int precond_alpha, double tol, int fixed, int max_iters,
+                 double* hist, mbg_report* report);
 /* Same solve with HOST b/x buffers (n*m doubles): uploads b and x0, solves,
  * downloads x.  The reference-facing end-to-end entry point. */
 int mbg_solve_host(mbg_ctx* ctx, const mbg_csr* a, int m, const double* b_host, double* x_host,
@@ -190,6 +202,13 @@ int mbg_solve_profile(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* b, mbg_mv* x
  * SpMVs, reduction points and dots per reduction (up to 8 entries). */
 int mbg_method_schedule(int method, int formulation, int* reads, int* writes, int* spmvs,
                         int* nreductions, int* dots_per_reduction);
+/* SPEC.md:236-244 form: vector transfers WITHOUT preconditioner traffic (e.g.
+ * PPipeBiCGStab merged 34) plus the M^-1 applications per iteration (each
+ * costs precond_alpha transfers; 0 when the fused formulation elides identity
+ * copies).  mbg_method_schedule above = this + 2 transfers per identity copy. */
+int mbg_method_schedule_pc(int method, int formulation, int precond_alpha, int* reads, int* writes,
+                           int* spmvs, int* precond_applications, int* nreductions,
+                           int* dots_per_reduction);
 
 /* ---- config generators (host) --------------------------------------------
  * kind 0 Poisson 7-pt (gen_poisson_7pt), 1 conv-diff 7-pt, 2 27-pt perturbed.

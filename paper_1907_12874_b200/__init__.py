@@ -36,7 +36,10 @@ import numpy as np
 
 from ._lib import BreakdownError, MbgReport, MbgStatement, build, check, lib  # noqa: F401
 
-METHODS = {"bicgstab": 0, "rbicgstab": 1, "pipebicgstab": 2}
+METHODS = {"bicgstab": 0, "rbicgstab": 1, "pipebicgstab": 2, "ibicgstab": 3, "pbicgstab": 4,
+           "ppipebicgstab": 5}
+# these take (and require) a preconditioner M^-1
+PRECONDITIONED = ("rbicgstab", "pbicgstab", "ppipebicgstab")
 FORMULATIONS = {"merged": 0, "basic": 1, "fused": 2}
 
 
@@ -333,6 +336,18 @@ def method_schedule(method: str, formulation: str = "merged") -> dict:
     return {"reads": r.value, "writes": w.value, "spmvs": s.value, "reductions": list(dots[: min(k.value, 8)])}
 
 
+def method_schedule_pc(method: str, formulation: str = "merged", precond_alpha: int | None = None) -> dict:
+    """SPEC.md:236-244 form: vector transfers without the preconditioner, plus
+    the M^-1 applications per iteration (each worth precond_alpha transfers)."""
+    pa = (2 if method in PRECONDITIONED else 0) if precond_alpha is None else precond_alpha
+    r, w, s, ap, k = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    dots = (C.c_int * 8)()
+    check(lib().mbg_method_schedule_pc(METHODS[method], FORMULATIONS[formulation], pa, C.byref(r), C.byref(w),
+                                       C.byref(s), C.byref(ap), C.byref(k), dots))
+    return {"vec": r.value + w.value, "reads": r.value, "writes": w.value, "spmvs": s.value,
+            "precond": ap.value, "reductions": list(dots[: min(k.value, 8)])}
+
+
 @dataclass
 class SolveReport:
     iterations: int
@@ -361,13 +376,21 @@ def _report(rep: MbgReport, hist: np.ndarray | None, m: int, maxit: int) -> Solv
 
 def solve(ctx: Context, a: DeviceCsr, b: MultiVector, x: MultiVector, method: str = "bicgstab",
           formulation: str = "merged", tol: float = 1e-8, fixed: bool = False, max_iters: int = 1000,
-          history: bool = True) -> SolveReport:
-    """Device-resident solve; x holds x0 on entry and the solution on exit."""
+          history: bool = True, precond_alpha: int | None = None) -> SolveReport:
+    """Device-resident solve; x holds x0 on entry and the solution on exit.
+
+    precond_alpha: None = identity M^-1 for the preconditioned methods (none
+    otherwise); 2 = identity; even >= 4 = synthetic(alpha) (SPEC.md:211-216)."""
     m = b.n_cols
     hist = np.full((max_iters + 1) * m, np.nan) if history else None
     rep = MbgReport()
-    rc = lib().mbg_solve(ctx.h, a.h, b.h, x.h, METHODS[method], FORMULATIONS[formulation], tol, int(bool(fixed)),
-                         max_iters, _ptr(hist) if hist is not None else None, C.byref(rep))
+    if precond_alpha is None:
+        rc = lib().mbg_solve(ctx.h, a.h, b.h, x.h, METHODS[method], FORMULATIONS[formulation], tol,
+                             int(bool(fixed)), max_iters, _ptr(hist) if hist is not None else None, C.byref(rep))
+    else:
+        rc = lib().mbg_solve_pc(ctx.h, a.h, b.h, x.h, METHODS[method], FORMULATIONS[formulation],
+                                int(precond_alpha), tol, int(bool(fixed)), max_iters,
+                                _ptr(hist) if hist is not None else None, C.byref(rep))
     check(rc)
     return _report(rep, hist, m, max_iters)
 

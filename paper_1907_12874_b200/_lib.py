@@ -102,10 +102,12 @@ def lib() -> C.CDLL:
         "mbg_split_basic_traffic": (i32, [vp, i32, i32, ip, ip, ip]),
         "mbg_execute_group": (i32, [vp, vp, i32, vp, i32, vp, i32]),
         "mbg_solve": (i32, [vp, vp, vp, vp, i32, i32, dbl, i32, i32, vp, C.POINTER(MbgReport)]),
+        "mbg_solve_pc": (i32, [vp, vp, vp, vp, i32, i32, i32, dbl, i32, i32, vp, C.POINTER(MbgReport)]),
         "mbg_solve_host": (i32, [vp, vp, i32, vp, vp, i32, i32, dbl, i32, i32, vp, C.POINTER(MbgReport)]),
         "mbg_solve_profile": (i32, [vp, vp, vp, vp, i32, i32, dbl, i32, i32, C.c_char_p, i32,
                                     C.POINTER(MbgReport)]),
         "mbg_method_schedule": (i32, [i32, i32, ip, ip, ip, ip, ip]),
+        "mbg_method_schedule_pc": (i32, [i32, i32, i32, ip, ip, ip, ip, ip, ip]),
         "mbg_gen_stencil": (i32, [i32, i32, i32, i32, C.c_uint64, C.POINTER(C.c_int64), vp, vp, vp]),
         "mbg_gen_banded": (i32, [i64, i64, i32, i32, C.c_uint64, C.POINTER(C.c_int64), vp, vp, vp]),
         "mbg_gen_rhs": (i32, [i64, i32, C.c_uint64, vp]),

@@ -188,6 +188,44 @@ static void csr_arrays_to_device(mbg_ctx* ctx, mbg_csr* a, int64_t n, const std:
     MBG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+namespace mbg {
+// A^T for IBiCGStab's f0 = A^T r0 (core::spmv_transpose, spmv.cpp:76-90): a
+// counting sort by column that visits rows in ascending order, so row j of
+// A^T lists its source rows ascending and the ordinary SpMM adds the terms of
+// y_j in exactly the reference's serial order.  Built once, cached on A.
+const mbg_csr* csr_transpose(mbg_ctx* ctx, const mbg_csr* a) {
+    auto* am = const_cast<mbg_csr*>(a);
+    if (am->transposed) return am->transposed.get();
+    const int64_t n = a->n, nnz = a->nnz;
+    std::vector<int32_t> off(static_cast<size_t>(n) + 1), col(static_cast<size_t>(nnz));
+    std::vector<double> val(static_cast<size_t>(nnz));
+    MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+    MBG_CUDA(cudaMemcpy(off.data(), a->off.p, off.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (nnz) {
+        MBG_CUDA(cudaMemcpy(col.data(), a->col.p, col.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        MBG_CUDA(cudaMemcpy(val.data(), a->val.p, val.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    std::vector<int32_t> toff(static_cast<size_t>(n) + 1, 0), tcol(static_cast<size_t>(nnz));
+    std::vector<double> tval(static_cast<size_t>(nnz));
+    for (int64_t k = 0; k < nnz; ++k) ++toff[static_cast<size_t>(col[k]) + 1];
+    for (int64_t j = 0; j < n; ++j) toff[j + 1] += toff[j];
+    std::vector<int32_t> pos(toff.begin(), toff.end() - 1);
+    for (int64_t i = 0; i < n; ++i)
+        for (int32_t k = off[i]; k < off[i + 1]; ++k) {
+            const int32_t q = pos[col[k]]++;
+            tcol[q] = static_cast<int32_t>(i);
+            tval[q] = val[k];
+        }
+    auto t = std::make_unique<mbg_csr>();
+    t->ctx = ctx;
+    t->device = ctx->device;
+    t->n_global = n;
+    csr_arrays_to_device(ctx, t.get(), n, toff, tcol.data(), tval.data(), nnz);
+    am->transposed = std::move(t);
+    return am->transposed.get();
+}
+}  // namespace mbg
+
 static void csr_to_device(mbg_ctx* ctx, mbg_csr* a, int64_t n, const int64_t* off, const int32_t* col,
                           const double* val) {
     const int64_t nnz = off[n];
@@ -518,8 +556,9 @@ static void check_solve_args(mbg_ctx* ctx, const mbg_csr* a, int m, double tol, 
 }
 
 static void do_solve(mbg_ctx* ctx, const mbg_csr* a, int m, const double* b, double* x, int method,
-                     int formulation, double tol, int fixed, int max_iters, double* hist, mbg_report* report) {
-    Solver s(ctx, a, m, method, formulation, tol, fixed, max_iters);
+                     int formulation, double tol, int fixed, int max_iters, double* hist, mbg_report* report,
+                     int precond_alpha = -1) {
+    Solver s(ctx, a, m, method, formulation, tol, fixed, max_iters, precond_alpha);
     s.run(b, x);
     mbg_report rep;
     s.report(hist, &rep);
@@ -540,6 +579,19 @@ extern "C" int mbg_solve(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* b, mbg_mv
         check_solve_args(ctx, a, b->m, tol, fixed, max_iters);
         if (b->n != a->n || x->n != a->n || b->m != x->m) throw Invalid("solve: shape mismatch");
         do_solve(ctx, a, b->m, b->data.p, x->data.p, method, formulation, tol, fixed, max_iters, hist, report);
+    });
+}
+
+extern "C" int mbg_solve_pc(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* b, mbg_mv* x, int method,
+                            int formulation, int precond_alpha, double tol, int fixed, int max_iters, double* hist,
+                            mbg_report* report) {
+    return guarded([&] {
+        if (!b || !x) throw Invalid("solve: null multivector");
+        if (precond_alpha < 0) throw Invalid("solve: precond_alpha must be >= 0");
+        check_solve_args(ctx, a, b->m, tol, fixed, max_iters);
+        if (b->n != a->n || x->n != a->n || b->m != x->m) throw Invalid("solve: shape mismatch");
+        do_solve(ctx, a, b->m, b->data.p, x->data.p, method, formulation, tol, fixed, max_iters, hist, report,
+                 precond_alpha);
     });
 }
 

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "mbstab_b200.h"
@@ -137,6 +138,7 @@ struct mbg_csr {
         mbg::DevBuf<int32_t> send_rows;       // local rows packed for this peer
     };
     std::vector<Peer> peers;
+    std::unique_ptr<mbg_csr> transposed;      // A^T, built on first use (IBiCGStab f0 = A^T r0)
 };
 
 struct mbg_mv {

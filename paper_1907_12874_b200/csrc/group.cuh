@@ -26,7 +26,7 @@
 
 namespace mbg {
 
-constexpr int GMAX_IN = 10, GMAX_OUT = 6, GMAX_CO = 8, GMAX_DOT = 4;
+constexpr int GMAX_IN = 10, GMAX_OUT = 6, GMAX_CO = 8, GMAX_DOT = 8;
 
 struct GroupArgs {
     int64_t len;                 // n*m
@@ -36,7 +36,6 @@ struct GroupArgs {
     const double* coef[GMAX_CO]; // device arrays of m doubles
     int64_t* slot[GMAX_DOT];     // long accumulators: m * NSLOT words each
     const int* ctl;              // ctl[0] != 0: solve stopped -> no-op
-    PostArgs post;               // scalar step run by the last block (scalar.cuh)
 };
 
 __device__ __forceinline__ double fmadd_rn(double acc, double c, double v) {
@@ -234,6 +233,124 @@ struct PPipeG45 {
         prod[3] = __dmul_rn(r0, in[8]);
     }
 };
+
+// ---- the other three methods of the paper ----------
+// Improved BiCGStab, Alg. 3 line 8:
+//   z = alpha'*r + cz2*z + cz3*v ; v = 1*u + beta'*v + (-delta')*q ; s = 1*r + (-alpha')*v
+struct PIbcgG1 {
+    static constexpr const char* NAME = "ibcg_g1";
+    static constexpr int NIN = 5, NOUT = 3, NCO = 6, NDOT = 0;
+    // in: r z v u q ; out: z v s ; co: alpha' cz2 cz3 beta' -delta' -alpha'
+    __device__ static void run(const double* in, double* out, double*, const double* co) {
+        const double r = in[0], z = in[1], v = in[2], u = in[3], q = in[4];
+        out[0] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, co[0], r), co[1], z), co[2], v);
+        const double vn = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, u), co[3], v), co[4], q);
+        out[1] = vn;
+        out[2] = fmadd_rn(fmadd_rn(0.0, 1.0, r), co[5], vn);
+    }
+};
+// Alg. 3 line 10: t = 1*u + (-alpha)*q ;
+//   phi=(r0,s) pi=(r0,q) gamma=(f0,s) eta=(f0,t) theta=(s,t) kappa=(t,t) nu=(s,s)
+// Seven expansions per column: one column per thread (VEC = 1) keeps them in registers.
+struct PIbcgG2 {
+    static constexpr const char* NAME = "ibcg_g2";
+    static constexpr int NIN = 5, NOUT = 1, NCO = 1, NDOT = 7, UNROLL = 1, VEC = 1;
+    // in: u q r0 s f0 ; out: t ; co: -alpha
+    __device__ static void run(const double* in, double* out, double* prod, const double* co) {
+        const double u = in[0], q = in[1], r0 = in[2], s = in[3], f0 = in[4];
+        const double t = fmadd_rn(fmadd_rn(0.0, 1.0, u), co[0], q);
+        out[0] = t;
+        prod[0] = __dmul_rn(r0, s);
+        prod[1] = __dmul_rn(r0, q);
+        prod[2] = __dmul_rn(f0, s);
+        prod[3] = __dmul_rn(f0, t);
+        prod[4] = __dmul_rn(s, t);
+        prod[5] = __dmul_rn(t, t);
+        prod[6] = __dmul_rn(s, s);
+    }
+};
+// Alg. 3 line 13: r = 1*s + (-omega)*t ; x = 1*x + 1*z + omega*s
+struct PIbcgG3 {
+    static constexpr const char* NAME = "ibcg_g3";
+    static constexpr int NIN = 4, NOUT = 2, NCO = 2, NDOT = 0;   // in: s t x z ; out: r x ; co: -omega omega
+    __device__ static void run(const double* in, double* out, double*, const double* co) {
+        out[0] = fmadd_rn(fmadd_rn(0.0, 1.0, in[0]), co[0], in[1]);
+        out[1] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, in[2]), 1.0, in[3]), co[1], in[0]);
+    }
+};
+// Preconditioned BiCGStab, Alg. 5: r = 1*s + (-omega)*t ; rho' = (r, r0)
+struct PRDot {
+    static constexpr const char* NAME = "pbcg_r";
+    static constexpr int NIN = 3, NOUT = 1, NCO = 1, NDOT = 1;   // in: s t r0 ; co: -omega
+    __device__ static void run(const double* in, double* out, double* prod, const double* co) {
+        const double r = fmadd_rn(fmadd_rn(0.0, 1.0, in[0]), co[0], in[1]);
+        out[0] = r;
+        prod[0] = __dmul_rn(r, in[2]);
+    }
+};
+// Preconditioned Pipelined BiCGStab, Alg. 7 line 4:
+//   ph = 1*rh + beta*ph + nbo*sh ; sh = 1*wh + beta*sh + nbo*zh ; qh = 1*rh + (-alpha)*sh
+struct PPpG1 {
+    static constexpr const char* NAME = "ppipe_g1";
+    static constexpr int NIN = 5, NOUT = 3, NCO = 3, NDOT = 0;   // in: rh ph sh wh zh ; co: beta nbo -alpha
+    __device__ static void run(const double* in, double* out, double*, const double* co) {
+        const double rh = in[0], ph = in[1], sh = in[2], wh = in[3], zh = in[4];
+        out[0] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, rh), co[0], ph), co[1], sh);
+        const double shn = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, wh), co[0], sh), co[1], zh);
+        out[1] = shn;
+        out[2] = fmadd_rn(fmadd_rn(0.0, 1.0, rh), co[2], shn);
+    }
+};
+// Alg. 7 line 5: s, z, q, y as Alg. 4 line 4 (no p) ; theta=(q,y) phi=(y,y) pi=(q,q)
+struct PPpG2 {
+    static constexpr int UNROLL = 1;
+    static constexpr const char* NAME = "ppipe_g2";
+    static constexpr int NIN = 6, NOUT = 4, NCO = 3, NDOT = 3;   // in: r s w z t v ; out: s z q y ; co: beta nbo -alpha
+    __device__ static void run(const double* in, double* out, double* prod, const double* co) {
+        const double r = in[0], s = in[1], w = in[2], z = in[3], t = in[4], v = in[5];
+        const double sn = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, w), co[0], s), co[1], z);
+        const double zn = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, t), co[0], z), co[1], v);
+        const double q = fmadd_rn(fmadd_rn(0.0, 1.0, r), co[2], sn);
+        const double y = fmadd_rn(fmadd_rn(0.0, 1.0, w), co[2], zn);
+        out[0] = sn; out[1] = zn; out[2] = q; out[3] = y;
+        prod[0] = __dmul_rn(q, y);
+        prod[1] = __dmul_rn(y, y);
+        prod[2] = __dmul_rn(q, q);
+    }
+};
+// Alg. 7 line 14: x = 1*x + alpha*ph + omega*qh ;
+//   rh = 1*qh + (-omega)*wh + (omega*alpha)*zh
+struct PPpG3 {
+    static constexpr const char* NAME = "ppipe_g3";
+    static constexpr int NIN = 5, NOUT = 2, NCO = 4, NDOT = 0;   // in: x ph qh wh zh ; co: alpha omega -omega omega*alpha
+    __device__ static void run(const double* in, double* out, double*, const double* co) {
+        out[0] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, in[0]), co[0], in[1]), co[1], in[2]);
+        out[1] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, in[2]), co[2], in[3]), co[3], in[4]);
+    }
+};
+// Alg. 7 line 15: r = 1*q + (-omega)*y ; w = 1*y + (-omega)*t + (omega*alpha)*v ;
+//   rho'=(r0,r) psi=(r0,z) sigma=(r0,w) delta=(r0,s)
+struct PPpG4 {
+    static constexpr int UNROLL = 1;
+    static constexpr const char* NAME = "ppipe_g4";
+    static constexpr int NIN = 7, NOUT = 2, NCO = 2, NDOT = 4;   // in: q y t v r0 z s ; out: r w ; co: -omega omega*alpha
+    __device__ static void run(const double* in, double* out, double* prod, const double* co) {
+        const double q = in[0], y = in[1], t = in[2], v = in[3], r0 = in[4];
+        const double r = fmadd_rn(fmadd_rn(0.0, 1.0, q), co[0], y);
+        const double w = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, y), co[0], t), co[1], v);
+        out[0] = r; out[1] = w;
+        prod[0] = __dmul_rn(r0, r);
+        prod[1] = __dmul_rn(r0, in[5]);
+        prod[2] = __dmul_rn(r0, w);
+        prod[3] = __dmul_rn(r0, in[6]);
+    }
+};
+
+// Widest packet a program may use (2 unless it declares VEC = 1).
+template <class P, class = void>
+struct vec_of { static constexpr int value = 2; };
+template <class P>
+struct vec_of<P, decltype(void(P::VEC))> { static constexpr int value = P::VEC; };
 
 // Register-pipelined loads for dot-heavy, byte-light programs (the dots'
 // TwoSum chains would otherwise serialise with the memory latency).
@@ -448,7 +565,6 @@ __global__ void __launch_bounds__(256, minblocks_of<P>::value) group_kernel(Grou
                                 },
                                 sh_dyn);
     }
-    if (a.post.enabled) post_step(a.post, sh_dyn);
 }
 
 // Block size for m columns: m * 2^q <= 256 (m <= 256), else m.

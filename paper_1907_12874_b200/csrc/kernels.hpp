@@ -38,7 +38,6 @@ struct SpmmEpi {
     int kind = 0;
     const double* aux = nullptr;
     int64_t* slot[3] = {nullptr, nullptr, nullptr};
-    PostArgs post{};     // scalar step run by the last block
 };
 int launch_spmm(cudaStream_t st, const SpmmTiles& tl, int64_t nrows, const int32_t* rows, const int32_t* off,
                 const int32_t* col, const double* val, int m, const double* x, double* y, const int* ctl,
@@ -87,16 +86,13 @@ template <class P>
 inline int launch_group(cudaStream_t st, const GroupArgs& a, int num_sms) {
     const int block = group_block(a.m);
     size_t smem = P::NDOT > 0 ? static_cast<size_t>(block) * KEXP * sizeof(double) : 0;
-    if (a.post.enabled) {
-        const size_t need = static_cast<size_t>(a.post.s.nd > 0 ? a.post.s.nd : 1) * a.m * sizeof(double);
-        if (need > smem) smem = need;
-    }
-    const bool vec2 = (a.m % 2 == 0 || a.m == 1) && a.len % 2 == 0;
-    if (vec2) {
-        const int grid =
-            group_grid(reinterpret_cast<const void*>(&group_kernel<P, 2>), block, smem, num_sms, a.len / 2);
-        group_kernel<P, 2><<<grid, block, smem, st>>>(a);
-        return grid;
+    if constexpr (vec_of<P>::value == 2) {
+        if ((a.m % 2 == 0 || a.m == 1) && a.len % 2 == 0) {
+            const int grid =
+                group_grid(reinterpret_cast<const void*>(&group_kernel<P, 2>), block, smem, num_sms, a.len / 2);
+            group_kernel<P, 2><<<grid, block, smem, st>>>(a);
+            return grid;
+        }
     }
     const int grid = group_grid(reinterpret_cast<const void*>(&group_kernel<P, 1>), block, smem, num_sms, a.len);
     group_kernel<P, 1><<<grid, block, smem, st>>>(a);

@@ -1,9 +1,7 @@
 // scalar.cuh -- per-column scalar recurrences of the three BiCGStab variants
 // (ColumnScalars arithmetic, types.hpp:39-83, on the device), convergence,
-// breakdown and iteration control.  Runs either as its own one-block kernel
-// or as the "post" step of the kernel that produced the dots: the last block
-// of that kernel to finish (atomic ticket) performs it, saving a launch per
-// reduction point.
+// breakdown and iteration control, run as a one-block kernel after each
+// reduction point (inside the iteration's CUDA graph).
 #pragma once
 
 #include <climits>
@@ -15,13 +13,18 @@ namespace mbg {
 // ---- scalar bank / control words ------------------------------------------
 enum Scal : int {
     S_ONE, S_MONE, S_BB, S_EPS2, S_RHO, S_ALPHA, S_NALPHA, S_OMEGA, S_NOMEGA,
-    S_BETA, S_NBO, S_OA, S_RES2, NSCAL
+    S_BETA, S_NBO, S_OA, S_RES2,
+    // Improved BiCGStab (Alg. 3) recurrences and group-1 coefficients
+    S_PHI, S_PI, S_SIGMA, S_SIGMAP, S_TAU, S_CZ2, S_CZ3, S_NDELTA,
+    // synthetic preconditioner scale factors (constant rows)
+    S_TWO, S_HALF, NSCAL
 };
 enum Ctl : int {
     C_STOP, C_CONV, C_ITER, C_ITERS, C_BD, C_BDITER, C_BDCOL, C_CONVERGED, NCTL = 16
 };
 enum Point : int {
-    P_SETUP, P_C_ALPHA, P_C_OMEGA, P_C_BETA, P_R_OMEGA, P_R_END, P_P_OMEGA, P_P_BETA
+    P_SETUP, P_C_ALPHA, P_C_OMEGA, P_C_BETA, P_R_OMEGA, P_R_END, P_P_OMEGA, P_P_BETA,
+    P_I_START, P_I_OMEGA
 };
 
 struct ScalArgs {
@@ -30,7 +33,7 @@ struct ScalArgs {
     double* sc;          // NSCAL * m
     int* ctl;
     double* hist;        // (maxit+1) * m
-    int64_t* D[4];       // long accumulators: rounded here (after any cross-GPU allreduce), then cleared
+    int64_t* D[8];       // long accumulators: rounded here (after any cross-GPU allreduce), then cleared
     int nd;
 };
 
@@ -74,7 +77,7 @@ static __device__ __forceinline__ void scalar_block(const ScalArgs& a, double* s
         for (int w = threadIdx.x; w < nslot * NSLOT; w += blockDim.x) base[w] = 0;
     }
 #define SCW(i, v) do { const double _v = (v); scv[i] = _v; sc[(i) * m + c] = _v; } while (0)
-    double d[4] = {0.0, 0.0, 0.0, 0.0};
+    double d[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     if (on)
         for (int i = 0; i < a.nd; ++i) d[i] = s_dots[i * m + c];
     int code1 = 0, code2 = 0;  // breakdown codes for s_bad1 / s_bad2
@@ -93,7 +96,13 @@ static __device__ __forceinline__ void scalar_block(const ScalArgs& a, double* s
                 if (c == 0) { ctl[C_STOP] = 1; ctl[C_CONVERGED] = 1; ctl[C_ITERS] = 0; }
                 return;
             }
-            if (a.method == MBG_PIPEBICGSTAB && on) {
+            if (a.method == MBG_IBICGSTAB && on) {
+                // Alg. 3 line 2: sigma_-1 = pi_0 = tau_0 = 0, sigma_0 = (r0,u0),
+                // rho_0 = alpha_0 = omega_0 = 1, phi_0 = (r0,r0)
+                SCW(S_PHI, d[0]); SCW(S_SIGMA, d[2]); SCW(S_SIGMAP, 0.0); SCW(S_PI, 0.0); SCW(S_TAU, 0.0);
+                SCW(S_RHO, 1.0); SCW(S_ALPHA, 1.0); SCW(S_OMEGA, 1.0);
+            }
+            if ((a.method == MBG_PIPEBICGSTAB || a.method == MBG_PPIPEBICGSTAB) && on) {
                 const double alpha = __ddiv_rn(d[0], d[2]);
                 SCW(S_ALPHA, alpha); SCW(S_NALPHA, -alpha);
                 SCW(S_BETA, 0.0); SCW(S_OMEGA, 0.0);
@@ -147,6 +156,55 @@ static __device__ __forceinline__ void scalar_block(const ScalArgs& a, double* s
                 if (!finite_d(beta)) atomicMin(&s_bad1, c);
             }
             code1 = 3;
+            break;
+        }
+        case P_I_START: {
+            // Alg. 3 lines 4-7 (expression trees pinned in oracle.c)
+            if (on) {
+                const double om = scv[S_OMEGA], al = scv[S_ALPHA], pi = scv[S_PI];
+                const double rhon = __dadd_rn(__dsub_rn(scv[S_PHI], __dmul_rn(om, scv[S_SIGMAP])),
+                                              __dmul_rn(__dmul_rn(om, al), pi));
+                const double delta = __dmul_rn(__ddiv_rn(rhon, scv[S_RHO]), al);
+                const double beta = __ddiv_rn(delta, om);
+                const double tau = __dsub_rn(__dadd_rn(scv[S_SIGMA], __dmul_rn(beta, scv[S_TAU])),
+                                             __dmul_rn(delta, pi));
+                const double an = __ddiv_rn(rhon, tau);
+                if (!finite_d(beta)) atomicMin(&s_bad2, c);
+                if (tau == 0.0 || !finite_d(an)) atomicMin(&s_bad1, c);
+                SCW(S_CZ2, __dmul_rn(beta, __ddiv_rn(an, al)));
+                SCW(S_CZ3, -__dmul_rn(an, delta));
+                SCW(S_NDELTA, -delta);
+                SCW(S_BETA, beta);
+                SCW(S_ALPHA, an); SCW(S_NALPHA, -an);
+                SCW(S_RHO, rhon); SCW(S_TAU, tau);
+            }
+            __syncthreads();
+            if (s_bad2 != INT_MAX) { code2 = 3; break; }
+            code1 = 1;
+            break;
+        }
+        case P_I_OMEGA: {  // d = phi pi gamma eta theta kappa nu   (Alg. 3 lines 10-12)
+            double omega = 0.0, res2 = 0.0;
+            if (on) {
+                const double theta = d[4], kappa = d[5], nu = d[6];
+                const bool lucky = kappa == 0.0 && nu == 0.0;
+                omega = lucky ? 0.0 : __ddiv_rn(theta, kappa);
+                SCW(S_OMEGA, omega); SCW(S_NOMEGA, -omega);
+                res2 = __dsub_rn(nu, __dmul_rn(omega, theta));
+                SCW(S_RES2, res2);
+                if ((kappa == 0.0 && !lucky) || !finite_d(omega)) atomicMin(&s_bad2, c);
+            }
+            __syncthreads();
+            if (s_bad2 != INT_MAX) { code2 = 2; break; }
+            if (on) {
+                SCW(S_SIGMAP, scv[S_SIGMA]);
+                SCW(S_SIGMA, __dsub_rn(d[2], __dmul_rn(omega, d[3])));
+                SCW(S_PHI, d[0]); SCW(S_PI, d[1]);
+                a.hist[static_cast<int64_t>(j + 1) * m + c] = hist_entry(res2, scv[S_BB]);
+                if (!(res2 < scv[S_EPS2])) s_all = 0;
+            }
+            __syncthreads();
+            if (c == 0 && !a.fixed && s_all) ctl[C_CONV] = 1;
             break;
         }
         case P_C_BETA: {
@@ -215,29 +273,5 @@ static __device__ __forceinline__ void scalar_block(const ScalArgs& a, double* s
     if (a.point == P_SETUP && a.maxit <= 0) ctl[C_STOP] = 1;
 }
 
-
-// Post step appended to a dot-producing kernel: the last block to finish runs
-// scalar_block.  Every thread fences its slot atomics before the block takes
-// its ticket; the last block fences again before reading the slots.
-struct PostArgs {
-    int enabled;
-    unsigned int* counter;
-    ScalArgs s;
-};
-
-__device__ __forceinline__ void post_step(const PostArgs& p, double* s_dots) {
-    __shared__ int s_last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned t = atomicAdd(p.counter, 1u);
-        s_last = t == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    scalar_block(p.s, s_dots);
-    if (threadIdx.x == 0) *p.counter = 0u;
-}
 
 }  // namespace mbg

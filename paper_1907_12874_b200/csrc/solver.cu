@@ -32,7 +32,7 @@
 
 namespace mbg {
 
-__global__ void scalar_kernel(ScalArgs a) {
+__global__ void __launch_bounds__(1024) scalar_kernel(ScalArgs a) {
     extern __shared__ double s_dots[];  // nd * m rounded dots
     scalar_block(a, s_dots);
 }
@@ -40,33 +40,64 @@ __global__ void scalar_kernel(ScalArgs a) {
 // ===========================================================================
 // Solver
 // ===========================================================================
+// Vector roles (indices into work_); 14 = x0 staging with halo room.
+enum {
+    V_R, V_R0, V_P, V_V, V_S, V_T, V_Z, V_VH, V_TH, V_RT, V_Q, V_W, V_Y, V_TMP, V_X0,
+    V_U, V_F0, V_PH, V_SH, V_QH, V_RH, V_WH, V_ZH, NWORK
+};
+
 Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulation, double tol,
-               int fixed, int maxit)
+               int fixed, int maxit, int precond_alpha)
     : ctx_(ctx), a_(a), m_(m), method_(method), form_(formulation), tol_(tol), fixed_(fixed),
       maxit_(maxit) {
-    if (method < 0 || method > 2) throw Invalid("solve: unknown method");
+    if (method < 0 || method > 5) throw Invalid("solve: unknown method");
     if (formulation < 0 || formulation > 2) throw Invalid("solve: unknown formulation");
     if (m < 1 || m > 1024) throw Invalid("solve: m must be in [1, 1024]");
     if (maxit < 0) throw Invalid("solve: negative iteration count");
     if (!fixed && !(tol > 0.0)) throw Invalid("solve: tol must be > 0 in converge mode");
+    // preconditioned ids require a preconditioner, the others reject one
+    const bool pre = preconditioned(method);
+    if (precond_alpha < 0) precond_alpha = pre ? 2 : 0;
+    if (pre && (precond_alpha < 2 || precond_alpha % 2))
+        throw Invalid("solve: a preconditioned method needs precond_alpha 2 (identity) or an even synthetic alpha >= 4");
+    if (!pre && precond_alpha != 0) throw Invalid("solve: this method takes no preconditioner");
+    pa_ = precond_alpha;
+    elide_ = formulation == MBG_FUSED && pa_ == 2;
+    if (method == MBG_IBICGSTAB) {
+        if (!a->peers.empty() || a->n_halo)
+            throw Invalid("solve: IBiCGStab needs f0 = A^T r0, supported on a single GPU only");
+        at_ = csr_transpose(ctx, a);
+    }
     n_ = a->n;
     len_ = n_ * m;
     rows_alloc_ = a->n + a->n_halo;
     // only the vectors the method uses (C4 at m=32 is 8.4 GB per vector)
-    static const std::vector<int> need[3] = {
-        {0, 1, 2, 3, 4, 5},                        // r r0 p v s t
-        {0, 1, 3, 4, 5, 6, 7, 8, 9, 10},           // r r0 v s t z vh th rt q (s, q unused when fused)
-        {0, 1, 2, 3, 4, 5, 6, 10, 11, 12, 13}};    // r r0 p v s t z q w y tmp
-    work_.resize(15);
+    std::vector<int> need;
+    switch (method) {
+        case MBG_BICGSTAB: need = {V_R, V_R0, V_P, V_V, V_S, V_T}; break;
+        case MBG_RBICGSTAB:
+            need = {V_R, V_R0, V_V, V_T, V_Z, V_VH, V_TH, V_RT};
+            if (!elide_) need.insert(need.end(), {V_S, V_Q});
+            break;
+        case MBG_PIPEBICGSTAB: need = {V_R, V_R0, V_P, V_V, V_S, V_T, V_Z, V_Q, V_W, V_Y, V_TMP}; break;
+        case MBG_IBICGSTAB: need = {V_R, V_R0, V_V, V_S, V_T, V_Z, V_Q, V_U, V_F0}; break;
+        case MBG_PBICGSTAB:
+            need = {V_R, V_R0, V_P, V_V, V_S, V_T};
+            if (!elide_) need.insert(need.end(), {V_PH, V_SH});
+            break;
+        default:
+            need = {V_R, V_R0, V_V, V_S, V_T, V_Z, V_Q, V_W, V_Y, V_TMP, V_PH, V_SH, V_QH, V_RH};
+            if (!elide_) need.insert(need.end(), {V_WH, V_ZH});
+            break;
+    }
+    work_.resize(NWORK);
     const size_t vlen = static_cast<size_t>(rows_alloc_) * m;
-    for (int i : need[method]) work_[i] = pool_take(ctx, vlen);
-    if (a->n_halo) work_[14] = pool_take(ctx, vlen);  // x0 staging with halo room
+    for (int i : need) work_[i] = pool_take(ctx, vlen);
+    if (a->n_halo) work_[V_X0] = pool_take(ctx, vlen);  // x0 staging with halo room
     scal_.alloc(static_cast<size_t>(NSCAL) * m);
     ctl_.alloc(NCTL);
     hist_.alloc(static_cast<size_t>(maxit + 1) * m);
-    slots_.alloc(static_cast<size_t>(4) * m * NSLOT);
-    ticket_.alloc(1);
-    MBG_CUDA(cudaMemsetAsync(ticket_.p, 0, sizeof(unsigned), ctx->stream));
+    slots_.alloc(static_cast<size_t>(8) * m * NSLOT);
     MBG_CUDA(cudaMemsetAsync(slots_.p, 0, slots_.n * sizeof(int64_t), ctx->stream));
     MBG_CUDA(cudaMemsetAsync(ctl_.p, 0, ctl_.n * sizeof(int), ctx->stream));
     if (!ctx->ctl_host) MBG_CUDA(cudaMallocHost(&ctx->ctl_host, 64 * sizeof(int)));
@@ -134,14 +165,6 @@ void Solver::spmm(const double* x, double* y, int epi_kind, const double* aux, i
     e.kind = epi_kind;
     e.aux = aux;
     for (int d = 0; d < 3; ++d) e.slot[d] = slot(first_slot + d);
-    // the scalar step can ride on a single fused-epilogue SpMM launch
-    const bool post = post_point >= 0 && epi_kind != 0 && can_post() && a_->peers.empty() &&
-                      (m_ == 1 || m_ == 2 || m_ == 4 || m_ == 8 || m_ == 16 || m_ == 32);
-    if (post) {
-        e.post.enabled = 1;
-        e.post.counter = ticket_.p;
-        e.post.s = scal_args(post_point, post_nd);
-    }
     const double extra = epi_kind == 1 ? 8.0 * len_ : 0.0;   // aux vector read
     mark_begin(epi_kind ? "spmm+dots" : "spmm", spmv_compulsory_bytes(a_->n, a_->nnz, m_) + extra);
     launches_ += apply_operator(ctx_, a_, m_, const_cast<double*>(x), y, ctl_.p, epi_kind ? &e : nullptr);
@@ -155,7 +178,7 @@ void Solver::spmm(const double* x, double* y, int epi_kind, const double* aux, i
         }
         if (nred > 0) reductions_++;
     }
-    if (post_point >= 0 && !post) scalars(post_point, post_nd);
+    if (post_point >= 0) scalars(post_point, post_nd);
 }
 
 template <class P>
@@ -172,12 +195,6 @@ void Solver::group(std::initializer_list<const double*> in, std::initializer_lis
     for (int s : co) g.coef[i++] = sc(s);
     for (int d = 0; d < P::NDOT; ++d) g.slot[d] = slot(first_slot + d);
     g.ctl = ctl_.p;
-    const bool post = post_point >= 0 && can_post();
-    if (post) {
-        g.post.enabled = 1;
-        g.post.counter = ticket_.p;
-        g.post.s = scal_args(post_point, post_nd);
-    }
     mark_begin(std::string("group:") + P::NAME, static_cast<double>(P::NIN + P::NOUT) * 8.0 * len_);
     launch_group<P>(ctx_->stream, g, ctx_->num_sms);
     MBG_CUDA(cudaGetLastError());
@@ -195,7 +212,22 @@ void Solver::group(std::initializer_list<const double*> in, std::initializer_lis
         }
         if (nred > 0) reductions_++;
     }
-    if (post_point >= 0 && !post) scalars(post_point, post_nd);
+    if (post_point >= 0) scalars(post_point, post_nd);
+}
+
+// M^-1: identity = one copy (1R + 1W); synthetic(alpha) =
+// alpha/2 in-place scale passes by 2.0, 0.5, ... with a last factor that makes
+// the product exactly 1 (oracle.c minv).
+void Solver::minv(const double* in, double* out) {
+    if (pa_ <= 2) {
+        copy(out, in);
+        return;
+    }
+    const int k = pa_ / 2;
+    for (int i = 0; i < k; ++i) {
+        const int c = i < k - 1 ? ((i & 1) ? S_HALF : S_TWO) : (((k - 1) & 1) ? S_HALF : S_ONE);
+        group<PUpd1>({i == 0 ? in : out}, {out}, {c}, 0);
+    }
 }
 
 void Solver::copy(double* dst, const double* src) {
@@ -221,15 +253,6 @@ ScalArgs Solver::scal_args(int point, int nd) {
     return s;
 }
 
-bool Solver::can_post() const {
-    // The fused scalar step needs every dot of the point locally (no pending
-    // cross-GPU allreduce) and whole warps.  Measured on B200 (C2): the separate
-    // one-block scalar kernel inside the CUDA graph is ~1% faster than the
-    // last-block post step (whose per-block fences lengthen the tail), so the
-    // post step is opt-in (MBG_POST=1).
-    static const bool enabled = std::getenv("MBG_POST") != nullptr;
-    return enabled && ctx_->comm == nullptr && group_block(m_) % 32 == 0;
-}
 
 void Solver::join() {
     if (pending_join_) comm_join(ctx_);
@@ -247,9 +270,6 @@ void Solver::scalars(int point, int nd) {
     launches_++;
 }
 
-// Vector roles (indices into work_):
-enum { V_R, V_R0, V_P, V_V, V_S, V_T, V_Z, V_VH, V_TH, V_RT, V_Q, V_W, V_Y, V_TMP };
-
 void Solver::setup(const double* b, double* x) {
     b_ = b;
     x_ = x;
@@ -257,28 +277,50 @@ void Solver::setup(const double* b, double* x) {
     double* r0 = w(V_R0);
     double* tmpv = w(V_V);
     if (a_->n_halo) {
-        copy(w(14), x);                                  // x0 into a buffer with halo room
-        spmm(w(14), tmpv);                               // z = A x0
+        copy(w(V_X0), x);                                // x0 into a buffer with halo room
+        spmm(w(V_X0), tmpv);                             // z = A x0
     } else {
         spmm(x, tmpv);                                   // z = A x0
     }
     group<PUpd2>({b, tmpv}, {r}, {S_ONE, S_MONE}, 0);    // r = 1*b + (-1)*z   (needs S_ONE set)
     group<PUpd1>({r}, {r0}, {S_ONE}, 0);                  // r0 = 1*r
     group<PDot1>({r0}, {}, {}, 0);                        // rho = (r0, r0)
-    if (method_ == MBG_BICGSTAB) {
+    auto zero = [&](int v) {
+        if (work_[v].p) MBG_CUDA(cudaMemsetAsync(w(v), 0, static_cast<size_t>(len_) * sizeof(double), ctx_->stream));
+    };
+    if (method_ == MBG_BICGSTAB || method_ == MBG_PBICGSTAB) {
         group<PUpd1>({r}, {w(V_P)}, {S_ONE}, 2);          // p = 1*r
         group<PDot1>({b}, {}, {}, 1, P_SETUP, 2);         // bb = (b, b)
     } else if (method_ == MBG_RBICGSTAB) {
-        copy(w(V_Z), r0);                                 // z0 = M^-1 r0 (identity)
+        minv(r0, w(V_Z));                                 // z0 = M^-1 r0
         copy(w(V_VH), w(V_Z));                            // v^0 = z0
         group<PDot1>({b}, {}, {}, 1, P_SETUP, 2);         // bb = (b, b)
-    } else {
+    } else if (method_ == MBG_IBICGSTAB) {
+        // Alg. 3 line 1: u0 = A r0, f0 = A^T r0, q0 = v0 = z0 = 0
+        spmm(r, w(V_U));
+        mark_begin("spmm_t", spmv_compulsory_bytes(at_->n, at_->nnz, m_));
+        launches_ += apply_operator(ctx_, at_, m_, r0, w(V_F0), ctl_.p);
+        mark_end();
+        for (int v : {V_Q, V_V, V_Z}) zero(v);
         group<PDot1>({b}, {}, {}, 1);                     // bb = (b, b)
-        for (int v : {V_P, V_S, V_Z, V_V})
-            if (v != V_V) MBG_CUDA(cudaMemsetAsync(w(v), 0, static_cast<size_t>(len_) * sizeof(double), ctx_->stream));
+        group<PDot2>({r0, w(V_U)}, {}, {}, 2, P_SETUP, 3); // sigma0 = (r0, u0)
+    } else if (method_ == MBG_PIPEBICGSTAB) {
+        group<PDot1>({b}, {}, {}, 1);                     // bb = (b, b)
+        for (int v : {V_P, V_S, V_Z}) zero(v);
         spmm(r, w(V_W));                                  // w0 = A r0
         spmm(w(V_W), w(V_T));                             // t0 = A w0
-        MBG_CUDA(cudaMemsetAsync(w(V_V), 0, static_cast<size_t>(len_) * sizeof(double), ctx_->stream));
+        zero(V_V);                                        // (served as A x0 scratch)
+        group<PDot2>({r0, w(V_W)}, {}, {}, 2, P_SETUP, 3); // (r0, w0) ; alpha0
+    } else {
+        // Alg. 7 line 1: r^0 = M^-1 r0, w0 = A r^0, w^0 = M^-1 w0, t0 = A w^0
+        group<PDot1>({b}, {}, {}, 1);                     // bb = (b, b)
+        for (int v : {V_PH, V_SH, V_S, V_Z, V_ZH}) zero(v);
+        minv(r, w(V_RH));
+        spmm(w(V_RH), w(V_W));
+        double* wh = elide_ ? w(V_W) : w(V_WH);
+        if (!elide_) minv(w(V_W), wh);
+        spmm(wh, w(V_T));
+        zero(V_V);
         group<PDot2>({r0, w(V_W)}, {}, {}, 2, P_SETUP, 3); // (r0, w0) ; alpha0
     }
 }
@@ -324,18 +366,19 @@ void Solver::iteration() {
         double *z = w(V_Z), *vh = w(V_VH), *v = w(V_V), *th = w(V_TH), *t = w(V_T);
         double *rt = w(V_RT);
         // identity M^-1: the fused formulation aliases s = v and q = t instead of copying
-        double* s = fused ? v : w(V_S);
-        double* q = fused ? t : w(V_Q);
+        double* s = elide_ ? v : w(V_S);
+        double* q = elide_ ? t : w(V_Q);
         if (fused) {
             spmm(vh, v, 1, r0, P_C_ALPHA, 1);                     // v = A vh ; delta = (v, r0) ; alpha
+            if (!elide_) minv(v, s);
         } else {
             spmm(vh, v);
-            copy(s, v);                                           // s = M^-1 v
+            minv(v, s);                                           // s = M^-1 v
             group<PDot2>({v, r0}, {}, {}, 0, P_C_ALPHA, 1);
         }
         group<PUpd2>({z, s}, {th}, {S_ONE, S_NALPHA}, 0);        // th = z - alpha s
         spmm(th, t);
-        if (!fused) copy(q, t);                                   // q = M^-1 t
+        if (!elide_) minv(t, q);                                  // q = M^-1 t
         if (basic) {
             group<PUpd2>({r, v}, {rt}, {S_ONE, S_NALPHA}, 0);
             group<PDot2>({t, rt}, {}, {}, 0);
@@ -354,13 +397,11 @@ void Solver::iteration() {
             group<PReordG12>({x, vh, th, q, s}, {x, z, vh}, {S_ALPHA, S_OMEGA, S_NOMEGA, S_BETA, S_NBO}, 0,
                              P_R_END, 0);
         }
-    } else {
+    } else if (method_ == MBG_PIPEBICGSTAB) {
         double *p = w(V_P), *s = w(V_S), *wv = w(V_W), *z = w(V_Z), *t = w(V_T), *v = w(V_V);
         double *q = w(V_Q), *y = w(V_Y), *tmp = w(V_TMP);
-        // On one GPU the scalar steps ride on the dot kernels (omega needs only
-        // G1's dots, alpha/beta only G5's); with a communicator they wait for the
-        // allreduce, which overlaps the following SpMM on the side stream.
-        const bool early = can_post();
+        // The scalar steps wait for the reductions, which overlap the following
+        // SpMM (on the side stream when a communicator allreduces them).
         if (basic) {
             group<PUpd3>({r, p, s}, {p}, {S_ONE, S_BETA, S_NBO}, 0);
             group<PUpd3>({wv, s, z}, {s}, {S_ONE, S_BETA, S_NBO}, 0);
@@ -369,13 +410,13 @@ void Solver::iteration() {
             group<PUpd2>({wv, z}, {y}, {S_ONE, S_NALPHA}, 0);
             group<PDot2>({q, y}, {}, {}, 0);
             group<PDot1>({y}, {}, {}, 1);
-            group<PDot1>({q}, {}, {}, 2, early ? P_P_OMEGA : -1, 3);
+            group<PDot1>({q}, {}, {}, 2, -1, 3);
         } else {
             group<PPipeG1>({r, p, s, wv, z, t, v}, {p, s, z, q, y}, {S_BETA, S_NBO, S_NALPHA}, 0,
-                           early ? P_P_OMEGA : -1, 3);
+                           -1, 3);
         }
         spmm(z, v);
-        if (!early) scalars(P_P_OMEGA, 3);
+        scalars(P_P_OMEGA, 3);
         if (basic) {
             group<PUpd3>({x, p, q}, {x}, {S_ONE, S_ALPHA, S_OMEGA}, 0);
             group<PUpd2>({q, y}, {r}, {S_ONE, S_NOMEGA}, 0);
@@ -384,16 +425,116 @@ void Solver::iteration() {
             group<PDot2>({r0, r}, {}, {}, 0);
             group<PDot2>({r0, z}, {}, {}, 1);
             group<PDot2>({r0, wv}, {}, {}, 2);
-            group<PDot2>({r0, s}, {}, {}, 3, early ? P_P_BETA : -1, 4);
+            group<PDot2>({r0, s}, {}, {}, 3, -1, 4);
         } else if (fused) {
             group<PPipeG45>({x, p, q, y, t, v, r0, z, s}, {x, r, wv}, {S_ALPHA, S_OMEGA, S_NOMEGA, S_OA}, 0,
-                            early ? P_P_BETA : -1, 4);
+                            -1, 4);
         } else {
             group<PPipeG4>({x, p, q, y}, {x, r}, {S_ALPHA, S_OMEGA, S_NOMEGA}, 0);
-            group<PPipeG5>({y, t, v, r0, r, z, s}, {wv}, {S_NOMEGA, S_OA}, 0, early ? P_P_BETA : -1, 4);
+            group<PPipeG5>({y, t, v, r0, r, z, s}, {wv}, {S_NOMEGA, S_OA}, 0, -1, 4);
         }
         spmm(wv, t);
-        if (!early) scalars(P_P_BETA, 4);
+        scalars(P_P_BETA, 4);
+    } else if (method_ == MBG_IBICGSTAB) {
+        // Alg. 3: one 7-dot reduction point per iteration
+        double *u = w(V_U), *f0 = w(V_F0), *q = w(V_Q), *v = w(V_V), *z = w(V_Z), *s = w(V_S), *t = w(V_T);
+        scalars(P_I_START, 0);                                    // rho', delta', beta', tau', alpha'
+        if (basic) {
+            group<PUpd3>({r, z, v}, {z}, {S_ALPHA, S_CZ2, S_CZ3}, 0);
+            group<PUpd3>({u, v, q}, {v}, {S_ONE, S_BETA, S_NDELTA}, 0);
+            group<PUpd2>({r, v}, {s}, {S_ONE, S_NALPHA}, 0);
+        } else {
+            group<PIbcgG1>({r, z, v, u, q}, {z, v, s}, {S_ALPHA, S_CZ2, S_CZ3, S_BETA, S_NDELTA, S_NALPHA}, 0);
+        }
+        spmm(v, q);
+        if (basic) {
+            group<PUpd2>({u, q}, {t}, {S_ONE, S_NALPHA}, 0);
+            group<PDot2>({r0, s}, {}, {}, 0);
+            group<PDot2>({r0, q}, {}, {}, 1);
+            group<PDot2>({f0, s}, {}, {}, 2);
+            group<PDot2>({f0, t}, {}, {}, 3);
+            group<PDot2>({s, t}, {}, {}, 4);
+            group<PDot1>({t}, {}, {}, 5);
+            group<PDot1>({s}, {}, {}, 6, P_I_OMEGA, 7);
+        } else {
+            group<PIbcgG2>({u, q, r0, s, f0}, {t}, {S_NALPHA}, 0, P_I_OMEGA, 7);
+        }
+        if (basic) {
+            group<PUpd2>({s, t}, {r}, {S_ONE, S_NOMEGA}, 0);
+            group<PUpd3>({x, z, s}, {x}, {S_ONE, S_ONE, S_OMEGA}, 0);
+        } else {
+            group<PIbcgG3>({s, t, x, z}, {r, x}, {S_NOMEGA, S_OMEGA}, 0);
+        }
+        scalars(P_R_END, 0);                                      // converged? next iteration
+        spmm(r, u);
+    } else if (method_ == MBG_PBICGSTAB) {
+        // Alg. 5; the x update (independent of beta) runs
+        // while the rho' reduction is in flight
+        double *p = w(V_P), *v = w(V_V), *s = w(V_S), *t = w(V_T);
+        double* ph = elide_ ? p : w(V_PH);
+        double* sh = elide_ ? s : w(V_SH);
+        if (!elide_) minv(p, ph);
+        spmm(ph, v);
+        group<PDot2>({v, r0}, {}, {}, 0, P_C_ALPHA, 1);
+        group<PUpd2>({r, v}, {s}, {S_ONE, S_NALPHA}, 0);
+        if (!elide_) minv(s, sh);
+        spmm(sh, t);
+        if (basic) {
+            group<PDot2>({t, s}, {}, {}, 0);
+            group<PDot1>({t}, {}, {}, 1);
+            group<PDot1>({s}, {}, {}, 2, P_C_OMEGA, 3);
+            group<PUpd2>({s, t}, {r}, {S_ONE, S_NOMEGA}, 0);
+            group<PUpd3>({x, ph, sh}, {x}, {S_ONE, S_ALPHA, S_OMEGA}, 0);
+            group<PDot2>({r, r0}, {}, {}, 0, P_C_BETA, 1);
+        } else {
+            group<PClassicOmega>({t, s}, {}, {}, 0, P_C_OMEGA, 3);
+            group<PRDot>({s, t, r0}, {r}, {S_NOMEGA}, 0);             // r ; rho' (reduction in flight)
+            group<PUpd3>({x, ph, sh}, {x}, {S_ONE, S_ALPHA, S_OMEGA}, 0);
+            scalars(P_C_BETA, 1);
+        }
+        group<PUpd3>({r, p, v}, {p}, {S_ONE, S_BETA, S_NBO}, 0);
+    } else {
+        // Alg. 7: both reductions overlap M^-1 + SpMM
+        double *rh = w(V_RH), *ph = w(V_PH), *sh = w(V_SH), *qh = w(V_QH), *wv = w(V_W), *t = w(V_T);
+        double *s = w(V_S), *z = w(V_Z), *q = w(V_Q), *y = w(V_Y), *v = w(V_V), *tmp = w(V_TMP);
+        double* wh = elide_ ? wv : w(V_WH);
+        double* zh = elide_ ? z : w(V_ZH);
+        if (basic) {
+            group<PUpd3>({rh, ph, sh}, {ph}, {S_ONE, S_BETA, S_NBO}, 0);
+            group<PUpd3>({wh, sh, zh}, {sh}, {S_ONE, S_BETA, S_NBO}, 0);
+            group<PUpd2>({rh, sh}, {qh}, {S_ONE, S_NALPHA}, 0);
+            group<PUpd3>({wv, s, z}, {s}, {S_ONE, S_BETA, S_NBO}, 0);
+            group<PUpd3>({t, z, v}, {z}, {S_ONE, S_BETA, S_NBO}, 0);
+            group<PUpd2>({r, s}, {q}, {S_ONE, S_NALPHA}, 0);
+            group<PUpd2>({wv, z}, {y}, {S_ONE, S_NALPHA}, 0);
+            group<PDot2>({q, y}, {}, {}, 0);
+            group<PDot1>({y}, {}, {}, 1);
+            group<PDot1>({q}, {}, {}, 2);
+        } else {
+            group<PPpG1>({rh, ph, sh, wh, zh}, {ph, sh, qh}, {S_BETA, S_NBO, S_NALPHA}, 0);
+            group<PPpG2>({r, s, wv, z, t, v}, {s, z, q, y}, {S_BETA, S_NBO, S_NALPHA}, 0);
+        }
+        if (!elide_) minv(z, zh);
+        spmm(zh, v);
+        scalars(P_P_OMEGA, 3);
+        if (basic) {
+            group<PUpd3>({x, ph, qh}, {x}, {S_ONE, S_ALPHA, S_OMEGA}, 0);
+            group<PUpd2>({wh, zh}, {tmp}, {S_NOMEGA, S_OA}, 0);   // split_basic: trailing pair
+            group<PUpd2>({qh, tmp}, {rh}, {S_ONE, S_ONE}, 0);
+            group<PUpd2>({q, y}, {r}, {S_ONE, S_NOMEGA}, 0);
+            group<PUpd2>({t, v}, {tmp}, {S_NOMEGA, S_OA}, 0);
+            group<PUpd2>({y, tmp}, {wv}, {S_ONE, S_ONE}, 0);
+            group<PDot2>({r0, r}, {}, {}, 0);
+            group<PDot2>({r0, z}, {}, {}, 1);
+            group<PDot2>({r0, wv}, {}, {}, 2);
+            group<PDot2>({r0, s}, {}, {}, 3);
+        } else {
+            group<PPpG3>({x, ph, qh, wh, zh}, {x, rh}, {S_ALPHA, S_OMEGA, S_NOMEGA, S_OA}, 0);
+            group<PPpG4>({q, y, t, v, r0, z, s}, {r, wv}, {S_NOMEGA, S_OA}, 0);
+        }
+        if (!elide_) minv(wv, wh);
+        spmm(wh, t);
+        scalars(P_P_BETA, 4);
     }
     join();   // a captured graph must end joined to the origin stream
 }
@@ -401,9 +542,17 @@ void Solver::iteration() {
 void Solver::run(const double* b, double* x, bool use_graph, int chunk) {
     if (profile_ || comm_is_local(ctx_)) use_graph = false;
     // S_ONE / S_MONE must exist before setup's first group
-    std::vector<double> init(static_cast<size_t>(2) * m_);
-    for (int c = 0; c < m_; ++c) { init[c] = 1.0; init[m_ + c] = -1.0; }
-    MBG_CUDA(cudaMemcpyAsync(sc(S_ONE), init.data(), init.size() * sizeof(double), cudaMemcpyHostToDevice,
+    std::vector<double> init(static_cast<size_t>(4) * m_);
+    for (int c = 0; c < m_; ++c) {
+        init[c] = 1.0;
+        init[m_ + c] = -1.0;
+        init[2 * m_ + c] = 2.0;
+        init[3 * m_ + c] = 0.5;
+    }
+    static_assert(S_MONE == S_ONE + 1 && S_HALF == S_TWO + 1, "constant rows");
+    MBG_CUDA(cudaMemcpyAsync(sc(S_ONE), init.data(), 2 * m_ * sizeof(double), cudaMemcpyHostToDevice,
+                             ctx_->stream));
+    MBG_CUDA(cudaMemcpyAsync(sc(S_TWO), init.data() + 2 * m_, 2 * m_ * sizeof(double), cudaMemcpyHostToDevice,
                              ctx_->stream));
     MBG_CUDA(cudaStreamSynchronize(ctx_->stream));  // init is a stack buffer
     if (ctx_->comm) comm_barrier(ctx_);
@@ -475,13 +624,15 @@ void Solver::report(double* hist_host, mbg_report* rep) {
         const size_t cnt = static_cast<size_t>(rep->iterations + 1) * m_;
         MBG_CUDA(cudaMemcpy(hist_host, hist_.p, cnt * sizeof(double), cudaMemcpyDeviceToHost));
     }
-    int reads = 0, writes = 0, spmvs = 0, nred = 0, dots[8];
-    method_schedule(method_, form_, &reads, &writes, &spmvs, &nred, dots);
+    int reads = 0, writes = 0, spmvs = 0, apps = 0, nred = 0, dots[8];
+    method_schedule_pc(method_, form_, pa_, &reads, &writes, &spmvs, &apps, &nred, dots);
     const int its = rep->iterations;
-    rep->vector_reads = static_cast<int64_t>(reads) * its;
-    rep->vector_writes = static_cast<int64_t>(writes) * its;
+    // TrafficCounter semantics: the preconditioner's transfers are tallied too
+    // (alpha/2 reads + alpha/2 writes per application)
+    rep->vector_reads = static_cast<int64_t>(reads + apps * pa_ / 2) * its;
+    rep->vector_writes = static_cast<int64_t>(writes + apps * pa_ / 2) * its;
     rep->spmv_bytes = static_cast<double>(spmvs) * its * spmv_traffic_bytes(a_->n, a_->nnz, m_);
-    rep->compulsory_bytes = iteration_bytes(method_, form_, a_->n, a_->nnz, m_) * its;
+    rep->compulsory_bytes = iteration_bytes(method_, form_, pa_, a_->n, a_->nnz, m_) * its;
     rep->reductions = static_cast<int64_t>(nred) * its;
     rep->gpu_launches = launches_;
     rep->loop_ms = loop_ms_;

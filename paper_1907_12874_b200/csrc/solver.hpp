@@ -13,15 +13,22 @@ namespace mbg {
 // Byte model.
 double spmv_traffic_bytes(int64_t n, int64_t nnz, int m);      // Eq. (3), spmv.cpp:10-16
 double spmv_compulsory_bytes(int64_t n, int64_t nnz, int m);   // x read once
-// Per-iteration schedule totals (Table 2 + identity M^-1 copies for Reordered).
+// Per-iteration schedule totals (Table 2 + identity M^-1 copies for the
+// preconditioned methods) and the SPEC.md form with the preconditioner apart.
+bool preconditioned(int method);
 void method_schedule(int method, int formulation, int* reads, int* writes, int* spmvs, int* nred,
                      int* dots_per_reduction);
-double iteration_bytes(int method, int formulation, int64_t n, int64_t nnz, int m);
+void method_schedule_pc(int method, int formulation, int precond_alpha, int* reads, int* writes, int* spmvs,
+                        int* precond_apps, int* nred, int* dots_per_reduction);
+double iteration_bytes(int method, int formulation, int precond_alpha, int64_t n, int64_t nnz, int m);
+// A^T of a single-GPU matrix, built once and cached on the matrix (api.cu).
+const mbg_csr* csr_transpose(mbg_ctx* ctx, const mbg_csr* a);
 
 class Solver {
 public:
+    // precond_alpha < 0: identity (2) for the preconditioned methods, none otherwise
     Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulation, double tol, int fixed,
-           int maxit);
+           int maxit, int precond_alpha = -1);
     ~Solver();
     Solver(const Solver&) = delete;
     Solver& operator=(const Solver&) = delete;
@@ -39,7 +46,10 @@ private:
     double* sc(int i);
     int64_t* slot(int i);
     // post_point >= 0: run the scalar step `post_point` over `post_nd` dots
-    // after this kernel -- fused into its last block when possible.
+    // after this kernel.  (Running it in the last block of the dot kernel --
+    // atomic ticket + fences -- was measured ~1% slower on B200 than the
+    // separate one-block kernel inside the CUDA graph, and its register
+    // footprint slowed the streaming kernels; removed.)
     void spmm(const double* x, double* y, int epi_kind = 0, const double* aux = nullptr, int post_point = -1,
               int post_nd = 0, int first_slot = 0, int reduce = -1);
     template <class P>
@@ -47,8 +57,8 @@ private:
                std::initializer_list<int> co, int first_slot, int post_point = -1, int post_nd = 0,
                int reduce = -1);
     struct ScalArgs scal_args(int point, int nd);
-    bool can_post() const;
     void copy(double* dst, const double* src);
+    void minv(const double* in, double* out);   // M^-1 application (identity or synthetic(alpha))
     void scalars(int point, int nd);
     void join();   // main stream waits for an in-flight dot allreduce
     void setup(const double* b, double* x);
@@ -57,6 +67,9 @@ private:
     mbg_ctx* ctx_;
     const mbg_csr* a_;
     int m_, method_, form_;
+    int pa_ = 0;            // preconditioner alpha (0 none, 2 identity, >= 4 synthetic)
+    bool elide_ = false;    // fused formulation with identity M^-1: applications aliased away
+    const mbg_csr* at_ = nullptr;   // A^T (IBiCGStab setup)
     double tol_;
     int fixed_, maxit_;
     int64_t n_ = 0, len_ = 0, rows_alloc_ = 0;
@@ -64,7 +77,6 @@ private:
     DevBuf<double> scal_, hist_;
     DevBuf<int> ctl_;
     DevBuf<int64_t> slots_;
-    DevBuf<unsigned> ticket_;
     int* ctl_host_ = nullptr;
     cudaEvent_t ev_[2] = {nullptr, nullptr};
     cudaEvent_t t0_ = nullptr, t1_ = nullptr;

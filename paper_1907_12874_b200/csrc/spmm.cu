@@ -260,7 +260,6 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
                                },
                                sh);
     }
-    if (epi.post.enabled) post_step(epi.post, reinterpret_cast<double*>(bufs));
 }
 
 // ---------------------------------------------------------------------------
@@ -405,7 +404,6 @@ __global__ void __launch_bounds__(256, M >= 32 ? 2 : (EPI == 2 ? 2 : (EPI == 0 ?
                                },
                                sh);
     }
-    if (epi.post.enabled) post_step(epi.post, reinterpret_cast<double*>(bufs));
 }
 
 // Rows longer than a tile's shared-memory capacity: one thread per (row,

@@ -104,7 +104,7 @@ mbg_statement Dt(int l, int r, int slot) {
 }
 
 // vector ids for the schedule tables
-enum { X, P, R, R0, V, S, T, Z, VH, TH, RT, Q, W, Y, TEMP = 100 };
+enum { X, P, R, R0, V, S, T, Z, VH, TH, RT, Q, W, Y, U_, F0, PH, SH, QH, RH, WH, ZH, TEMP = 100 };
 
 using Group = std::vector<mbg_statement>;
 
@@ -128,9 +128,28 @@ std::vector<Group> schedule(int method) {
                      Dt(Q, Y, 0), Dt(Y, Y, 1), Dt(Q, Q, 2)},
                     {U(X, {X, P, Q}), U(R, {Q, Y})},
                     {U(W, {Y, T, V}), Dt(R0, R, 0), Dt(R0, Z, 1), Dt(R0, W, 2), Dt(R0, S, 3)}};
+        case MBG_IBICGSTAB:  // Alg. 3, PAPER.md:1455-1471 (Eq. (15): 20 transfers, one 7-dot reduction)
+            return {{U(Z, {R, Z, V}), U(V, {U_, V, Q}), U(S, {R, V})},
+                    {U(T, {U_, Q}), Dt(R0, S, 0), Dt(R0, Q, 1), Dt(F0, S, 2), Dt(F0, T, 3), Dt(S, T, 4),
+                     Dt(T, T, 5), Dt(S, S, 6)},
+                    {U(R, {S, T}), U(X, {X, Z, S})}};
+        case MBG_PBICGSTAB:  // Alg. 5, PAPER.md:1536-1556 (Eq. (17): 19 transfers + 2 M^-1)
+            return {{Dt(V, R0, 0)},
+                    {U(S, {R, V})},
+                    {Dt(T, S, 0), Dt(T, T, 1), Dt(S, S, 2)},
+                    {U(R, {S, T}), Dt(R, R0, 0)},
+                    {U(X, {X, PH, SH})},
+                    {U(P, {R, P, V})}};
+        case MBG_PPIPEBICGSTAB:  // Alg. 7, PAPER.md:1611-1631 (Eq. (19): 34 transfers + 2 M^-1)
+            return {{U(PH, {RH, PH, SH}), U(SH, {WH, SH, ZH}), U(QH, {RH, SH})},
+                    {U(S, {W, S, Z}), U(Z, {T, Z, V}), U(Q, {R, S}), U(Y, {W, Z}), Dt(Q, Y, 0), Dt(Y, Y, 1),
+                     Dt(Q, Q, 2)},
+                    {U(X, {X, PH, QH}), U(RH, {QH, WH, ZH})},
+                    {U(R, {Q, Y}), U(W, {Y, T, V}), Dt(R0, R, 0), Dt(R0, Z, 1), Dt(R0, W, 2), Dt(R0, S, 3)}};
     }
     throw Invalid("unknown method");
 }
+
 
 // Fused formulation: dots fused into SpMM epilogues read one aux
 // vector there (aux_reads); identity M^-1 copies are elided (s = v, q = t);
@@ -167,6 +186,10 @@ std::vector<Group> schedule_fused(int method, int* aux_reads, int* spmm_dots) {
 
 }  // namespace
 
+bool preconditioned(int method) {
+    return method == MBG_RBICGSTAB || method == MBG_PBICGSTAB || method == MBG_PPIPEBICGSTAB;
+}
+
 double spmv_traffic_bytes(int64_t n, int64_t nnz, int m) {
     const double dn = static_cast<double>(n), dz = static_cast<double>(nnz);
     return 8.0 * m * (dn + dz) + 4.0 * (dn + 3.0 * dz);
@@ -177,10 +200,17 @@ double spmv_compulsory_bytes(int64_t n, int64_t nnz, int m) {
     return 16.0 * m * dn + 12.0 * dz + 4.0 * (dn + 1.0);
 }
 
-void method_schedule(int method, int formulation, int* reads, int* writes, int* spmvs, int* nred,
-                     int* dots) {
+// Per-iteration totals, SPEC.md:236-244 form: reads/writes exclude the
+// preconditioner, whose applications are returned separately (each costs
+// precond_alpha transfers; identity copies elided by the fused formulation).
+void method_schedule_pc(int method, int formulation, int precond_alpha, int* reads, int* writes, int* spmvs,
+                        int* precond_apps, int* nred, int* dots) {
+    if (method < 0 || method > 5) throw Invalid("unknown method");
     int r = 0, w = 0, k = 0;
-    if (formulation == MBG_FUSED) {
+    const int apps = preconditioned(method) ? 2 : 0;
+    *precond_apps = (formulation == MBG_FUSED && precond_alpha == 2) ? 0 : apps;
+    *spmvs = 2;
+    if (formulation == MBG_FUSED && method <= MBG_PIPEBICGSTAB) {
         int aux = 0, sd[2] = {0, 0};
         for (const auto& g : schedule_fused(method, &aux, sd)) {
             int gr, gw;
@@ -198,18 +228,19 @@ void method_schedule(int method, int formulation, int* reads, int* writes, int* 
             if (dots && i < 8) dots[i] = red[i];
         *reads = r;
         *writes = w;
-        *spmvs = 2;
         *nred = static_cast<int>(red.size());
         return;
     }
+    // the fused formulation of Alg. 3 / 5 / 7 is the merged schedule (with
+    // identity M^-1 applications elided)
     for (const auto& g : schedule(method)) {
         if (formulation == MBG_BASIC) {
-            for (const auto& s : split(g.data(), static_cast<int>(g.size()), TEMP)) {
+            for (const auto& st : split(g.data(), static_cast<int>(g.size()), TEMP)) {
                 int gr, gw;
-                analyze(&s, 1, &gr, &gw);
+                analyze(&st, 1, &gr, &gw);
                 r += gr;
                 w += gw;
-                if (s.kind == MBG_STMT_DOT) {
+                if (st.kind == MBG_STMT_DOT) {
                     if (dots && k < 8) dots[k] = 1;
                     ++k;
                 }
@@ -220,27 +251,32 @@ void method_schedule(int method, int formulation, int* reads, int* writes, int* 
             r += gr;
             w += gw;
             int nd = 0;
-            for (const auto& s : g) nd += s.kind == MBG_STMT_DOT;
+            for (const auto& st : g) nd += st.kind == MBG_STMT_DOT;
             if (nd) {
                 if (dots && k < 8) dots[k] = nd;
                 ++k;
             }
         }
     }
-    if (method == MBG_RBICGSTAB) {  // two identity M^-1 applications: 1R + 1W each
-        r += 2;
-        w += 2;
-    }
     *reads = r;
     *writes = w;
-    *spmvs = 2;
     *nred = k;
 }
 
-double iteration_bytes(int method, int formulation, int64_t n, int64_t nnz, int m) {
-    int r, w, s, k, d[8];
-    method_schedule(method, formulation, &r, &w, &s, &k, d);
-    return static_cast<double>(r + w) * 8.0 * static_cast<double>(n) * m +
+// Legacy totals: the preconditioner's transfers folded into reads/writes
+// (alpha/2 read + alpha/2 write per application; 1 + 1 for an identity copy).
+void method_schedule(int method, int formulation, int* reads, int* writes, int* spmvs, int* nred, int* dots) {
+    const int pa = preconditioned(method) ? 2 : 0;
+    int apps = 0;
+    method_schedule_pc(method, formulation, pa, reads, writes, spmvs, &apps, nred, dots);
+    *reads += apps * pa / 2;
+    *writes += apps * pa / 2;
+}
+
+double iteration_bytes(int method, int formulation, int precond_alpha, int64_t n, int64_t nnz, int m) {
+    int r, w, s, apps, k, d[8];
+    method_schedule_pc(method, formulation, precond_alpha, &r, &w, &s, &apps, &k, d);
+    return static_cast<double>(r + w + apps * precond_alpha) * 8.0 * static_cast<double>(n) * m +
            s * spmv_compulsory_bytes(n, nnz, m);
 }
 
@@ -285,6 +321,23 @@ extern "C" int mbg_method_schedule(int method, int formulation, int* reads, int*
         if (formulation != MBG_MERGED && formulation != MBG_BASIC && formulation != MBG_FUSED)
             throw mbg::Invalid("unknown formulation");
         mbg::method_schedule(method, formulation, reads, writes, spmvs, nreductions, dots_per_reduction);
+        return MBG_OK;
+    } catch (const mbg::Invalid& e) {
+        mbg::set_error(e.what());
+        return MBG_ERR_INVALID;
+    }
+}
+
+extern "C" int mbg_method_schedule_pc(int method, int formulation, int precond_alpha, int* reads, int* writes,
+                                      int* spmvs, int* precond_applications, int* nreductions,
+                                      int* dots_per_reduction) {
+    try {
+        if (formulation != MBG_MERGED && formulation != MBG_BASIC && formulation != MBG_FUSED)
+            throw mbg::Invalid("unknown formulation");
+        if (mbg::preconditioned(method) ? (precond_alpha < 2 || precond_alpha % 2) : precond_alpha != 0)
+            throw mbg::Invalid("method_schedule: preconditioner presence mismatch");
+        mbg::method_schedule_pc(method, formulation, precond_alpha, reads, writes, spmvs, precond_applications,
+                                nreductions, dots_per_reduction);
         return MBG_OK;
     } catch (const mbg::Invalid& e) {
         mbg::set_error(e.what());

@@ -75,6 +75,36 @@ def test_method_schedule_reductions():
     assert P.method_schedule("bicgstab", "basic")["reductions"] == [1] * 5
 
 
+EQ14_19 = {  # merged vector transfers of Eqs. (14)-(19), preconditioner apart
+    "bicgstab": (18, 0, [1, 3, 1]), "ibicgstab": (20, 0, [7]), "pipebicgstab": (26, 0, [3, 4]),
+    "pbicgstab": (19, 2, [1, 3, 1]), "rbicgstab": (21, 2, [1, 4]), "ppipebicgstab": (34, 2, [3, 4]),
+}
+
+
+@pytest.mark.parametrize("method", list(EQ14_19))
+def test_method_schedule_pc_eq14_19(method):
+    s = P.method_schedule_pc(method)
+    assert (s["vec"], s["precond"], s["reductions"]) == EQ14_19[method]
+    assert s["spmvs"] == 2
+
+
+def test_method_schedule_pc_variants():
+    # basic: every dot its own reduction; split_basic peels the 4-vector updates of Alg. 7
+    assert P.method_schedule_pc("ibicgstab", "basic")["reductions"] == [1] * 7
+    pp = P.method_schedule_pc("ppipebicgstab", "basic")
+    assert pp["reductions"] == [1] * 7 and pp["vec"] > 34
+    # fused + identity: the M^-1 copies are elided; a synthetic preconditioner is not
+    assert P.method_schedule_pc("pbicgstab", "fused")["precond"] == 0
+    assert P.method_schedule_pc("pbicgstab", "fused", 4)["precond"] == 2
+    # legacy totals fold one read + one write per identity application in
+    assert P.method_schedule("pbicgstab")["reads"] == 15 + 2
+    assert P.method_schedule("ppipebicgstab")["writes"] == 11 + 2
+    with pytest.raises(ValueError):
+        P.method_schedule_pc("bicgstab", "merged", 2)
+    with pytest.raises(ValueError):
+        P.method_schedule_pc("pbicgstab", "merged", 3)
+
+
 # merged lines as (kind, ...) tuples with symbolic vector ids
 X, P_, R, R0, V, S, T, Z, VH, TH, RT, Q, W, Y = range(14)
 GROUPS = {
