@@ -367,10 +367,14 @@ template <class P>
 struct unroll_of<P, decltype(void(P::UNROLL))> { static constexpr int value = P::UNROLL; };
 
 // Resident blocks to budget registers for: pipelined programs are latency
-// bound and need 4 blocks of 256 threads (<= 64 registers); the rest 2.
+// bound and need 4 blocks of 256 threads (<= 64 registers).
 template <class P>
 struct minblocks_of {
-    static constexpr int value = prefetch_of<P>::value ? (P::NDOT >= 3 ? 3 : 4) : 2;
+    // small pure updates: 3 blocks (<= 85 registers) -- with 2, ptxas spends
+    // the budget on a deeper schedule and the 3-term update drops ~5% (B200,
+    // C2); wider updates would spill under that cap
+    static constexpr int value =
+        prefetch_of<P>::value ? (P::NDOT >= 3 ? 3 : 4) : (P::NDOT == 0 && P::NIN + P::NOUT <= 5 ? 3 : 2);
 };
 
 // ---------------------------------------------------------------------------

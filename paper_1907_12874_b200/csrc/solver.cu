@@ -63,6 +63,11 @@ Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulatio
     if (!pre && precond_alpha != 0) throw Invalid("solve: this method takes no preconditioner");
     pa_ = precond_alpha;
     elide_ = formulation == MBG_FUSED && pa_ == 2;
+    // delta in the SpMM epilogue pays off for short rows only: with > 12
+    // nonzeros per row the gather-bound SpMM loses more to the epilogue's
+    // registers than the separate 2-vector dot pass costs (B200: C3 27-point
+    // 8.90 vs 8.07 ms/iteration, C5 m=8 5.28 vs 4.97; C2 7-point 0.76 vs 0.84)
+    epi_delta_ = formulation == MBG_FUSED && a->nnz <= 12 * a->n;
     if (method == MBG_IBICGSTAB) {
         if (!a->peers.empty() || a->n_halo)
             throw Invalid("solve: IBiCGStab needs f0 = A^T r0, supported on a single GPU only");
@@ -368,12 +373,12 @@ void Solver::iteration() {
         // identity M^-1: the fused formulation aliases s = v and q = t instead of copying
         double* s = elide_ ? v : w(V_S);
         double* q = elide_ ? t : w(V_Q);
-        if (fused) {
+        if (fused && epi_delta_) {
             spmm(vh, v, 1, r0, P_C_ALPHA, 1);                     // v = A vh ; delta = (v, r0) ; alpha
             if (!elide_) minv(v, s);
         } else {
             spmm(vh, v);
-            minv(v, s);                                           // s = M^-1 v
+            if (!elide_) minv(v, s);                              // s = M^-1 v
             group<PDot2>({v, r0}, {}, {}, 0, P_C_ALPHA, 1);
         }
         group<PUpd2>({z, s}, {th}, {S_ONE, S_NALPHA}, 0);        // th = z - alpha s
@@ -629,10 +634,14 @@ void Solver::report(double* hist_host, mbg_report* rep) {
     const int its = rep->iterations;
     // TrafficCounter semantics: the preconditioner's transfers are tallied too
     // (alpha/2 reads + alpha/2 writes per application)
+    if (method_ == MBG_RBICGSTAB && form_ == MBG_FUSED && !epi_delta_) reads += 1;   // delta pass: v, r0 vs aux r0
     rep->vector_reads = static_cast<int64_t>(reads + apps * pa_ / 2) * its;
     rep->vector_writes = static_cast<int64_t>(writes + apps * pa_ / 2) * its;
     rep->spmv_bytes = static_cast<double>(spmvs) * its * spmv_traffic_bytes(a_->n, a_->nnz, m_);
-    rep->compulsory_bytes = iteration_bytes(method_, form_, pa_, a_->n, a_->nnz, m_) * its;
+    rep->compulsory_bytes =
+        (iteration_bytes(method_, form_, pa_, a_->n, a_->nnz, m_) +
+         ((method_ == MBG_RBICGSTAB && form_ == MBG_FUSED && !epi_delta_) ? 8.0 * static_cast<double>(len_) : 0.0)) *
+        its;
     rep->reductions = static_cast<int64_t>(nred) * its;
     rep->gpu_launches = launches_;
     rep->loop_ms = loop_ms_;

@@ -69,6 +69,7 @@ private:
     int m_, method_, form_;
     int pa_ = 0;            // preconditioner alpha (0 none, 2 identity, >= 4 synthetic)
     bool elide_ = false;    // fused formulation with identity M^-1: applications aliased away
+    bool epi_delta_ = false;  // fused Reordered: delta = (v, r0) in the SpMM epilogue
     const mbg_csr* at_ = nullptr;   // A^T (IBiCGStab setup)
     double tol_;
     int fixed_, maxit_;
