@@ -319,8 +319,27 @@ inline void execute_group(const StatementGroup& group, std::span<core::MultiVect
 
 namespace solvers {  // SPEC.md:198-278 (missing from the reference tree)
 
-enum class Method { BiCGStab = MBG_BICGSTAB, RBiCGStab = MBG_RBICGSTAB, PipeBiCGStab = MBG_PIPEBICGSTAB };
-enum class Formulation { basic = MBG_BASIC, merged = MBG_MERGED };
+// the six methods; RBiCGStab, PBiCGStab, PPipeBiCGStab are preconditioned
+enum class Method {
+    BiCGStab = MBG_BICGSTAB, RBiCGStab = MBG_RBICGSTAB, PipeBiCGStab = MBG_PIPEBICGSTAB,
+    IBiCGStab = MBG_IBICGSTAB, PBiCGStab = MBG_PBICGSTAB, PPipeBiCGStab = MBG_PPIPEBICGSTAB
+};
+enum class Formulation { basic = MBG_BASIC, merged = MBG_MERGED, fused = MBG_FUSED };
+inline bool is_preconditioned(Method m) {
+    return m == Method::RBiCGStab || m == Method::PBiCGStab || m == Method::PPipeBiCGStab;
+}
+
+// identity (2 transfers per application) or synthetic(alpha)
+// (alpha transfers: alpha/2 scale passes whose factors multiply to exactly 1).
+struct Preconditioner {
+    enum class Kind { identity, synthetic } kind = Kind::identity;
+    int alpha = 2;
+    static Preconditioner identity() { return {Kind::identity, 2}; }
+    static Preconditioner synthetic(int a) {
+        if (a < 2 || a % 2) throw std::invalid_argument("synthetic preconditioner: alpha must be even and >= 2");
+        return {Kind::synthetic, a};
+    }
+};
 struct Mode {
     bool fixed = false;
     int iterations = 1000;   // max (converge) or exact (fixed)
@@ -341,12 +360,16 @@ struct BreakdownError : std::runtime_error {
 };
 
 // Device-resident solve: X holds x0 on entry and the solution on exit.
+// precond: required by the preconditioned methods, rejected by the others
+// (std::invalid_argument); nullptr = identity for the former.
 inline SolveReport solve(Device& dev, const DeviceMatrix& A, const DeviceVector& B, DeviceVector& X, int m,
-                         Method method, Formulation form, double tol, Mode mode) {
+                         Method method, Formulation form, double tol, Mode mode,
+                         const Preconditioner* precond = nullptr) {
     std::vector<double> hist(static_cast<std::size_t>(mode.iterations + 1) * m);
     mbg_report rep{};
-    const int rc = mbg_solve(dev.get(), A.get(), B.get(), X.get(), static_cast<int>(method),
-                             static_cast<int>(form), tol, mode.fixed, mode.iterations, hist.data(), &rep);
+    const int pa = precond ? precond->alpha : (is_preconditioned(method) ? 2 : 0);
+    const int rc = mbg_solve_pc(dev.get(), A.get(), B.get(), X.get(), static_cast<int>(method),
+                                static_cast<int>(form), pa, tol, mode.fixed, mode.iterations, hist.data(), &rep);
     if (rc == MBG_ERR_BREAKDOWN) throw BreakdownError(mbg_last_error());
     check(rc);
     SolveReport r;
@@ -366,12 +389,12 @@ inline SolveReport solve(Device& dev, const DeviceMatrix& A, const DeviceVector&
 
 // Host-container solve: uploads A, B and x0, downloads X.
 inline SolveReport solve(const core::CsrMatrix& A, const core::MultiVector& B, core::MultiVector& X, Method method,
-                         Formulation form, double tol, Mode mode) {
+                         Formulation form, double tol, Mode mode, const Preconditioner* precond = nullptr) {
     if (!B.same_shape(X) || B.n_rows != A.n_rows) throw std::invalid_argument("solve: shape mismatch");
     Device& dev = Device::default_device();
     DeviceMatrix dA(dev, A);
     DeviceVector dB(dev, B), dX(dev, X);
-    SolveReport r = solve(dev, dA, dB, dX, B.n_cols, method, form, tol, mode);
+    SolveReport r = solve(dev, dA, dB, dX, B.n_cols, method, form, tol, mode, precond);
     dX.download(X);
     return r;
 }

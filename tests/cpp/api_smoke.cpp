@@ -65,6 +65,26 @@ int main() {
     double worst = 0.0;
     for (std::size_t i = 0; i < R.data.size(); ++i) worst = std::fmax(worst, std::fabs(R.data[i] - B.data[i]));
     if (worst > 1e-7) { std::printf("residual %g\n", worst); return 1; }
+    // the preconditioned methods with a synthetic preconditioner, and the
+    // SPEC.md:205 presence rule
+    {
+        core::MultiVector X2(A.n_rows, m);
+        auto pc = solvers::Preconditioner::synthetic(4);
+        auto r2 = solvers::solve(A, B, X2, solvers::Method::PPipeBiCGStab, solvers::Formulation::merged, 1e-10,
+                                 solvers::Mode::converge(500), &pc);
+        core::MultiVector X3(A.n_rows, m);
+        auto r3 = solvers::solve(A, B, X3, solvers::Method::IBiCGStab, solvers::Formulation::merged, 1e-10,
+                                 solvers::Mode::converge(500));
+        if (!r2.converged || !r3.converged) { std::puts("preconditioned / improved solve"); return 1; }
+        try {
+            core::MultiVector X4(A.n_rows, m);
+            solvers::solve(A, B, X4, solvers::Method::BiCGStab, solvers::Formulation::merged, 1e-10,
+                           solvers::Mode::converge(10), &pc);
+            std::puts("preconditioner on an unpreconditioned method not rejected");
+            return 1;
+        } catch (const std::invalid_argument&) {
+        }
+    }
     // API misuse throws std::invalid_argument like the reference
     try {
         core::spmv(A, x, x);
