@@ -210,6 +210,22 @@ int mbg_method_schedule_pc(int method, int formulation, int precond_alpha, int* 
                            int* spmvs, int* precond_applications, int* nreductions,
                            int* dots_per_reduction);
 
+/* ---- MatrixMarket ingest (host; core::read_matrix_market / write_matrix_market,
+ * proj/src/core/matrix_market.cpp:38-113,121-133) ------------
+ * mbg_mm_read parses a coordinate real/integer, general/symmetric file (all
+ * host threads) into a host CSR held by *handle: n, nnz returned; errors are
+ * the reference's "<name>:<line>: message" (MBG_ERR_RUNTIME).  Symmetric
+ * files are expanded, duplicates summed (file order), rows sorted by column.
+ * mbg_mm_copy fills caller arrays (offsets n+1, cols/vals nnz; any may be
+ * NULL); mbg_mm_free releases the handle.  The arrays feed mbg_csr_upload or
+ * mbg_csr_upload_partitioned (general halo plan) unchanged. */
+int mbg_mm_read(const char* path, void** handle, int64_t* n, int64_t* nnz);
+int mbg_mm_copy(const void* handle, int64_t* offsets, int32_t* cols, double* vals);
+void mbg_mm_free(void* handle);
+/* "matrix coordinate real general", 1-based, values printed with %.17g. */
+int mbg_mm_write(const char* path, int64_t n, const int64_t* offsets, const int32_t* cols,
+                 const double* vals);
+
 /* ---- config generators (host) --------------------------------------------
  * kind 0 Poisson 7-pt (gen_poisson_7pt), 1 conv-diff 7-pt, 2 27-pt perturbed.
  * Two-phase: call with NULL cols/vals to get nnz (offsets may be NULL too). */

@@ -22,6 +22,8 @@
 #include "mbstab/core/csr.hpp"
 #include "mbstab/core/generators.hpp"
 #include "mbstab/core/spmv.hpp"
+#include "mbstab/core/matrix_market.hpp"
+#include "mbstab/core/matrix_market.hpp"
 #include "mbstab/core/types.hpp"
 #include "mbstab/kernels/execute.hpp"
 #include "mbstab/kernels/statement.hpp"
@@ -116,6 +118,29 @@ extern "C" int ref_spmv_transpose(int64_t n, const int64_t* off, const int32_t* 
         MultiVector X = make_mv(n, m, x), Y(n, m);
         core::spmv_transpose(A, X, Y, nullptr);
         std::memcpy(y, Y.data.data(), sizeof(double) * n * m);
+        return 0;
+    } catch (const std::exception& e) { g_err = e.what(); return 1; }
+}
+
+// core::read_matrix_market: two-phase (arrays NULL -> sizes only; the file is re-read).
+extern "C" int ref_read_matrix_market(const char* path, int64_t* n, int64_t* nnz, int64_t* off, int32_t* col,
+                                      double* val) {
+    try {
+        CsrMatrix A = core::read_matrix_market(std::string(path));
+        *n = A.n_rows;
+        *nnz = A.nnz();
+        if (off) std::memcpy(off, A.row_offsets.data(), sizeof(int64_t) * (A.n_rows + 1));
+        if (col) std::memcpy(col, A.col_indices.data(), sizeof(int32_t) * A.nnz());
+        if (val) std::memcpy(val, A.values.data(), sizeof(double) * A.nnz());
+        return 0;
+    } catch (const std::exception& e) { g_err = e.what(); return 1; }
+}
+
+extern "C" int ref_write_matrix_market(const char* path, int64_t n, const int64_t* off, const int32_t* col,
+                                       const double* val) {
+    try {
+        CsrMatrix A = make_csr(n, off, col, val);
+        core::write_matrix_market(A, std::string(path));
         return 0;
     } catch (const std::exception& e) { g_err = e.what(); return 1; }
 }

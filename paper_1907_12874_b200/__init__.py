@@ -474,3 +474,25 @@ def exact_round(digits: np.ndarray, count: int) -> np.ndarray:
     d = np.ascontiguousarray(digits, np.int64)
     check(lib().mbg_exact_round_host(_ptr(d), count, _ptr(out)))
     return out
+
+
+# ---- MatrixMarket (core::read_matrix_market / write_matrix_market) ----------
+def read_matrix_market(path) -> CsrMatrix:
+    """Coordinate real/integer, general/symmetric MatrixMarket file -> CsrMatrix
+    (matrix_market.cpp:38-113 contract; RuntimeError "<name>:<line>: message")."""
+    h = C.c_void_p()
+    n, nnz = C.c_int64(), C.c_int64()
+    check(lib().mbg_mm_read(str(path).encode(), C.byref(h), C.byref(n), C.byref(nnz)))
+    try:
+        off = np.empty(n.value + 1, np.int64)
+        col = np.empty(nnz.value, np.int32)
+        val = np.empty(nnz.value, np.float64)
+        check(lib().mbg_mm_copy(h, _ptr(off), _ptr(col), _ptr(val)))
+    finally:
+        lib().mbg_mm_free(h)
+    return CsrMatrix(int(n.value), off, col, val)
+
+
+def write_matrix_market(a: CsrMatrix, path) -> None:
+    check(lib().mbg_mm_write(str(path).encode(), a.n_rows, _ptr(a.row_offsets), _ptr(a.col_indices),
+                             _ptr(a.values)))

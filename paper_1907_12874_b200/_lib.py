@@ -111,6 +111,10 @@ def lib() -> C.CDLL:
         "mbg_gen_stencil": (i32, [i32, i32, i32, i32, C.c_uint64, C.POINTER(C.c_int64), vp, vp, vp]),
         "mbg_gen_banded": (i32, [i64, i64, i32, i32, C.c_uint64, C.POINTER(C.c_int64), vp, vp, vp]),
         "mbg_gen_rhs": (i32, [i64, i32, C.c_uint64, vp]),
+        "mbg_mm_read": (i32, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+        "mbg_mm_copy": (i32, [vp, vp, vp, vp]),
+        "mbg_mm_free": (None, [vp]),
+        "mbg_mm_write": (i32, [C.c_char_p, i64, vp, vp, vp]),
         "mbg_exact_slot_words": (i32, []),
         "mbg_exact_accumulate_host": (i32, [i64, i32, vp, vp, vp]),
         "mbg_exact_round_host": (i32, [vp, i32, vp]),

@@ -90,6 +90,9 @@ def ref() -> C.CDLL:
         lib.ref_validate.argtypes = [C.c_int64, _i64p, _i32p, _f64p]
         lib.ref_spmv.argtypes = [C.c_int64, _i64p, _i32p, _f64p, C.c_int, _f64p, _f64p, C.c_int]
         lib.ref_spmv_transpose.argtypes = [C.c_int64, _i64p, _i32p, _f64p, C.c_int, _f64p, _f64p]
+        lib.ref_read_matrix_market.argtypes = [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                               C.c_void_p, C.c_void_p, C.c_void_p]
+        lib.ref_write_matrix_market.argtypes = [C.c_char_p, C.c_int64, _i64p, _i32p, _f64p]
         lib.ref_spmv_traffic_bytes.restype = C.c_double
         lib.ref_spmv_traffic_bytes.argtypes = [C.c_int64, C.c_int64, C.c_int]
         lib.ref_solve.argtypes = [C.c_int, C.c_int64, _i64p, _i32p, _f64p, C.c_int, _f64p, _f64p,
@@ -246,6 +249,24 @@ def ref_spmv_transpose(a: Csr, x: np.ndarray, m: int) -> np.ndarray:
     rc = ref().ref_spmv_transpose(a.n, a.off, a.col, a.val, m, np.ascontiguousarray(x), y)
     assert rc == 0, ref().ref_last_error()
     return y
+
+
+def ref_read_matrix_market(path):
+    """core::read_matrix_market from the reference sources: Csr or raises RuntimeError(msg)."""
+    lib = ref()
+    n, nnz = C.c_int64(), C.c_int64()
+    if lib.ref_read_matrix_market(str(path).encode(), C.byref(n), C.byref(nnz), None, None, None):
+        raise RuntimeError(lib.ref_last_error().decode())
+    off = np.empty(n.value + 1, np.int64)
+    col = np.empty(nnz.value, np.int32)
+    val = np.empty(nnz.value)
+    assert lib.ref_read_matrix_market(str(path).encode(), C.byref(n), C.byref(nnz), off.ctypes.data,
+                                      col.ctypes.data, val.ctypes.data) == 0
+    return Csr(n.value, off, col, val)
+
+
+def ref_write_matrix_market(a: Csr, path) -> None:
+    assert ref().ref_write_matrix_market(str(path).encode(), a.n, a.off, a.col, a.val) == 0
 
 
 def ref_solve(a: Csr, b: np.ndarray, m: int, method="bicgstab", tol=1e-8, fixed=False, maxit=1000,

@@ -143,3 +143,24 @@ def test_ibicgstab_partitioned_rejected(ctx):
     a = O.gen_stencil("convdiff7", 8, 8, 8)
     with pytest.raises(AssertionError, match="single GPU"):
         run_partitioned(a, O.rhs(a.n, 2, 1), 2, [0, 256, 512], "ibicgstab", "merged", tol=1e-8)
+
+
+def test_matrix_market_ingest_partitioned(ctx, tmp_path):
+    """a MatrixMarket file (arbitrary sparsity) ->
+    device CSR with the general halo plan over uneven row blocks -> the same
+    bits as the single-GPU / oracle solve."""
+    a = O.gen_banded(30_000, 9_000, 8, 20, 4)
+    path = tmp_path / "band.mtx"
+    P.write_matrix_market(P.CsrMatrix(a.n, a.off, a.col, a.val), path)
+    m_ = P.read_matrix_market(path)
+    assert np.array_equal(m_.values.view(np.int64), a.val.view(np.int64))
+    a2 = O.Csr(m_.n_rows, m_.row_offsets, m_.col_indices, m_.values)
+    m = 4
+    b = O.rhs(a2.n, m, 4)
+    bounds = [0, 7_001, 19_500, 30_000]
+    want = O.solve(a2, b, m, "pipebicgstab", fixed=True, maxit=20)
+    parts = run_partitioned(a2, b, m, bounds, "pipebicgstab", "merged", fixed=True, max_iters=20)
+    for r, (rep, x) in enumerate(parts):
+        assert rep.iterations == 20
+        assert np.array_equal(rep.residual_history.view(np.int64), want["hist"].view(np.int64))
+        assert np.array_equal(x.view(np.int64), want["x"][bounds[r] * m:bounds[r + 1] * m].view(np.int64))
