@@ -226,6 +226,14 @@ void mbg_mm_free(void* handle);
 int mbg_mm_write(const char* path, int64_t n, const int64_t* offsets, const int32_t* cols,
                  const double* vals);
 
+/* ---- fusion micro-benchmark (Fig. 2 / Table 1)
+ * Runs #1 (three passes, 9N transfers), #2 (two updates merged, 5N) and #3
+ * (three updates merged, 5N) over n doubles, each timed over reps launches with
+ * CUDA events.  ms_per_run[3], gbs_per_run[3] (may be NULL); identical = 1 when
+ * run #3 reproduced run #1's y and z bit for bit. */
+int mbg_fusion_bench(mbg_ctx* ctx, int64_t n, int reps, double* ms_per_run, double* gbs_per_run,
+                     int* identical);
+
 /* ---- config generators (host) --------------------------------------------
  * kind 0 Poisson 7-pt (gen_poisson_7pt), 1 conv-diff 7-pt, 2 27-pt perturbed.
  * Two-phase: call with NULL cols/vals to get nnz (offsets may be NULL too). */

@@ -496,3 +496,17 @@ def read_matrix_market(path) -> CsrMatrix:
 def write_matrix_market(a: CsrMatrix, path) -> None:
     check(lib().mbg_mm_write(str(path).encode(), a.n_rows, _ptr(a.row_offsets), _ptr(a.col_indices),
                              _ptr(a.values)))
+
+
+def fusion_bench(ctx: Context, n: int = 100_000_000, reps: int = 10) -> dict:
+    """Fig. 2 runs #1-#3: ms and GB/s per run, run1/run2
+    ratio (paper: ~1.76, memory-traffic ratio 1.8, flop ratio 1.5), and whether
+    run #3 reproduced run #1 bit for bit."""
+    ms = np.zeros(3)
+    gbs = np.zeros(3)
+    same = C.c_int(0)
+    check(lib().mbg_fusion_bench(ctx.h, n, reps, _ptr(ms), _ptr(gbs), C.byref(same)))
+    return {"n": n, "reps": reps, "ms": ms.tolist(), "GBps": gbs.tolist(),
+            "run1_over_run2": float(ms[0] / ms[1]), "run3_over_run2": float(ms[2] / ms[1]),
+            "run3_equals_run1": bool(same.value)}
+

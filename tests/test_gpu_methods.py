@@ -164,3 +164,11 @@ def test_matrix_market_ingest_partitioned(ctx, tmp_path):
         assert rep.iterations == 20
         assert np.array_equal(rep.residual_history.view(np.int64), want["hist"].view(np.int64))
         assert np.array_equal(x.view(np.int64), want["x"][bounds[r] * m:bounds[r + 1] * m].view(np.int64))
+
+
+def test_fusion_bench_runs_agree(ctx):
+    """Fig. 2: run #3 (three updates in one pass) computes exactly what run #1
+    (three passes) computes; the merged runs move 5N instead of 9N elements."""
+    r = P.fusion_bench(ctx, n=1 << 22, reps=3)
+    assert r["run3_equals_run1"]
+    assert all(t > 0 for t in r["ms"])
