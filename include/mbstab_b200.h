@@ -191,6 +191,12 @@ int mbg_solve_host(mbg_ctx* ctx, const mbg_csr* a, int m, const double* b_host, 
                    int method, int formulation, double tol, int fixed, int max_iters,
                    double* hist, mbg_report* report);
 
+/* Page-locked host buffers for mbg_solve_host / mbg_mv_upload-style traffic:
+ * pinned b / x are DMA'd directly at link rate (55 GB/s on the GPU box);
+ * pageable ones go through an internal pinned staging pipeline. */
+int mbg_host_alloc(size_t bytes, void** out);
+int mbg_host_free(void* p);
+
 /* Profiling solve (bench.py roofline): identical numerics, launched without a
  * graph with CUDA events around every kernel of the iteration loop; writes
  * {"label": [launches, total_ms, algorithmic_bytes_per_launch], ...} to json. */

@@ -510,3 +510,26 @@ def fusion_bench(ctx: Context, n: int = 100_000_000, reps: int = 10) -> dict:
             "run1_over_run2": float(ms[0] / ms[1]), "run3_over_run2": float(ms[2] / ms[1]),
             "run3_equals_run1": bool(same.value)}
 
+
+class _PinnedBlock:
+    def __init__(self, nbytes: int):
+        self.ptr = C.c_void_p()
+        check(lib().mbg_host_alloc(nbytes, C.byref(self.ptr)))
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                lib().mbg_host_free(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
+
+
+def pinned_empty(n: int, dtype=np.float64) -> np.ndarray:
+    """A numpy array in page-locked host memory (DMA'd directly by solve_host)."""
+    dt = np.dtype(dtype)
+    blk = _PinnedBlock(max(1, n * dt.itemsize))
+    buf = (C.c_char * max(1, n * dt.itemsize)).from_address(blk.ptr.value)
+    buf._owner = blk   # the array's base (buf) keeps the pinned block alive
+    return np.frombuffer(buf, dtype=dt, count=n)
+

@@ -116,6 +116,8 @@ def lib() -> C.CDLL:
         "mbg_mm_free": (None, [vp]),
         "mbg_mm_write": (i32, [C.c_char_p, i64, vp, vp, vp]),
         "mbg_fusion_bench": (i32, [vp, i64, i32, vp, vp, C.POINTER(C.c_int)]),
+        "mbg_host_alloc": (i32, [C.c_size_t, C.POINTER(C.c_void_p)]),
+        "mbg_host_free": (i32, [vp]),
         "mbg_exact_slot_words": (i32, []),
         "mbg_exact_accumulate_host": (i32, [i64, i32, vp, vp, vp]),
         "mbg_exact_round_host": (i32, [vp, i32, vp]),

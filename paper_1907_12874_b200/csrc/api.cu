@@ -2,7 +2,12 @@
 // execute_group and solve.  No exception crosses the boundary; invalid usage
 // maps to MBG_ERR_INVALID with the reference's message text.
 #include <algorithm>
+#include <chrono>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <condition_variable>
+#include <mutex>
 #include <thread>
 #include <cstring>
 #include <string>
@@ -596,52 +601,168 @@ extern "C" int mbg_solve_pc(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* b, mbg
 }
 
 // Host <-> device copies of user (pageable) buffers: a multi-threaded memcpy
-// into a context-owned pinned staging buffer, then one DMA.  Pageable
-// cudaMemcpy runs at a few GB/s; this reaches PCIe rates.
-static void parallel_memcpy(void* dst, const void* src, size_t bytes) {
-    const size_t per = 8u << 20;
-    unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    nt = static_cast<unsigned>(std::min<size_t>(nt, (bytes + per - 1) / per));
-    if (nt <= 1) {
-        std::memcpy(dst, src, bytes);
-        return;
+// into pinned staging, pipelined against the DMA.  Measured on the GPU box
+// (tools/h2d_lab.cu): pageable cudaMemcpy 11-17 GB/s, pinned DMA 55 GB/s,
+// host memcpy 64 GB/s with 8 threads -- so 8 persistent copy workers.
+class CopyPool {
+public:
+    static CopyPool& get() {
+        static CopyPool pool;
+        return pool;
     }
-    std::vector<std::thread> th;
-    const size_t chunk = (bytes + nt - 1) / nt;
-    for (unsigned t = 0; t < nt; ++t) {
-        const size_t b = std::min(bytes, t * chunk), e = std::min(bytes, b + chunk);
-        if (b < e)
-            th.emplace_back([=] {
-                std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, e - b);
-            });
+    void run(void* dst, const void* src, size_t bytes) {
+        if (bytes < (4u << 20) || workers_.empty()) {
+            std::memcpy(dst, src, bytes);
+            return;
+        }
+        std::unique_lock<std::mutex> lk(mu_);
+        dst_ = static_cast<char*>(dst);
+        src_ = static_cast<const char*>(src);
+        bytes_ = bytes;
+        pending_ = static_cast<int>(workers_.size());
+        ++gen_;
+        cv_.notify_all();
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
     }
-    for (auto& x : th) x.join();
-}
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+            cv_.notify_all();
+        }
+        for (auto& t : workers_) t.join();
+    }
 
-static unsigned char* stage_buffer(mbg_ctx* ctx, size_t bytes) {
-    if (ctx->stage_bytes < bytes) {
-        if (ctx->stage) cudaFreeHost(ctx->stage);
-        ctx->stage = nullptr;
-        ctx->stage_bytes = 0;
-        MBG_CUDA(cudaMallocHost(&ctx->stage, bytes));
-        ctx->stage_bytes = bytes;
+private:
+    CopyPool() {
+        const unsigned nt = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+        for (unsigned t = 0; t < nt; ++t) workers_.emplace_back([this, t, nt] { loop(t, nt); });
+    }
+    void loop(unsigned t, unsigned nt) {
+        long seen = 0;
+        for (;;) {
+            char* d;
+            const char* s;
+            size_t n;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+                d = dst_;
+                s = src_;
+                n = bytes_;
+            }
+            const size_t b = n * t / nt, e = n * (t + 1) / nt;
+            if (b < e) std::memcpy(d + b, s + b, e - b);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_cv_.notify_one();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t bytes_ = 0;
+    int pending_ = 0;
+    long gen_ = 0;
+    bool stop_ = false;
+};
+
+static void parallel_memcpy(void* dst, const void* src, size_t bytes) { CopyPool::get().run(dst, src, bytes); }
+
+// Two pinned staging halves of STAGE_CHUNK bytes: the host memcpy of chunk k
+// overlaps the DMA of chunk k-1 (upload) / the DMA of chunk k+1 overlaps the
+// host memcpy of chunk k (download).
+constexpr size_t STAGE_CHUNK = 64u << 20;
+
+static unsigned char* stage_buffer(mbg_ctx* ctx) {
+    if (!ctx->stage) {
+        MBG_CUDA(cudaMallocHost(&ctx->stage, 2 * STAGE_CHUNK));
+        ctx->stage_bytes = 2 * STAGE_CHUNK;
     }
     return ctx->stage;
 }
 
+// Page-locked host memory (cudaMallocHost / mbg_host_alloc / registered) is
+// DMA'd directly at link rate; pageable memory goes through the staging
+// pipeline (host memory bandwidth shared by memcpy and DMA caps it near 27 GB/s).
+static bool host_pinned(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
 static void upload_host(mbg_ctx* ctx, double* dev, const double* host, size_t count) {
-    unsigned char* st = stage_buffer(ctx, count * sizeof(double));
-    MBG_CUDA(cudaStreamSynchronize(ctx->stream));   // staging buffer free
-    parallel_memcpy(st, host, count * sizeof(double));
-    MBG_CUDA(cudaMemcpyAsync(dev, st, count * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    if (host_pinned(host)) {
+        MBG_CUDA(cudaMemcpyAsync(dev, host, count * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+        return;
+    }
+    unsigned char* st = stage_buffer(ctx);
+    MBG_CUDA(cudaStreamSynchronize(ctx->stream));   // staging halves free
+    cudaEvent_t done[2];
+    for (auto& e : done) MBG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    const size_t bytes = count * sizeof(double);
+    const auto* src = reinterpret_cast<const unsigned char*>(host);
+    auto* dst = reinterpret_cast<unsigned char*>(dev);
+    size_t k = 0;
+    for (size_t o = 0; o < bytes; o += STAGE_CHUNK, ++k) {
+        const size_t n = std::min(STAGE_CHUNK, bytes - o);
+        unsigned char* half = st + (k & 1) * STAGE_CHUNK;
+        if (k >= 2) MBG_CUDA(cudaEventSynchronize(done[k & 1]));   // DMA out of this half finished
+        parallel_memcpy(half, src + o, n);
+        MBG_CUDA(cudaMemcpyAsync(dst + o, half, n, cudaMemcpyHostToDevice, ctx->stream));
+        MBG_CUDA(cudaEventRecord(done[k & 1], ctx->stream));
+    }
     MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (auto& e : done) cudaEventDestroy(e);
 }
 
 static void download_host(mbg_ctx* ctx, double* host, const double* dev, size_t count) {
-    unsigned char* st = stage_buffer(ctx, count * sizeof(double));
-    MBG_CUDA(cudaMemcpyAsync(st, dev, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    MBG_CUDA(cudaStreamSynchronize(ctx->stream));
-    parallel_memcpy(host, st, count * sizeof(double));
+    if (host_pinned(host)) {
+        MBG_CUDA(cudaMemcpyAsync(host, dev, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+        return;
+    }
+    unsigned char* st = stage_buffer(ctx);
+    cudaEvent_t ready[2];
+    for (auto& e : ready) MBG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    const size_t bytes = count * sizeof(double);
+    const auto* src = reinterpret_cast<const unsigned char*>(dev);
+    auto* dst = reinterpret_cast<unsigned char*>(host);
+    const size_t nchunks = (bytes + STAGE_CHUNK - 1) / STAGE_CHUNK;
+    auto issue = [&](size_t k) {
+        const size_t o = k * STAGE_CHUNK, n = std::min(STAGE_CHUNK, bytes - o);
+        MBG_CUDA(cudaMemcpyAsync(st + (k & 1) * STAGE_CHUNK, src + o, n, cudaMemcpyDeviceToHost, ctx->stream));
+        MBG_CUDA(cudaEventRecord(ready[k & 1], ctx->stream));
+    };
+    if (nchunks) issue(0);
+    for (size_t k = 0; k < nchunks; ++k) {
+        MBG_CUDA(cudaEventSynchronize(ready[k & 1]));
+        if (k + 1 < nchunks) issue(k + 1);   // the other half is free: its copy-out finished last trip
+        const size_t o = k * STAGE_CHUNK, n = std::min(STAGE_CHUNK, bytes - o);
+        parallel_memcpy(dst + o, st + (k & 1) * STAGE_CHUNK, n);
+    }
+    for (auto& e : ready) cudaEventDestroy(e);
+}
+
+extern "C" int mbg_host_alloc(size_t bytes, void** out) {
+    return guarded([&] {
+        if (!out) throw Invalid("host_alloc: null output");
+        *out = nullptr;
+        if (bytes) MBG_CUDA(cudaMallocHost(out, bytes));
+    });
+}
+
+extern "C" int mbg_host_free(void* p) {
+    return guarded([&] {
+        if (p) MBG_CUDA(cudaFreeHost(p));
+    });
 }
 
 extern "C" int mbg_solve_host(mbg_ctx* ctx, const mbg_csr* a, int m, const double* b_host, double* x_host,
@@ -658,15 +779,24 @@ extern "C" int mbg_solve_host(mbg_ctx* ctx, const mbg_csr* a, int m, const doubl
             DevBuf<double>& b;
             ~Give() { pool_give(c, std::move(a)); pool_give(c, std::move(b)); }
         } give{ctx, db, dx};
+        static const bool trace = std::getenv("MBG_TRACE_E2E") != nullptr;
+        auto now = [] { return std::chrono::duration<double, std::milli>(
+                            std::chrono::steady_clock::now().time_since_epoch()).count(); };
+        const double t0 = now();
         upload_host(ctx, db.p, b_host, cnt);
         upload_host(ctx, dx.p, x_host, cnt);
+        const double t1 = now();
         try {
             do_solve(ctx, a, m, db.p, dx.p, method, formulation, tol, fixed, max_iters, hist, report);
         } catch (const Breakdown&) {
             download_host(ctx, x_host, dx.p, cnt);
             throw;
         }
+        const double t2 = now();
         download_host(ctx, x_host, dx.p, cnt);
+        if (trace)
+            std::fprintf(stderr, "solve_host: upload %.2f ms, solve %.2f ms, download %.2f ms\n", t1 - t0, t2 - t1,
+                         now() - t2);
     });
 }
 

@@ -286,3 +286,19 @@ def test_graph_replay_overshoot_is_noop(ctx):
     want, rep, X = run_both(ctx, a, b, 1, "bicgstab", maxit=1000)
     assert rep.iterations < 64 and rep.gpu_launches > 0
     assert_same_solve(want, rep, X, "overshoot")
+
+
+def test_solve_host_pinned_buffers(ctx):
+    """Page-locked host buffers take the direct-DMA path of mbg_solve_host."""
+    a = O.gen_stencil("convdiff7", 20, 18, 16)
+    m = 4
+    b = O.rhs(a.n, m, 1)
+    want = O.solve(a, b, m, "bicgstab")
+    d = ctx.upload(to_prod(a))
+    bp = P.pinned_empty(a.n * m)
+    bp[:] = b
+    xp = P.pinned_empty(a.n * m)
+    xp[:] = 0.0
+    rep = P.solve_host(ctx, d, bp, xp, m, "bicgstab")
+    assert rep.iterations == want["iterations"]
+    assert_bitwise(xp, want["x"], "pinned solve_host x")
