@@ -92,6 +92,12 @@ int mbg_halo_plan(int64_t n, const int64_t* offsets, const int32_t* cols, const 
                   int32_t* loc_off, int32_t* loc_col, double* loc_val, int64_t* halo_global, int* npeers,
                   int* peer_part, int64_t* peer_send_count, int32_t* peer_send_rows,
                   int64_t* peer_recv_offset, int64_t* peer_recv_count);
+/* Same as mbg_csr_upload but a row's column indices may come in any order
+ * (each row is still summed in the given order; no duplicates checked
+ * beyond range) -- for permuted operators P A P^T that keep every row's
+ * original summation order. */
+int mbg_csr_upload_any_order(mbg_ctx* ctx, int64_t n, const int64_t* offsets, const int32_t* cols,
+                             const double* vals, mbg_csr** out);
 int mbg_csr_free(mbg_csr* a);
 int64_t mbg_csr_rows(const mbg_csr* a);   /* local rows */
 int64_t mbg_csr_nnz(const mbg_csr* a);    /* local nnz */

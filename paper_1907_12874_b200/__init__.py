@@ -160,8 +160,9 @@ class Context:
     def init_comm(self, rank: int, world: int, nccl_id: bytes) -> None:
         check(lib().mbg_ctx_init_comm(self.h, rank, world, nccl_id))
 
-    def upload(self, a: CsrMatrix, parts: Sequence[int] | None = None, my_part: int = 0) -> "DeviceCsr":
-        return DeviceCsr(self, a, parts, my_part)
+    def upload(self, a: CsrMatrix, parts: Sequence[int] | None = None, my_part: int = 0,
+               any_order: bool = False) -> "DeviceCsr":
+        return DeviceCsr(self, a, parts, my_part, any_order)
 
     def multivector(self, n: int, m: int, data: np.ndarray | None = None) -> "MultiVector":
         v = MultiVector(self, n, m)
@@ -183,12 +184,12 @@ def comm_unique_id() -> bytes:
 
 
 class DeviceCsr:
-    def __init__(self, ctx: Context, a: CsrMatrix, parts=None, my_part: int = 0):
+    def __init__(self, ctx: Context, a: CsrMatrix, parts=None, my_part: int = 0, any_order: bool = False):
         self.ctx = ctx
         h = C.c_void_p()
         if parts is None:
-            check(lib().mbg_csr_upload(ctx.h, a.n_rows, _ptr(a.row_offsets), _ptr(a.col_indices),
-                                       _ptr(a.values), C.byref(h)))
+            up = lib().mbg_csr_upload_any_order if any_order else lib().mbg_csr_upload
+            check(up(ctx.h, a.n_rows, _ptr(a.row_offsets), _ptr(a.col_indices), _ptr(a.values), C.byref(h)))
             self.row_begin, self.row_end = 0, a.n_rows
         else:
             b = np.ascontiguousarray(parts, dtype=np.int64)

@@ -46,7 +46,7 @@ static void use(mbg_ctx* ctx) {
 }
 
 // CsrMatrix::validate (csr.cpp:8-32), same messages.
-static void validate_csr(int64_t n, const int64_t* off, const int32_t* col, int64_t nnz) {
+static void validate_csr(int64_t n, const int64_t* off, const int32_t* col, int64_t nnz, bool sorted = true) {
     if (n < 0) throw Invalid("csr: negative row count");
     if (!off) throw Invalid("csr: row_offsets length must be n_rows+1");
     if (off[0] != 0) throw Invalid("csr: row_offsets[0] must be 0");
@@ -57,7 +57,7 @@ static void validate_csr(int64_t n, const int64_t* off, const int32_t* col, int6
         for (int64_t k = off[i]; k < off[i + 1]; ++k) {
             const int32_t c = col[k];
             if (c < 0 || c >= n) throw Invalid("csr: column index out of range in row " + std::to_string(i));
-            if (k > off[i] && col[k - 1] >= c)
+            if (sorted && k > off[i] && col[k - 1] >= c)
                 throw Invalid("csr: column indices not strictly increasing in row " + std::to_string(i));
         }
     }
@@ -246,6 +246,29 @@ extern "C" int mbg_csr_upload(mbg_ctx* ctx, int64_t n, const int64_t* off, const
         use(ctx);
         if (!out) throw Invalid("null output");
         validate_csr(n, off, col, off ? off[n] : 0);
+        auto* a = new mbg_csr();
+        try {
+            a->ctx = ctx;
+            a->device = ctx->device;
+            a->n_global = n;
+            csr_to_device(ctx, a, n, off, col, val);
+        } catch (...) {
+            delete a;
+            throw;
+        }
+        *out = a;
+    });
+}
+
+// Operator upload without the sorted-columns rule (a row's nonzeros are summed
+// in the given order): permuted operators P A P^T that keep each row's
+// original summation order (tools/reorder_lab.py).
+extern "C" int mbg_csr_upload_any_order(mbg_ctx* ctx, int64_t n, const int64_t* off, const int32_t* col,
+                                        const double* val, mbg_csr** out) {
+    return guarded([&] {
+        use(ctx);
+        if (!out) throw Invalid("null output");
+        validate_csr(n, off, col, off ? off[n] : 0, /*sorted=*/false);
         auto* a = new mbg_csr();
         try {
             a->ctx = ctx;

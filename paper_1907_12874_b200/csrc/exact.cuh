@@ -27,6 +27,16 @@
 
 namespace mbg {
 
+#ifdef __CUDACC__
+// Programmatic dependent launch (sm_90+): a kernel launched with
+// programmaticStreamSerialization may start while its predecessor drains;
+// pdl_wait() blocks until the predecessor has completed and its writes are
+// visible, pdl_trigger() lets the successor launch early.  Every solver kernel
+// calls pdl_wait() before touching global state (including the stop word).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#endif
+
 constexpr int NDIG = 68;          // 68*32 bits >= 2098-bit double range + carry room
 constexpr int NSLOT = 72;         // digits + 3 non-finite counters + pad (int64 words)
 constexpr int IDX_PINF = NDIG, IDX_NINF = NDIG + 1, IDX_NAN = NDIG + 2;

@@ -452,6 +452,7 @@ __device__ __forceinline__ void block_combine(double (&acc)[NX][KEXP], int class
 // ---------------------------------------------------------------------------
 template <class P, int VEC>
 __global__ void __launch_bounds__(256, minblocks_of<P>::value) group_kernel(GroupArgs a) {
+    pdl_wait();
     if (a.ctl && a.ctl[0]) return;
     extern __shared__ double sh_dyn[];
     const int m = a.m;
@@ -544,6 +545,7 @@ __global__ void __launch_bounds__(256, minblocks_of<P>::value) group_kernel(Grou
                 for (int i = 0; i < P::NIN; ++i) cur[u][i] = nxt[u][i];
         }
     }
+    pdl_trigger();   // streaming done: the successor may start filling freed SM slots
     if constexpr (P::NDOT > 0) {
         int classes;
         if constexpr (VEC == 2) {

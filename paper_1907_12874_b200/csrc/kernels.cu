@@ -1,3 +1,4 @@
+#include <cstdlib>
 // kernels.cu -- SpMM, exact-dot fold/round and the generic group interpreter
 // for sm_100a.
 #include <mutex>
@@ -7,6 +8,14 @@
 #include "kernels.hpp"
 
 namespace mbg {
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("MBG_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 __global__ void round_kernel(int64_t* D, int nslots, int m, double* out) {
     const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);   // one warp per slot

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <utility>
 #include <vector>
 
 #include "group.cuh"
@@ -79,6 +80,26 @@ void launch_generic_group(cudaStream_t st, const GenericGroup& g, int num_sms, i
 // Round long accumulators into doubles out[s*m + c] and clear them (kernels.cu).
 void launch_round(cudaStream_t st, int64_t* D, int nslots, int m, double* out);
 
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while its stream predecessor drains (it calls pdl_wait() first).  MBG_PDL=0
+// turns it off (A/B measurements).
+bool pdl_enabled();
+template <class... KArgs, class... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    MBG_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 // Occupancy-sized persistent grid for a group kernel instantiation.
 int group_grid(const void* kernel, int block, size_t smem, int num_sms, int64_t len);
 
@@ -90,12 +111,12 @@ inline int launch_group(cudaStream_t st, const GroupArgs& a, int num_sms) {
         if ((a.m % 2 == 0 || a.m == 1) && a.len % 2 == 0) {
             const int grid =
                 group_grid(reinterpret_cast<const void*>(&group_kernel<P, 2>), block, smem, num_sms, a.len / 2);
-            group_kernel<P, 2><<<grid, block, smem, st>>>(a);
+            launch_pdl(group_kernel<P, 2>, dim3(grid), dim3(block), smem, st, a);
             return grid;
         }
     }
     const int grid = group_grid(reinterpret_cast<const void*>(&group_kernel<P, 1>), block, smem, num_sms, a.len);
-    group_kernel<P, 1><<<grid, block, smem, st>>>(a);
+    launch_pdl(group_kernel<P, 1>, dim3(grid), dim3(block), smem, st, a);
     return grid;
 }
 

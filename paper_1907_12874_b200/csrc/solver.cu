@@ -34,6 +34,8 @@ namespace mbg {
 
 __global__ void __launch_bounds__(1024) scalar_kernel(ScalArgs a) {
     extern __shared__ double s_dots[];  // nd * m rounded dots
+    pdl_wait();
+    pdl_trigger();
     scalar_block(a, s_dots);
 }
 
@@ -269,7 +271,8 @@ void Solver::scalars(int point, int nd) {
     ScalArgs s = scal_args(point, nd);
     const int threads = std::min(1024, std::max(((m_ + 31) / 32) * 32, 32 * nd * m_));
     mark_begin("scalar", 0.0);
-    scalar_kernel<<<1, threads, static_cast<size_t>(nd > 0 ? nd : 1) * m_ * sizeof(double), ctx_->stream>>>(s);
+    launch_pdl(scalar_kernel, dim3(1), dim3(threads), static_cast<size_t>(nd > 0 ? nd : 1) * m_ * sizeof(double),
+               ctx_->stream, s);
     MBG_CUDA(cudaGetLastError());
     mark_end();
     launches_++;

@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
                                                        const double* __restrict__ val,
                                                        const double* __restrict__ x, double* __restrict__ y,
                                                        const int* __restrict__ ctl, SpmmEpi epi) {
+    pdl_wait();
     if (ctl && ctl[0]) return;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
@@ -250,6 +251,7 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
         __syncthreads();  // every thread is done with stage b
         if (tid == 0) issue(i + STAGES, b);
     }
+    pdl_trigger();
     if constexpr (EPI >= 1 && EPI <= 3) {
         // no bulk copy is in flight any more: the stage memory is free scratch
         double* sh = reinterpret_cast<double*>(bufs);
@@ -296,6 +298,8 @@ __global__ void __launch_bounds__(256, M >= 32 ? 2 : (EPI == 2 ? 2 : (EPI == 0 ?
                       const double* __restrict__ x, double* __restrict__ y, const int* __restrict__ ctl,
                       SpmmEpi epi) {
     static_assert(M >= 4, "x rows of >= 32 bytes");
+    pdl_wait();
+    pdl_trigger();
     if (ctl && ctl[0]) return;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
@@ -413,6 +417,8 @@ __global__ void spmm_long_rows_kernel(int nlong, const int32_t* __restrict__ row
                                       const int32_t* __restrict__ col, const double* __restrict__ val, int m,
                                       const double* __restrict__ x, double* __restrict__ y,
                                       const int* __restrict__ ctl) {
+    pdl_wait();
+    pdl_trigger();
     if (ctl && ctl[0]) return;
     const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (e >= static_cast<int64_t>(nlong) * m) return;
@@ -432,6 +438,8 @@ __global__ void __launch_bounds__(256) spmm_generic_kernel(int64_t nrows, const 
                                                            const double* __restrict__ x,
                                                            double* __restrict__ y,
                                                            const int* __restrict__ ctl) {
+    pdl_wait();
+    pdl_trigger();
     if (ctl && ctl[0]) return;
     const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (e >= nrows * m) return;
@@ -457,8 +465,8 @@ static void launch_tma(cudaStream_t st, const SpmmTiles& tl, const int32_t* off,
         if (occ < 1) occ = 1;
     }
     const int grid = static_cast<int>(std::min<int64_t>(tl.count, static_cast<int64_t>(num_sms) * occ));
-    spmm_tma_kernel<M, EPI><<<grid, 256, SPMM_SMEM, st>>>(tl.tiles, static_cast<int>(tl.count), off, col, val, x,
-                                                          y, ctl, epi);
+    launch_pdl(spmm_tma_kernel<M, EPI>, dim3(grid), dim3(256), SPMM_SMEM, st, tl.tiles, static_cast<int>(tl.count),
+               off, col, val, x, y, ctl, epi);
 }
 
 template <int M>
@@ -488,7 +496,8 @@ static void launch_stage(cudaStream_t st, const SpmmTiles& tl, const int32_t* of
         if (occ < 1) occ = 1;
     }
     const int grid = static_cast<int>(std::min<int64_t>(tl.scount, static_cast<int64_t>(num_sms) * occ));
-    spmm_stage_kernel<M, EPI><<<grid, 256, smem, st>>>(tl.stiles, tl.umeta, static_cast<int>(tl.scount), off,
+    launch_pdl(spmm_stage_kernel<M, EPI>, dim3(grid), dim3(256), static_cast<size_t>(smem), st, tl.stiles, tl.umeta,
+               static_cast<int>(tl.scount), off,
                                                        tl.lcol, val, tl.ucols, x, y, ctl, epi);
 }
 
