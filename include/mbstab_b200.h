@@ -98,6 +98,14 @@ int mbg_halo_plan(int64_t n, const int64_t* offsets, const int32_t* cols, const 
  * original summation order. */
 int mbg_csr_upload_any_order(mbg_ctx* ctx, int64_t n, const int64_t* offsets, const int32_t* cols,
                              const double* vals, mbg_csr** out);
+/* Structured-grid hint (rows = nx*ny*nz lexicographic points): for long-row
+ * stencils (> 12 nonzeros per row, e.g. the 27-point C3 operator) the solver
+ * then works on a brick-reordered copy P A P^T (8x8x4 bricks; each row keeps
+ * its summation order) whose SpMM tiles have compact x neighbourhoods.  b and
+ * x are gathered / scattered at solve entry / exit; results are bitwise
+ * identical (exact dots).  Short-row operators are left as is.  Single GPU. */
+int mbg_csr_set_grid(mbg_ctx* ctx, mbg_csr* a, int nx, int ny, int nz);
+int mbg_csr_reordered(const mbg_csr* a);   /* 1 when the solver uses a reordered twin */
 int mbg_csr_free(mbg_csr* a);
 int64_t mbg_csr_rows(const mbg_csr* a);   /* local rows */
 int64_t mbg_csr_nnz(const mbg_csr* a);    /* local nnz */

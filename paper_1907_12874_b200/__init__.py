@@ -201,6 +201,12 @@ class DeviceCsr:
         self.n = int(lib().mbg_csr_rows(h))
         self.nnz = int(lib().mbg_csr_nnz(h))
 
+    def set_grid(self, nx: int, ny: int, nz: int) -> bool:
+        """Structured-grid hint: long-row stencils get a brick-reordered twin
+        for the solver (bitwise-identical results).  Returns True if reordered."""
+        check(lib().mbg_csr_set_grid(self.ctx.h, self.h, nx, ny, nz))
+        return bool(lib().mbg_csr_reordered(self.h))
+
     def stage_info(self):
         """(staged, reuse): whether the gather-once SpMM tiling is in use."""
         st, ru = C.c_int(0), C.c_double(0.0)

@@ -139,6 +139,11 @@ struct mbg_csr {
     };
     std::vector<Peer> peers;
     std::unique_ptr<mbg_csr> transposed;      // A^T, built on first use (IBiCGStab f0 = A^T r0)
+    // locality reordering (mbg_csr_set_grid): P A P^T with every row's
+    // nonzeros in their original order, and perm[new] = old row
+    std::unique_ptr<mbg_csr> reordered;
+    mbg::DevBuf<int32_t> perm;
+    std::vector<int32_t> perm_host;
 };
 
 struct mbg_mv {

@@ -45,8 +45,22 @@ __global__ void __launch_bounds__(1024) scalar_kernel(ScalArgs a) {
 // Vector roles (indices into work_); 14 = x0 staging with halo room.
 enum {
     V_R, V_R0, V_P, V_V, V_S, V_T, V_Z, V_VH, V_TH, V_RT, V_Q, V_W, V_Y, V_TMP, V_X0,
-    V_U, V_F0, V_PH, V_SH, V_QH, V_RH, V_WH, V_ZH, NWORK
+    V_U, V_F0, V_PH, V_SH, V_QH, V_RH, V_WH, V_ZH, V_BP, V_XP, NWORK
 };
+
+// Locality-reordered operator (mbg_csr_set_grid): b, x0 gathered into the
+// operator's row order before the solve, x scattered back after it.
+__global__ void permute_rows_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                    const int32_t* __restrict__ perm, int64_t n, int m, int scatter) {
+    const int64_t len = n * m;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < len;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = e / m;
+        const int64_t src = static_cast<int64_t>(perm[i]) * m + (e - i * m);
+        if (scatter) out[src] = in[e];
+        else out[e] = in[src];
+    }
+}
 
 Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulation, double tol,
                int fixed, int maxit, int precond_alpha)
@@ -65,6 +79,11 @@ Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulatio
     if (!pre && precond_alpha != 0) throw Invalid("solve: this method takes no preconditioner");
     pa_ = precond_alpha;
     elide_ = formulation == MBG_FUSED && pa_ == 2;
+    // a locality-reordered twin of the operator, if the caller provided the grid
+    if (a->reordered && a->peers.empty()) {
+        orig_ = a;
+        a_ = a = a->reordered.get();
+    }
     // delta in the SpMM epilogue pays off for short rows only: with > 12
     // nonzeros per row the gather-bound SpMM loses more to the epilogue's
     // registers than the separate 2-vector dot pass costs (B200: C3 27-point
@@ -73,7 +92,7 @@ Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulatio
     if (method == MBG_IBICGSTAB) {
         if (!a->peers.empty() || a->n_halo)
             throw Invalid("solve: IBiCGStab needs f0 = A^T r0, supported on a single GPU only");
-        at_ = csr_transpose(ctx, a);
+        at_ = orig_ ? csr_transpose_reordered(ctx, orig_) : csr_transpose(ctx, a);
     }
     n_ = a->n;
     len_ = n_ * m;
@@ -97,6 +116,7 @@ Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulatio
             if (!elide_) need.insert(need.end(), {V_WH, V_ZH});
             break;
     }
+    if (orig_) need.insert(need.end(), {V_BP, V_XP});
     work_.resize(NWORK);
     const size_t vlen = static_cast<size_t>(rows_alloc_) * m;
     for (int i : need) work_[i] = pool_take(ctx, vlen);
@@ -279,6 +299,16 @@ void Solver::scalars(int point, int nd) {
 }
 
 void Solver::setup(const double* b, double* x) {
+    x_user_ = x;
+    if (orig_) {   // gather b and x0 into the reordered operator's row order
+        const unsigned grid = static_cast<unsigned>(ctx_->num_sms) * 4;
+        permute_rows_kernel<<<grid, 256, 0, ctx_->stream>>>(b, w(V_BP), orig_->perm.p, n_, m_, 0);
+        permute_rows_kernel<<<grid, 256, 0, ctx_->stream>>>(x, w(V_XP), orig_->perm.p, n_, m_, 0);
+        MBG_CUDA(cudaGetLastError());
+        launches_ += 2;
+        b = w(V_BP);
+        x = w(V_XP);
+    }
     b_ = b;
     x_ = x;
     double* r = w(V_R);
@@ -611,6 +641,12 @@ void Solver::run(const double* b, double* x, bool use_graph, int chunk) {
             have_prev = true;
             ++k;
         }
+    }
+    if (orig_) {   // scatter the solution back to the caller's row order
+        permute_rows_kernel<<<static_cast<unsigned>(ctx_->num_sms) * 4, 256, 0, ctx_->stream>>>(
+            x_, x_user_, orig_->perm.p, n_, m_, 1);
+        MBG_CUDA(cudaGetLastError());
+        launches_++;
     }
     MBG_CUDA(cudaEventRecord(t1_, ctx_->stream));
     MBG_CUDA(cudaStreamSynchronize(ctx_->stream));

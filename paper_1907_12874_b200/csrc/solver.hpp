@@ -23,6 +23,8 @@ void method_schedule_pc(int method, int formulation, int precond_alpha, int* rea
 double iteration_bytes(int method, int formulation, int precond_alpha, int64_t n, int64_t nnz, int m);
 // A^T of a single-GPU matrix, built once and cached on the matrix (api.cu).
 const mbg_csr* csr_transpose(mbg_ctx* ctx, const mbg_csr* a);
+// A^T of a reordered operator, terms in the original (reference) order.
+const mbg_csr* csr_transpose_reordered(mbg_ctx* ctx, const mbg_csr* orig);
 
 class Solver {
 public:
@@ -71,6 +73,8 @@ private:
     bool elide_ = false;    // fused formulation with identity M^-1: applications aliased away
     bool epi_delta_ = false;  // fused Reordered: delta = (v, r0) in the SpMM epilogue
     const mbg_csr* at_ = nullptr;   // A^T (IBiCGStab setup)
+    const mbg_csr* orig_ = nullptr; // caller's operator when a_ is its reordered twin
+    double* x_user_ = nullptr;
     double tol_;
     int fixed_, maxit_;
     int64_t n_ = 0, len_ = 0, rows_alloc_ = 0;

@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--configs", default="1,2,3,4,5")
     ap.add_argument("--formulations", default="merged,fused")
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--natural", action="store_true", help="no structured-grid hint (no brick reordering)")
     ap.add_argument("--methods", default="", help="comma list to restrict the methods (default: all of the config)")
     args = ap.parse_args()
     ctx = P.Context(0)
@@ -47,6 +48,8 @@ def main():
                 t = time.time()
                 a = P.gen_banded(dims[0], 65536, 16, 32, seed) if kind == "banded" else P.gen_stencil(kind, *dims, seed=seed)
                 d = ctx.upload(a)
+                if kind != "banded" and not args.natural:
+                    d.set_grid(*dims)   # brick-reordered twin for long-row stencils (C3)
                 cache[key] = (a, d, time.time() - t)
             a, d, tgen = cache[key]
             b = P.gen_rhs(a.n_rows, m, seed)
