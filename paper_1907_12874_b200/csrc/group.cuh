@@ -50,6 +50,7 @@ __device__ __forceinline__ double fmadd_rn(double acc, double c, double v) {
 
 // Dot (a, b)                                   e.g. delta = (v, r0)
 struct PDot2 {
+    static constexpr bool REDO_SAFE = true;
     static constexpr const char* NAME = "dot2";
     static constexpr int NIN = 2, NOUT = 0, NCO = 0, NDOT = 1;
     __device__ static void run(const double* in, double*, double* prod, const double*) {
@@ -58,6 +59,7 @@ struct PDot2 {
 };
 // Dot (a, a)                                   e.g. psi = (t, t)
 struct PDot1 {
+    static constexpr bool REDO_SAFE = true;
     static constexpr const char* NAME = "dot1";
     static constexpr int NIN = 1, NOUT = 0, NCO = 0, NDOT = 1;
     __device__ static void run(const double* in, double*, double* prod, const double*) {
@@ -95,6 +97,7 @@ struct PUpd3 {
 // spread over two memory-bound passes instead of one compute-bound one).
 //   s = 1*r + (-alpha)*v ; theta = (s, s)
 struct PUpd2Sq {
+    static constexpr bool REDO_SAFE = true;
     static constexpr const char* NAME = "upd2_sq";
     static constexpr int NIN = 2, NOUT = 1, NCO = 2, NDOT = 1;
     __device__ static void run(const double* in, double* out, double* prod, const double* co) {
@@ -105,6 +108,7 @@ struct PUpd2Sq {
 };
 // ... and phi = (t,s), psi = (t,t) in the pass after t = A s
 struct PClassicPhiPsi {
+    static constexpr bool REDO_SAFE = true;
     static constexpr const char* NAME = "classic_phipsi";
     static constexpr int NIN = 2, NOUT = 0, NCO = 0, NDOT = 2;   // in: t s
     __device__ static void run(const double* in, double*, double* prod, const double*) {
@@ -115,6 +119,7 @@ struct PClassicPhiPsi {
 
 // Classical, Alg. 2 line 9: phi=(t,s), psi=(t,t), theta=(s,s)
 struct PClassicOmega {
+    static constexpr bool REDO_SAFE = true;
     static constexpr int UNROLL = 1;  // register budget: 3+ dot expansions per column pair
     static constexpr const char* NAME = "classic_omega";
     static constexpr int NIN = 2, NOUT = 0, NCO = 0, NDOT = 3;   // in: t s
@@ -127,6 +132,7 @@ struct PClassicOmega {
 // Classical, Alg. 2 line 15:
 //   x = 1*x + alpha*p + omega*s ; r = 1*s + (-omega)*t ; rho' = (r, r0)
 struct PClassicXR {
+    static constexpr bool REDO_SAFE = true;
     static constexpr const char* NAME = "classic_xr";
     static constexpr int NIN = 5, NOUT = 2, NCO = 3, NDOT = 1;   // in: x p s t r0; co: alpha omega -omega
     __device__ static void run(const double* in, double* out, double* prod, const double* co) {
@@ -140,6 +146,7 @@ struct PClassicXR {
 // Reordered, Alg. 6 line 11:
 //   rt = 1*r + (-alpha)*v ; theta=(t,rt), phi=(t,t), psi=(t,r0), eta=(rt,rt)
 struct PReordG7 {
+    static constexpr bool REDO_SAFE = true;
     static constexpr int UNROLL = 1;  // register budget: 3+ dot expansions per column pair
     static constexpr const char* NAME = "reord_g7";
     static constexpr int NIN = 4, NOUT = 1, NCO = 1, NDOT = 4;   // in: r v t r0; co: -alpha
@@ -198,6 +205,7 @@ struct PPipeG4 {
 // Pipelined, Alg. 4 line 12:
 //   w = 1*y + (-omega)*t + (omega*alpha)*v ; rho'=(r0,r), psi=(r0,z), sigma=(r0,w), delta=(r0,s)
 struct PPipeG5 {
+    static constexpr bool REDO_SAFE = true;
     static constexpr int UNROLL = 1;  // register budget: 3+ dot expansions per column pair
     static constexpr const char* NAME = "pipe_g5";
     static constexpr int NIN = 7, NOUT = 1, NCO = 2, NDOT = 4;   // in: y t v r0 r z s; co: -omega omega*alpha
@@ -217,6 +225,7 @@ struct PPipeG5 {
 // discard): x = 1*x + alpha*p + omega*q ; r = 1*q + (-omega)*y ;
 // w = 1*y + (-omega)*t + (omega*alpha)*v ; rho'=(r0,r), psi=(r0,z), sigma=(r0,w), delta=(r0,s)
 struct PPipeG45 {
+    static constexpr bool REDO_SAFE = true;
     static constexpr const char* NAME = "pipe_g45";
     static constexpr int NIN = 9, NOUT = 3, NCO = 4, NDOT = 4, UNROLL = 1;
     // in: x p q y t v r0 z s ; out: x r w ; co: alpha omega -omega omega*alpha
@@ -253,6 +262,7 @@ struct PIbcgG1 {
 //   phi=(r0,s) pi=(r0,q) gamma=(f0,s) eta=(f0,t) theta=(s,t) kappa=(t,t) nu=(s,s)
 // Seven expansions per column: one column per thread (VEC = 1) keeps them in registers.
 struct PIbcgG2 {
+    static constexpr bool REDO_SAFE = true;
     static constexpr const char* NAME = "ibcg_g2";
     static constexpr int NIN = 5, NOUT = 1, NCO = 1, NDOT = 7, UNROLL = 1, VEC = 1;
     // in: u q r0 s f0 ; out: t ; co: -alpha
@@ -280,6 +290,7 @@ struct PIbcgG3 {
 };
 // Preconditioned BiCGStab, Alg. 5: r = 1*s + (-omega)*t ; rho' = (r, r0)
 struct PRDot {
+    static constexpr bool REDO_SAFE = true;
     static constexpr const char* NAME = "pbcg_r";
     static constexpr int NIN = 3, NOUT = 1, NCO = 1, NDOT = 1;   // in: s t r0 ; co: -omega
     __device__ static void run(const double* in, double* out, double* prod, const double* co) {
@@ -331,6 +342,7 @@ struct PPpG3 {
 // Alg. 7 line 15: r = 1*q + (-omega)*y ; w = 1*y + (-omega)*t + (omega*alpha)*v ;
 //   rho'=(r0,r) psi=(r0,z) sigma=(r0,w) delta=(r0,s)
 struct PPpG4 {
+    static constexpr bool REDO_SAFE = true;
     static constexpr int UNROLL = 1;
     static constexpr const char* NAME = "ppipe_g4";
     static constexpr int NIN = 7, NOUT = 2, NCO = 2, NDOT = 4;   // in: q y t v r0 z s ; out: r w ; co: -omega omega*alpha
@@ -345,6 +357,15 @@ struct PPpG4 {
         prod[3] = __dmul_rn(r0, in[6]);
     }
 };
+
+// Programs whose dot products can be recomputed from the pass's inputs after
+// the pass (no input overwritten in place feeds a product): their streaming
+// loop uses the optimistic grow_fast and re-walks a thread's elements with the
+// careful grow only if that thread met a non-finite value.
+template <class P, class = void>
+struct redo_safe_of { static constexpr bool value = false; };
+template <class P>
+struct redo_safe_of<P, decltype(void(P::REDO_SAFE))> { static constexpr bool value = P::REDO_SAFE; };
 
 // Widest packet a program may use (2 unless it declares VEC = 1).
 template <class P, class = void>
@@ -500,6 +521,8 @@ __global__ void __launch_bounds__(256, minblocks_of<P>::value) group_kernel(Grou
     // (only kernels with dots pipeline: the plain updates are memory-bound
     // already and the extra registers would cost occupancy)
     constexpr bool PF = prefetch_of<P>::value;
+    constexpr bool RS = redo_safe_of<P>::value && P::NDOT > 0;
+    bool bad = false;
     if constexpr (PF) load(cur, q);
     for (; q < npk; q += UNR * stride) {
         const int64_t qn = q + UNR * stride;
@@ -525,8 +548,13 @@ __global__ void __launch_bounds__(256, minblocks_of<P>::value) group_kernel(Grou
                 for (int i = 0; i < P::NOUT; ++i) reinterpret_cast<double2*>(a.out[i])[qu] = make_double2(o0[i], o1[i]);
 #pragma unroll
                 for (int d = 0; d < P::NDOT; ++d) {
-                    grow(acc[2 * d], p0[d], slot0[d]);
-                    grow(acc[2 * d + 1], p1[d], slot1[d]);
+                    if constexpr (RS) {
+                        grow_fast(acc[2 * d], p0[d], slot0[d], bad);
+                        grow_fast(acc[2 * d + 1], p1[d], slot1[d], bad);
+                    } else {
+                        grow(acc[2 * d], p0[d], slot0[d]);
+                        grow(acc[2 * d + 1], p1[d], slot1[d]);
+                    }
                 }
             } else {
 #pragma unroll
@@ -535,7 +563,10 @@ __global__ void __launch_bounds__(256, minblocks_of<P>::value) group_kernel(Grou
 #pragma unroll
                 for (int i = 0; i < P::NOUT; ++i) a.out[i][qu] = o0[i];
 #pragma unroll
-                for (int d = 0; d < P::NDOT; ++d) grow(acc[d], p0[d], slot0[d]);
+                for (int d = 0; d < P::NDOT; ++d) {
+                    if constexpr (RS) grow_fast(acc[d], p0[d], slot0[d], bad);
+                    else grow(acc[d], p0[d], slot0[d]);
+                }
             }
         }
         if constexpr (PF) {
@@ -546,6 +577,42 @@ __global__ void __launch_bounds__(256, minblocks_of<P>::value) group_kernel(Grou
         }
     }
     pdl_trigger();   // streaming done: the successor may start filling freed SM slots
+    if constexpr (RS) {
+        if (bad) {
+            // this thread met a non-finite value: recompute its products from the
+            // (unchanged) inputs and accumulate them with the careful grow
+#pragma unroll
+            for (int d = 0; d < ND * VEC; ++d)
+#pragma unroll
+                for (int i = 0; i < KEXP; ++i) acc[d][i] = 0.0;
+            for (int64_t qr = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; qr < npk; qr += stride) {
+                double in[P::NIN], o0[NO], p0[ND];
+                if constexpr (VEC == 2) {
+                    double o1[NO], p1[ND];
+                    Pk v[P::NIN];
+#pragma unroll
+                    for (int i = 0; i < P::NIN; ++i) v[i] = reinterpret_cast<const Pk*>(a.in[i])[qr];
+#pragma unroll
+                    for (int i = 0; i < P::NIN; ++i) in[i] = v[i].x;
+                    P::run(in, o0, p0, co0);
+#pragma unroll
+                    for (int i = 0; i < P::NIN; ++i) in[i] = v[i].y;
+                    P::run(in, o1, p1, co1);
+#pragma unroll
+                    for (int d = 0; d < P::NDOT; ++d) {
+                        grow(acc[2 * d], p0[d], slot0[d]);
+                        grow(acc[2 * d + 1], p1[d], slot1[d]);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < P::NIN; ++i) in[i] = a.in[i][qr];
+                    P::run(in, o0, p0, co0);
+#pragma unroll
+                    for (int d = 0; d < P::NDOT; ++d) grow(acc[d], p0[d], slot0[d]);
+                }
+            }
+        }
+    }
     if constexpr (P::NDOT > 0) {
         int classes;
         if constexpr (VEC == 2) {

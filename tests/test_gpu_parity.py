@@ -302,3 +302,23 @@ def test_solve_host_pinned_buffers(ctx):
     rep = P.solve_host(ctx, d, bp, xp, m, "bicgstab")
     assert rep.iterations == want["iterations"]
     assert_bitwise(xp, want["x"], "pinned solve_host x")
+
+
+@pytest.mark.parametrize("method,form", [("bicgstab", "fused"), ("bicgstab", "merged"), ("pipebicgstab", "fused"),
+                                         ("rbicgstab", "merged"), ("ibicgstab", "merged")])
+def test_solve_overflowing_dots_match_oracle(ctx, method, form):
+    """Products overflowing to inf (column 0 scaled by 1e200) take the
+    streaming kernels' careful recomputation path; NaN in another column
+    poisons only that column's dots.  The GPU must follow the oracle exactly."""
+    a = O.gen_stencil("poisson7", 10, 9, 8)
+    m = 3
+    b = O.rhs(a.n, m, 0)
+    b[0::m] *= 1e200
+    b[5 * m + 2] = np.nan
+    want, rep, X = run_both(ctx, a, b, m, method, form, fixed=True, maxit=6)
+    if rep is None:
+        assert want["breakdown"] != 0
+        return
+    assert rep.iterations == want["iterations"]
+    assert_bitwise(rep.residual_history, want["hist"], f"{method}/{form} overflow history")
+    assert_bitwise(X.download(), want["x"], f"{method}/{form} overflow x")
