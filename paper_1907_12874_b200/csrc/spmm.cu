@@ -265,33 +265,38 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
 }
 
 // ---------------------------------------------------------------------------
-// Gather-once SpMM for matrices whose tiles reuse x rows (stencils: a 27-point
-// row shares most of its columns with its neighbours).  Per tile the distinct
-// columns (<= STAGE_UCOLS) are gathered ONCE into shared memory with 16-byte
-// cp.async, then every nonzero reads its x row from shared memory through a
-// 16-bit local index (2 B/nnz instead of the 4 B column).  Same arithmetic as
-// spmm_tma_kernel: per (row, column) sequential CSR-order adds from 0.0.
-// x traffic from L2 drops from nnz*8m to U*8m bytes per tile (27-point:
-// ~2.8x), which is what bounds the plain kernel on C3.
+// Gather-ahead SpMM ("staged" tiling).  Per tile the distinct columns
+// (<= STAGE_UCOLS) are gathered ONCE into shared memory with 16-byte cp.async
+// and every nonzero reads its x row from there through a 16-bit local index
+// (2 B/nnz instead of the 4 B column).  The gathers of tile i+1 are issued
+// before tile i is computed (two x buffers, three CSR stages), so the L2
+// latency of the gathers -- what bounds the register-gather kernel (a lane
+// waits ~2 L2 round trips per row) -- overlaps the arithmetic of the previous
+// tile.  Same arithmetic as spmm_tma_kernel: per (row, column) sequential
+// CSR-order adds from 0.0.
 // ---------------------------------------------------------------------------
-constexpr int S_STAGES = 2;
+constexpr int S_STAGES = 3;
 constexpr int S_OFF_CAP = STAGE_ROWS + 8;     // int32
 constexpr int S_LCOL_CAP = STAGE_NNZ + 16;    // uint16 (k0 rounded down to 8)
 constexpr int S_VAL_CAP = STAGE_NNZ + 4;      // double (k0 rounded down to 2)
 constexpr int S_UCOL_CAP = STAGE_UCOLS + 8;   // int32 (u0 rounded down to 4)
 constexpr int S_BUF = S_OFF_CAP * 4 + S_LCOL_CAP * 2 + S_VAL_CAP * 8 + S_UCOL_CAP * 4;
-constexpr int S_HEAD = 128;                   // 2 mbarriers + 2 x 2 int4 metas
+constexpr int S_HEAD = 128;                   // 3 mbarriers + 3 x 2 int4 metas
 static_assert(S_BUF % 16 == 0 && (S_OFF_CAP * 4) % 16 == 0 && (S_LCOL_CAP * 2) % 16 == 0 &&
                   (S_VAL_CAP * 8) % 16 == 0, "stage alignment");
 static_assert(S_STAGES * S_BUF >= 256 * KEXP * 8, "combine scratch aliases the stages");
-constexpr int stage_smem(int m) { return S_HEAD + S_STAGES * S_BUF + STAGE_UCOLS * m * 8; }
+static_assert(8 * S_STAGES <= 32 && 32 + 32 * S_STAGES <= S_HEAD, "head layout");
+constexpr int stage_smem(int m) { return S_HEAD + S_STAGES * S_BUF + 2 * STAGE_UCOLS * m * 8; }
+constexpr int stage_minb(int m, int epi) {
+    return (m >= 32 || epi == 2) ? 1 : (m >= 16 ? 2 : (epi == 0 ? 3 : 2));
+}
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
 template <int M, int EPI>
-__global__ void __launch_bounds__(256, M >= 32 ? 2 : (EPI == 2 ? 2 : (EPI == 0 ? 4 : 3)))
+__global__ void __launch_bounds__(256, stage_minb(M, EPI))
     spmm_stage_kernel(const int4* __restrict__ tiles, const int2* __restrict__ umeta, int ntiles,
                       const int32_t* __restrict__ off, const uint16_t* __restrict__ lcol,
                       const double* __restrict__ val, const int32_t* __restrict__ ucols,
@@ -299,13 +304,12 @@ __global__ void __launch_bounds__(256, M >= 32 ? 2 : (EPI == 2 ? 2 : (EPI == 0 ?
                       SpmmEpi epi) {
     static_assert(M >= 4, "x rows of >= 32 bytes");
     pdl_wait();
-    pdl_trigger();
     if (ctl && ctl[0]) return;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
     int4* meta = reinterpret_cast<int4*>(smem + 32);   // [stage][2]
     unsigned char* bufs = smem + S_HEAD;
-    double* xs = reinterpret_cast<double*>(smem + S_HEAD + S_STAGES * S_BUF);
+    double* xsb = reinterpret_cast<double*>(smem + S_HEAD + S_STAGES * S_BUF);   // [2][STAGE_UCOLS * M]
     const int tid = threadIdx.x;
 
     if (tid == 0) {
@@ -330,6 +334,7 @@ __global__ void __launch_bounds__(256, M >= 32 ? 2 : (EPI == 2 ? 2 : (EPI == 0 ?
         const uint32_t blc = static_cast<uint32_t>(k1l - k0l) * 2u;
         const uint32_t bval = static_cast<uint32_t>(k1v - k0v) * 8u;
         const uint32_t buc = static_cast<uint32_t>(u1a - u0a) * 4u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bars[b], boff + blc + bval + buc);
         bulk_g2s(buf, off + r0a, boff, &bars[b]);
         if (blc) bulk_g2s(buf + S_OFF_CAP * 4, lcol + k0l, blc, &bars[b]);
@@ -351,28 +356,48 @@ __global__ void __launch_bounds__(256, M >= 32 ? 2 : (EPI == 2 ? 2 : (EPI == 0 ?
 #pragma unroll
         for (int i = 0; i < KEXP; ++i) ex[q][i] = 0.0;
 
-    for (int i = 0;; ++i) {
-        const int t = blockIdx.x + i * gridDim.x;
-        if (t >= ntiles) break;
+    auto wait_stage = [&](int i) {
         const int b = i % S_STAGES;
         while (!mbar_try_wait(&bars[b], static_cast<uint32_t>((i / S_STAGES) & 1))) {
         }
-        const int4 mt = meta[2 * b];
+    };
+    // issue the cp.async gathers of tile i's distinct x rows into x buffer i & 1
+    auto gather = [&](int i) {
+        const int b = i % S_STAGES;
         const int4 mu = meta[2 * b + 1];
-        const int r0 = mt.x, r1 = mt.y, r0a = mt.z, k0l = mt.w, k0v = mu.x, ush = mu.y, U = mu.z;
-        const unsigned char* buf = bufs + b * S_BUF;
-        const int32_t* s_off = reinterpret_cast<const int32_t*>(buf);
-        const uint16_t* s_lc = reinterpret_cast<const uint16_t*>(buf + S_OFF_CAP * 4) - k0l;   // global k
-        const double* s_val = reinterpret_cast<const double*>(buf + S_OFF_CAP * 4 + S_LCOL_CAP * 2) - k0v;
         const int32_t* s_uc =
-            reinterpret_cast<const int32_t*>(buf + S_OFF_CAP * 4 + S_LCOL_CAP * 2 + S_VAL_CAP * 8) + ush;
-        // gather the tile's distinct x rows once
+            reinterpret_cast<const int32_t*>(bufs + b * S_BUF + S_OFF_CAP * 4 + S_LCOL_CAP * 2 + S_VAL_CAP * 8) + mu.y;
+        double* xs = xsb + (i & 1) * (STAGE_UCOLS * M);
+        const int U = mu.z;
         for (int c = tid; c < U * CPR; c += 256) {
             const int u = c / CPR, part = c - u * CPR;
             cp_async16(xs + u * M + part * 2, x + static_cast<int64_t>(s_uc[u]) * M + part * 2);
         }
-        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-        __syncthreads();
+    };
+    if (static_cast<int>(blockIdx.x) < ntiles) {
+        wait_stage(0);
+        gather(0);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+
+    for (int i = 0;; ++i) {
+        const int t = blockIdx.x + i * gridDim.x;
+        if (t >= ntiles) break;
+        if (t + static_cast<int>(gridDim.x) < ntiles) {   // the next tile's gathers fly during this tile
+            wait_stage(i + 1);
+            gather(i + 1);
+        }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 1;" ::: "memory");
+        __syncthreads();   // tile i's x rows (every thread's cp.async) are in shared memory
+        const int b = i % S_STAGES;
+        const int4 mt = meta[2 * b];
+        const int4 mu = meta[2 * b + 1];
+        const int r0 = mt.x, r1 = mt.y, r0a = mt.z, k0l = mt.w, k0v = mu.x;
+        const unsigned char* buf = bufs + b * S_BUF;
+        const int32_t* s_off = reinterpret_cast<const int32_t*>(buf);
+        const uint16_t* s_lc = reinterpret_cast<const uint16_t*>(buf + S_OFF_CAP * 4) - k0l;   // global k
+        const double* s_val = reinterpret_cast<const double*>(buf + S_OFF_CAP * 4 + S_LCOL_CAP * 2) - k0v;
+        const double* xs = xsb + (i & 1) * (STAGE_UCOLS * M);
         for (int rr = tid / LPR; rr < r1 - r0; rr += RPP) {
             const int row = r0 + rr;
             const int k0 = s_off[row - r0a], k1 = s_off[row + 1 - r0a];
@@ -397,9 +422,11 @@ __global__ void __launch_bounds__(256, M >= 32 ? 2 : (EPI == 2 ? 2 : (EPI == 0 ?
             *reinterpret_cast<double2*>(y + static_cast<int64_t>(row) * M + cp) = make_double2(a0, a1);
             if constexpr (EPI >= 1 && EPI <= 3) spmm_epi_row<M, EPI, VW, ND>(ex, epi, cp, row, a0, a1, x);
         }
-        __syncthreads();  // stage b and xs are free
+        __syncthreads();  // stage b and x buffer i & 1 are free
         if (tid == 0) issue(i + S_STAGES, b);
     }
+    pdl_trigger();
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     if constexpr (EPI >= 1 && EPI <= 3) {
         double* sh = reinterpret_cast<double*>(bufs);
         block_combine<ND * VW>(ex, LPR,
