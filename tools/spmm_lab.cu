@@ -183,7 +183,8 @@ __device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-template <int M, int TR, int TN, int ST, int RPT, int B, int MINB, int NT = 256, bool CONTIG = false, int PFD = 0>
+template <int M, int TR, int TN, int ST, int RPT, int B, int MINB, int NT = 256, bool CONTIG = false, int PFD = 0,
+          int VWP = 0>
 __global__ void __launch_bounds__(NT, MINB) k_tma(const int4* __restrict__ tiles, int ntiles, const int* __restrict__ off,
                                                    const int* __restrict__ col, const double* __restrict__ val,
                                                    const double* __restrict__ x, double* __restrict__ y) {
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(NT, MINB) k_tma(const int4* __restrict__ tiles
     };
     if (tid == 0)
         for (int b = 0; b < ST; ++b) issue(b, b);
-    constexpr int VW = M >= 2 ? 2 : 1;
+    constexpr int VW = VWP ? VWP : (M >= 2 ? 2 : 1);
     constexpr int LPR = M / VW, RPP = NT / LPR;
     const int cp = (tid % LPR) * VW;
     for (int i = 0;; ++i) {
@@ -242,14 +243,28 @@ __global__ void __launch_bounds__(NT, MINB) k_tma(const int4* __restrict__ tiles
         for (int rr = tid / LPR; rr < r1 - r0; rr += RPP) {
             const int row = r0 + rr;
             const int k0 = s_off[row - r0a], k1 = s_off[row + 1 - r0a];
-            double a0 = 0.0, a1 = 0.0;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
             for (int k = k0; k < k1; k += B) {
                 int j[B];
                 double v[B];
 #pragma unroll
                 for (int q = 0; q < B; ++q)
                     if (k + q < k1) { j[q] = s_col[k + q]; v[q] = s_val[k + q]; }
-                if constexpr (VW == 2) {
+                if constexpr (VW == 4) {
+                    double2 xv[B], xw[B];
+#pragma unroll
+                    for (int q = 0; q < B; ++q)
+                        if (k + q < k1) {
+                            xv[q] = __ldg((const double2*)(x + (int64_t)j[q] * M + cp));
+                            xw[q] = __ldg((const double2*)(x + (int64_t)j[q] * M + cp + 2));
+                        }
+#pragma unroll
+                    for (int q = 0; q < B; ++q)
+                        if (k + q < k1) {
+                            a0 = __dadd_rn(a0, __dmul_rn(v[q], xv[q].x)); a1 = __dadd_rn(a1, __dmul_rn(v[q], xv[q].y));
+                            a2 = __dadd_rn(a2, __dmul_rn(v[q], xw[q].x)); a3 = __dadd_rn(a3, __dmul_rn(v[q], xw[q].y));
+                        }
+                } else if constexpr (VW == 2) {
                     double2 xv[B];
 #pragma unroll
                     for (int q = 0; q < B; ++q)
@@ -267,7 +282,10 @@ __global__ void __launch_bounds__(NT, MINB) k_tma(const int4* __restrict__ tiles
                         if (k + q < k1) a0 = __dadd_rn(a0, __dmul_rn(v[q], xv[q]));
                 }
             }
-            if constexpr (VW == 2) *(double2*)(y + (int64_t)row * M + cp) = make_double2(a0, a1);
+            if constexpr (VW == 4) {
+                *(double2*)(y + (int64_t)row * M + cp) = make_double2(a0, a1);
+                *(double2*)(y + (int64_t)row * M + cp + 2) = make_double2(a2, a3);
+            } else if constexpr (VW == 2) *(double2*)(y + (int64_t)row * M + cp) = make_double2(a0, a1);
             else y[row] = a0;
         }
         __syncthreads();
@@ -321,7 +339,8 @@ void timeit(const char* name, Ctx& c, F launch) {
     printf("%-34s %8.1f us  %7.1f GB/s  %s\n", name, us, c.bytes / us / 1e3, ok ? "bitwise-ok" : "MISMATCH");
 }
 
-template <int M, int TR, int TN, int ST, int RPT, int B, int MINB, int NT = 256, bool CONTIG = false, int PFD = 0>
+template <int M, int TR, int TN, int ST, int RPT, int B, int MINB, int NT = 256, bool CONTIG = false, int PFD = 0,
+          int VWP = 0>
 void run_tma(Ctx& c, const char* name) {
     auto tiles = make_tiles(c.hoff, c.n, TR, TN);
     int4* dt;
@@ -329,7 +348,7 @@ void run_tma(Ctx& c, const char* name) {
     CK(cudaMemcpy(dt, tiles.data(), tiles.size() * sizeof(int4), cudaMemcpyHostToDevice));
     constexpr int BUF = (TR + 8) * 4 + (TN + 8) * 12;
     const int smem = 192 + ST * BUF;
-    auto kern = k_tma<M, TR, TN, ST, RPT, B, MINB, NT, CONTIG, PFD>;
+    auto kern = k_tma<M, TR, TN, ST, RPT, B, MINB, NT, CONTIG, PFD, VWP>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int occ;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem));
@@ -435,11 +454,13 @@ int run_all(int g) {
         k_ref<<<(unsigned)(((int64_t)n * M + 255) / 256), 256>>>(n, c.off, c.col, c.val, M, c.x, c.y);
     });
     run_tma<M, 192, 1920, 2, 1, 4, 4>(c, "tma 192r 2st B4 minb4");
-    run_tma<M, 192, 1920, 2, 1, 4, 4, 256, false, 2>(c, "tma 192r 2st B4 minb4 pf2");
-    run_tma<M, 192, 1920, 2, 1, 4, 4, 256, false, 3>(c, "tma 192r 2st B4 minb4 pf3");
-    run_tma<M, 192, 1920, 2, 1, 4, 4, 256, false, 5>(c, "tma 192r 2st B4 minb4 pf5");
-    run_tma<M, 192, 1920, 2, 1, 4, 3, 256, false, 3>(c, "tma 192r 2st B4 minb3 pf3");
-    run_tma<M, 128, 1280, 2, 1, 4, 4, 256, false, 4>(c, "tma 128r 2st B4 minb4 pf4");
+    if constexpr (M >= 8) {
+        run_tma<M, 256, 1920, 2, 1, 4, 4, 256, false, 0, 4>(c, "tma 256r 2st B4 minb4 VW4");
+        run_tma<M, 256, 1920, 2, 1, 2, 4, 256, false, 0, 4>(c, "tma 256r 2st B2 minb4 VW4");
+        run_tma<M, 256, 1920, 2, 1, 4, 3, 256, false, 0, 4>(c, "tma 256r 2st B4 minb3 VW4");
+        run_tma<M, 128, 1280, 2, 1, 4, 4, 256, false, 0, 4>(c, "tma 128r 2st B4 minb4 VW4");
+        run_tma<M, 256, 1920, 3, 1, 4, 3, 256, false, 0, 4>(c, "tma 256r 3st B4 minb3 VW4");
+    }
     return 0;
 }
 
