@@ -113,9 +113,8 @@ __device__ __forceinline__ void spmm_epi_row(double (&ex)[ND * VW][KEXP], const 
 }
 
 // EPI: 0 plain; 1/2/3 fused dot epilogues (kernels.hpp SpmmEpi kinds); 4 plain
-// with a 3-block register budget -- measured faster only for long rows (>12
-// nonzeros on average) at m = 32 (C5: 14.2 vs 17.7 ms/iteration), slower at
-// m <= 16 (C3, C5 m=8), so it is used for that case only.
+// for long rows (> 12 nonzeros on average) at m = 32: 6 gathers in flight per
+// lane, 3-block register budget.
 template <int M, int EPI>
 __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_tma_kernel(const int4* __restrict__ tiles, int ntiles,
                                                        const int32_t* __restrict__ off,
@@ -159,6 +158,12 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
         for (int b = 0; b < STAGES; ++b) issue(b, b);
 
     constexpr int VW = M >= 2 ? 2 : 1;        // columns per lane
+    // gathers in flight per lane: 4 (4 blocks/SM); EPI 4 = the long-row m = 32
+    // variant, 6 per lane with a 3-block register budget.  In the solver
+    // (tools/sweep.py) it is faster only at m = 32 (C5 15.6 -> 13.9 ms/it);
+    // at m = 8/16 (C5) and on the 27-point C3 it loses 4-12 % although the
+    // isolated SpMM (tools/spmm_lab.cu) prefers it there too.
+    constexpr int BATCH = EPI == 4 ? 6 : 4;
     constexpr int LPR = M / VW;               // lanes per row
     constexpr int RPP = 256 / LPR;            // rows per pass of the block
     constexpr int ND = EPI == 2 ? 3 : 1;      // dots of the fused epilogue
@@ -208,33 +213,33 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
                 const int row = r0 + rr;
                 const int k0 = s_off[row - r0a], k1 = s_off[row + 1 - r0a];
                 double a0 = 0.0, a1 = 0.0;
-                // batches of 4 nonzeros: index/value loads, then the gathers, then
-                // the ordered adds (4 gathers in flight per lane; more costs occupancy)
-                for (int k = k0; k < k1; k += 4) {
-                    int j[4];
-                    double va[4];
+                // batches of BATCH nonzeros: index/value loads, then the gathers, then
+                // the ordered adds (BATCH gathers in flight per lane)
+                for (int k = k0; k < k1; k += BATCH) {
+                    int j[BATCH];
+                    double va[BATCH];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
+                    for (int q = 0; q < BATCH; ++q)
                         if (k + q < k1) { j[q] = cs[k + q]; va[q] = vs[k + q]; }
                     if constexpr (VW == 2) {
-                        double2 xa[4];
+                        double2 xa[BATCH];
 #pragma unroll
-                        for (int q = 0; q < 4; ++q)
+                        for (int q = 0; q < BATCH; ++q)
                             if (k + q < k1)
                                 xa[q] = __ldg(reinterpret_cast<const double2*>(x + static_cast<int64_t>(j[q]) * M + cp));
 #pragma unroll
-                        for (int q = 0; q < 4; ++q)
+                        for (int q = 0; q < BATCH; ++q)
                             if (k + q < k1) {
                                 a0 = __dadd_rn(a0, __dmul_rn(va[q], xa[q].x));
                                 a1 = __dadd_rn(a1, __dmul_rn(va[q], xa[q].y));
                             }
                     } else {
-                        double xa[4];
+                        double xa[BATCH];
 #pragma unroll
-                        for (int q = 0; q < 4; ++q)
+                        for (int q = 0; q < BATCH; ++q)
                             if (k + q < k1) xa[q] = __ldg(x + j[q]);
 #pragma unroll
-                        for (int q = 0; q < 4; ++q)
+                        for (int q = 0; q < BATCH; ++q)
                             if (k + q < k1) a0 = __dadd_rn(a0, __dmul_rn(va[q], xa[q]));
                     }
                 }

@@ -454,12 +454,13 @@ int run_all(int g) {
         k_ref<<<(unsigned)(((int64_t)n * M + 255) / 256), 256>>>(n, c.off, c.col, c.val, M, c.x, c.y);
     });
     run_tma<M, 192, 1920, 2, 1, 4, 4>(c, "tma 192r 2st B4 minb4");
+    run_tma<M, 192, 1920, 2, 1, 8, 3>(c, "tma 192r 2st B8 minb3");
+    run_tma<M, 192, 1920, 2, 1, 8, 2>(c, "tma 192r 2st B8 minb2");
+    run_tma<M, 192, 1920, 2, 1, 6, 3>(c, "tma 192r 2st B6 minb3");
     if constexpr (M >= 8) {
-        run_tma<M, 256, 1920, 2, 1, 4, 4, 256, false, 0, 4>(c, "tma 256r 2st B4 minb4 VW4");
-        run_tma<M, 256, 1920, 2, 1, 2, 4, 256, false, 0, 4>(c, "tma 256r 2st B2 minb4 VW4");
         run_tma<M, 256, 1920, 2, 1, 4, 3, 256, false, 0, 4>(c, "tma 256r 2st B4 minb3 VW4");
-        run_tma<M, 128, 1280, 2, 1, 4, 4, 256, false, 0, 4>(c, "tma 128r 2st B4 minb4 VW4");
-        run_tma<M, 256, 1920, 3, 1, 4, 3, 256, false, 0, 4>(c, "tma 256r 3st B4 minb3 VW4");
+        run_tma<M, 256, 1920, 2, 1, 2, 4, 256, false, 0, 4>(c, "tma 256r 2st B2 minb4 VW4");
+        run_tma<M, 256, 1920, 2, 1, 8, 2, 256, false, 0, 4>(c, "tma 256r 2st B8 minb2 VW4");
     }
     return 0;
 }
