@@ -147,6 +147,8 @@ struct PClassicXR {
 //   rt = 1*r + (-alpha)*v ; theta=(t,rt), phi=(t,t), psi=(t,r0), eta=(rt,rt)
 struct PReordG7 {
     static constexpr bool REDO_SAFE = true;
+    static constexpr bool PREFETCH = true;   // 4 dots: overlap the next packet's loads with the TwoSum chains
+    static constexpr int MINB = 2;           // ... with the registers that takes
     static constexpr int UNROLL = 1;  // register budget: 3+ dot expansions per column pair
     static constexpr const char* NAME = "reord_g7";
     static constexpr int NIN = 4, NOUT = 1, NCO = 1, NDOT = 4;   // in: r v t r0; co: -alpha
@@ -177,6 +179,8 @@ struct PReordG12 {
 //   p = 1*r + beta*p + nbo*s ; s = 1*w + beta*s + nbo*z ; z = 1*t + beta*z + nbo*v ;
 //   q = 1*r + (-alpha)*s ; y = 1*w + (-alpha)*z ; theta=(q,y), phi=(y,y), pi=(q,q)
 struct PPipeG1 {
+    static constexpr bool PREFETCH = true;
+    static constexpr int MINB = 2;
     static constexpr int UNROLL = 1;  // register budget: 3+ dot expansions per column pair
     static constexpr const char* NAME = "pipe_g1";
     static constexpr int NIN = 7, NOUT = 5, NCO = 3, NDOT = 3;   // in: r p s w z t v; out: p s z q y; co: beta nbo -alpha
@@ -205,6 +209,8 @@ struct PPipeG4 {
 // Pipelined, Alg. 4 line 12:
 //   w = 1*y + (-omega)*t + (omega*alpha)*v ; rho'=(r0,r), psi=(r0,z), sigma=(r0,w), delta=(r0,s)
 struct PPipeG5 {
+    static constexpr bool PREFETCH = true;
+    static constexpr int MINB = 2;
     static constexpr bool REDO_SAFE = true;
     static constexpr int UNROLL = 1;  // register budget: 3+ dot expansions per column pair
     static constexpr const char* NAME = "pipe_g5";
@@ -262,6 +268,8 @@ struct PIbcgG1 {
 //   phi=(r0,s) pi=(r0,q) gamma=(f0,s) eta=(f0,t) theta=(s,t) kappa=(t,t) nu=(s,s)
 // Seven expansions per column: one column per thread (VEC = 1) keeps them in registers.
 struct PIbcgG2 {
+    static constexpr bool PREFETCH = true;
+    static constexpr int MINB = 2;
     static constexpr bool REDO_SAFE = true;
     static constexpr const char* NAME = "ibcg_g2";
     static constexpr int NIN = 5, NOUT = 1, NCO = 1, NDOT = 7, UNROLL = 1, VEC = 1;
@@ -314,6 +322,8 @@ struct PPpG1 {
 };
 // Alg. 7 line 5: s, z, q, y as Alg. 4 line 4 (no p) ; theta=(q,y) phi=(y,y) pi=(q,q)
 struct PPpG2 {
+    static constexpr bool PREFETCH = true;
+    static constexpr int MINB = 2;
     static constexpr int UNROLL = 1;
     static constexpr const char* NAME = "ppipe_g2";
     static constexpr int NIN = 6, NOUT = 4, NCO = 3, NDOT = 3;   // in: r s w z t v ; out: s z q y ; co: beta nbo -alpha
@@ -342,6 +352,8 @@ struct PPpG3 {
 // Alg. 7 line 15: r = 1*q + (-omega)*y ; w = 1*y + (-omega)*t + (omega*alpha)*v ;
 //   rho'=(r0,r) psi=(r0,z) sigma=(r0,w) delta=(r0,s)
 struct PPpG4 {
+    static constexpr bool PREFETCH = true;
+    static constexpr int MINB = 2;
     static constexpr bool REDO_SAFE = true;
     static constexpr int UNROLL = 1;
     static constexpr const char* NAME = "ppipe_g4";
@@ -373,12 +385,19 @@ struct vec_of { static constexpr int value = 2; };
 template <class P>
 struct vec_of<P, decltype(void(P::VEC))> { static constexpr int value = P::VEC; };
 
-// Register-pipelined loads for dot-heavy, byte-light programs (the dots'
-// TwoSum chains would otherwise serialise with the memory latency).
-template <class P>
+// Register-pipelined loads for dot-heavy programs (the dots' TwoSum chains
+// would otherwise serialise with the memory latency): byte-light ones by
+// default, multi-dot lines by declaring PREFETCH (+ MINB = 2 for the
+// registers).  Measured on B200 (tools/sweep.py, C2/C3): Reordered -3..-5 %,
+// Pipelined merged -3.6 %, IBiCGStab -10 %, PPipeBiCGStab -3.5 %; the classical
+// x/r line and the fused Pipelined line lose (spills / occupancy) and keep
+// the unrolled loads.
+template <class P, class = void>
 struct prefetch_of {
     static constexpr bool value = P::NDOT >= 1 && P::NIN + P::NOUT <= 3;
 };
+template <class P>
+struct prefetch_of<P, decltype(void(P::PREFETCH))> { static constexpr bool value = P::PREFETCH; };
 
 // Unroll (pairs of packets per trip) unless a program declares UNROLL = 1;
 // pipelined programs get their memory parallelism from the prefetch instead.
@@ -389,7 +408,7 @@ struct unroll_of<P, decltype(void(P::UNROLL))> { static constexpr int value = P:
 
 // Resident blocks to budget registers for: pipelined programs are latency
 // bound and need 4 blocks of 256 threads (<= 64 registers).
-template <class P>
+template <class P, class = void>
 struct minblocks_of {
     // small pure updates: 3 blocks (<= 85 registers) -- with 2, ptxas spends
     // the budget on a deeper schedule and the 3-term update drops ~5% (B200,
@@ -397,6 +416,8 @@ struct minblocks_of {
     static constexpr int value =
         prefetch_of<P>::value ? (P::NDOT >= 3 ? 3 : 4) : (P::NDOT == 0 && P::NIN + P::NOUT <= 5 ? 3 : 2);
 };
+template <class P>
+struct minblocks_of<P, decltype(void(P::MINB))> { static constexpr int value = P::MINB; };
 
 // ---------------------------------------------------------------------------
 // Block-level exact combine.  Threads of a block fall into `classes` column
