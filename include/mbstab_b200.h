@@ -127,6 +127,10 @@ double* mbg_mv_device_ptr(mbg_mv* v);
  * y(i,c) = sum_k A(i,k) x(k,c); throws invalid on shape mismatch or x == y
  * (spmv.cpp:20-25).  Enqueued on the context stream. */
 int mbg_spmv(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* x, mbg_mv* y);
+/* core::spmv_transpose (include/mbstab/core/spmv.hpp:19-21, src/core/spmv.cpp:76-90):
+ * y = A^T x, every y(j, c) summed over source rows i in ascending order from
+ * 0.0 (the reference's serial loop), bit for bit.  Single-GPU matrices. */
+int mbg_spmv_transpose(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* x, mbg_mv* y);
 double mbg_spmv_traffic_bytes(int64_t n, int64_t nnz, int m);           /* Eq. (3) */
 double mbg_spmv_compulsory_bytes(int64_t n, int64_t nnz, int m);        /* x once */
 

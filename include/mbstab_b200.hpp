@@ -180,6 +180,20 @@ inline void spmv(const CsrMatrix& A, const MultiVector& x, MultiVector& y, Traff
     if (counter) counter->spmv_bytes += spmv_traffic_bytes(A, x.n_cols);
 }
 
+/// y = A^T x, same traffic formula (spmv.hpp:19-21; setup-only in the solvers)
+inline void spmv_transpose(const CsrMatrix& A, const MultiVector& x, MultiVector& y,
+                           TrafficCounter* counter = nullptr) {
+    if (x.n_rows != A.n_rows || y.n_rows != A.n_rows || x.n_cols != y.n_cols)
+        throw std::invalid_argument("spmv: dimension mismatch");
+    if (x.data.data() == y.data.data()) throw std::invalid_argument("spmv: x and y must be distinct storage");
+    Device& dev = Device::default_device();
+    DeviceMatrix dA(dev, A);
+    DeviceVector dx(dev, x), dy(dev, y.n_rows, y.n_cols);
+    check(mbg_spmv_transpose(dev.get(), dA.get(), dx.get(), dy.get()));
+    dy.download(y);
+    if (counter) counter->spmv_bytes += spmv_traffic_bytes(A, x.n_cols);
+}
+
 }  // namespace core
 
 namespace kernels {  // statement.hpp:10-75, execute.hpp:10-30

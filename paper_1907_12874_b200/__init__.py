@@ -263,6 +263,11 @@ def spmv(ctx: Context, a: DeviceCsr, x: MultiVector, y: MultiVector) -> None:
     check(lib().mbg_spmv(ctx.h, a.h, x.h, y.h))
 
 
+def spmv_transpose(ctx: Context, a: DeviceCsr, x: MultiVector, y: MultiVector) -> None:
+    """core::spmv_transpose: y = A^T x in the reference's serial summation order."""
+    check(lib().mbg_spmv_transpose(ctx.h, a.h, x.h, y.h))
+
+
 def spmv_traffic_bytes(n: int, nnz: int, m: int) -> float:
     return float(lib().mbg_spmv_traffic_bytes(n, nnz, m))
 

@@ -573,6 +573,22 @@ extern "C" int mbg_spmv(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* x, mbg_mv*
     });
 }
 
+// core::spmv_transpose (spmv.cpp:76-90): y = A^T x through the cached
+// transpose whose rows list their source rows ascending -- the reference's
+// serial summation order, bit for bit.  Single-GPU matrices.
+extern "C" int mbg_spmv_transpose(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* x, mbg_mv* y) {
+    return guarded([&] {
+        use(ctx);
+        if (!a || !x || !y) throw Invalid("spmv_transpose: null argument");
+        if (x->n != a->n || y->n != a->n || x->m != y->m) throw Invalid("spmv: dimension mismatch");
+        if (x == y || x->data.p == y->data.p) throw Invalid("spmv: x and y must be distinct storage");
+        if (!a->peers.empty() || a->n_halo) throw Invalid("spmv_transpose: single-GPU matrices only");
+        const mbg_csr* at = csr_transpose(ctx, a);
+        ctx->launches += apply_operator(ctx, at, x->m, x->data.p, y->data.p, nullptr);
+        MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 // kernels::execute_group (execute.cpp:123-172), exact dots.
 extern "C" int mbg_execute_group(mbg_ctx* ctx, const mbg_statement* st, int ns, mbg_mv* const* vectors,
                                  int nvec, double* dot_results, int nslots) {

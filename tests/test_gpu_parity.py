@@ -322,3 +322,16 @@ def test_solve_overflowing_dots_match_oracle(ctx, method, form):
     assert rep.iterations == want["iterations"]
     assert_bitwise(rep.residual_history, want["hist"], f"{method}/{form} overflow history")
     assert_bitwise(X.download(), want["x"], f"{method}/{form} overflow x")
+
+
+@pytest.mark.parametrize("mname", list(MATRICES))
+@pytest.mark.parametrize("m", [1, 3, 8])
+def test_spmv_transpose_bitwise(ctx, mname, m):
+    """core::spmv_transpose: the oracle (pinned to the compiled reference) bit for bit."""
+    a = MATRICES[mname]()
+    x = np.random.default_rng(50 + m).standard_normal(a.n * m)
+    d = ctx.upload(to_prod(a))
+    X = ctx.multivector(a.n, m, x)
+    Y = ctx.multivector(a.n, m)
+    P.spmv_transpose(ctx, d, X, Y)
+    assert_bitwise(Y.download(), O.spmv_transpose(a, x, m), f"spmv_transpose {mname} m={m}")
