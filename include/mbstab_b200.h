@@ -259,7 +259,8 @@ int mbg_fusion_bench(mbg_ctx* ctx, int64_t n, int reps, double* ms_per_run, doub
                      int* identical);
 
 /* ---- config generators (host) --------------------------------------------
- * kind 0 Poisson 7-pt (gen_poisson_7pt), 1 conv-diff 7-pt, 2 27-pt perturbed.
+ * kind 0 Poisson 7-pt (gen_poisson_7pt), 1 conv-diff 7-pt, 2 27-pt perturbed,
+ * 3 Poisson 5-pt (gen_poisson_5pt, generators.cpp:69-91; nz must be 1).
  * Two-phase: call with NULL cols/vals to get nnz (offsets may be NULL too). */
 int mbg_gen_stencil(int kind, int nx, int ny, int nz, uint64_t seed, int64_t* nnz,
                     int64_t* offsets, int32_t* cols, double* vals);

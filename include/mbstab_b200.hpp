@@ -107,6 +107,39 @@ inline CsrMatrix gen_poisson_7pt(int nx, int ny, int nz) {  // generators.cpp:37
     return A;
 }
 
+inline CsrMatrix gen_poisson_5pt(int nx, int ny) {  // generators.cpp:69-91
+    CsrMatrix A;
+    A.n_rows = static_cast<index_t>(nx) * ny;
+    std::int64_t nnz = 0;
+    A.row_offsets.resize(A.n_rows + 1);
+    check(mbg_gen_stencil(3, nx, ny, 1, 0, &nnz, A.row_offsets.data(), nullptr, nullptr));
+    A.col_indices.resize(nnz);
+    A.values.resize(nnz);
+    check(mbg_gen_stencil(3, nx, ny, 1, 0, &nnz, A.row_offsets.data(), A.col_indices.data(), A.values.data()));
+    return A;
+}
+
+// core::read_matrix_market / write_matrix_market (matrix_market.hpp:15-20)
+inline CsrMatrix read_matrix_market(const std::string& path) {
+    void* h = nullptr;
+    std::int64_t n = 0, nnz = 0;
+    const int rc = mbg_mm_read(path.c_str(), &h, &n, &nnz);
+    if (rc != MBG_OK) throw std::runtime_error(mbg_last_error());
+    CsrMatrix A;
+    A.n_rows = n;
+    A.row_offsets.resize(n + 1);
+    A.col_indices.resize(nnz);
+    A.values.resize(nnz);
+    mbg_mm_copy(h, A.row_offsets.data(), A.col_indices.data(), A.values.data());
+    mbg_mm_free(h);
+    return A;
+}
+
+inline void write_matrix_market(const CsrMatrix& A, const std::string& path) {
+    const int rc = mbg_mm_write(path.c_str(), A.n_rows, A.row_offsets.data(), A.col_indices.data(), A.values.data());
+    if (rc != MBG_OK) throw std::runtime_error(mbg_last_error());
+}
+
 }  // namespace core
 
 // ---- device-resident objects ------------------------------------------------

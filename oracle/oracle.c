@@ -71,7 +71,7 @@ static int stencil_row_count(int kind, int nx, int ny, int nz, int64_t row) {
 }
 
 int orc_gen_stencil(int kind, int nx, int ny, int nz, uint64_t seed, orc_csr* out) {
-    if (nx < 1 || ny < 1 || nz < 1 || kind < 0 || kind > 2) return -1;
+    if (nx < 1 || ny < 1 || nz < 1 || kind < 0 || kind > 3 || (kind == 3 && nz != 1)) return -1;
     const int64_t n = (int64_t)nx * ny * nz;
     const int64_t plane = (int64_t)nx * ny;
     out->n = n;
@@ -111,7 +111,7 @@ int orc_gen_stencil(int kind, int nx, int ny, int nz, uint64_t seed, orc_csr* ou
             if (z > 0)      { out->col[k] = (int32_t)(row - plane); out->val[k++] = -1.0; }
             if (y > 0)      { out->col[k] = (int32_t)(row - nx);    out->val[k++] = -1.0; }
             if (x > 0)      { out->col[k] = (int32_t)(row - 1);     out->val[k++] = west; }
-            out->col[k] = (int32_t)row; out->val[k++] = 6.0;
+            out->col[k] = (int32_t)row; out->val[k++] = kind == 3 ? 4.0 : 6.0;   /* 3: gen_poisson_5pt */
             if (x < nx - 1) { out->col[k] = (int32_t)(row + 1);     out->val[k++] = east; }
             if (y < ny - 1) { out->col[k] = (int32_t)(row + nx);    out->val[k++] = -1.0; }
             if (z < nz - 1) { out->col[k] = (int32_t)(row + plane); out->val[k++] = -1.0; }

@@ -51,6 +51,7 @@ double orc_u11(uint64_t seed, uint64_t stream, uint64_t a, uint64_t b);   /* [-1
  * kind 1: 7-pt convection-diffusion (west -1.3, east -0.7, y/z -1, diag 6)
  * kind 2: 27-pt (diag 26, off -1 + 0.1*u11(seed, matrix stream, row, col))
  * Returns 0 on success. */
+/* kind 0 Poisson 7-pt, 1 conv-diff 7-pt, 2 27-pt perturbed, 3 Poisson 5-pt (nz = 1) */
 int orc_gen_stencil(int kind, int nx, int ny, int nz, uint64_t seed, orc_csr* out);
 /* random banded: n rows, per-row count U{kmin..kmax} incl. diagonal, columns
  * uniform in [i-band, i+band] clipped, off-diag -u01, diag 1.1*sum|off| */

@@ -95,6 +95,18 @@ extern "C" int ref_gen_poisson_7pt(int nx, int ny, int nz, int64_t* nnz, int64_t
     } catch (const std::exception& e) { g_err = e.what(); return 1; }
 }
 
+extern "C" int ref_gen_poisson_5pt(int nx, int ny, int64_t* nnz, int64_t* off, int32_t* col, double* val) {
+    try {
+        if (!off) { *nnz = core::poisson_5pt_nnz(nx, ny); return 0; }
+        CsrMatrix A = core::gen_poisson_5pt(nx, ny);
+        *nnz = A.nnz();
+        std::memcpy(off, A.row_offsets.data(), sizeof(int64_t) * (A.n_rows + 1));
+        std::memcpy(col, A.col_indices.data(), sizeof(int32_t) * A.nnz());
+        std::memcpy(val, A.values.data(), sizeof(double) * A.nnz());
+        return 0;
+    } catch (const std::exception& e) { g_err = e.what(); return 1; }
+}
+
 extern "C" int ref_validate(int64_t n, const int64_t* off, const int32_t* col, const double* val) {
     try { make_csr(n, off, col, val).validate(); return 0; }
     catch (const std::exception& e) { g_err = e.what(); return 1; }

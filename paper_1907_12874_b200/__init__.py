@@ -76,7 +76,7 @@ class CsrMatrix:
 
 def gen_stencil(kind: str, nx: int, ny: int, nz: int, seed: int = 0) -> CsrMatrix:
     """kind: 'poisson7' (gen_poisson_7pt), 'convdiff7' or 'stencil27' (BASELINE configs)."""
-    k = {"poisson7": 0, "convdiff7": 1, "stencil27": 2}[kind]
+    k = {"poisson7": 0, "convdiff7": 1, "stencil27": 2, "poisson5": 3}[kind]
     n = nx * ny * nz
     nnz = C.c_int64()
     off = np.empty(n + 1, np.int64)
@@ -89,6 +89,11 @@ def gen_stencil(kind: str, nx: int, ny: int, nz: int, seed: int = 0) -> CsrMatri
 
 def gen_poisson_7pt(nx: int, ny: int, nz: int) -> CsrMatrix:
     return gen_stencil("poisson7", nx, ny, nz)
+
+
+def gen_poisson_5pt(nx: int, ny: int) -> CsrMatrix:
+    """core::gen_poisson_5pt (generators.cpp:69-91): 2-D, diagonal 4, neighbours -1."""
+    return gen_stencil("poisson5", nx, ny, 1)
 
 
 def gen_banded(n: int, band: int = 65536, kmin: int = 16, kmax: int = 32, seed: int = 4) -> CsrMatrix:

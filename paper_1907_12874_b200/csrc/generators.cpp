@@ -72,7 +72,8 @@ extern "C" int mbg_gen_stencil(int kind, int nx, int ny, int nz, uint64_t seed, 
                                int64_t* off, int32_t* col, double* val) {
     using namespace mbg;
     try {
-        if (kind < 0 || kind > 2) throw Invalid("gen_stencil: unknown kind");
+        if (kind < 0 || kind > 3) throw Invalid("gen_stencil: unknown kind");
+        if (kind == 3 && nz != 1) throw Invalid("gen_stencil: the 5-point Poisson operator is 2-D (nz = 1)");
         if (nx < 1 || ny < 1 || nz < 1) throw Invalid("grid dimensions must be >= 1");
         const int64_t n = static_cast<int64_t>(nx) * ny * nz;
         if (n > INT32_MAX) throw Invalid("grid dimension overflow");
@@ -107,7 +108,7 @@ extern "C" int mbg_gen_stencil(int kind, int nx, int ny, int nz, uint64_t seed, 
                 if (z > 0) put(row - plane, -1.0);
                 if (y > 0) put(row - nx, -1.0);
                 if (x > 0) put(row - 1, west);
-                put(row, 6.0);
+                put(row, kind == 3 ? 4.0 : 6.0);   // kind 3: gen_poisson_5pt (generators.cpp:69-91)
                 if (x < nx - 1) put(row + 1, east);
                 if (y < ny - 1) put(row + nx, -1.0);
                 if (z < nz - 1) put(row + plane, -1.0);

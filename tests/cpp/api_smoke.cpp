@@ -85,6 +85,21 @@ int main() {
         } catch (const std::invalid_argument&) {
         }
     }
+    // 5-point generator, transpose SpMV and the MatrixMarket round trip
+    {
+        core::CsrMatrix P5 = core::gen_poisson_5pt(9, 7);
+        if (P5.n_rows != 63 || P5.values[0] != 4.0) { std::puts("gen_poisson_5pt"); return 1; }
+        core::MultiVector xs(P5.n_rows, 2), y1(P5.n_rows, 2), y2(P5.n_rows, 2);
+        for (std::size_t i = 0; i < xs.data.size(); ++i) xs.data[i] = std::sin(0.7 * double(i));
+        core::spmv(P5, xs, y1);
+        core::spmv_transpose(P5, xs, y2);   // symmetric operator: A^T x == A x elementwise
+        for (std::size_t i = 0; i < y1.data.size(); ++i)
+            if (std::fabs(y1.data[i] - y2.data[i]) > 1e-14) { std::puts("spmv_transpose"); return 1; }
+        const std::string path = "/tmp/mbg_api_smoke.mtx";
+        core::write_matrix_market(P5, path);
+        core::CsrMatrix R = core::read_matrix_market(path);
+        if (R.values != P5.values || R.col_indices != P5.col_indices) { std::puts("matrix market"); return 1; }
+    }
     // API misuse throws std::invalid_argument like the reference
     try {
         core::spmv(A, x, x);

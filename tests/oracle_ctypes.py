@@ -88,6 +88,8 @@ def ref() -> C.CDLL:
         lib.ref_gen_poisson_7pt.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64),
                                             C.c_void_p, C.c_void_p, C.c_void_p]
         lib.ref_validate.argtypes = [C.c_int64, _i64p, _i32p, _f64p]
+        lib.ref_gen_poisson_5pt.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_int64), C.c_void_p, C.c_void_p,
+                                            C.c_void_p]
         lib.ref_spmv.argtypes = [C.c_int64, _i64p, _i32p, _f64p, C.c_int, _f64p, _f64p, C.c_int]
         lib.ref_spmv_transpose.argtypes = [C.c_int64, _i64p, _i32p, _f64p, C.c_int, _f64p, _f64p]
         lib.ref_read_matrix_market.argtypes = [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
@@ -138,7 +140,7 @@ def _from_orc(s: OrcCsr) -> Csr:
     return Csr(n, off, col, val)
 
 
-STENCIL_KINDS = {"poisson7": 0, "convdiff7": 1, "stencil27": 2}
+STENCIL_KINDS = {"poisson7": 0, "convdiff7": 1, "stencil27": 2, "poisson5": 3}
 
 
 def gen_stencil(kind: str, nx: int, ny: int, nz: int, seed: int = 0) -> Csr:
@@ -234,6 +236,18 @@ def ref_gen_poisson_7pt(nx, ny, nz) -> Csr:
     val = np.empty(nnz.value)
     assert lib.ref_gen_poisson_7pt(nx, ny, nz, C.byref(nnz), off.ctypes.data, col.ctypes.data,
                                    val.ctypes.data) == 0
+    return Csr(n, off, col, val)
+
+
+def ref_gen_poisson_5pt(nx, ny) -> Csr:
+    lib = ref()
+    nnz = C.c_int64()
+    assert lib.ref_gen_poisson_5pt(nx, ny, C.byref(nnz), None, None, None) == 0
+    n = nx * ny
+    off = np.empty(n + 1, np.int64)
+    col = np.empty(nnz.value, np.int32)
+    val = np.empty(nnz.value)
+    assert lib.ref_gen_poisson_5pt(nx, ny, C.byref(nnz), off.ctypes.data, col.ctypes.data, val.ctypes.data) == 0
     return Csr(n, off, col, val)
 
 

@@ -342,3 +342,26 @@ def test_new_methods_converge_like_classical(method):
     r = O.solve(a, b, 2, method, tol=1e-10)
     assert r["converged"] and abs(r["iterations"] - ref["iterations"]) <= 10
     assert np.max(np.abs(r["x"] - ref["x"])) <= 1e-6 * np.max(np.abs(ref["x"]))
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("dims", [(1, 1), (10, 10), (17, 5), (64, 3)])
+def test_poisson5_matches_reference_live(dims):
+    """gen_poisson_5pt (generators.cpp:69-91): oracle and product generator = reference, bitwise."""
+    want = O.ref_gen_poisson_5pt(*dims)
+    got = O.gen_stencil("poisson5", dims[0], dims[1], 1)
+    assert np.array_equal(got.off, want.off) and np.array_equal(got.col, want.col)
+    assert np.array_equal(got.val, want.val)
+    import paper_1907_12874_b200 as PP
+    p = PP.gen_poisson_5pt(*dims)
+    assert np.array_equal(p.row_offsets, want.off) and np.array_equal(p.values, want.val)
+
+
+def test_poisson5_solves_dense_oracle():
+    """gen_poisson_5pt(10,10), m=1, tol 1e-10 -> dense LU to <= 1e-8, all six methods."""
+    a = O.gen_stencil("poisson5", 10, 10, 1)
+    b = O.rhs(a.n, 1, 3)
+    x = np.linalg.solve(a.to_scipy().toarray(), b)
+    for method in METHODS:
+        r = O.solve(a, b, 1, method, tol=1e-10)
+        assert r["converged"] and np.max(np.abs(r["x"] - x)) <= 1e-8, method
