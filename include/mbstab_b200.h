@@ -194,6 +194,10 @@ typedef struct mbg_report {
 int mbg_solve(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* b, mbg_mv* x, int method,
               int formulation, double tol, int fixed, int max_iters, double* hist,
               mbg_report* report);
+/* True relative residual per column, out[c] = ||b - A x||_2 / ||b||_2 (the
+ * SolveReport's recomputed residual), exact dots. */
+int mbg_true_residual(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* b, const mbg_mv* x, double* out);
+
 /* Explicit preconditioner: precond_alpha 0 = none (required
  * by BiCGStab, IBiCGStab, PipeBiCGStab), 2 = identity M^-1 (one copy per
  * application), even alpha >= 4 = synthetic(alpha): alpha/2 scale passes by

@@ -268,6 +268,13 @@ def spmv(ctx: Context, a: DeviceCsr, x: MultiVector, y: MultiVector) -> None:
     check(lib().mbg_spmv(ctx.h, a.h, x.h, y.h))
 
 
+def true_residual(ctx: Context, a: DeviceCsr, b: MultiVector, x: MultiVector) -> np.ndarray:
+    """||b - A x||_2 / ||b||_2 per column (exact dots)."""
+    out = np.empty(b.n_cols)
+    check(lib().mbg_true_residual(ctx.h, a.h, b.h, x.h, _ptr(out)))
+    return out
+
+
 def spmv_transpose(ctx: Context, a: DeviceCsr, x: MultiVector, y: MultiVector) -> None:
     """core::spmv_transpose: y = A^T x in the reference's serial summation order."""
     check(lib().mbg_spmv_transpose(ctx.h, a.h, x.h, y.h))

@@ -3,6 +3,7 @@
 // maps to MBG_ERR_INVALID with the reference's message text.
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -682,6 +683,49 @@ extern "C" int mbg_execute_group(mbg_ctx* ctx, const mbg_statement* st, int ns, 
         } else {
             MBG_CUDA(cudaStreamSynchronize(ctx->stream));
         }
+    });
+}
+
+// SolveReport's true residual: out[c] = ||b - A x||_2 / ||b||_2
+// per column (||b - A x||_2 when b's column is zero), with exact dots, so the
+// value is the same on any GPU count.
+extern "C" int mbg_true_residual(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* b, const mbg_mv* x, double* out) {
+    return guarded([&] {
+        use(ctx);
+        if (!a || !b || !x || !out) throw Invalid("true_residual: null argument");
+        if (b->n != a->n || x->n != a->n || b->m != x->m) throw Invalid("true_residual: shape mismatch");
+        const int m = b->m;
+        mbg_mv *y = nullptr, *r = nullptr;
+        auto chk = [](int rc) {
+            if (rc != MBG_OK) throw std::runtime_error(mbg_last_error());
+        };
+        chk(mbg_mv_alloc(ctx, a->n, m, &y));
+        struct Free {
+            mbg_mv*& p;
+            ~Free() { if (p) mbg_mv_free(p); }
+        } fy{y}, fr{r};
+        chk(mbg_mv_alloc(ctx, a->n, m, &r));
+        chk(mbg_spmv(ctx, a, x, y));
+        std::vector<double> one(static_cast<size_t>(m), 1.0), mone(static_cast<size_t>(m), -1.0);
+        mbg_statement st[3] = {};
+        st[0].kind = MBG_STMT_UPDATE;      // r = 1*b + (-1)*y
+        st[0].out = 2;
+        st[0].nterms = 2;
+        st[0].term_vec[0] = 0;
+        st[0].term_vec[1] = 1;
+        st[0].term_coeff[0] = one.data();
+        st[0].term_coeff[1] = mone.data();
+        st[1].kind = MBG_STMT_DOT;         // (r, r)
+        st[1].left = st[1].right = 2;
+        st[1].slot = 0;
+        st[2].kind = MBG_STMT_DOT;         // (b, b)
+        st[2].left = st[2].right = 0;
+        st[2].slot = 1;
+        mbg_mv* vecs[3] = {const_cast<mbg_mv*>(b), y, r};
+        std::vector<double> dots(static_cast<size_t>(2) * m);
+        chk(mbg_execute_group(ctx, st, 3, vecs, 3, dots.data(), 2));
+        for (int c = 0; c < m; ++c)
+            out[c] = dots[m + c] > 0.0 ? std::sqrt(dots[c] / dots[m + c]) : std::sqrt(dots[c]);
     });
 }
 

@@ -204,3 +204,22 @@ def test_grid_hint_ignored_for_short_rows(ctx):
     assert not d.set_grid(12, 10, 8)
     with pytest.raises(ValueError):
         d.set_grid(12, 10, 9)
+
+
+@pytest.mark.parametrize("method", ["bicgstab", "ibicgstab", "ppipebicgstab"])
+def test_true_residual_after_solve(ctx, method):
+    """The recomputed ||b - Ax|| / ||b|| of a converged solve is small and
+    agrees with a host double-precision evaluation."""
+    a = O.gen_stencil("convdiff7", 16, 14, 12)
+    m = 3
+    b = O.rhs(a.n, m, 1)
+    d = ctx.upload(to_prod(a))
+    B = ctx.multivector(a.n, m, b)
+    X = ctx.multivector(a.n, m)
+    rep = P.solve(ctx, d, B, X, method, tol=1e-10)
+    tr = P.true_residual(ctx, d, B, X)
+    x = X.download().reshape(a.n, m)
+    r = b.reshape(a.n, m) - a.to_scipy() @ x
+    host = np.linalg.norm(r, axis=0) / np.linalg.norm(b.reshape(a.n, m), axis=0)
+    assert rep.converged and np.all(tr < 1e-8)
+    assert np.allclose(tr, host, rtol=1e-6, atol=1e-14)

@@ -72,7 +72,8 @@ def main():
                     "formulation": form, "iterations": best.iterations, "converged": best.converged,
                     "ms_per_iteration": round(msit, 4), "rhs_it_per_s": round(m * best.iterations / (best.loop_ms / 1e3), 1),
                     "bytes_per_iteration": bi, "hbm_GBps": round(bi / (msit / 1e3) / 1e9, 1),
-                    "hbm_frac": round(bi / (msit / 1e3) / 1e9 / PEAK, 3), "gen_upload_s": round(tgen, 1)}), flush=True)
+                    "hbm_frac": round(bi / (msit / 1e3) / 1e9 / PEAK, 3), "gen_upload_s": round(tgen, 1),
+                    "true_res_max": float(P.true_residual(ctx, d, B, X).max())}), flush=True)
             del B, X
 
 
