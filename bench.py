@@ -184,7 +184,9 @@ def run_reference(args):
         "ms_per_step": 1000.0 * args.m * args.cpu_iters / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded counter RNG, DESIGN.md Inputs)",
-        "config": {"workload": workload_desc(args, 1), "step": f"{args.cpu_iters} fixed iterations (bounded sample)"},
+        "config": {"workload": workload_desc(args, args.gpus),
+                   "step": f"{args.cpu_iters} fixed iterations on one 128^3 slab (bounded sample; the CPU's "
+                           "slab-RHS-iterations/s do not depend on how many slabs the job has)"},
         "cpu_baseline": cb,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
