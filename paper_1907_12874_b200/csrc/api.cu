@@ -599,6 +599,8 @@ extern "C" int mbg_execute_group(mbg_ctx* ctx, const mbg_statement* st, int ns, 
         if (ns == 0) return;  // empty group: no-op (execute.cpp:129)
         if (ns > GEN_MAX_STMT) throw Invalid("execute_group: too many statements");
         if (nvec > GEN_MAX_VEC) throw Invalid("execute_group: too many vectors");
+        for (int i = 0; i < nvec; ++i)
+            if (vectors[i] && vectors[i]->m > 256) throw Invalid("execute_group: at most 256 columns");
         auto vec = [&](int id) -> mbg_mv* {
             if (id < 0 || id >= nvec || !vectors[id]) throw Invalid("execute_group: unbound vector id");
             return vectors[id];

@@ -662,7 +662,7 @@ __global__ void __launch_bounds__(256, minblocks_of<P>::value) group_kernel(Grou
 }
 
 // Block size for m columns: m * 2^q <= 256 (m <= 256), else m.
-inline int group_block(int m) {
+inline int group_block(int m) {   // m <= 256 (checked by the callers)
     if (m > 256) return m;
     int b = m;
     while (b * 2 <= 256) b *= 2;

@@ -68,7 +68,8 @@ Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulatio
       maxit_(maxit) {
     if (method < 0 || method > 5) throw Invalid("solve: unknown method");
     if (formulation < 0 || formulation > 2) throw Invalid("solve: unknown formulation");
-    if (m < 1 || m > 1024) throw Invalid("solve: m must be in [1, 1024]");
+    // a block holds whole column classes (group_block): up to 256 right-hand sides
+    if (m < 1 || m > 256) throw Invalid("solve: m must be in [1, 256]");
     if (maxit < 0) throw Invalid("solve: negative iteration count");
     if (!fixed && !(tol > 0.0)) throw Invalid("solve: tol must be > 0 in converge mode");
     // preconditioned ids require a preconditioner, the others reject one

@@ -335,3 +335,17 @@ def test_spmv_transpose_bitwise(ctx, mname, m):
     Y = ctx.multivector(a.n, m)
     P.spmv_transpose(ctx, d, X, Y)
     assert_bitwise(Y.download(), O.spmv_transpose(a, x, m), f"spmv_transpose {mname} m={m}")
+
+
+def test_too_many_columns_rejected(ctx):
+    a = O.gen_stencil("poisson7", 4, 4, 4)
+    d = ctx.upload(to_prod(a))
+    m = 300
+    B = ctx.multivector(a.n, m, np.ones(a.n * m))
+    X = ctx.multivector(a.n, m)
+    with pytest.raises(ValueError, match="256"):
+        P.solve(ctx, d, B, X, "bicgstab")
+    # the SpMM itself takes any m (generic kernel)
+    Y = ctx.multivector(a.n, m)
+    P.spmv(ctx, d, B, Y)
+    assert_bitwise(Y.download(), O.spmv(a, np.ones(a.n * m), m), "spmv m=300")
