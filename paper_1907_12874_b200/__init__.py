@@ -207,10 +207,17 @@ class DeviceCsr:
         self.nnz = int(lib().mbg_csr_nnz(h))
 
     def set_grid(self, nx: int, ny: int, nz: int) -> bool:
-        """Structured-grid hint: long-row stencils get a brick-reordered twin
-        for the solver (bitwise-identical results).  Returns True if reordered."""
+        """Structured-grid hint: a grid-neighbour operator gets a stencil twin
+        (implicit columns, TMA-staged x planes; m in {8, 16, 32}) and long-row
+        stencils a brick-reordered twin for the other m (bitwise-identical
+        results).  Returns True if reordered."""
         check(lib().mbg_csr_set_grid(self.ctx.h, self.h, nx, ny, nz))
         return bool(lib().mbg_csr_reordered(self.h))
+
+    @property
+    def stencil_kind(self) -> int:
+        """7 or 27 when the stencil twin is in place, else 0."""
+        return int(lib().mbg_csr_stencil_kind(self.h))
 
     def stage_info(self):
         """(staged, reuse): whether the gather-once SpMM tiling is in use."""

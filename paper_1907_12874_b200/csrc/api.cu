@@ -18,6 +18,7 @@
 #include "common.hpp"
 #include "kernels.hpp"
 #include "solver.hpp"
+#include "stencil.hpp"
 
 namespace mbg {
 
@@ -449,6 +450,8 @@ extern "C" int mbg_csr_set_grid(mbg_ctx* ctx, mbg_csr* a, int nx, int ny, int nz
         if (nx < 1 || ny < 1 || nz < 1 || static_cast<int64_t>(nx) * ny * nz != a->n)
             throw Invalid("set_grid: nx*ny*nz must equal the number of rows");
         if (!a->peers.empty() || a->n_halo) throw Invalid("set_grid: single-GPU matrices only");
+        // stencil twin: implicit columns, x staged as TMA plane boxes (stencil.cu)
+        if (!a->stencil) a->stencil = build_stencil(ctx, a, nx, ny, nz);
         if (a->nnz <= 12 * a->n || a->reordered) return;
         const int bx = std::min(nx, 8), by = std::min(ny, 8), bz = std::min(nz, 4);
         const int64_t n = a->n;
@@ -479,6 +482,8 @@ extern "C" int mbg_csr_stage_info(const mbg_csr* a, int* staged, double* reuse) 
 }
 
 extern "C" int mbg_csr_reordered(const mbg_csr* a) { return a && a->reordered ? 1 : 0; }
+
+extern "C" int mbg_csr_stencil_kind(const mbg_csr* a) { return a && a->stencil ? a->stencil->kind : 0; }
 
 extern "C" int mbg_mv_alloc(mbg_ctx* ctx, int64_t n, int m, mbg_mv** out) {
     return guarded([&] {

@@ -17,6 +17,7 @@
 
 #include "comm.hpp"
 #include "kernels.hpp"
+#include "stencil.hpp"
 
 namespace mbg {
 
@@ -114,6 +115,7 @@ int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, 
         return r;
     };
     if (a->peers.empty()) {
+        if ((!epi || epi->kind == 0) && stencil_handles(a, m)) return launch_stencil_spmm(ctx, a, m, x, y, ctl);
         return launch_spmm(ctx->stream, tiles(a->tiles_all, a->long_all, a->stiles_all, a->umeta_all, a->ucols_all, a->lcol_all), a->n, nullptr, a->off.p, a->col.p, a->val.p, m, x,
                            y, ctl, ctx->num_sms, epi);
     }

@@ -62,7 +62,8 @@ struct DevBuf {
     }
 };
 
-struct Comm;  // comm.cu
+struct Comm;        // comm.cu
+struct StencilOp;   // stencil.hpp
 
 }  // namespace mbg
 
@@ -144,6 +145,8 @@ struct mbg_csr {
     std::unique_ptr<mbg_csr> reordered;
     mbg::DevBuf<int32_t> perm;
     std::vector<int32_t> perm_host;
+    // structured-grid twin (mbg_csr_set_grid; stencil.cu): implicit columns
+    std::shared_ptr<mbg::StencilOp> stencil;
 };
 
 struct mbg_mv {

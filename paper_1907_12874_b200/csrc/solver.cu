@@ -29,6 +29,7 @@
 #include "kernels.hpp"
 #include "scalar.cuh"
 #include "solver.hpp"
+#include "stencil.hpp"
 
 namespace mbg {
 
@@ -81,7 +82,9 @@ Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulatio
     pa_ = precond_alpha;
     elide_ = formulation == MBG_FUSED && pa_ == 2;
     // a locality-reordered twin of the operator, if the caller provided the grid
-    if (a->reordered && a->peers.empty()) {
+    // (not needed when the stencil SpMM handles this m: it stages x planes itself)
+    stencil_ = stencil_handles(a, m);
+    if (a->reordered && a->peers.empty() && !stencil_) {
         orig_ = a;
         a_ = a = a->reordered.get();
     }
@@ -89,7 +92,8 @@ Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulatio
     // nonzeros per row the gather-bound SpMM loses more to the epilogue's
     // registers than the separate 2-vector dot pass costs (B200: C3 27-point
     // 8.90 vs 8.07 ms/iteration, C5 m=8 5.28 vs 4.97; C2 7-point 0.76 vs 0.84)
-    epi_delta_ = formulation == MBG_FUSED && a->nnz <= 12 * a->n;
+    // (the stencil SpMM has no epilogue)
+    epi_delta_ = formulation == MBG_FUSED && a->nnz <= 12 * a->n && !stencil_;
     if (method == MBG_IBICGSTAB) {
         if (!a->peers.empty() || a->n_halo)
             throw Invalid("solve: IBiCGStab needs f0 = A^T r0, supported on a single GPU only");
@@ -194,7 +198,9 @@ void Solver::spmm(const double* x, double* y, int epi_kind, const double* aux, i
     e.aux = aux;
     for (int d = 0; d < 3; ++d) e.slot[d] = slot(first_slot + d);
     const double extra = epi_kind == 1 ? 8.0 * len_ : 0.0;   // aux vector read
-    mark_begin(epi_kind ? "spmm+dots" : "spmm", spmv_compulsory_bytes(a_->n, a_->nnz, m_) + extra);
+    mark_begin(epi_kind ? "spmm+dots" : "spmm",
+               (stencil_ ? stencil_spmm_bytes(a_->n, a_->nnz, m_) : spmv_compulsory_bytes(a_->n, a_->nnz, m_)) +
+                   extra);
     launches_ += apply_operator(ctx_, a_, m_, const_cast<double*>(x), y, ctl_.p, epi_kind ? &e : nullptr);
     mark_end();
     if (epi_kind) {
@@ -680,7 +686,9 @@ void Solver::report(double* hist_host, mbg_report* rep) {
     rep->spmv_bytes = static_cast<double>(spmvs) * its * spmv_traffic_bytes(a_->n, a_->nnz, m_);
     rep->compulsory_bytes =
         (iteration_bytes(method_, form_, pa_, a_->n, a_->nnz, m_) +
-         ((method_ == MBG_RBICGSTAB && form_ == MBG_FUSED && !epi_delta_) ? 8.0 * static_cast<double>(len_) : 0.0)) *
+         ((method_ == MBG_RBICGSTAB && form_ == MBG_FUSED && !epi_delta_) ? 8.0 * static_cast<double>(len_) : 0.0) -
+         // stencil SpMM: no column indices (8 B instead of 12 B per nonzero)
+         (stencil_ ? 4.0 * spmvs * static_cast<double>(a_->nnz) : 0.0)) *
         its;
     rep->reductions = static_cast<int64_t>(nred) * its;
     rep->gpu_launches = launches_;

@@ -71,7 +71,8 @@ private:
     int m_, method_, form_;
     int pa_ = 0;            // preconditioner alpha (0 none, 2 identity, >= 4 synthetic)
     bool elide_ = false;    // fused formulation with identity M^-1: applications aliased away
-    bool epi_delta_ = false;  // fused Reordered: delta = (v, r0) in the SpMM epilogue
+    bool epi_delta_ = false;
+    bool stencil_ = false;    // the operator's SpMM runs on its stencil twin (stencil.cu)  // fused Reordered: delta = (v, r0) in the SpMM epilogue
     const mbg_csr* at_ = nullptr;   // A^T (IBiCGStab setup)
     const mbg_csr* orig_ = nullptr; // caller's operator when a_ is its reordered twin
     double* x_user_ = nullptr;

@@ -1,0 +1,604 @@
+// stencil.cu -- SpMM  Y = A X  for operators declared on a structured grid.
+//
+// Same arithmetic as spmv_rows (spmv.cpp:40-46) and spmm.cu: each (row,
+// column) is the sequential sum, in CSR order from 0.0, of separately rounded
+// products val[k]*x(col[k], c).  On an nx*ny*nz grid (lexicographic rows) a
+// nonzero that couples a point with a neighbour (dz, dy, dx) in {-1,0,1}^3
+// has a "slot"; ascending columns are ascending slots, so summing a row's
+// present slots in slot order IS the CSR order.  The twin built at
+// mbg_csr_set_grid therefore drops the column indices:
+//
+//   chunk (tile t, plane z) = values[S][32*BY] (slot-major, 0 where a slot is
+//                             absent) | mask[32*BY] (bit s: slot s present)
+//
+// for xy-tiles of 32 x BY points.  One block computes one tile over a range
+// of planes ("z-march"): a ring of four x planes, each a TMA tensor box
+// (m, 34|35, BY+2, 1) of the x block viewed as an (nz, ny, nx, m) tensor
+// (out-of-grid points zero-filled, never used: their slots are absent),
+// and a ring of two value chunks (cp.async.bulk); plane z+2 and chunk z+1
+// are in flight while plane z computes.  A lane owns 4 consecutive points
+// along x and 2 columns: the 6 x points of one stencil line are loaded from
+// shared memory once and reused by the 3 dx slots of the 4 rows.
+//
+// Bytes per SpMM (the roofline's algorithmic count): 16*N*m (x once, y once)
+// + 8*nnz (values) + 4*N (masks); versus 16*N*m + 12*nnz + 4*N for CSR.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstdio>
+#include <mutex>
+#include <vector>
+
+#include "comm.hpp"
+#include "common.hpp"
+#include "exact.cuh"
+#include "kernels.hpp"
+#include "stencil.hpp"
+#include "tma.cuh"
+
+namespace mbg {
+
+// ---- analysis and layout (device kernels over the uploaded CSR) -----------
+
+__device__ __forceinline__ void grid_coords(int64_t i, int nx, int ny, int& x, int& y, int& z) {
+    x = static_cast<int>(i % nx);
+    const int64_t t = i / nx;
+    y = static_cast<int>(t % ny);
+    z = static_cast<int>(t / ny);
+}
+
+// 7-point slot order = ascending column order: -z, -y, -x, centre, +x, +y, +z
+__device__ __forceinline__ int face_slot(int dz, int dy, int dx) {
+    if (dz) return dz < 0 ? 0 : 6;
+    if (dy) return dy < 0 ? 1 : 5;
+    return 3 + dx;
+}
+
+// flags: 1 = a nonzero outside the 3x3x3 neighbourhood; 2 = a non-face
+// neighbour (27-point); 4 = slots not strictly ascending within a row
+__global__ void stencil_scan_kernel(int64_t n, int nx, int ny, const int32_t* __restrict__ off,
+                                    const int32_t* __restrict__ col, unsigned* flags) {
+    unsigned f = 0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int xi, yi, zi;
+        grid_coords(i, nx, ny, xi, yi, zi);
+        int prev = -1;
+        for (int k = off[i]; k < off[i + 1]; ++k) {
+            int xj, yj, zj;
+            grid_coords(col[k], nx, ny, xj, yj, zj);
+            const int dx = xj - xi, dy = yj - yi, dz = zj - zi;
+            if (dx < -1 || dx > 1 || dy < -1 || dy > 1 || dz < -1 || dz > 1) {
+                f |= 1u;
+                continue;
+            }
+            const int s = (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1);
+            if (s <= prev) f |= 4u;
+            prev = s;
+            if ((dx != 0) + (dy != 0) + (dz != 0) > 1) f |= 2u;
+        }
+    }
+    if (f) atomicOr(flags, f);
+}
+
+// Absent slots hold -0.0: their x operand is either the TMA zero fill of an
+// out-of-grid point (+0.0), making the term exactly -0.0, the identity of
+// IEEE addition (acc + -0.0 == acc for every acc, signed zeros and NaNs
+// included), or -- for an in-grid neighbour the CSR leaves out -- the row is
+// flagged (mask bit 31) and takes the predicated path.
+__global__ void stencil_clear_kernel(int64_t nchunks, int S, int RT, int64_t chunk_bytes, unsigned char* chunks) {
+    const int64_t per = chunk_bytes / 8;   // 8-byte words per chunk
+    const int64_t nval = static_cast<int64_t>(S) * RT;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < nchunks * per;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t w = e % per;
+        reinterpret_cast<unsigned long long*>(chunks)[e] = w < nval ? 0x8000000000000000ull : 0ull;
+    }
+}
+
+__global__ void stencil_fill_kernel(int64_t n, int nx, int ny, int nz, int by, int S, int ntx, int64_t chunk_bytes,
+                                    const int32_t* __restrict__ off, const int32_t* __restrict__ col,
+                                    const double* __restrict__ val, unsigned char* __restrict__ chunks) {
+    const int RT = STENCIL_BX * by;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int xi, yi, zi;
+        grid_coords(i, nx, ny, xi, yi, zi);
+        const int64_t t = static_cast<int64_t>(yi / by) * ntx + xi / STENCIL_BX;
+        const int r = (yi % by) * STENCIL_BX + xi % STENCIL_BX;
+        unsigned char* c = chunks + (t * nz + zi) * chunk_bytes;
+        double* V = reinterpret_cast<double*>(c);
+        uint32_t* MK = reinterpret_cast<uint32_t*>(c + static_cast<int64_t>(S) * RT * 8);
+        uint32_t mask = 0;
+        for (int k = off[i]; k < off[i + 1]; ++k) {
+            int xj, yj, zj;
+            grid_coords(col[k], nx, ny, xj, yj, zj);
+            const int dx = xj - xi, dy = yj - yi, dz = zj - zi;
+            const int s = S == 27 ? (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1) : face_slot(dz, dy, dx);
+            V[static_cast<int64_t>(s) * RT + r] = val[k];
+            mask |= 1u << s;
+        }
+        // an absent slot whose neighbour lies inside the grid needs the predicated path
+        bool check = false;
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    if (S == 7 && (dx != 0) + (dy != 0) + (dz != 0) > 1) continue;
+                    const int s = S == 27 ? (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1) : face_slot(dz, dy, dx);
+                    const bool inside = xi + dx >= 0 && xi + dx < nx && yi + dy >= 0 && yi + dy < ny &&
+                                        zi + dz >= 0 && zi + dz < nz;
+                    if (inside && !((mask >> s) & 1u)) check = true;
+                }
+        MK[r] = mask | (check ? 0x80000000u : 0u);
+    }
+}
+
+// ---- the SpMM kernel --------------------------------------------------------
+
+struct StencilGeom {
+    int nx, ny, nz;
+    int ntx;              // tiles along x
+    int64_t steps;        // tile-planes per column half: ntiles * nz
+    int nranges;          // step ranges (persistent blocks per column half)
+    int pd;               // L2 prefetch distance in steps beyond the rings (0: none)
+    unsigned long long* trace;   // lab: per block (smid, t0, t1) when non-null (MBG_STENCIL_TRACE)
+    int mode;             // lab switch (MBG_STENCIL_MODE): 0 normal, 1 no arithmetic, 2 no data movement
+    const unsigned char* chunks;
+    int64_t chunk_bytes;
+};
+
+template <int MC, int BY>
+struct StencilShape {
+    static constexpr int LPR = MC / 2;                       // lanes per 4-point group (2 columns each)
+    static constexpr int THREADS = 8 * BY * LPR;             // compute threads: 8 groups along x, BY along y
+    static constexpr int NCW = THREADS / 32;                 // compute warps (+1 producer warp)
+    static constexpr int LW = MC == 8 ? 35 : 34;             // x-plane line width (35: bank spread at m = 8)
+    static constexpr int RT = STENCIL_BX * BY;               // rows per tile plane
+    static constexpr int PLANE = LW * (BY + 2) * MC;         // doubles per x plane
+};
+
+template <int ST, int BY>
+__host__ __device__ constexpr int stencil_chunk_bytes() { return ST * STENCIL_BX * BY * 8 + STENCIL_BX * BY * 4; }
+
+constexpr int STENCIL_XR = 5, STENCIL_VR = 3;   // ring depths: x planes, value chunks
+constexpr int STENCIL_HEAD = 256;               // mbarriers
+
+template <int MC, int ST, int BY>
+__host__ __device__ constexpr int stencil_smem() {
+    return STENCIL_HEAD + STENCIL_XR * StencilShape<MC, BY>::PLANE * 8 + STENCIL_VR * stencil_chunk_bytes<ST, BY>();
+}
+
+// acc[r][c] += v * x: the reference's  acc = acc + val*x  (no FMA)
+#define MBG_ACC(r, v, xv)                                        \
+    do {                                                         \
+        acc[r][0] = __dadd_rn(acc[r][0], __dmul_rn((v), (xv).x)); \
+        acc[r][1] = __dadd_rn(acc[r][1], __dmul_rn((v), (xv).y)); \
+    } while (0)
+
+template <int MC, int ST, int BY, bool CHECK>
+__device__ __forceinline__ void stencil_rows(double (&acc)[4][2], const double* __restrict__ P0,
+                                             const double* __restrict__ P1, const double* __restrict__ P2,
+                                             const double* __restrict__ V, const uint32_t (&mk)[4], int gy, int lx0,
+                                             int cp, int r0) {
+    using SH = StencilShape<MC, BY>;
+    constexpr int LW = SH::LW, RT = SH::RT;
+    auto ld2 = [](const double* p) { return *reinterpret_cast<const double2*>(p); };
+    auto vals = [&](int s, double (&v)[4]) {
+        const double2 a = ld2(V + s * RT + r0), b = ld2(V + s * RT + r0 + 2);
+        v[0] = a.x;
+        v[1] = a.y;
+        v[2] = b.x;
+        v[3] = b.y;
+    };
+    // point (line ly, x offset j from lx0 - 1) of a plane
+    auto pt = [&](const double* P, int ly, int j) { return ld2(P + ((gy + ly) * LW + lx0 + j) * MC + cp); };
+    if constexpr (ST == 27) {
+#pragma unroll
+        for (int dz = 0; dz < 3; ++dz) {
+            const double* P = dz == 0 ? P0 : (dz == 1 ? P1 : P2);
+#pragma unroll
+            for (int dy = 0; dy < 3; ++dy) {
+                double2 xp[6];
+#pragma unroll
+                for (int j = 0; j < 6; ++j) xp[j] = pt(P, dy, j);
+#pragma unroll
+                for (int dx = 0; dx < 3; ++dx) {
+                    const int s = dz * 9 + dy * 3 + dx;
+                    double v[4];
+                    vals(s, v);
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+                        if (!CHECK || ((mk[r] >> s) & 1u)) MBG_ACC(r, v[r], xp[r + dx]);
+                }
+            }
+        }
+    } else {
+        // slots: 0 (-z), 1 (-y), 2 3 4 (-x, centre, +x), 5 (+y), 6 (+z)
+        auto line1 = [&](const double* P, int ly, int s) {
+            double2 xp[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) xp[r] = pt(P, ly, r + 1);
+            double v[4];
+            vals(s, v);
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                if (!CHECK || ((mk[r] >> s) & 1u)) MBG_ACC(r, v[r], xp[r]);
+        };
+        line1(P0, 1, 0);
+        line1(P1, 0, 1);
+        {
+            double2 xp[6];
+#pragma unroll
+            for (int j = 0; j < 6; ++j) xp[j] = pt(P1, 1, j);
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) {
+                double v[4];
+                vals(2 + dx, v);
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    if (!CHECK || ((mk[r] >> (2 + dx)) & 1u)) MBG_ACC(r, v[r], xp[r + dx]);
+            }
+        }
+        line1(P1, 2, 5);
+        line1(P2, 1, 6);
+    }
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+
+// Persistent, warp-specialised: block b owns an equal range of the step
+// sequence s = tile * nz + z (z fastest) of one column half; the range is
+// cut into z-segments at tile boundaries.  The producer warp streams, per
+// segment, the x planes za-1 .. zb (TMA tensor boxes) and the value chunks
+// za .. zb-1 (bulk copies) through the rings, gated by "empty" barriers that
+// the compute warps arrive on when they are done with a slot; compute warps
+// never wait on each other.  MT: columns of the block vector; MC: columns of
+// one block (MT / MC column halves run as adjacent blocks over the same
+// range, so the second read of a value chunk hits L2).
+template <int MT, int MC, int ST, int BY>
+__global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
+    stencil_spmm_kernel(const __grid_constant__ CUtensorMap xmap, StencilGeom g, double* __restrict__ y,
+                        const int* __restrict__ ctl) {
+    using SH = StencilShape<MC, BY>;
+    constexpr int CS = MT / MC;
+    constexpr int XR = STENCIL_XR, VR = STENCIL_VR;
+    constexpr int CB = stencil_chunk_bytes<ST, BY>();
+    pdl_wait();
+    if (ctl && ctl[0]) return;
+    unsigned long long tr0 = 0;
+    if (g.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* xfull = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* xempty = xfull + XR;
+    uint64_t* vfull = xempty + XR;
+    uint64_t* vempty = vfull + VR;
+    double* xr = reinterpret_cast<double*>(smem + STENCIL_HEAD);
+    unsigned char* vr = smem + STENCIL_HEAD + XR * SH::PLANE * 8;
+
+    const int h = blockIdx.x % CS;
+    const int rb = blockIdx.x / CS;
+    const int64_t s0 = g.steps * rb / g.nranges, s1 = g.steps * (rb + 1) / g.nranges;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int b = 0; b < XR; ++b) {
+            mbar_init(&xfull[b], 1);
+            mbar_init(&xempty[b], SH::NCW);
+        }
+        for (int b = 0; b < VR; ++b) {
+            mbar_init(&vfull[b], 1);
+            mbar_init(&vempty[b], SH::NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (tid >= SH::THREADS) {   // ---- producer warp
+        if (tid == SH::THREADS && g.mode != 2) {
+            int64_t Q = 0, j = 0;   // plane loads / chunk loads issued so far
+            auto plane = [&](int t, int p) {
+                const int b = static_cast<int>(Q % XR);
+                if (Q >= XR) mbar_wait(&xempty[b], static_cast<uint32_t>((Q / XR - 1) & 1));
+                mbar_expect_tx(&xfull[b], static_cast<uint32_t>(SH::PLANE * 8));
+                tensor4d_g2s(xr + b * SH::PLANE, &xmap, h * MC, (t % g.ntx) * STENCIL_BX - 1,
+                             (t / g.ntx) * BY - 1, p, &xfull[b]);
+                ++Q;
+            };
+            auto chunk = [&](int t, int z) {
+                const int b = static_cast<int>(j % VR);
+                if (j >= VR) mbar_wait(&vempty[b], static_cast<uint32_t>((j / VR - 1) & 1));
+                mbar_expect_tx(&vfull[b], static_cast<uint32_t>(CB));
+                bulk_g2s(vr + b * CB, g.chunks + (static_cast<int64_t>(t) * g.nz + z) * g.chunk_bytes,
+                         static_cast<uint32_t>(CB), &vfull[b]);
+                ++j;
+            };
+            // L2 prefetch of the step pd steps beyond the one being loaded
+            // (same tile only; a new tile's first planes are not prefetched)
+            auto pref = [&](int t, int z) {
+                if (g.pd <= 0) return;
+                const int zp = z + g.pd;
+                if (zp >= g.nz) return;
+                prefetch_tensor4d_l2(&xmap, h * MC, (t % g.ntx) * STENCIL_BX - 1, (t / g.ntx) * BY - 1, zp + 1);
+                prefetch_bulk_l2(g.chunks + (static_cast<int64_t>(t) * g.nz + zp) * g.chunk_bytes,
+                                 static_cast<uint32_t>(CB));
+            };
+            for (int64_t s = s0; s < s1;) {
+                const int t = static_cast<int>(s / g.nz), za = static_cast<int>(s % g.nz);
+                const int64_t left = s1 - s;
+                const int steps = static_cast<int>(left < g.nz - za ? left : g.nz - za);
+                plane(t, za - 1);
+                plane(t, za);
+                for (int i = 0; i < steps; ++i) {
+                    plane(t, za + i + 1);
+                    chunk(t, za + i);
+                    pref(t, za + i);
+                }
+                s += steps;
+            }
+        }
+        pdl_trigger();
+        return;
+    }
+
+    // ---- compute warps: lane -> (4-point group gx along x, line gy, column pair cl)
+    const int lane = tid & 31, warp = tid >> 5;
+    const int cl = lane % SH::LPR, gl = lane / SH::LPR;
+    int gx, gy;
+    if constexpr (SH::LPR == 8) {   // 4 groups per warp, one line
+        gx = (warp & 1) * 4 + gl;
+        gy = warp >> 1;
+    } else {                        // 8 groups per warp, two lines
+        gx = (warp & 1) * 4 + (gl & 3);
+        gy = (warp >> 1) * 2 + (gl >> 2);
+    }
+    const int lx0 = gx * 4, cp = cl * 2, r0 = gy * STENCIL_BX + lx0;
+    int64_t Q = 0, j = 0;
+    for (int64_t s = s0; s < s1;) {
+        const int t = static_cast<int>(s / g.nz), za = static_cast<int>(s % g.nz);
+        const int64_t left = s1 - s;
+                const int steps = static_cast<int>(left < g.nz - za ? left : g.nz - za);
+        const int xg0 = (t % g.ntx) * STENCIL_BX + lx0, yg = (t / g.ntx) * BY + gy;
+        const bool yok = yg < g.ny;
+        for (int i = 0; i < steps; ++i, ++j) {
+            if (g.mode != 2) {
+                for (int64_t q = (i == 0 ? Q : Q + i + 2); q <= Q + i + 2; ++q)
+                    mbar_wait(&xfull[q % XR], static_cast<uint32_t>((q / XR) & 1));
+                mbar_wait(&vfull[j % VR], static_cast<uint32_t>((j / VR) & 1));
+            }
+            const double* P0 = xr + ((Q + i) % XR) * SH::PLANE;
+            const double* P1 = xr + ((Q + i + 1) % XR) * SH::PLANE;
+            const double* P2 = xr + ((Q + i + 2) % XR) * SH::PLANE;
+            const unsigned char* ch = vr + (j % VR) * CB;
+            const double* V = reinterpret_cast<const double*>(ch);
+            const uint4 m4 = *reinterpret_cast<const uint4*>(ch + ST * SH::RT * 8 + r0 * 4);
+            const uint32_t mk[4] = {m4.x, m4.y, m4.z, m4.w};
+            double acc[4][2];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[r][0] = acc[r][1] = 0.0;
+            if (g.mode == 1) {
+            } else if (!((m4.x | m4.y | m4.z | m4.w) & 0x80000000u) || g.mode == 2)
+                stencil_rows<MC, ST, BY, false>(acc, P0, P1, P2, V, mk, gy, lx0, cp, r0);
+            else
+                stencil_rows<MC, ST, BY, true>(acc, P0, P1, P2, V, mk, gy, lx0, cp, r0);
+            __syncwarp();
+            if (lane == 0 && g.mode != 2) {   // this warp is done with plane Q+i (as z-1) and chunk j
+                mbar_arrive(&xempty[(Q + i) % XR]);
+                mbar_arrive(&vempty[j % VR]);
+            }
+            if (yok) {
+                const int64_t rowz = (static_cast<int64_t>(za + i) * g.ny + yg) * g.nx;
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    if (xg0 + r < g.nx)
+                        *reinterpret_cast<double2*>(y + (rowz + xg0 + r) * MT + h * MC + cp) =
+                            make_double2(acc[r][0], acc[r][1]);
+            }
+        }
+        if (lane == 0 && g.mode != 2) {   // the segment's last two planes
+            mbar_arrive(&xempty[(Q + steps) % XR]);
+            mbar_arrive(&xempty[(Q + steps + 1) % XR]);
+        }
+        Q += steps + 2;
+        s += steps;
+    }
+    pdl_trigger();
+    if (g.trace) {
+        __syncwarp();
+        if (tid == 0) {
+            unsigned long long tr1;
+            unsigned smid;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr1));
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            g.trace[3 * blockIdx.x] = smid;
+            g.trace[3 * blockIdx.x + 1] = tr0;
+            g.trace[3 * blockIdx.x + 2] = tr1;
+        }
+    }
+}
+#undef MBG_ACC
+
+// ---- host side ----------------------------------------------------------------
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        MBG_CUDA(cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+bool stencil_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("MBG_STENCIL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e && *e ? std::atoi(e) : dflt;
+}
+
+StencilLayout& layout_for(mbg_ctx* ctx, const mbg_csr* a, int by) {
+    StencilOp& op = *a->stencil;
+    for (auto& l : op.layouts)
+        if (l->by == by) return *l;
+    auto l = std::make_unique<StencilLayout>();
+    l->by = by;
+    const int S = op.kind;
+    const int RT = STENCIL_BX * by;
+    l->chunk_bytes = static_cast<int64_t>(S) * RT * 8 + RT * 4;
+    const int64_t ntx = (op.nx + STENCIL_BX - 1) / STENCIL_BX, nty = (op.ny + by - 1) / by;
+    const size_t bytes = static_cast<size_t>(ntx * nty * op.nz * l->chunk_bytes);
+    l->chunks.alloc(bytes);
+    const int grid = ctx->num_sms * 8;
+    stencil_clear_kernel<<<grid, 256, 0, ctx->stream>>>(ntx * nty * op.nz, S, RT, l->chunk_bytes, l->chunks.p);
+    stencil_fill_kernel<<<grid, 256, 0, ctx->stream>>>(a->n, op.nx, op.ny, op.nz, by, S, static_cast<int>(ntx),
+                                                       l->chunk_bytes, a->off.p, a->col.p, a->val.p, l->chunks.p);
+    MBG_CUDA(cudaGetLastError());
+    MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+    op.layouts.push_back(std::move(l));
+    return *op.layouts.back();
+}
+
+template <int MT, int MC, int ST, int BY>
+void launch_one(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const double* x, double* y,
+                const int* ctl) {
+    const StencilOp& op = *a->stencil;
+    constexpr int smem = stencil_smem<MC, ST, BY>();
+    constexpr int threads = StencilShape<MC, BY>::THREADS + 32;   // + producer warp
+    constexpr int CS = MT / MC;
+    static int occ = -1;
+    if (occ < 0) {
+        MBG_CUDA(cudaFuncSetAttribute(stencil_spmm_kernel<MT, MC, ST, BY>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        MBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil_spmm_kernel<MT, MC, ST, BY>, threads,
+                                                               smem));
+        if (occ < 1) occ = 1;
+    }
+    // x viewed as a (nz, ny, nx, MT) fp64 tensor; box (MC, LW, BY + 2, 1)
+    CUtensorMap tm;
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(MT), static_cast<cuuint64_t>(op.nx),
+                                static_cast<cuuint64_t>(op.ny), static_cast<cuuint64_t>(op.nz)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(MT) * 8, static_cast<cuuint64_t>(op.nx) * MT * 8,
+                                   static_cast<cuuint64_t>(op.nx) * op.ny * MT * 8};
+    const cuuint32_t box[4] = {static_cast<cuuint32_t>(MC), static_cast<cuuint32_t>(StencilShape<MC, BY>::LW),
+                               static_cast<cuuint32_t>(BY + 2), 1u};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(x), dims, strides,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("stencil SpMM: cuTensorMapEncodeTiled failed (" +
+                                                    std::to_string(static_cast<int>(r)) + ")");
+    StencilGeom gm{};
+    gm.nx = op.nx;
+    gm.ny = op.ny;
+    gm.nz = op.nz;
+    gm.ntx = (op.nx + STENCIL_BX - 1) / STENCIL_BX;
+    gm.steps = static_cast<int64_t>(gm.ntx) * ((op.ny + BY - 1) / BY) * op.nz;
+    gm.chunks = L.chunks.p;
+    gm.chunk_bytes = L.chunk_bytes;
+    static const int mode = env_int("MBG_STENCIL_MODE", 0);
+    gm.mode = mode;
+    static const int pd = env_int("MBG_STENCIL_PD", 0);
+    gm.pd = pd;
+    // persistent grid: every resident slot gets an equal share of the steps
+    const int64_t slots = static_cast<int64_t>(occ) * ctx->num_sms / CS;
+    gm.nranges = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(slots, gm.steps)));
+    const int grid = gm.nranges * CS;
+    static const int trace = env_int("MBG_STENCIL_TRACE", 0);
+    static DevBuf<unsigned long long> tbuf;
+    if (trace) {
+        tbuf.ensure(static_cast<size_t>(grid) * 3);
+        gm.trace = tbuf.p;
+    }
+    launch_pdl(stencil_spmm_kernel<MT, MC, ST, BY>, dim3(grid), dim3(threads), static_cast<size_t>(smem),
+               ctx->stream, tm, gm, y, ctl);
+    if (trace) {   // lab: dump (block, smid, start ns, end ns) of this launch
+        std::vector<unsigned long long> h(static_cast<size_t>(grid) * 3);
+        MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+        MBG_CUDA(cudaMemcpy(h.data(), tbuf.p, h.size() * 8, cudaMemcpyDeviceToHost));
+        FILE* f = std::fopen("gpurun_out/stencil_trace.txt", "w");
+        if (f) {
+            for (int b = 0; b < grid; ++b)
+                std::fprintf(f, "%d %llu %llu %llu\n", b, h[3 * b], h[3 * b + 1], h[3 * b + 2]);
+            std::fclose(f);
+        }
+    }
+}
+
+}  // namespace
+
+std::shared_ptr<StencilOp> build_stencil(mbg_ctx* ctx, const mbg_csr* a, int nx, int ny, int nz) {
+    if (!a->peers.empty() || a->n_halo) return nullptr;
+    if (static_cast<int64_t>(nx) * ny * nz != a->n || a->n == 0) return nullptr;
+    DevBuf<unsigned> flags(1);
+    MBG_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(unsigned), ctx->stream));
+    stencil_scan_kernel<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(a->n, nx, ny, a->off.p, a->col.p, flags.p);
+    MBG_CUDA(cudaGetLastError());
+    unsigned f = 0;
+    MBG_CUDA(cudaMemcpyAsync(&f, flags.p, sizeof f, cudaMemcpyDeviceToHost, ctx->stream));
+    MBG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (f & 5u) return nullptr;
+    auto op = std::make_shared<StencilOp>();
+    op->nx = nx;
+    op->ny = ny;
+    op->nz = nz;
+    op->kind = (f & 2u) ? 27 : 7;
+    op->nnz = a->nnz;
+    return op;
+}
+
+bool stencil_handles(const mbg_csr* a, int m) {
+    return a && a->stencil && stencil_enabled() && (m == 8 || m == 16 || m == 32);
+}
+
+double stencil_spmm_bytes(int64_t n, int64_t nnz, int m) {
+    return 16.0 * static_cast<double>(n) * m + 8.0 * static_cast<double>(nnz) + 4.0 * static_cast<double>(n);
+}
+
+template <int BY>
+void launch_by(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y, const int* ctl) {
+    const StencilLayout& L = layout_for(ctx, a, BY);
+    const int kind = a->stencil->kind;
+    switch (m) {
+        case 8:
+            if (kind == 27) launch_one<8, 8, 27, BY>(ctx, a, L, x, y, ctl);
+            else launch_one<8, 8, 7, BY>(ctx, a, L, x, y, ctl);
+            break;
+        case 16:
+            if (kind == 27) launch_one<16, 16, 27, BY>(ctx, a, L, x, y, ctl);
+            else launch_one<16, 16, 7, BY>(ctx, a, L, x, y, ctl);
+            break;
+        case 32:
+            if (kind == 27) launch_one<32, 16, 27, BY>(ctx, a, L, x, y, ctl);
+            else launch_one<32, 16, 7, BY>(ctx, a, L, x, y, ctl);
+            break;
+        default:
+            throw Invalid("stencil SpMM: m must be 8, 16 or 32");
+    }
+}
+
+int launch_stencil_spmm(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y, const int* ctl) {
+    static const int by = env_int("MBG_STENCIL_BY", 4);
+    if (by == 2) launch_by<2>(ctx, a, m, x, y, ctl);
+    else launch_by<4>(ctx, a, m, x, y, ctl);
+    return 1;
+}
+
+}  // namespace mbg

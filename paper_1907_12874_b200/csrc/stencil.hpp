@@ -1,0 +1,50 @@
+// stencil.hpp -- structured-grid SpMM (stencil.cu).
+//
+// When the caller declares the grid (mbg_csr_set_grid) and every nonzero of
+// the CSR couples a point with one of its 26 grid neighbours (or itself), the
+// operator gets a stencil twin: per xy-tile plane a chunk of values laid out
+// slot-major plus a per-row slot mask.  Column indices are then implicit, so
+// the SpMM streams 8 B per nonzero instead of 12 (+4 B/row mask instead of
+// the 4 B/row offsets) and stages x as TMA tensor boxes of grid planes in
+// shared memory.  Each (row, column) is still summed in CSR order from 0.0
+// (ascending column == ascending slot on a grid), so results are bitwise
+// those of the CSR SpMM (spmv.cpp:40-46).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "common.hpp"
+
+namespace mbg {
+
+constexpr int STENCIL_BX = 32;   // tile width along x (grid points)
+
+struct StencilLayout {
+    int by = 0;                     // tile height along y
+    int64_t chunk_bytes = 0;        // S * 32*by * 8 (values) + 32*by * 4 (masks)
+    DevBuf<unsigned char> chunks;   // [(tile * nz + z)] chunks
+};
+
+struct StencilOp {
+    int nx = 0, ny = 0, nz = 0;
+    int kind = 0;          // 7 (face neighbours only) or 27
+    int64_t nnz = 0;
+    std::vector<std::unique_ptr<StencilLayout>> layouts;   // built lazily per tile height
+};
+
+// Analyse the device CSR of `a` on the grid; returns nullptr when some
+// nonzero is not a grid neighbour (the CSR SpMM stays in use).
+std::shared_ptr<StencilOp> build_stencil(mbg_ctx* ctx, const mbg_csr* a, int nx, int ny, int nz);
+// True when the stencil SpMM handles m (and it is not disabled by MBG_STENCIL=0).
+bool stencil_handles(const mbg_csr* a, int m);
+// y = A x through the stencil twin; returns the number of kernel launches.
+int launch_stencil_spmm(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y, const int* ctl);
+// Algorithmic bytes of one stencil SpMM: x read once, y written once, 8 B per
+// nonzero value, 4 B per row mask.
+double stencil_spmm_bytes(int64_t n, int64_t nnz, int m);
+
+}  // namespace mbg

@@ -1,0 +1,123 @@
+"""GPU parity of the stencil SpMM (stencil.cu): operators declared on a grid
+(mbg_csr_set_grid) run with implicit columns and TMA-staged x planes; the
+result must be bit for bit the CSR oracle's (spmv.cpp:40-46 arithmetic), for
+full stencils, stencils with absent entries, partial tiles, special values,
+and whole solves."""
+import numpy as np
+import pytest
+
+import oracle_ctypes as O
+import paper_1907_12874_b200 as P
+from test_gpu_parity import assert_bitwise, to_prod
+
+pytestmark = pytest.mark.gpu
+
+GRIDS = {
+    # odd sizes: partial 32 x 4 tiles, short z ranges
+    "poisson7_37x19x11": ("poisson7", (37, 19, 11), 0),
+    "convdiff7_64x8x5": ("convdiff7", (64, 8, 5), 1),
+    "stencil27_33x10x7": ("stencil27", (33, 10, 7), 2),
+    "stencil27_3x3x3": ("stencil27", (3, 3, 3), 2),
+    "convdiff7_1x1x40": ("convdiff7", (1, 1, 40), 1),
+}
+
+
+def grid_matrix(name):
+    kind, dims, seed = GRIDS[name]
+    return O.gen_stencil(kind, *dims, seed=seed), dims, (27 if kind == "stencil27" else 7)
+
+
+@pytest.mark.parametrize("name", list(GRIDS))
+@pytest.mark.parametrize("m", [8, 16, 32])
+def test_stencil_spmv_bitwise(ctx, name, m):
+    a, dims, kind = grid_matrix(name)
+    d = ctx.upload(to_prod(a))
+    d.set_grid(*dims)
+    assert d.stencil_kind == kind
+    x = np.random.default_rng(m).standard_normal(a.n * m)
+    X, Y = ctx.multivector(a.n, m, x), ctx.multivector(a.n, m)
+    P.spmv(ctx, d, X, Y)
+    assert_bitwise(Y.download(), O.spmv(a, x, m), f"stencil spmv {name} m={m}")
+
+
+def drop_entries(a: O.Csr, every: int) -> O.Csr:
+    """Remove every `every`-th off-diagonal nonzero (absent slots inside the grid)."""
+    off, cols, vals = [0], [], []
+    k = 0
+    for i in range(a.n):
+        for q in range(a.off[i], a.off[i + 1]):
+            k += 1
+            if a.col[q] != i and k % every == 0:
+                continue
+            cols.append(a.col[q])
+            vals.append(a.val[q])
+        off.append(len(cols))
+    return O.Csr(a.n, np.array(off), np.array(cols, np.int32), np.array(vals))
+
+
+@pytest.mark.parametrize("kind,dims", [("stencil27", (40, 9, 6)), ("convdiff7", (40, 9, 6))])
+def test_stencil_absent_slots(ctx, kind, dims):
+    a = drop_entries(O.gen_stencil(kind, *dims, seed=3), 5)
+    d = ctx.upload(to_prod(a))
+    d.set_grid(*dims)
+    assert d.stencil_kind in (7, 27)
+    for m in (8, 16, 32):
+        x = np.random.default_rng(11).standard_normal(a.n * m)
+        X, Y = ctx.multivector(a.n, m, x), ctx.multivector(a.n, m)
+        P.spmv(ctx, d, X, Y)
+        assert_bitwise(Y.download(), O.spmv(a, x, m), f"absent slots {kind} m={m}")
+
+
+def test_stencil_special_values(ctx):
+    # -0.0 sums, infinities and NaNs must propagate exactly as in CSR order
+    a = O.gen_stencil("stencil27", 34, 6, 5, seed=2)
+    m = 8
+    x = np.random.default_rng(5).standard_normal(a.n * m)
+    x[::97] = -0.0
+    x[5 * m + 3] = np.inf
+    x[77 * m + 1] = -np.inf
+    x[301 * m + 6] = np.nan
+    x[900 * m:901 * m] = 1e308
+    d = ctx.upload(to_prod(a))
+    d.set_grid(34, 6, 5)
+    X, Y = ctx.multivector(a.n, m, x), ctx.multivector(a.n, m)
+    P.spmv(ctx, d, X, Y)
+    got, want = Y.download(), O.spmv(a, x, m)
+    nan = np.isnan(want)
+    assert np.array_equal(np.isnan(got), nan)
+    assert_bitwise(got[~nan], want[~nan], "special values")
+
+
+def test_stencil_rejects_non_grid(ctx):
+    a = O.gen_banded(4096, 200, 4, 8, 4)
+    d = ctx.upload(to_prod(a))
+    d.set_grid(16, 16, 16)
+    assert d.stencil_kind == 0
+    # a 7-point operator declared on the wrong grid is no stencil either
+    b = O.gen_stencil("poisson7", 8, 8, 8)
+    e = ctx.upload(to_prod(b))
+    e.set_grid(16, 4, 8)
+    assert e.stencil_kind == 0
+    m = 8
+    x = np.random.default_rng(1).standard_normal(b.n * m)
+    X, Y = ctx.multivector(b.n, m, x), ctx.multivector(b.n, m)
+    P.spmv(ctx, e, X, Y)
+    assert_bitwise(Y.download(), O.spmv(b, x, m), "wrong grid -> CSR path")
+
+
+@pytest.mark.parametrize("method,form", [("bicgstab", "fused"), ("rbicgstab", "fused"), ("pipebicgstab", "merged"),
+                                         ("pbicgstab", "fused"), ("ibicgstab", "merged")])
+@pytest.mark.parametrize("kind,dims,m", [("convdiff7", (36, 9, 8), 8), ("stencil27", (20, 12, 9), 16),
+                                         ("convdiff7", (33, 5, 6), 32)])
+def test_stencil_solve_bitwise(ctx, method, form, kind, dims, m):
+    a = O.gen_stencil(kind, *dims, seed=2)
+    b = O.rhs(a.n, m, 3)
+    want = O.solve(a, b, m, method, form, 1e-8, maxit=400)
+    d = ctx.upload(to_prod(a))
+    d.set_grid(*dims)
+    assert d.stencil_kind in (7, 27)
+    B, X = ctx.multivector(a.n, m, b), ctx.multivector(a.n, m)
+    rep = P.solve(ctx, d, B, X, method, form, 1e-8, max_iters=400)
+    assert rep.iterations == want["iterations"]
+    assert_bitwise(rep.residual_history, want["hist"], f"{method} history")
+    assert_bitwise(X.download(), want["x"], f"{method} x")
