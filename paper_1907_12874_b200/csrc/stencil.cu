@@ -144,6 +144,7 @@ struct StencilGeom {
     int nranges;          // step ranges (persistent blocks per column half)
     int pd;               // L2 prefetch distance in steps beyond the rings (0: none)
     unsigned long long* trace;   // lab: per block (smid, t0, t1) when non-null (MBG_STENCIL_TRACE)
+    int trigger;          // call griddepcontrol.launch_dependents (else dependents start at exit)
     int mode;             // lab switch (MBG_STENCIL_MODE): 0 normal, 1 no arithmetic, 2 no data movement
     const unsigned char* chunks;
     int64_t chunk_bytes;
@@ -343,7 +344,7 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
                 s += steps;
             }
         }
-        pdl_trigger();
+        if (g.trigger) pdl_trigger();
         return;
     }
 
@@ -408,7 +409,7 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
         Q += steps + 2;
         s += steps;
     }
-    pdl_trigger();
+    if (g.trigger) pdl_trigger();
     if (g.trace) {
         __syncwarp();
         if (tid == 0) {
@@ -515,6 +516,8 @@ void launch_one(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const do
     gm.chunk_bytes = L.chunk_bytes;
     static const int mode = env_int("MBG_STENCIL_MODE", 0);
     gm.mode = mode;
+    static const int trig = env_int("MBG_STENCIL_TRIGGER", 0);
+    gm.trigger = trig;
     static const int pd = env_int("MBG_STENCIL_PD", 0);
     gm.pd = pd;
     // persistent grid: every resident slot gets an equal share of the steps
@@ -527,8 +530,14 @@ void launch_one(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const do
         tbuf.ensure(static_cast<size_t>(grid) * 3);
         gm.trace = tbuf.p;
     }
-    launch_pdl(stencil_spmm_kernel<MT, MC, ST, BY>, dim3(grid), dim3(threads), static_cast<size_t>(smem),
-               ctx->stream, tm, gm, y, ctl);
+    static const int spdl = env_int("MBG_STENCIL_PDL", 1);
+    if (spdl) {
+        launch_pdl(stencil_spmm_kernel<MT, MC, ST, BY>, dim3(grid), dim3(threads), static_cast<size_t>(smem),
+                   ctx->stream, tm, gm, y, ctl);
+    } else {
+        stencil_spmm_kernel<MT, MC, ST, BY><<<grid, threads, smem, ctx->stream>>>(tm, gm, y, ctl);
+        MBG_CUDA(cudaGetLastError());
+    }
     if (trace) {   // lab: dump (block, smid, start ns, end ns) of this launch
         std::vector<unsigned long long> h(static_cast<size_t>(grid) * 3);
         MBG_CUDA(cudaStreamSynchronize(ctx->stream));
