@@ -115,7 +115,7 @@ int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, 
         return r;
     };
     if (a->peers.empty()) {
-        if ((!epi || epi->kind == 0) && stencil_handles(a, m)) return launch_stencil_spmm(ctx, a, m, x, y, ctl);
+        if (stencil_handles(a, m)) return launch_stencil_spmm(ctx, a, m, x, y, ctl, epi);
         return launch_spmm(ctx->stream, tiles(a->tiles_all, a->long_all, a->stiles_all, a->umeta_all, a->ucols_all, a->lcol_all), a->n, nullptr, a->off.p, a->col.p, a->val.p, m, x,
                            y, ctl, ctx->num_sms, epi);
     }

@@ -429,16 +429,23 @@ struct minblocks_of<P, decltype(void(P::MINB))> { static constexpr int value = P
 // integer atomics -- so no partial buffer and no fold kernel are needed; the
 // scalar kernel rounds the slot directly.
 // ---------------------------------------------------------------------------
-template <int NX, class SlotOf>
+struct SyncBlock {
+    __device__ void operator()() const { __syncthreads(); }
+};
+// nthreads < 0: the whole block; else the first nthreads threads (a power-of-two
+// number of warps), synchronised by `sync` (e.g. a named barrier)
+template <int NX, class SlotOf, class Sync = SyncBlock>
 __device__ __forceinline__ void block_combine(double (&acc)[NX][KEXP], int classes, SlotOf slot_of,
-                                              double* sh /* blockDim * KEXP doubles */) {
+                                              double* sh /* blockDim * KEXP doubles */, Sync sync = Sync(),
+                                              int nthreads = -1) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nthr = nthreads < 0 ? static_cast<int>(blockDim.x) : nthreads;
     const int k = tid % classes;
 #pragma unroll
     for (int x = 0; x < NX; ++x) {
         double (&mine)[KEXP] = acc[x];
         int64_t* slot = slot_of(x, k);
-        if (classes <= 32 && (32 % classes) == 0 && (blockDim.x & 31) == 0) {
+        if (classes <= 32 && (32 % classes) == 0 && (nthr & 31) == 0) {
             for (int off = 16; off >= classes; off >>= 1) {
                 double t[KEXP];
 #pragma unroll
@@ -448,12 +455,12 @@ __device__ __forceinline__ void block_combine(double (&acc)[NX][KEXP], int class
                     for (int i = 0; i < KEXP; ++i) grow(mine, t[i], slot);
                 }
             }
-            const int nw = blockDim.x >> 5;
+            const int nw = nthr >> 5;
             if (lane < classes) {
 #pragma unroll
                 for (int i = 0; i < KEXP; ++i) sh[(warp * 32 + lane) * KEXP + i] = mine[i];
             }
-            __syncthreads();
+            sync();
             for (int s = nw >> 1; s >= 1; s >>= 1) {
                 if (warp < s && lane < classes) {
 #pragma unroll
@@ -461,27 +468,27 @@ __device__ __forceinline__ void block_combine(double (&acc)[NX][KEXP], int class
 #pragma unroll
                     for (int i = 0; i < KEXP; ++i) sh[(warp * 32 + lane) * KEXP + i] = mine[i];
                 }
-                __syncthreads();
+                sync();
             }
         } else {
 #pragma unroll
             for (int i = 0; i < KEXP; ++i) sh[tid * KEXP + i] = mine[i];
-            __syncthreads();
-            for (int s = (blockDim.x / classes) >> 1; s >= 1; s >>= 1) {
+            sync();
+            for (int s = (nthr / classes) >> 1; s >= 1; s >>= 1) {
                 if (tid < s * classes) {
 #pragma unroll
                     for (int i = 0; i < KEXP; ++i) grow(mine, sh[(tid + s * classes) * KEXP + i], slot);
 #pragma unroll
                     for (int i = 0; i < KEXP; ++i) sh[tid * KEXP + i] = mine[i];
                 }
-                __syncthreads();
+                sync();
             }
         }
         if (tid < classes) {
 #pragma unroll
             for (int i = 0; i < KEXP; ++i) digits_add_atomic(slot, mine[i]);
         }
-        __syncthreads();
+        sync();
     }
 }
 

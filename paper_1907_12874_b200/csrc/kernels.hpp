@@ -35,6 +35,7 @@ struct SpmmTiles {
 //   kind 1: slot[0] += exact (y, aux)                    e.g. delta = (v, r0)
 //   kind 2: slot[0..2] += exact (y, x), (y, y), (x, x)    phi, psi, theta of Alg. 2
 //   kind 3: slot[0] += exact (y, y)                       e.g. psi = (t, t)
+//   kind 4: slot[0..1] += exact (y, x), (y, y)            phi, psi of Alg. 2 (stencil SpMM only)
 struct SpmmEpi {
     int kind = 0;
     const double* aux = nullptr;

@@ -92,8 +92,8 @@ Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulatio
     // nonzeros per row the gather-bound SpMM loses more to the epilogue's
     // registers than the separate 2-vector dot pass costs (B200: C3 27-point
     // 8.90 vs 8.07 ms/iteration, C5 m=8 5.28 vs 4.97; C2 7-point 0.76 vs 0.84)
-    // (the stencil SpMM has no epilogue)
-    epi_delta_ = formulation == MBG_FUSED && a->nnz <= 12 * a->n && !stencil_;
+    // (stencil SpMM: only with MBG_STENCIL_EPI=1 -- measured slower)
+    epi_delta_ = formulation == MBG_FUSED && (stencil_ ? stencil_epilogues() : a->nnz <= 12 * a->n);
     if (method == MBG_IBICGSTAB) {
         if (!a->peers.empty() || a->n_halo)
             throw Invalid("solve: IBiCGStab needs f0 = A^T r0, supported on a single GPU only");
@@ -198,7 +198,7 @@ void Solver::spmm(const double* x, double* y, int epi_kind, const double* aux, i
     e.aux = aux;
     for (int d = 0; d < 3; ++d) e.slot[d] = slot(first_slot + d);
     const double extra = epi_kind == 1 ? 8.0 * len_ : 0.0;   // aux vector read
-    mark_begin(epi_kind ? "spmm+dots" : "spmm",
+    mark_begin(epi_kind ? "spmm+dots" + std::to_string(epi_kind) : std::string("spmm"),
                (stencil_ ? stencil_spmm_bytes(a_->n, a_->nnz, m_) : spmv_compulsory_bytes(a_->n, a_->nnz, m_)) +
                    extra);
     launches_ += apply_operator(ctx_, a_, m_, const_cast<double*>(x), y, ctl_.p, epi_kind ? &e : nullptr);
@@ -376,10 +376,17 @@ void Solver::iteration() {
     double *r = w(V_R), *r0 = w(V_R0), *x = x_;
     if (method_ == MBG_BICGSTAB) {
         double *p = w(V_P), *v = w(V_V), *s = w(V_S), *t = w(V_T);
-        if (fused) {
+        if (fused && stencil_ && stencil_epilogues()) {
+            // stencil SpMM (registers to spare; x of the row staged in shared
+            // memory): delta = (v, r0) and phi = (t, s), psi = (t, t) in the SpMM
+            // epilogues, theta where s is produced -- 15 vector transfers
+            spmm(p, v, 1, r0, P_C_ALPHA, 1, 0, 1);                          // v ; delta -> slot 0 ; alpha
+            group<PUpd2Sq>({r, v}, {s}, {S_ONE, S_NALPHA}, 2, -1, 0, 0);   // s ; theta = (s,s) -> slot 2
+            spmm(s, t, 4, nullptr, P_C_OMEGA, 3, 0, 3);                    // t ; phi psi -> slots 0,1 ; omega
+        } else if (fused) {
             // theta computed where s is produced (spreads the exact-dot work over
             // two passes); delta and phi/psi stay in their own passes: fusing
-            // them into the SpMM epilogue costs the SpMM more than it saves
+            // them into the CSR SpMM epilogue costs the SpMM more than it saves
             // (measured on B200)
             spmm(p, v);
             group<PDot2>({v, r0}, {}, {}, 0, P_C_ALPHA, 1);
@@ -681,12 +688,17 @@ void Solver::report(double* hist_host, mbg_report* rep) {
     // TrafficCounter semantics: the preconditioner's transfers are tallied too
     // (alpha/2 reads + alpha/2 writes per application)
     if (method_ == MBG_RBICGSTAB && form_ == MBG_FUSED && !epi_delta_) reads += 1;   // delta pass: v, r0 vs aux r0
+    // classical fused on the stencil SpMM: delta pass (v, r0) -> aux r0 in the
+    // SpMM epilogue; phi/psi pass (t, s) -> the second SpMM's epilogue
+    const int classic_epi = (method_ == MBG_BICGSTAB && form_ == MBG_FUSED && stencil_ && stencil_epilogues()) ? 3 : 0;
+    reads -= classic_epi;
     rep->vector_reads = static_cast<int64_t>(reads + apps * pa_ / 2) * its;
     rep->vector_writes = static_cast<int64_t>(writes + apps * pa_ / 2) * its;
     rep->spmv_bytes = static_cast<double>(spmvs) * its * spmv_traffic_bytes(a_->n, a_->nnz, m_);
     rep->compulsory_bytes =
         (iteration_bytes(method_, form_, pa_, a_->n, a_->nnz, m_) +
          ((method_ == MBG_RBICGSTAB && form_ == MBG_FUSED && !epi_delta_) ? 8.0 * static_cast<double>(len_) : 0.0) -
+         8.0 * classic_epi * static_cast<double>(len_) -
          // stencil SpMM: no column indices (8 B instead of 12 B per nonzero)
          (stencil_ ? 4.0 * spmvs * static_cast<double>(a_->nnz) : 0.0)) *
         its;

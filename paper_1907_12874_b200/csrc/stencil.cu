@@ -34,6 +34,7 @@
 #include "comm.hpp"
 #include "common.hpp"
 #include "exact.cuh"
+#include "group.cuh"
 #include "kernels.hpp"
 #include "stencil.hpp"
 #include "tma.cuh"
@@ -141,7 +142,9 @@ struct StencilGeom {
     int nx, ny, nz;
     int ntx;              // tiles along x
     int64_t steps;        // tile-planes per column half: ntiles * nz
-    int nranges;          // step ranges (persistent blocks per column half)
+    int nranges;          // step ranges (blocks per column half)
+    int kt;               // whole tiles per range (kt >= 1, zseg == nz) ...
+    int zseg;             // ... or one z-segment of zseg planes of one tile per range (kt == 0)
     int pd;               // L2 prefetch distance in steps beyond the rings (0: none)
     unsigned long long* trace;   // lab: per block (smid, t0, t1) when non-null (MBG_STENCIL_TRACE)
     int trigger;          // call griddepcontrol.launch_dependents (else dependents start at exit)
@@ -264,10 +267,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // never wait on each other.  MT: columns of the block vector; MC: columns of
 // one block (MT / MC column halves run as adjacent blocks over the same
 // range, so the second read of a value chunk hits L2).
-template <int MT, int MC, int ST, int BY>
+// EPI (kernels.hpp SpmmEpi kinds): 0 none; 1 (y, aux); 2 (y, x), (y, y),
+// (x, x); 3 (y, y); 4 (y, x), (y, y) -- exact dots of the finished rows, x
+// being the SpMM input at the row itself (the centre point of the staged plane).
+template <int EPI>
+struct StencilEpiDots {
+    static constexpr int value = EPI == 2 ? 3 : (EPI == 4 ? 2 : 1);
+};
+
+template <int MT, int MC, int ST, int BY, int EPI>
 __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
     stencil_spmm_kernel(const __grid_constant__ CUtensorMap xmap, StencilGeom g, double* __restrict__ y,
-                        const int* __restrict__ ctl) {
+                        const int* __restrict__ ctl, SpmmEpi epi) {
     using SH = StencilShape<MC, BY>;
     constexpr int CS = MT / MC;
     constexpr int XR = STENCIL_XR, VR = STENCIL_VR;
@@ -286,7 +297,19 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
 
     const int h = blockIdx.x % CS;
     const int rb = blockIdx.x / CS;
-    const int64_t s0 = g.steps * rb / g.nranges, s1 = g.steps * (rb + 1) / g.nranges;
+    // ranges move through z in lockstep (every range starts at the same z), so
+    // a plane of x is read by all its neighbouring tiles at about the same time
+    int64_t s0, s1;
+    if (g.kt > 0) {
+        s0 = static_cast<int64_t>(rb) * g.kt * g.nz;
+        s1 = s0 + static_cast<int64_t>(g.kt) * g.nz;
+    } else {
+        const int nseg = (g.nz + g.zseg - 1) / g.zseg;
+        const int t = rb / nseg, sg = rb % nseg;
+        s0 = static_cast<int64_t>(t) * g.nz + static_cast<int64_t>(sg) * g.zseg;
+        s1 = static_cast<int64_t>(t) * g.nz + min(g.nz, (sg + 1) * g.zseg);
+    }
+    if (s1 > g.steps) s1 = g.steps;
     const int tid = threadIdx.x;
     if (tid == 0) {
         for (int b = 0; b < XR; ++b) {
@@ -360,6 +383,16 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
         gy = (warp >> 1) * 2 + (gl >> 2);
     }
     const int lx0 = gx * 4, cp = cl * 2, r0 = gy * STENCIL_BX + lx0;
+    // one expansion per (dot, column); (one per row of the lane's 4 as well
+    // -- independent chains -- was measured slower: 226 registers, 1 block/SM)
+    constexpr int ND = StencilEpiDots<EPI>::value;
+    constexpr int NEX = EPI ? ND * 2 : 1;
+    double ex[NEX][KEXP];
+#pragma unroll
+    for (int q = 0; q < NEX; ++q)
+#pragma unroll
+        for (int i = 0; i < KEXP; ++i) ex[q][i] = 0.0;
+    const int col0 = h * MC + cp;   // this lane's first column
     int64_t Q = 0, j = 0;
     for (int64_t s = s0; s < s1;) {
         const int t = static_cast<int>(s / g.nz), za = static_cast<int>(s % g.nz);
@@ -376,6 +409,17 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
             const double* P0 = xr + ((Q + i) % XR) * SH::PLANE;
             const double* P1 = xr + ((Q + i + 1) % XR) * SH::PLANE;
             const double* P2 = xr + ((Q + i + 2) % XR) * SH::PLANE;
+            // epilogue operand (y, aux): issued before the arithmetic so its
+            // latency hides behind it
+            double2 axs[4];
+            if constexpr (EPI == 1) {
+                const int64_t rowz = (static_cast<int64_t>(za + i) * g.ny + yg) * g.nx;
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    axs[r] = (yok && xg0 + r < g.nx)
+                                 ? __ldg(reinterpret_cast<const double2*>(epi.aux + (rowz + xg0 + r) * MT + col0))
+                                 : make_double2(0.0, 0.0);
+            }
             const unsigned char* ch = vr + (j % VR) * CB;
             const double* V = reinterpret_cast<const double*>(ch);
             const uint4 m4 = *reinterpret_cast<const uint4*>(ch + ST * SH::RT * 8 + r0 * 4);
@@ -397,9 +441,32 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
                 const int64_t rowz = (static_cast<int64_t>(za + i) * g.ny + yg) * g.nx;
 #pragma unroll
                 for (int r = 0; r < 4; ++r)
-                    if (xg0 + r < g.nx)
-                        *reinterpret_cast<double2*>(y + (rowz + xg0 + r) * MT + h * MC + cp) =
-                            make_double2(acc[r][0], acc[r][1]);
+                    if (xg0 + r < g.nx) {
+                        const int64_t e = (rowz + xg0 + r) * MT + col0;
+                        *reinterpret_cast<double2*>(y + e) = make_double2(acc[r][0], acc[r][1]);
+                        if constexpr (EPI != 0) {
+                            double2 xs = make_double2(0.0, 0.0);
+                            if constexpr (EPI == 1)
+                                xs = axs[r];
+                            else if constexpr (EPI == 2 || EPI == 4)
+                                xs = *reinterpret_cast<const double2*>(P1 + ((gy + 1) * SH::LW + lx0 + r + 1) * MC + cp);
+#pragma unroll
+                            for (int c = 0; c < 2; ++c) {
+                                const double yv = acc[r][c], xv = c ? xs.y : xs.x;
+                                int64_t* s0p = epi.slot[0] + static_cast<int64_t>(col0 + c) * NSLOT;
+                                // expansion index: dot * 2 + column
+                                if constexpr (EPI == 1 || EPI == 2 || EPI == 4)
+                                    grow(ex[c], __dmul_rn(yv, xv), s0p);
+                                if constexpr (EPI == 3) grow(ex[c], __dmul_rn(yv, yv), s0p);
+                                if constexpr (EPI == 2 || EPI == 4)
+                                    grow(ex[2 + c], __dmul_rn(yv, yv),
+                                         epi.slot[1] + static_cast<int64_t>(col0 + c) * NSLOT);
+                                if constexpr (EPI == 2)
+                                    grow(ex[4 + c], __dmul_rn(xv, xv),
+                                         epi.slot[2] + static_cast<int64_t>(col0 + c) * NSLOT);
+                            }
+                        }
+                    }
             }
         }
         if (lane == 0 && g.mode != 2) {   // the segment's last two planes
@@ -410,6 +477,21 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
         s += steps;
     }
     if (g.trigger) pdl_trigger();
+    if constexpr (EPI != 0) {
+        // every load was consumed: the x ring is free scratch for the combine
+        // (compute warps only: named barrier 1 over SH::THREADS threads)
+        struct SyncCompute {
+            __device__ void operator()() const {
+                asm volatile("bar.sync 1, %0;" ::"n"(SH::THREADS) : "memory");
+            }
+        };
+        SyncCompute{}();   // every compute warp is done reading the rings
+        block_combine<ND * 2>(ex, SH::LPR,
+                              [&](int q, int k) {
+                                  return epi.slot[q / 2] + static_cast<int64_t>(h * MC + k * 2 + q % 2) * NSLOT;
+                              },
+                              xr, SyncCompute{}, SH::THREADS);
+    }
     if (g.trace) {
         __syncwarp();
         if (tid == 0) {
@@ -477,18 +559,18 @@ StencilLayout& layout_for(mbg_ctx* ctx, const mbg_csr* a, int by) {
     return *op.layouts.back();
 }
 
-template <int MT, int MC, int ST, int BY>
+template <int MT, int MC, int ST, int BY, int EPI>
 void launch_one(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const double* x, double* y,
-                const int* ctl) {
+                const int* ctl, const SpmmEpi& epi) {
     const StencilOp& op = *a->stencil;
     constexpr int smem = stencil_smem<MC, ST, BY>();
     constexpr int threads = StencilShape<MC, BY>::THREADS + 32;   // + producer warp
     constexpr int CS = MT / MC;
     static int occ = -1;
     if (occ < 0) {
-        MBG_CUDA(cudaFuncSetAttribute(stencil_spmm_kernel<MT, MC, ST, BY>,
+        MBG_CUDA(cudaFuncSetAttribute(stencil_spmm_kernel<MT, MC, ST, BY, EPI>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        MBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil_spmm_kernel<MT, MC, ST, BY>, threads,
+        MBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil_spmm_kernel<MT, MC, ST, BY, EPI>, threads,
                                                                smem));
         if (occ < 1) occ = 1;
     }
@@ -522,7 +604,19 @@ void launch_one(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const do
     gm.pd = pd;
     // persistent grid: every resident slot gets an equal share of the steps
     const int64_t slots = static_cast<int64_t>(occ) * ctx->num_sms / CS;
-    gm.nranges = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(slots, gm.steps)));
+    // work split: whole tiles per block when there are at least as many tiles
+    // as block slots, else every tile cut into equal z-segments
+    const int64_t ntiles = gm.steps / op.nz;
+    if (ntiles >= slots) {
+        gm.kt = static_cast<int>((ntiles + slots - 1) / slots);
+        gm.zseg = op.nz;
+        gm.nranges = static_cast<int>((ntiles + gm.kt - 1) / gm.kt);
+    } else {
+        const int k = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(slots / ntiles, op.nz)));
+        gm.kt = 0;
+        gm.zseg = (op.nz + k - 1) / k;
+        gm.nranges = static_cast<int>(ntiles * ((op.nz + gm.zseg - 1) / gm.zseg));
+    }
     const int grid = gm.nranges * CS;
     static const int trace = env_int("MBG_STENCIL_TRACE", 0);
     static DevBuf<unsigned long long> tbuf;
@@ -532,10 +626,10 @@ void launch_one(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const do
     }
     static const int spdl = env_int("MBG_STENCIL_PDL", 1);
     if (spdl) {
-        launch_pdl(stencil_spmm_kernel<MT, MC, ST, BY>, dim3(grid), dim3(threads), static_cast<size_t>(smem),
-                   ctx->stream, tm, gm, y, ctl);
+        launch_pdl(stencil_spmm_kernel<MT, MC, ST, BY, EPI>, dim3(grid), dim3(threads), static_cast<size_t>(smem),
+                   ctx->stream, tm, gm, y, ctl, epi);
     } else {
-        stencil_spmm_kernel<MT, MC, ST, BY><<<grid, threads, smem, ctx->stream>>>(tm, gm, y, ctl);
+        stencil_spmm_kernel<MT, MC, ST, BY, EPI><<<grid, threads, smem, ctx->stream>>>(tm, gm, y, ctl, epi);
         MBG_CUDA(cudaGetLastError());
     }
     if (trace) {   // lab: dump (block, smid, start ns, end ns) of this launch
@@ -573,6 +667,11 @@ std::shared_ptr<StencilOp> build_stencil(mbg_ctx* ctx, const mbg_csr* a, int nx,
     return op;
 }
 
+bool stencil_epilogues() {
+    static const bool on = env_int("MBG_STENCIL_EPI", 0) != 0;
+    return on;
+}
+
 bool stencil_handles(const mbg_csr* a, int m) {
     return a && a->stencil && stencil_enabled() && (m == 8 || m == 16 || m == 32);
 }
@@ -581,32 +680,46 @@ double stencil_spmm_bytes(int64_t n, int64_t nnz, int m) {
     return 16.0 * static_cast<double>(n) * m + 8.0 * static_cast<double>(nnz) + 4.0 * static_cast<double>(n);
 }
 
+template <int MT, int MC, int ST, int BY>
+void launch_epi(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const double* x, double* y, const int* ctl,
+                const SpmmEpi* epi) {
+    const SpmmEpi none{};
+    switch (epi ? epi->kind : 0) {
+        case 0: launch_one<MT, MC, ST, BY, 0>(ctx, a, L, x, y, ctl, none); break;
+        case 1: launch_one<MT, MC, ST, BY, 1>(ctx, a, L, x, y, ctl, *epi); break;
+        case 2: launch_one<MT, MC, ST, BY, 2>(ctx, a, L, x, y, ctl, *epi); break;
+        case 3: launch_one<MT, MC, ST, BY, 3>(ctx, a, L, x, y, ctl, *epi); break;
+        case 4: launch_one<MT, MC, ST, BY, 4>(ctx, a, L, x, y, ctl, *epi); break;
+        default: throw Invalid("stencil SpMM: unknown epilogue kind");
+    }
+}
+
 template <int BY>
-void launch_by(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y, const int* ctl) {
+void launch_by(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y, const int* ctl,
+               const SpmmEpi* epi) {
     const StencilLayout& L = layout_for(ctx, a, BY);
     const int kind = a->stencil->kind;
     switch (m) {
         case 8:
-            if (kind == 27) launch_one<8, 8, 27, BY>(ctx, a, L, x, y, ctl);
-            else launch_one<8, 8, 7, BY>(ctx, a, L, x, y, ctl);
+            if (kind == 27) launch_epi<8, 8, 27, BY>(ctx, a, L, x, y, ctl, epi);
+            else launch_epi<8, 8, 7, BY>(ctx, a, L, x, y, ctl, epi);
             break;
         case 16:
-            if (kind == 27) launch_one<16, 16, 27, BY>(ctx, a, L, x, y, ctl);
-            else launch_one<16, 16, 7, BY>(ctx, a, L, x, y, ctl);
+            if (kind == 27) launch_epi<16, 16, 27, BY>(ctx, a, L, x, y, ctl, epi);
+            else launch_epi<16, 16, 7, BY>(ctx, a, L, x, y, ctl, epi);
             break;
         case 32:
-            if (kind == 27) launch_one<32, 16, 27, BY>(ctx, a, L, x, y, ctl);
-            else launch_one<32, 16, 7, BY>(ctx, a, L, x, y, ctl);
+            if (kind == 27) launch_epi<32, 16, 27, BY>(ctx, a, L, x, y, ctl, epi);
+            else launch_epi<32, 16, 7, BY>(ctx, a, L, x, y, ctl, epi);
             break;
         default:
             throw Invalid("stencil SpMM: m must be 8, 16 or 32");
     }
 }
 
-int launch_stencil_spmm(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y, const int* ctl) {
-    static const int by = env_int("MBG_STENCIL_BY", 4);
-    if (by == 2) launch_by<2>(ctx, a, m, x, y, ctl);
-    else launch_by<4>(ctx, a, m, x, y, ctl);
+int launch_stencil_spmm(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y, const int* ctl,
+                        const SpmmEpi* epi) {
+    launch_by<4>(ctx, a, m, x, y, ctl, epi);
     return 1;
 }
 

@@ -41,8 +41,16 @@ struct StencilOp {
 std::shared_ptr<StencilOp> build_stencil(mbg_ctx* ctx, const mbg_csr* a, int nx, int ny, int nz);
 // True when the stencil SpMM handles m (and it is not disabled by MBG_STENCIL=0).
 bool stencil_handles(const mbg_csr* a, int m);
+// MBG_STENCIL_EPI=1: the solver moves exact dots into the stencil SpMM's
+// epilogue (classical delta, phi/psi; Reordered delta).  Measured slower on
+// B200 (the TwoSum chains of the epilogue are latency-bound at the stencil
+// kernel's 8-10 warps per SM), hence off by default.
+bool stencil_epilogues();
 // y = A x through the stencil twin; returns the number of kernel launches.
-int launch_stencil_spmm(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y, const int* ctl);
+// epi: optional fused exact-dot epilogue (kernels.hpp SpmmEpi, kinds 1-4).
+struct SpmmEpi;
+int launch_stencil_spmm(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y, const int* ctl,
+                        const SpmmEpi* epi = nullptr);
 // Algorithmic bytes of one stencil SpMM: x read once, y written once, 8 B per
 // nonzero value, 4 B per row mask.
 double stencil_spmm_bytes(int64_t n, int64_t nnz, int m);

@@ -121,3 +121,48 @@ def test_stencil_solve_bitwise(ctx, method, form, kind, dims, m):
     assert rep.iterations == want["iterations"]
     assert_bitwise(rep.residual_history, want["hist"], f"{method} history")
     assert_bitwise(X.download(), want["x"], f"{method} x")
+
+
+EPI_SCRIPT = r"""
+import sys
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import test_gpu_stencil as T, paper_1907_12874_b200 as P
+c = P.Context(0)
+for method in ("bicgstab", "rbicgstab"):
+    T.check_fused_multistep(c, method)
+print("ok")
+"""
+
+
+def test_stencil_fused_epilogues_opt_in():
+    # MBG_STENCIL_EPI=1 (read once per process): the dot epilogues of the
+    # stencil SpMM, bitwise vs the oracle over many planes per block
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    here = Path(__file__).resolve().parent
+    code = EPI_SCRIPT.format(root=str(here.parent), tests=str(here))
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "MBG_STENCIL_EPI": "1"},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("method", ["bicgstab", "rbicgstab"])
+def test_stencil_fused_epilogue_multistep(ctx, method):
+    check_fused_multistep(ctx, method)
+
+
+def check_fused_multistep(ctx, method):
+    # enough planes per block that warps drift apart (fused dot epilogues and
+    # the end-of-kernel combine must not race the last steps)
+    kind, dims, m = "convdiff7", (64, 64, 48), 8
+    a = O.gen_stencil(kind, *dims, seed=1)
+    b = O.rhs(a.n, m, 1)
+    want = O.solve(a, b, m, method, "fused", 1e-8, fixed=True, maxit=6)
+    d = ctx.upload(to_prod(a))
+    d.set_grid(*dims)
+    B, X = ctx.multivector(a.n, m, b), ctx.multivector(a.n, m)
+    rep = P.solve(ctx, d, B, X, method, "fused", 1e-8, fixed=True, max_iters=6)
+    assert_bitwise(rep.residual_history, want["hist"], f"{method} fused history")
+    assert_bitwise(X.download(), want["x"], f"{method} fused x")

@@ -18,6 +18,7 @@ ap.add_argument("--method", default="bicgstab")
 ap.add_argument("--formulation", default="merged")
 ap.add_argument("--iters", type=int, default=4)
 ap.add_argument("--seed", type=int, default=1)
+ap.add_argument("--hint", action="store_true", help="declare the grid (stencil twin)")
 args = ap.parse_args()
 
 g = args.grid
@@ -25,6 +26,8 @@ a = P.gen_stencil(args.kind, g, g, g, seed=args.seed) if args.kind != "banded" e
 b = P.gen_rhs(a.n_rows, args.m, args.seed)
 ctx = P.Context(0)
 d = ctx.upload(a)
+if args.hint and args.kind != "banded":
+    d.set_grid(g, g, g)
 B = ctx.multivector(a.n_rows, args.m, b)
 X = ctx.multivector(a.n_rows, args.m)
 rep = P.solve(ctx, d, B, X, args.method, args.formulation, fixed=True, max_iters=args.iters)
