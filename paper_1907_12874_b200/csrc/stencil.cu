@@ -166,12 +166,22 @@ struct StencilShape {
 template <int ST, int BY>
 __host__ __device__ constexpr int stencil_chunk_bytes() { return ST * STENCIL_BX * BY * 8 + STENCIL_BX * BY * 4; }
 
-constexpr int STENCIL_XR = 5, STENCIL_VR = 3;   // ring depths: x planes, value chunks
+#ifndef MBG_STENCIL_XR8
+#define MBG_STENCIL_XR8 5
+#define MBG_STENCIL_VR8 3
+#endif
+// ring depths (x planes, value chunks); m = 8 blocks may trade depth for occupancy
+template <int MC>
+struct StencilRings {
+    static constexpr int XR = MC == 8 ? MBG_STENCIL_XR8 : 5;
+    static constexpr int VR = MC == 8 ? MBG_STENCIL_VR8 : 3;
+};
 constexpr int STENCIL_HEAD = 256;               // mbarriers
 
 template <int MC, int ST, int BY>
 __host__ __device__ constexpr int stencil_smem() {
-    return STENCIL_HEAD + STENCIL_XR * StencilShape<MC, BY>::PLANE * 8 + STENCIL_VR * stencil_chunk_bytes<ST, BY>();
+    return STENCIL_HEAD + StencilRings<MC>::XR * StencilShape<MC, BY>::PLANE * 8 +
+           StencilRings<MC>::VR * stencil_chunk_bytes<ST, BY>();
 }
 
 // acc[r][c] += v * x: the reference's  acc = acc + val*x  (no FMA)
@@ -281,7 +291,7 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
                         const int* __restrict__ ctl, SpmmEpi epi) {
     using SH = StencilShape<MC, BY>;
     constexpr int CS = MT / MC;
-    constexpr int XR = STENCIL_XR, VR = STENCIL_VR;
+    constexpr int XR = StencilRings<MC>::XR, VR = StencilRings<MC>::VR;
     constexpr int CB = stencil_chunk_bytes<ST, BY>();
     pdl_wait();
     if (ctl && ctl[0]) return;
