@@ -219,11 +219,12 @@ def main():
         d = ctx.upload(a, bounds, rank)
     else:
         d = ctx.upload(a)
-        # structured-grid hint (mbg_csr_set_grid): the 7-point operator gets its
-        # stencil twin (implicit columns, TMA-staged x planes; bitwise the CSR result)
-        if not args.no_grid_hint:
-            d.set_grid(args.grid, args.grid, args.grid)
-    stencil = d.stencil_kind if world == 1 else 0
+    # structured-grid hint (mbg_csr_set_grid, global grid): the 7-point operator
+    # (each rank's z-slab of it) gets its stencil twin -- implicit columns,
+    # TMA-staged x planes, bitwise the CSR result
+    if not args.no_grid_hint:
+        d.set_grid(args.grid, args.grid, args.grid * world)
+    stencil = d.stencil_kind
     r0, r1 = d.row_begin, d.row_end
     b_loc = np.ascontiguousarray(b_full[r0 * m:r1 * m])
     B = ctx.multivector(d.n, m, b_loc)

@@ -98,12 +98,13 @@ int mbg_halo_plan(int64_t n, const int64_t* offsets, const int32_t* cols, const 
  * original summation order. */
 int mbg_csr_upload_any_order(mbg_ctx* ctx, int64_t n, const int64_t* offsets, const int32_t* cols,
                              const double* vals, mbg_csr** out);
-/* Structured-grid hint (rows = nx*ny*nz lexicographic points): for long-row
- * stencils (> 12 nonzeros per row, e.g. the 27-point C3 operator) the solver
- * then works on a brick-reordered copy P A P^T (8x8x4 bricks; each row keeps
- * its summation order) whose SpMM tiles have compact x neighbourhoods.  b and
- * x are gathered / scattered at solve entry / exit; results are bitwise
- * identical (exact dots).  Short-row operators are left as is.  Single GPU. */
+/* Structured-grid hint (rows = nx*ny*nz lexicographic points, the GLOBAL
+ * grid): an operator whose nonzeros all couple grid neighbours gets a stencil
+ * twin (see mbg_csr_stencil_kind); a z-slab partition (whole planes per rank,
+ * halo = the two neighbouring planes) gets one for its slab.  On one GPU,
+ * long-row stencils (> 12 nonzeros per row) also get a brick-reordered copy
+ * P A P^T (8x8x4 bricks; each row keeps its summation order) used for the m
+ * the stencil twin does not cover.  Results are bitwise identical (exact dots). */
 int mbg_csr_set_grid(mbg_ctx* ctx, mbg_csr* a, int nx, int ny, int nz);
 int mbg_csr_reordered(const mbg_csr* a);   /* 1 when the solver uses a reordered twin */
 /* Stencil twin built by mbg_csr_set_grid when every nonzero couples a grid

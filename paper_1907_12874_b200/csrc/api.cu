@@ -447,11 +447,12 @@ extern "C" int mbg_csr_set_grid(mbg_ctx* ctx, mbg_csr* a, int nx, int ny, int nz
     return guarded([&] {
         use(ctx);
         if (!a) throw Invalid("set_grid: null matrix");
-        if (nx < 1 || ny < 1 || nz < 1 || static_cast<int64_t>(nx) * ny * nz != a->n)
+        if (nx < 1 || ny < 1 || nz < 1 || static_cast<int64_t>(nx) * ny * nz != a->n_global)
             throw Invalid("set_grid: nx*ny*nz must equal the number of rows");
-        if (!a->peers.empty() || a->n_halo) throw Invalid("set_grid: single-GPU matrices only");
-        // stencil twin: implicit columns, x staged as TMA plane boxes (stencil.cu)
+        // stencil twin: implicit columns, x staged as TMA plane boxes (stencil.cu);
+        // a z-slab partition (whole planes per rank) gets one for its slab
         if (!a->stencil) a->stencil = build_stencil(ctx, a, nx, ny, nz);
+        if (!a->peers.empty() || a->n_halo) return;   // no reordered twin across ranks
         if (a->nnz <= 12 * a->n || a->reordered) return;
         const int bx = std::min(nx, 8), by = std::min(ny, 8), bz = std::min(nz, 4);
         const int64_t n = a->n;

@@ -184,6 +184,16 @@ int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, 
     }
     MBG_NCCL(ncclGroupEnd());
     }
+    if (stencil_handles(a, m)) {
+        // z-slab on the stencil twin: the interior planes overlap the
+        // exchange, the two face planes wait for the halo planes
+        const int nzl = a->stencil->nz;
+        launches += launch_stencil_spmm(ctx, a, m, x, y, ctl, epi, 1, nzl - 1);
+        side_to_main(ctx);
+        launches += launch_stencil_spmm(ctx, a, m, x, y, ctl, epi, 0, 1);
+        if (nzl > 1) launches += launch_stencil_spmm(ctx, a, m, x, y, ctl, epi, nzl - 1, nzl);
+        return launches;
+    }
     // interior rows overlap the exchange; boundary rows wait for the halo
     launches += launch_spmm(ctx->stream, tiles(a->tiles_interior, a->long_interior, a->stiles_interior, a->umeta_interior,
                                                       a->ucols_interior, a->lcol_split), a->n_interior, a->interior_rows.p, a->off.p,

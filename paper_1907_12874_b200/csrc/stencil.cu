@@ -59,17 +59,17 @@ __device__ __forceinline__ int face_slot(int dz, int dy, int dx) {
 
 // flags: 1 = a nonzero outside the 3x3x3 neighbourhood; 2 = a non-face
 // neighbour (27-point); 4 = slots not strictly ascending within a row
-__global__ void stencil_scan_kernel(int64_t n, int nx, int ny, const int32_t* __restrict__ off,
-                                    const int32_t* __restrict__ col, unsigned* flags) {
+__global__ void stencil_scan_kernel(GridMap gm, const int32_t* __restrict__ off, const int32_t* __restrict__ col,
+                                    unsigned* flags) {
     unsigned f = 0;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < gm.n_own;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         int xi, yi, zi;
-        grid_coords(i, nx, ny, xi, yi, zi);
+        grid_coords(gm.row_begin + i, gm.nx, gm.ny, xi, yi, zi);
         int prev = -1;
         for (int k = off[i]; k < off[i + 1]; ++k) {
             int xj, yj, zj;
-            grid_coords(col[k], nx, ny, xj, yj, zj);
+            grid_coords(gm.global_col(col[k]), gm.nx, gm.ny, xj, yj, zj);
             const int dx = xj - xi, dy = yj - yi, dz = zj - zi;
             if (dx < -1 || dx > 1 || dy < -1 || dy > 1 || dz < -1 || dz > 1) {
                 f |= 1u;
@@ -99,23 +99,24 @@ __global__ void stencil_clear_kernel(int64_t nchunks, int S, int RT, int64_t chu
     }
 }
 
-__global__ void stencil_fill_kernel(int64_t n, int nx, int ny, int nz, int by, int S, int ntx, int64_t chunk_bytes,
+__global__ void stencil_fill_kernel(GridMap gm, int nzg, int by, int S, int ntx, int64_t chunk_bytes,
                                     const int32_t* __restrict__ off, const int32_t* __restrict__ col,
                                     const double* __restrict__ val, unsigned char* __restrict__ chunks) {
     const int RT = STENCIL_BX * by;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+    const int nx = gm.nx, ny = gm.ny;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < gm.n_own;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         int xi, yi, zi;
-        grid_coords(i, nx, ny, xi, yi, zi);
+        grid_coords(gm.row_begin + i, nx, ny, xi, yi, zi);
         const int64_t t = static_cast<int64_t>(yi / by) * ntx + xi / STENCIL_BX;
         const int r = (yi % by) * STENCIL_BX + xi % STENCIL_BX;
-        unsigned char* c = chunks + (t * nz + zi) * chunk_bytes;
+        unsigned char* c = chunks + (t * gm.nzl + (zi - gm.z0)) * chunk_bytes;
         double* V = reinterpret_cast<double*>(c);
         uint32_t* MK = reinterpret_cast<uint32_t*>(c + static_cast<int64_t>(S) * RT * 8);
         uint32_t mask = 0;
         for (int k = off[i]; k < off[i + 1]; ++k) {
             int xj, yj, zj;
-            grid_coords(col[k], nx, ny, xj, yj, zj);
+            grid_coords(gm.global_col(col[k]), nx, ny, xj, yj, zj);
             const int dx = xj - xi, dy = yj - yi, dz = zj - zi;
             const int s = S == 27 ? (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1) : face_slot(dz, dy, dx);
             V[static_cast<int64_t>(s) * RT + r] = val[k];
@@ -129,7 +130,7 @@ __global__ void stencil_fill_kernel(int64_t n, int nx, int ny, int nz, int by, i
                     if (S == 7 && (dx != 0) + (dy != 0) + (dz != 0) > 1) continue;
                     const int s = S == 27 ? (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1) : face_slot(dz, dy, dx);
                     const bool inside = xi + dx >= 0 && xi + dx < nx && yi + dy >= 0 && yi + dy < ny &&
-                                        zi + dz >= 0 && zi + dz < nz;
+                                        zi + dz >= 0 && zi + dz < nzg;
                     if (inside && !((mask >> s) & 1u)) check = true;
                 }
         MK[r] = mask | (check ? 0x80000000u : 0u);
@@ -139,7 +140,11 @@ __global__ void stencil_fill_kernel(int64_t n, int nx, int ny, int nz, int by, i
 // ---- the SpMM kernel --------------------------------------------------------
 
 struct StencilGeom {
-    int nx, ny, nz;
+    int nx, ny;
+    int nz;               // planes of this launch's range [zbeg, zbeg + nz)
+    int zbeg;             // first local plane of the range
+    int nzl;              // local planes (chunk layout); planes -1 / nzl come from the halo map
+    int lower, upper;     // halo planes present below / above (z-slab partition)
     int ntx;              // tiles along x
     int64_t steps;        // tile-planes per column half: ntiles * nz
     int nranges;          // step ranges (blocks per column half)
@@ -287,8 +292,8 @@ struct StencilEpiDots {
 
 template <int MT, int MC, int ST, int BY, int EPI>
 __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
-    stencil_spmm_kernel(const __grid_constant__ CUtensorMap xmap, StencilGeom g, double* __restrict__ y,
-                        const int* __restrict__ ctl, SpmmEpi epi) {
+    stencil_spmm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
+                        StencilGeom g, double* __restrict__ y, const int* __restrict__ ctl, SpmmEpi epi) {
     using SH = StencilShape<MC, BY>;
     constexpr int CS = MT / MC;
     constexpr int XR = StencilRings<MC>::XR, VR = StencilRings<MC>::VR;
@@ -337,19 +342,29 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
     if (tid >= SH::THREADS) {   // ---- producer warp
         if (tid == SH::THREADS && g.mode != 2) {
             int64_t Q = 0, j = 0;   // plane loads / chunk loads issued so far
-            auto plane = [&](int t, int p) {
+            auto plane = [&](int t, int p) {   // p: plane within the range
                 const int b = static_cast<int>(Q % XR);
                 if (Q >= XR) mbar_wait(&xempty[b], static_cast<uint32_t>((Q / XR - 1) & 1));
                 mbar_expect_tx(&xfull[b], static_cast<uint32_t>(SH::PLANE * 8));
-                tensor4d_g2s(xr + b * SH::PLANE, &xmap, h * MC, (t % g.ntx) * STENCIL_BX - 1,
-                             (t / g.ntx) * BY - 1, p, &xfull[b]);
+                const int pl = g.zbeg + p;   // local plane; -1 / nzl: halo (or zero fill)
+                const void* map = &xmap;
+                int pz = pl;
+                if (pl < 0 && g.lower) {
+                    map = &hmap;
+                    pz = 0;
+                } else if (pl >= g.nzl && g.upper) {
+                    map = &hmap;
+                    pz = g.lower;
+                }
+                tensor4d_g2s(xr + b * SH::PLANE, map, h * MC, (t % g.ntx) * STENCIL_BX - 1, (t / g.ntx) * BY - 1, pz,
+                             &xfull[b]);
                 ++Q;
             };
             auto chunk = [&](int t, int z) {
                 const int b = static_cast<int>(j % VR);
                 if (j >= VR) mbar_wait(&vempty[b], static_cast<uint32_t>((j / VR - 1) & 1));
                 mbar_expect_tx(&vfull[b], static_cast<uint32_t>(CB));
-                bulk_g2s(vr + b * CB, g.chunks + (static_cast<int64_t>(t) * g.nz + z) * g.chunk_bytes,
+                bulk_g2s(vr + b * CB, g.chunks + (static_cast<int64_t>(t) * g.nzl + g.zbeg + z) * g.chunk_bytes,
                          static_cast<uint32_t>(CB), &vfull[b]);
                 ++j;
             };
@@ -359,8 +374,10 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
                 if (g.pd <= 0) return;
                 const int zp = z + g.pd;
                 if (zp >= g.nz) return;
-                prefetch_tensor4d_l2(&xmap, h * MC, (t % g.ntx) * STENCIL_BX - 1, (t / g.ntx) * BY - 1, zp + 1);
-                prefetch_bulk_l2(g.chunks + (static_cast<int64_t>(t) * g.nz + zp) * g.chunk_bytes,
+                if (g.zbeg + zp + 1 < g.nzl)
+                    prefetch_tensor4d_l2(&xmap, h * MC, (t % g.ntx) * STENCIL_BX - 1, (t / g.ntx) * BY - 1,
+                                         g.zbeg + zp + 1);
+                prefetch_bulk_l2(g.chunks + (static_cast<int64_t>(t) * g.nzl + g.zbeg + zp) * g.chunk_bytes,
                                  static_cast<uint32_t>(CB));
             };
             for (int64_t s = s0; s < s1;) {
@@ -423,7 +440,7 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
             // latency hides behind it
             double2 axs[4];
             if constexpr (EPI == 1) {
-                const int64_t rowz = (static_cast<int64_t>(za + i) * g.ny + yg) * g.nx;
+                const int64_t rowz = (static_cast<int64_t>(g.zbeg + za + i) * g.ny + yg) * g.nx;
 #pragma unroll
                 for (int r = 0; r < 4; ++r)
                     axs[r] = (yok && xg0 + r < g.nx)
@@ -448,7 +465,7 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
                 mbar_arrive(&vempty[j % VR]);
             }
             if (yok) {
-                const int64_t rowz = (static_cast<int64_t>(za + i) * g.ny + yg) * g.nx;
+                const int64_t rowz = (static_cast<int64_t>(g.zbeg + za + i) * g.ny + yg) * g.nx;
 #pragma unroll
                 for (int r = 0; r < 4; ++r)
                     if (xg0 + r < g.nx) {
@@ -561,18 +578,23 @@ StencilLayout& layout_for(mbg_ctx* ctx, const mbg_csr* a, int by) {
     l->chunks.alloc(bytes);
     const int grid = ctx->num_sms * 8;
     stencil_clear_kernel<<<grid, 256, 0, ctx->stream>>>(ntx * nty * op.nz, S, RT, l->chunk_bytes, l->chunks.p);
-    stencil_fill_kernel<<<grid, 256, 0, ctx->stream>>>(a->n, op.nx, op.ny, op.nz, by, S, static_cast<int>(ntx),
-                                                       l->chunk_bytes, a->off.p, a->col.p, a->val.p, l->chunks.p);
+    stencil_fill_kernel<<<grid, 256, 0, ctx->stream>>>(op.map, op.nzg, by, S, static_cast<int>(ntx), l->chunk_bytes,
+                                                       a->off.p, a->col.p, a->val.p, l->chunks.p);
     MBG_CUDA(cudaGetLastError());
     MBG_CUDA(cudaStreamSynchronize(ctx->stream));
     op.layouts.push_back(std::move(l));
     return *op.layouts.back();
 }
 
+struct ZRange {
+    int zbeg, zend;   // local planes [zbeg, zend)
+};
+
 template <int MT, int MC, int ST, int BY, int EPI>
 void launch_one(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const double* x, double* y,
-                const int* ctl, const SpmmEpi& epi) {
+                const int* ctl, const SpmmEpi& epi, ZRange zr) {
     const StencilOp& op = *a->stencil;
+    if (zr.zend <= zr.zbeg) return;
     constexpr int smem = stencil_smem<MC, ST, BY>();
     constexpr int threads = StencilShape<MC, BY>::THREADS + 32;   // + producer warp
     constexpr int CS = MT / MC;
@@ -584,26 +606,38 @@ void launch_one(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const do
                                                                smem));
         if (occ < 1) occ = 1;
     }
-    // x viewed as a (nz, ny, nx, MT) fp64 tensor; box (MC, LW, BY + 2, 1)
-    CUtensorMap tm;
-    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(MT), static_cast<cuuint64_t>(op.nx),
-                                static_cast<cuuint64_t>(op.ny), static_cast<cuuint64_t>(op.nz)};
-    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(MT) * 8, static_cast<cuuint64_t>(op.nx) * MT * 8,
-                                   static_cast<cuuint64_t>(op.nx) * op.ny * MT * 8};
-    const cuuint32_t box[4] = {static_cast<cuuint32_t>(MC), static_cast<cuuint32_t>(StencilShape<MC, BY>::LW),
-                               static_cast<cuuint32_t>(BY + 2), 1u};
-    const cuuint32_t estr[4] = {1, 1, 1, 1};
-    const CUresult r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(x), dims, strides,
-                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw std::runtime_error("stencil SpMM: cuTensorMapEncodeTiled failed (" +
-                                                    std::to_string(static_cast<int>(r)) + ")");
+    // x viewed as a (planes, ny, nx, MT) fp64 tensor; box (MC, LW, BY + 2, 1):
+    // the owned planes, and the halo planes appended after them (z-slabs)
+    auto encode = [&](CUtensorMap& tm, const double* base, int planes) {
+        const cuuint64_t dims[4] = {static_cast<cuuint64_t>(MT), static_cast<cuuint64_t>(op.nx),
+                                    static_cast<cuuint64_t>(op.ny), static_cast<cuuint64_t>(planes)};
+        const cuuint64_t strides[3] = {static_cast<cuuint64_t>(MT) * 8, static_cast<cuuint64_t>(op.nx) * MT * 8,
+                                       static_cast<cuuint64_t>(op.nx) * op.ny * MT * 8};
+        const cuuint32_t box[4] = {static_cast<cuuint32_t>(MC), static_cast<cuuint32_t>(StencilShape<MC, BY>::LW),
+                                   static_cast<cuuint32_t>(BY + 2), 1u};
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        const CUresult r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims,
+                                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            throw std::runtime_error("stencil SpMM: cuTensorMapEncodeTiled failed (" +
+                                     std::to_string(static_cast<int>(r)) + ")");
+    };
+    CUtensorMap tm, hm;
+    encode(tm, x, op.nz);
+    const int nhp = op.map.lower + op.upper;
+    if (nhp) encode(hm, x + a->n * MT, nhp);
+    else hm = tm;
     StencilGeom gm{};
     gm.nx = op.nx;
     gm.ny = op.ny;
-    gm.nz = op.nz;
+    gm.nz = zr.zend - zr.zbeg;
+    gm.zbeg = zr.zbeg;
+    gm.nzl = op.nz;
+    gm.lower = op.map.lower;
+    gm.upper = op.upper;
     gm.ntx = (op.nx + STENCIL_BX - 1) / STENCIL_BX;
-    gm.steps = static_cast<int64_t>(gm.ntx) * ((op.ny + BY - 1) / BY) * op.nz;
+    gm.steps = static_cast<int64_t>(gm.ntx) * ((op.ny + BY - 1) / BY) * gm.nz;
     gm.chunks = L.chunks.p;
     gm.chunk_bytes = L.chunk_bytes;
     static const int mode = env_int("MBG_STENCIL_MODE", 0);
@@ -616,16 +650,16 @@ void launch_one(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const do
     const int64_t slots = static_cast<int64_t>(occ) * ctx->num_sms / CS;
     // work split: whole tiles per block when there are at least as many tiles
     // as block slots, else every tile cut into equal z-segments
-    const int64_t ntiles = gm.steps / op.nz;
+    const int64_t ntiles = gm.steps / gm.nz;
     if (ntiles >= slots) {
         gm.kt = static_cast<int>((ntiles + slots - 1) / slots);
-        gm.zseg = op.nz;
+        gm.zseg = gm.nz;
         gm.nranges = static_cast<int>((ntiles + gm.kt - 1) / gm.kt);
     } else {
-        const int k = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(slots / ntiles, op.nz)));
+        const int k = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(slots / ntiles, gm.nz)));
         gm.kt = 0;
-        gm.zseg = (op.nz + k - 1) / k;
-        gm.nranges = static_cast<int>(ntiles * ((op.nz + gm.zseg - 1) / gm.zseg));
+        gm.zseg = (gm.nz + k - 1) / k;
+        gm.nranges = static_cast<int>(ntiles * ((gm.nz + gm.zseg - 1) / gm.zseg));
     }
     const int grid = gm.nranges * CS;
     static const int trace = env_int("MBG_STENCIL_TRACE", 0);
@@ -637,9 +671,9 @@ void launch_one(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const do
     static const int spdl = env_int("MBG_STENCIL_PDL", 1);
     if (spdl) {
         launch_pdl(stencil_spmm_kernel<MT, MC, ST, BY, EPI>, dim3(grid), dim3(threads), static_cast<size_t>(smem),
-                   ctx->stream, tm, gm, y, ctl, epi);
+                   ctx->stream, tm, hm, gm, y, ctl, epi);
     } else {
-        stencil_spmm_kernel<MT, MC, ST, BY, EPI><<<grid, threads, smem, ctx->stream>>>(tm, gm, y, ctl, epi);
+        stencil_spmm_kernel<MT, MC, ST, BY, EPI><<<grid, threads, smem, ctx->stream>>>(tm, hm, gm, y, ctl, epi);
         MBG_CUDA(cudaGetLastError());
     }
     if (trace) {   // lab: dump (block, smid, start ns, end ns) of this launch
@@ -658,11 +692,25 @@ void launch_one(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const do
 }  // namespace
 
 std::shared_ptr<StencilOp> build_stencil(mbg_ctx* ctx, const mbg_csr* a, int nx, int ny, int nz) {
-    if (!a->peers.empty() || a->n_halo) return nullptr;
-    if (static_cast<int64_t>(nx) * ny * nz != a->n || a->n == 0) return nullptr;
+    const int64_t nxy = static_cast<int64_t>(nx) * ny;
+    if (nx < 1 || ny < 1 || nz < 1 || nxy * nz != a->n_global || a->n == 0) return nullptr;
+    // a partition must own whole planes; its halo must be exactly the planes
+    // next to the slab (plan.cpp orders them by ascending global id)
+    if (a->row_begin % nxy || a->n % nxy) return nullptr;
+    GridMap gm{};
+    gm.nx = nx;
+    gm.ny = ny;
+    gm.row_begin = a->row_begin;
+    gm.n_own = a->n;
+    gm.z0 = static_cast<int>(a->row_begin / nxy);
+    gm.nzl = static_cast<int>(a->n / nxy);
+    const bool partitioned = !a->peers.empty() || a->n_halo;
+    gm.lower = partitioned && gm.z0 > 0;
+    const bool upper = partitioned && gm.z0 + gm.nzl < nz;
+    if (a->n_halo != nxy * (gm.lower + upper)) return nullptr;
     DevBuf<unsigned> flags(1);
     MBG_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(unsigned), ctx->stream));
-    stencil_scan_kernel<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(a->n, nx, ny, a->off.p, a->col.p, flags.p);
+    stencil_scan_kernel<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(gm, a->off.p, a->col.p, flags.p);
     MBG_CUDA(cudaGetLastError());
     unsigned f = 0;
     MBG_CUDA(cudaMemcpyAsync(&f, flags.p, sizeof f, cudaMemcpyDeviceToHost, ctx->stream));
@@ -671,7 +719,10 @@ std::shared_ptr<StencilOp> build_stencil(mbg_ctx* ctx, const mbg_csr* a, int nx,
     auto op = std::make_shared<StencilOp>();
     op->nx = nx;
     op->ny = ny;
-    op->nz = nz;
+    op->nz = gm.nzl;
+    op->nzg = nz;
+    op->map = gm;
+    op->upper = upper;
     op->kind = (f & 2u) ? 27 : 7;
     op->nnz = a->nnz;
     return op;
@@ -692,35 +743,35 @@ double stencil_spmm_bytes(int64_t n, int64_t nnz, int m) {
 
 template <int MT, int MC, int ST, int BY>
 void launch_epi(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const double* x, double* y, const int* ctl,
-                const SpmmEpi* epi) {
+                const SpmmEpi* epi, ZRange zr) {
     const SpmmEpi none{};
     switch (epi ? epi->kind : 0) {
-        case 0: launch_one<MT, MC, ST, BY, 0>(ctx, a, L, x, y, ctl, none); break;
-        case 1: launch_one<MT, MC, ST, BY, 1>(ctx, a, L, x, y, ctl, *epi); break;
-        case 2: launch_one<MT, MC, ST, BY, 2>(ctx, a, L, x, y, ctl, *epi); break;
-        case 3: launch_one<MT, MC, ST, BY, 3>(ctx, a, L, x, y, ctl, *epi); break;
-        case 4: launch_one<MT, MC, ST, BY, 4>(ctx, a, L, x, y, ctl, *epi); break;
+        case 0: launch_one<MT, MC, ST, BY, 0>(ctx, a, L, x, y, ctl, none, zr); break;
+        case 1: launch_one<MT, MC, ST, BY, 1>(ctx, a, L, x, y, ctl, *epi, zr); break;
+        case 2: launch_one<MT, MC, ST, BY, 2>(ctx, a, L, x, y, ctl, *epi, zr); break;
+        case 3: launch_one<MT, MC, ST, BY, 3>(ctx, a, L, x, y, ctl, *epi, zr); break;
+        case 4: launch_one<MT, MC, ST, BY, 4>(ctx, a, L, x, y, ctl, *epi, zr); break;
         default: throw Invalid("stencil SpMM: unknown epilogue kind");
     }
 }
 
 template <int BY>
 void launch_by(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y, const int* ctl,
-               const SpmmEpi* epi) {
+               const SpmmEpi* epi, ZRange zr) {
     const StencilLayout& L = layout_for(ctx, a, BY);
     const int kind = a->stencil->kind;
     switch (m) {
         case 8:
-            if (kind == 27) launch_epi<8, 8, 27, BY>(ctx, a, L, x, y, ctl, epi);
-            else launch_epi<8, 8, 7, BY>(ctx, a, L, x, y, ctl, epi);
+            if (kind == 27) launch_epi<8, 8, 27, BY>(ctx, a, L, x, y, ctl, epi, zr);
+            else launch_epi<8, 8, 7, BY>(ctx, a, L, x, y, ctl, epi, zr);
             break;
         case 16:
-            if (kind == 27) launch_epi<16, 16, 27, BY>(ctx, a, L, x, y, ctl, epi);
-            else launch_epi<16, 16, 7, BY>(ctx, a, L, x, y, ctl, epi);
+            if (kind == 27) launch_epi<16, 16, 27, BY>(ctx, a, L, x, y, ctl, epi, zr);
+            else launch_epi<16, 16, 7, BY>(ctx, a, L, x, y, ctl, epi, zr);
             break;
         case 32:
-            if (kind == 27) launch_epi<32, 16, 27, BY>(ctx, a, L, x, y, ctl, epi);
-            else launch_epi<32, 16, 7, BY>(ctx, a, L, x, y, ctl, epi);
+            if (kind == 27) launch_epi<32, 16, 27, BY>(ctx, a, L, x, y, ctl, epi, zr);
+            else launch_epi<32, 16, 7, BY>(ctx, a, L, x, y, ctl, epi, zr);
             break;
         default:
             throw Invalid("stencil SpMM: m must be 8, 16 or 32");
@@ -728,8 +779,13 @@ void launch_by(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y
 }
 
 int launch_stencil_spmm(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y, const int* ctl,
-                        const SpmmEpi* epi) {
-    launch_by<4>(ctx, a, m, x, y, ctl, epi);
+                        const SpmmEpi* epi, int zbeg, int zend) {
+    const int nz = a->stencil->nz;
+    if (zend < 0) zend = nz;
+    zbeg = std::max(0, zbeg);
+    zend = std::min(nz, zend);
+    if (zend <= zbeg) return 0;
+    launch_by<4>(ctx, a, m, x, y, ctl, epi, ZRange{zbeg, zend});
     return 1;
 }
 

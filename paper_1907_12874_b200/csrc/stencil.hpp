@@ -29,8 +29,35 @@ struct StencilLayout {
     DevBuf<unsigned char> chunks;   // [(tile * nz + z)] chunks
 };
 
+// Local numbering of a (possibly z-slab partitioned) operator: owned rows are
+// the global rows [row_begin, row_begin + n_own) = whole planes z0 .. z0+nzl-1;
+// halo columns (plan.cpp: ascending global ids after the owned rows) are the
+// plane z0-1 (when `lower`) followed by the plane z0+nzl (when the op's `upper`).
+struct GridMap {
+    int nx, ny;
+    int64_t row_begin, n_own;
+    int z0, nzl;
+    int lower;
+#ifdef __CUDACC__
+    __device__ int64_t global_col(int64_t j) const {
+        if (j < n_own) return row_begin + j;
+        const int64_t nxy = static_cast<int64_t>(nx) * ny;
+        int64_t h = j - n_own;
+        if (lower) {
+            if (h < nxy) return static_cast<int64_t>(z0 - 1) * nxy + h;
+            h -= nxy;
+        }
+        return static_cast<int64_t>(z0 + nzl) * nxy + h;
+    }
+#endif
+};
+
 struct StencilOp {
-    int nx = 0, ny = 0, nz = 0;
+    int nx = 0, ny = 0;
+    int nz = 0;            // local planes (the whole grid on one GPU)
+    int nzg = 0;           // global planes
+    GridMap map{};         // local -> global numbering
+    int upper = 0;         // halo plane above the slab
     int kind = 0;          // 7 (face neighbours only) or 27
     int64_t nnz = 0;
     std::vector<std::unique_ptr<StencilLayout>> layouts;   // built lazily per tile height
@@ -49,8 +76,10 @@ bool stencil_epilogues();
 // y = A x through the stencil twin; returns the number of kernel launches.
 // epi: optional fused exact-dot epilogue (kernels.hpp SpmmEpi, kinds 1-4).
 struct SpmmEpi;
+// [zbeg, zend): local planes to compute (default: all); a z-slab partition
+// runs its interior planes while the halo planes travel, then the two faces.
 int launch_stencil_spmm(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y, const int* ctl,
-                        const SpmmEpi* epi = nullptr);
+                        const SpmmEpi* epi = nullptr, int zbeg = 0, int zend = -1);
 // Algorithmic bytes of one stencil SpMM: x read once, y written once, 8 B per
 // nonzero value, 4 B per row mask.
 double stencil_spmm_bytes(int64_t n, int64_t nnz, int m);

@@ -18,7 +18,7 @@ def bits(x):
     return np.ascontiguousarray(x, dtype=np.float64).view(np.int64)
 
 
-def run_partitioned(a, b, m, bounds, method, form, **kw):
+def run_partitioned(a, b, m, bounds, method, form, grid=None, **kw):
     world = len(bounds) - 1
     ctxs = [P.Context(0) for _ in range(world)]
     P.local_group(ctxs)
@@ -29,6 +29,9 @@ def run_partitioned(a, b, m, bounds, method, form, **kw):
     def rank(r):
         try:
             d = ctxs[r].upload(A, bounds, r)
+            if grid is not None:   # z-slab on the stencil twin
+                d.set_grid(*grid)
+                assert d.stencil_kind in (7, 27), "slab stencil twin not built"
             r0, r1 = bounds[r], bounds[r + 1]
             B = ctxs[r].multivector(r1 - r0, m, b[r0 * m:r1 * m])
             X = ctxs[r].multivector(r1 - r0, m)
@@ -77,3 +80,23 @@ def test_banded_uneven_partition(ctx):
         assert rep.iterations == 25
         assert np.array_equal(bits(rep.residual_history), bits(want["hist"]))
         assert np.array_equal(bits(x), bits(want["x"][bounds[r] * m:bounds[r + 1] * m]))
+
+
+@pytest.mark.parametrize("world,planes", [(2, 5), (3, 1), (4, 2), (2, 1)])
+@pytest.mark.parametrize("kind,m,method,form", [("convdiff7", 8, "bicgstab", "fused"),
+                                                ("stencil27", 16, "rbicgstab", "fused"),
+                                                ("convdiff7", 32, "pipebicgstab", "merged")])
+def test_zslab_stencil_twin_equals_single_gpu(ctx, world, planes, kind, m, method, form):
+    # each rank's slab runs on its stencil twin: interior planes while the halo
+    # planes travel, then the two faces reading the halo through a second
+    # tensor map -- bitwise the single-GPU oracle
+    nx, ny, nz = 33, 9, planes * world
+    a = O.gen_stencil(kind, nx, ny, nz, seed=2)
+    b = O.rhs(a.n, m, 1)
+    bounds = [p * nx * ny * planes for p in range(world + 1)]
+    want = O.solve(a, b, m, method, form, fixed=True, maxit=12)
+    parts = run_partitioned(a, b, m, bounds, method, form, grid=(nx, ny, nz), fixed=True, max_iters=12)
+    for r, (rep, x) in enumerate(parts):
+        assert np.array_equal(bits(rep.residual_history), bits(want["hist"])), r
+        r0, r1 = bounds[r], bounds[r + 1]
+        assert np.array_equal(bits(x), bits(want["x"][r0 * m:r1 * m])), r
