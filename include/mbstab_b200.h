@@ -92,6 +92,14 @@ int mbg_halo_plan(int64_t n, const int64_t* offsets, const int32_t* cols, const 
                   int32_t* loc_off, int32_t* loc_col, double* loc_val, int64_t* halo_global, int* npeers,
                   int* peer_part, int64_t* peer_send_count, int32_t* peer_send_rows,
                   int64_t* peer_recv_offset, int64_t* peer_recv_count);
+/* The same plan for A^T (rows = this part's columns of A, nonzeros in ascending
+ * source row -- spmv_transpose's order, src/core/spmv.cpp:76-90): what
+ * mbg_csr_upload_partitioned builds for IBiCGStab's f0 = A^T r0 across ranks. */
+int mbg_transpose_halo_plan(int64_t n, const int64_t* offsets, const int32_t* cols, const double* vals, int nparts,
+                            const int64_t* bounds, int my_part, int64_t* n_own, int64_t* n_halo,
+                            int64_t* nnz_local, int32_t* loc_off, int32_t* loc_col, double* loc_val,
+                            int64_t* halo_global, int* npeers, int* peer_part, int64_t* peer_send_count,
+                            int32_t* peer_send_rows, int64_t* peer_recv_offset, int64_t* peer_recv_count);
 /* Same as mbg_csr_upload but a row's column indices may come in any order
  * (each row is still summed in the given order; no duplicates checked
  * beyond range) -- for permuted operators P A P^T that keep every row's

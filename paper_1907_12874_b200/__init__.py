@@ -457,13 +457,15 @@ def solve_host(ctx: Context, a: DeviceCsr, b: np.ndarray, x: np.ndarray, m: int,
 # ---------------------------------------------------------------------------
 # partition / exact-dot host hooks (used by the multi-rank CPU tests)
 # ---------------------------------------------------------------------------
-def halo_plan(a: CsrMatrix, bounds: Sequence[int], my_part: int) -> dict:
+def halo_plan(a: CsrMatrix, bounds: Sequence[int], my_part: int, transpose: bool = False) -> dict:
+    """Host-only halo plan of part `my_part` (of A^T when transpose=True)."""
     L = lib()
+    fn = L.mbg_transpose_halo_plan if transpose else L.mbg_halo_plan
     b = np.ascontiguousarray(bounds, dtype=np.int64)
     n_own, n_halo, nnz, npeers = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int()
     args0 = [a.n_rows, _ptr(a.row_offsets), _ptr(a.col_indices), _ptr(a.values), b.size - 1, _ptr(b), my_part,
              C.byref(n_own), C.byref(n_halo), C.byref(nnz)]
-    check(L.mbg_halo_plan(*args0, None, None, None, None, C.byref(npeers), None, None, None, None, None))
+    check(fn(*args0, None, None, None, None, C.byref(npeers), None, None, None, None, None))
     off = np.empty(n_own.value + 1, np.int32)
     col = np.empty(nnz.value, np.int32)
     val = np.empty(nnz.value, np.float64)
@@ -474,8 +476,8 @@ def halo_plan(a: CsrMatrix, bounds: Sequence[int], my_part: int) -> dict:
     prc = np.empty(max(1, npeers.value), np.int64)
     # send rows: at most n_own per peer
     psr = np.empty(max(1, npeers.value * max(1, n_own.value)), np.int32)
-    check(L.mbg_halo_plan(*args0, _ptr(off), _ptr(col), _ptr(val), _ptr(hg), C.byref(npeers), _ptr(pp), _ptr(psc),
-                          _ptr(psr), _ptr(pro), _ptr(prc)))
+    check(fn(*args0, _ptr(off), _ptr(col), _ptr(val), _ptr(hg), C.byref(npeers), _ptr(pp), _ptr(psc),
+             _ptr(psr), _ptr(pro), _ptr(prc)))
     peers, so = [], 0
     for i in range(npeers.value):
         cnt = int(psc[i])

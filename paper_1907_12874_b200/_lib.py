@@ -85,6 +85,8 @@ def lib() -> C.CDLL:
         "mbg_csr_upload_partitioned": (i32, [vp, i64, vp, vp, vp, i32, vp, i32, pp]),
         "mbg_halo_plan": (i32, [i64, vp, vp, vp, i32, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                 vp, vp]),
+        "mbg_transpose_halo_plan": (i32, [i64, vp, vp, vp, i32, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                vp, vp]),
         "mbg_csr_free": (i32, [vp]),
         "mbg_csr_rows": (i64, [vp]),
         "mbg_csr_nnz": (i64, [vp]),

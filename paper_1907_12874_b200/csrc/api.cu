@@ -343,6 +343,46 @@ extern "C" int mbg_csr_upload_any_order(mbg_ctx* ctx, int64_t n, const int64_t* 
     });
 }
 
+// Device CSR of one rank from its halo plan (local CSR, tile lists, interior /
+// boundary split, per-peer send lists).
+static std::unique_ptr<mbg_csr> csr_from_plan(mbg_ctx* ctx, int64_t n, int64_t row_begin, int nparts,
+                                              const HaloPlan& pl) {
+    auto a = std::make_unique<mbg_csr>();
+    a->ctx = ctx;
+    a->device = ctx->device;
+    a->n_global = n;
+    a->row_begin = row_begin;
+    a->n = pl.n_own;
+    a->nnz = pl.nnz;
+    a->n_halo = pl.n_halo;
+    csr_arrays_to_device(ctx, a.get(), pl.n_own, pl.off, pl.col.data(), pl.val.data(), pl.nnz);
+    a->nnz = pl.nnz;
+    if (nparts > 1) {
+        auto ti = build_spmm_tiles(pl.off, pl.interior);
+        auto tb = build_spmm_tiles(pl.off, pl.boundary);
+        upload(a->tiles_interior, ti.data(), ti.size(), ctx->stream);
+        upload(a->tiles_boundary, tb.data(), tb.size(), ctx->stream);
+        auto li = long_rows_of(ti), lb = long_rows_of(tb);
+        upload(a->long_interior, li.data(), li.size(), ctx->stream);
+        upload(a->long_boundary, lb.data(), lb.size(), ctx->stream);
+        stage_tilings(ctx, a.get(), pl.off, pl.col.data(), nullptr, &pl.interior, &pl.boundary);
+        upload(a->interior_rows, pl.interior.data(), pl.interior.size(), ctx->stream);
+        upload(a->boundary_rows, pl.boundary.data(), pl.boundary.size(), ctx->stream);
+        a->n_interior = static_cast<int64_t>(pl.interior.size());
+        a->n_boundary = static_cast<int64_t>(pl.boundary.size());
+        for (auto& p : pl.peers) {
+            mbg_csr::Peer q;
+            q.rank = p.part;
+            q.send_count = static_cast<int64_t>(p.send_rows.size());
+            q.recv_count = p.recv_count;
+            q.recv_offset = p.recv_offset;
+            upload(q.send_rows, p.send_rows.data(), p.send_rows.size(), ctx->stream);
+            a->peers.push_back(std::move(q));
+        }
+    }
+    return a;
+}
+
 // Partitioned upload: parts given by bounds[nparts+1]; this context's rank is
 // my_part.  Builds the halo plan from the full host CSR.
 extern "C" int mbg_csr_upload_partitioned(mbg_ctx* ctx, int64_t n, const int64_t* off, const int32_t* col,
@@ -353,40 +393,14 @@ extern "C" int mbg_csr_upload_partitioned(mbg_ctx* ctx, int64_t n, const int64_t
         if (!out) throw Invalid("null output");
         validate_csr(n, off, col, off ? off[n] : 0);
         HaloPlan pl = build_halo_plan(n, off, col, val, nparts, bounds, my_part);
-        auto* a = new mbg_csr();
+        mbg_csr* a = nullptr;
         try {
-            a->ctx = ctx;
-            a->device = ctx->device;
-            a->n_global = n;
-            a->row_begin = bounds[my_part];
-            a->n = pl.n_own;
-            a->nnz = pl.nnz;
-            a->n_halo = pl.n_halo;
-            csr_arrays_to_device(ctx, a, pl.n_own, pl.off, pl.col.data(), pl.val.data(), pl.nnz);
-            a->nnz = pl.nnz;
-            if (nparts > 1) {
-                auto ti = build_spmm_tiles(pl.off, pl.interior);
-                auto tb = build_spmm_tiles(pl.off, pl.boundary);
-                upload(a->tiles_interior, ti.data(), ti.size(), ctx->stream);
-                upload(a->tiles_boundary, tb.data(), tb.size(), ctx->stream);
-                auto li = long_rows_of(ti), lb = long_rows_of(tb);
-                upload(a->long_interior, li.data(), li.size(), ctx->stream);
-                upload(a->long_boundary, lb.data(), lb.size(), ctx->stream);
-                stage_tilings(ctx, a, pl.off, pl.col.data(), nullptr, &pl.interior, &pl.boundary);
-                upload(a->interior_rows, pl.interior.data(), pl.interior.size(), ctx->stream);
-                upload(a->boundary_rows, pl.boundary.data(), pl.boundary.size(), ctx->stream);
-                a->n_interior = static_cast<int64_t>(pl.interior.size());
-                a->n_boundary = static_cast<int64_t>(pl.boundary.size());
-                for (auto& p : pl.peers) {
-                    mbg_csr::Peer q;
-                    q.rank = p.part;
-                    q.send_count = static_cast<int64_t>(p.send_rows.size());
-                    q.recv_count = p.recv_count;
-                    q.recv_offset = p.recv_offset;
-                    upload(q.send_rows, p.send_rows.data(), p.send_rows.size(), ctx->stream);
-                    a->peers.push_back(std::move(q));
-                }
-            }
+            a = csr_from_plan(ctx, n, bounds[my_part], nparts, pl).release();
+            // A^T with its own halo plan (IBiCGStab's f0 = A^T r0 across ranks)
+            if (nparts > 1)
+                a->transposed =
+                    csr_from_plan(ctx, n, bounds[my_part], nparts,
+                                  build_transpose_plan(n, off, col, val, nparts, bounds, my_part));
             MBG_CUDA(cudaStreamSynchronize(ctx->stream));
         } catch (...) {
             delete a;
@@ -397,13 +411,41 @@ extern "C" int mbg_csr_upload_partitioned(mbg_ctx* ctx, int64_t n, const int64_t
 }
 
 // Host-only halo plan for tests of the partition logic (no device needed).
+static int export_plan(bool transpose, int64_t n, const int64_t* off, const int32_t* col, const double* val,
+                       int nparts, const int64_t* bounds, int my_part, int64_t* n_own, int64_t* n_halo,
+                       int64_t* nnz_local, int32_t* loc_off, int32_t* loc_col, double* loc_val,
+                       int64_t* halo_global, int* npeers, int* peer_part, int64_t* peer_send_count,
+                       int32_t* peer_send_rows, int64_t* peer_recv_offset, int64_t* peer_recv_count);
+
 extern "C" int mbg_halo_plan(int64_t n, const int64_t* off, const int32_t* col, const double* val, int nparts,
                              const int64_t* bounds, int my_part, int64_t* n_own, int64_t* n_halo,
                              int64_t* nnz_local, int32_t* loc_off, int32_t* loc_col, double* loc_val,
                              int64_t* halo_global, int* npeers, int* peer_part, int64_t* peer_send_count,
                              int32_t* peer_send_rows, int64_t* peer_recv_offset, int64_t* peer_recv_count) {
+    return export_plan(false, n, off, col, val, nparts, bounds, my_part, n_own, n_halo, nnz_local, loc_off, loc_col,
+                       loc_val, halo_global, npeers, peer_part, peer_send_count, peer_send_rows, peer_recv_offset,
+                       peer_recv_count);
+}
+
+extern "C" int mbg_transpose_halo_plan(int64_t n, const int64_t* off, const int32_t* col, const double* val,
+                                       int nparts, const int64_t* bounds, int my_part, int64_t* n_own,
+                                       int64_t* n_halo, int64_t* nnz_local, int32_t* loc_off, int32_t* loc_col,
+                                       double* loc_val, int64_t* halo_global, int* npeers, int* peer_part,
+                                       int64_t* peer_send_count, int32_t* peer_send_rows,
+                                       int64_t* peer_recv_offset, int64_t* peer_recv_count) {
+    return export_plan(true, n, off, col, val, nparts, bounds, my_part, n_own, n_halo, nnz_local, loc_off, loc_col,
+                       loc_val, halo_global, npeers, peer_part, peer_send_count, peer_send_rows, peer_recv_offset,
+                       peer_recv_count);
+}
+
+static int export_plan(bool transpose, int64_t n, const int64_t* off, const int32_t* col, const double* val,
+                       int nparts, const int64_t* bounds, int my_part, int64_t* n_own, int64_t* n_halo,
+                       int64_t* nnz_local, int32_t* loc_off, int32_t* loc_col, double* loc_val,
+                       int64_t* halo_global, int* npeers, int* peer_part, int64_t* peer_send_count,
+                       int32_t* peer_send_rows, int64_t* peer_recv_offset, int64_t* peer_recv_count) {
     return guarded([&] {
-        HaloPlan pl = build_halo_plan(n, off, col, val, nparts, bounds, my_part);
+        HaloPlan pl = transpose ? build_transpose_plan(n, off, col, val, nparts, bounds, my_part)
+                                : build_halo_plan(n, off, col, val, nparts, bounds, my_part);
         *n_own = pl.n_own;
         *n_halo = pl.n_halo;
         *nnz_local = pl.nnz;

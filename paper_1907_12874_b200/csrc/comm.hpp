@@ -47,5 +47,8 @@ struct HaloPlan {
 };
 HaloPlan build_halo_plan(int64_t n, const int64_t* off, const int32_t* col, const double* val,
                          int nparts, const int64_t* begin, int my_part);
+// The same for A^T (rows = owned columns of A, nonzeros in ascending source row).
+HaloPlan build_transpose_plan(int64_t n, const int64_t* off, const int32_t* col, const double* val,
+                              int nparts, const int64_t* begin, int my_part);
 
 }  // namespace mbg

@@ -87,4 +87,86 @@ HaloPlan build_halo_plan(int64_t n, const int64_t* off, const int32_t* col, cons
     return pl;
 }
 
+// Halo plan of A^T for the same row partition (IBiCGStab's f0 = A^T r0,
+// PAPER.md:1441-1447, across ranks).  Row j of A^T lists the nonzeros A(i, j)
+// in ascending source row i -- the summation order of spmv_transpose
+// (spmv.cpp:76-90) -- so the ordinary distributed SpMM on this operator
+// reproduces the reference bit for bit.  Its halo is the rows i of other
+// ranks that couple to an owned column j; built from the full host CSR in
+// one O(nnz) pass, without forming the global transpose.
+HaloPlan build_transpose_plan(int64_t n, const int64_t* off, const int32_t* col, const double* val, int nparts,
+                              const int64_t* begin, int my) {
+    if (nparts < 1 || my < 0 || my >= nparts) throw Invalid("partition: bad part index");
+    const int64_t rb = begin[my], re = begin[my + 1];
+    HaloPlan pl;
+    pl.n_own = re - rb;
+    // pass 1: row lengths of the local A^T and the halo source rows
+    std::vector<int64_t> len(static_cast<size_t>(pl.n_own), 0);
+    std::vector<int64_t> halo;
+    for (int64_t i = 0; i < n; ++i) {
+        bool touches = false;
+        for (int64_t k = off[i]; k < off[i + 1]; ++k) {
+            const int64_t j = col[k];
+            if (j >= rb && j < re) {
+                ++len[j - rb];
+                touches = true;
+            }
+        }
+        if (touches && (i < rb || i >= re)) halo.push_back(i);   // ascending already
+    }
+    pl.n_halo = static_cast<int64_t>(halo.size());
+    pl.halo_global = halo;
+    int64_t nnz = 0;
+    for (int64_t v : len) nnz += v;
+    if (nnz > std::numeric_limits<int32_t>::max() || pl.n_own + pl.n_halo > std::numeric_limits<int32_t>::max())
+        throw Invalid("partition: local transpose exceeds int32");
+    pl.nnz = nnz;
+    pl.off.assign(static_cast<size_t>(pl.n_own) + 1, 0);
+    for (int64_t j = 0; j < pl.n_own; ++j) pl.off[j + 1] = pl.off[j] + static_cast<int32_t>(len[j]);
+    pl.col.resize(static_cast<size_t>(nnz));
+    pl.val.resize(static_cast<size_t>(nnz));
+    // pass 2: fill in ascending source row order
+    std::vector<int32_t> pos(pl.off.begin(), pl.off.end() - 1);
+    std::vector<char> bnd(static_cast<size_t>(pl.n_own), 0);
+    size_t hcur = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        int32_t li;
+        const bool own = i >= rb && i < re;
+        if (own) {
+            li = static_cast<int32_t>(i - rb);
+        } else {
+            while (hcur < halo.size() && halo[hcur] < i) ++hcur;
+            li = (hcur < halo.size() && halo[hcur] == i) ? static_cast<int32_t>(pl.n_own + hcur) : -1;
+        }
+        for (int64_t k = off[i]; k < off[i + 1]; ++k) {
+            const int64_t j = col[k];
+            if (j < rb || j >= re) continue;
+            const int32_t q = pos[j - rb]++;
+            pl.col[q] = li;
+            pl.val[q] = val[k];
+            if (!own) bnd[j - rb] = 1;
+        }
+    }
+    for (int64_t j = 0; j < pl.n_own; ++j) (bnd[j] ? pl.boundary : pl.interior).push_back(static_cast<int32_t>(j));
+    // peers: receive the halo rows owned by q; send my rows i with a nonzero in q's columns
+    for (int q = 0; q < nparts; ++q) {
+        if (q == my) continue;
+        HaloPlan::Peer peer;
+        peer.part = q;
+        const int64_t qb = begin[q], qe = begin[q + 1];
+        auto lo = std::lower_bound(halo.begin(), halo.end(), qb);
+        auto hi = std::lower_bound(halo.begin(), halo.end(), qe);
+        peer.recv_offset = lo - halo.begin();
+        peer.recv_count = hi - lo;
+        for (int64_t i = rb; i < re; ++i)
+            for (int64_t k = off[i]; k < off[i + 1]; ++k)
+                if (col[k] >= qb && col[k] < qe) {
+                    peer.send_rows.push_back(static_cast<int32_t>(i - rb));
+                    break;
+                }
+        if (peer.recv_count || !peer.send_rows.empty()) pl.peers.push_back(std::move(peer));
+    }
+    return pl;
+}
+
 }  // namespace mbg

@@ -95,13 +95,18 @@ Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulatio
     // (stencil SpMM: only with MBG_STENCIL_EPI=1 -- measured slower)
     epi_delta_ = formulation == MBG_FUSED && (stencil_ ? stencil_epilogues() : a->nnz <= 12 * a->n);
     if (method == MBG_IBICGSTAB) {
-        if (!a->peers.empty() || a->n_halo)
-            throw Invalid("solve: IBiCGStab needs f0 = A^T r0, supported on a single GPU only");
-        at_ = orig_ ? csr_transpose_reordered(ctx, orig_) : csr_transpose(ctx, a);
+        if (!a->peers.empty() || a->n_halo) {
+            // partitioned: A^T and its own halo plan were built at upload
+            if (!a->transposed) throw Invalid("solve: IBiCGStab on a partitioned matrix needs its A^T plan");
+            at_ = a->transposed.get();
+        } else {
+            at_ = orig_ ? csr_transpose_reordered(ctx, orig_) : csr_transpose(ctx, a);
+        }
     }
     n_ = a->n;
     len_ = n_ * m;
-    rows_alloc_ = a->n + a->n_halo;
+    // (room for the halo rows of A, and of A^T when f0 = A^T r0 is exchanged)
+    rows_alloc_ = a->n + std::max(a->n_halo, at_ ? at_->n_halo : 0);
     // only the vectors the method uses (C4 at m=32 is 8.4 GB per vector)
     std::vector<int> need;
     switch (method) {

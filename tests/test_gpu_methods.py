@@ -139,10 +139,18 @@ def test_new_methods_partitioned(ctx, world, method, form):
         assert np.array_equal(x.view(np.int64), want["x"][r0 * m:r1 * m].view(np.int64))
 
 
-def test_ibicgstab_partitioned_rejected(ctx):
+def test_ibicgstab_partitioned(ctx):
+    # f0 = A^T r0 across ranks (A^T halo plan built at upload), bitwise
     a = O.gen_stencil("convdiff7", 8, 8, 8)
-    with pytest.raises(AssertionError, match="single GPU"):
-        run_partitioned(a, O.rhs(a.n, 2, 1), 2, [0, 256, 512], "ibicgstab", "merged", tol=1e-8)
+    m = 2
+    b = O.rhs(a.n, m, 1)
+    want = O.solve(a, b, m, "ibicgstab", "merged", 1e-8)
+    parts = run_partitioned(a, b, m, [0, 256, 512], "ibicgstab", "merged", tol=1e-8)
+    for r, (rep, x) in enumerate(parts):
+        assert rep.iterations == want["iterations"]
+        assert np.array_equal(rep.residual_history.view(np.int64), want["hist"].view(np.int64))
+        r0, r1 = [0, 256, 512][r], [0, 256, 512][r + 1]
+        assert np.array_equal(x.view(np.int64), want["x"][r0 * m:r1 * m].view(np.int64))
 
 
 def test_matrix_market_ingest_partitioned(ctx, tmp_path):

@@ -53,7 +53,7 @@ def run_partitioned(a, b, m, bounds, method, form, grid=None, **kw):
 
 @pytest.mark.parametrize("world", [2, 3, 4])
 @pytest.mark.parametrize("method,form", [("bicgstab", "merged"), ("rbicgstab", "fused"), ("pipebicgstab", "merged"),
-                                         ("bicgstab", "fused"), ("pipebicgstab", "basic")])
+                                         ("bicgstab", "fused"), ("pipebicgstab", "basic"), ("ibicgstab", "merged")])
 def test_zslab_partition_equals_single_gpu(ctx, world, method, form):
     nx, ny, nz = 20, 18, 6 * world
     a = O.gen_stencil("convdiff7", nx, ny, nz)
@@ -100,3 +100,18 @@ def test_zslab_stencil_twin_equals_single_gpu(ctx, world, planes, kind, m, metho
         assert np.array_equal(bits(rep.residual_history), bits(want["hist"])), r
         r0, r1 = bounds[r], bounds[r + 1]
         assert np.array_equal(bits(x), bits(want["x"][r0 * m:r1 * m])), r
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ibicgstab_banded_partition_transpose_halo(ctx, world):
+    # f0 = A^T r0 across ranks: the random band is not structurally symmetric,
+    # so A^T's halo plan differs from A's; bitwise the single-GPU oracle
+    a = O.gen_banded(30_000, 5_000, 8, 16, 7)
+    m = 4
+    b = O.rhs(a.n, m, 2)
+    bounds = [0, 9_000, 30_000] if world == 2 else [0, 7_000, 19_500, 30_000]
+    want = O.solve(a, b, m, "ibicgstab", "merged", fixed=True, maxit=15)
+    parts = run_partitioned(a, b, m, bounds, "ibicgstab", "merged", fixed=True, max_iters=15)
+    for r, (rep, x) in enumerate(parts):
+        assert np.array_equal(bits(rep.residual_history), bits(want["hist"])), r
+        assert np.array_equal(bits(x), bits(want["x"][bounds[r] * m:bounds[r + 1] * m])), r

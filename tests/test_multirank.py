@@ -44,32 +44,39 @@ def _worker(rank, world, port, case, q):
             bounds = [p * nx * ny * 6 for p in range(world + 1)]
         x = np.random.default_rng(42).standard_normal(n * m)   # every rank can regenerate x ...
         r0, r1 = bounds[rank], bounds[rank + 1]
+
+        def exchange_and_multiply(pl):
+            # ... but only uses its own rows plus what the halo exchange delivers
+            xl = np.zeros((pl["n_own"] + pl["n_halo"]) * m)
+            xl[: pl["n_own"] * m] = x[r0 * m:r1 * m]
+            reqs, bufs = [], []
+            for peer in pl["peers"]:
+                if len(peer["send_rows"]):
+                    rows = peer["send_rows"].astype(np.int64)
+                    buf = torch.from_numpy(xl.reshape(-1, m)[rows].copy())
+                    bufs.append(buf)
+                    reqs.append(dist.isend(buf, dst=peer["part"]))
+            recv = []
+            for peer in pl["peers"]:
+                if peer["recv_count"]:
+                    buf = torch.zeros(peer["recv_count"], m, dtype=torch.float64)
+                    recv.append((peer, buf))
+                    reqs.append(dist.irecv(buf, src=peer["part"]))
+            for r in reqs:
+                r.wait()
+            for peer, buf in recv:
+                o = (pl["n_own"] + peer["recv_offset"]) * m
+                xl[o:o + buf.numel()] = buf.numpy().reshape(-1)
+            return O.spmv(O.Csr(pl["n_own"], pl["off"].astype(np.int64), pl["col"], pl["val"]), xl, m)
+
         pl = P.halo_plan(a, bounds, rank)
-        # ... but only uses its own rows plus what the halo exchange delivers
-        xl = np.zeros((pl["n_own"] + pl["n_halo"]) * m)
-        xl[: pl["n_own"] * m] = x[r0 * m:r1 * m]
-        reqs, bufs = [], []
-        for peer in pl["peers"]:
-            if len(peer["send_rows"]):
-                rows = peer["send_rows"].astype(np.int64)
-                buf = torch.from_numpy(xl.reshape(-1, m)[rows].copy())
-                bufs.append(buf)
-                reqs.append(dist.isend(buf, dst=peer["part"]))
-        recv = []
-        for peer in pl["peers"]:
-            if peer["recv_count"]:
-                buf = torch.zeros(peer["recv_count"], m, dtype=torch.float64)
-                recv.append((peer, buf))
-                reqs.append(dist.irecv(buf, src=peer["part"]))
-        for r in reqs:
-            r.wait()
-        for peer, buf in recv:
-            o = (pl["n_own"] + peer["recv_offset"]) * m
-            xl[o:o + buf.numel()] = buf.numpy().reshape(-1)
-        loc = O.Csr(pl["n_own"], pl["off"].astype(np.int64), pl["col"], pl["val"])
-        y_loc = O.spmv(loc, xl, m)
-        y_ref = O.spmv(O.Csr(n, a.row_offsets, a.col_indices, a.values), x, m)[r0 * m:r1 * m]
-        spmv_ok = bool(np.array_equal(y_loc.view(np.int64), y_ref.view(np.int64)))
+        glob = O.Csr(n, a.row_offsets, a.col_indices, a.values)
+        y_ref = O.spmv(glob, x, m)[r0 * m:r1 * m]
+        spmv_ok = bool(np.array_equal(exchange_and_multiply(pl).view(np.int64), y_ref.view(np.int64)))
+        # A^T x with the transpose plan (IBiCGStab's f0) == spmv_transpose, bitwise
+        yt_ref = O.spmv_transpose(glob, x, m)[r0 * m:r1 * m]
+        plt = P.halo_plan(a, bounds, rank, transpose=True)
+        spmvt_ok = bool(np.array_equal(exchange_and_multiply(plt).view(np.int64), yt_ref.view(np.int64)))
 
         # exact dot over the partition: int64 limb allreduce
         b = np.random.default_rng(7).standard_normal(n * m) * np.exp2(
@@ -80,7 +87,7 @@ def _worker(rank, world, port, case, q):
         got = P.exact_round(t.numpy(), m)
         want = O.dot_exact(x, b, m)
         dot_ok = bool(np.array_equal(got.view(np.int64), want.view(np.int64)))
-        q.put((rank, spmv_ok, dot_ok, len(pl["peers"])))
+        q.put((rank, spmv_ok, dot_ok, len(pl["peers"]), spmvt_ok))
     finally:
         dist.destroy_process_group()
 
@@ -102,3 +109,4 @@ def test_partitioned_spmv_and_exact_allreduce(world, case):
     assert all(r[1] for r in res), f"partitioned spmv mismatch: {res}"
     assert all(r[2] for r in res), f"limb allreduce mismatch: {res}"
     assert all(r[3] >= 1 for r in res)
+    assert all(r[4] for r in res), f"partitioned A^T x mismatch: {res}"
