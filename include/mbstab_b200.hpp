@@ -161,8 +161,15 @@ private:
 
 class DeviceMatrix {
 public:
-    DeviceMatrix(Device& dev, const core::CsrMatrix& A) {
+    DeviceMatrix(Device& dev, const core::CsrMatrix& A) : dev_(&dev) {
         check(mbg_csr_upload(dev.get(), A.n_rows, A.row_offsets.data(), A.col_indices.data(), A.values.data(), &h_));
+    }
+    // Structured-grid hint (mbg_csr_set_grid): a grid-neighbour operator gets the
+    // stencil twin (implicit columns, TMA-staged x planes); same bits.  Returns
+    // the stencil kind (7, 27) or 0.
+    int set_grid(int nx, int ny, int nz) {
+        check(mbg_csr_set_grid(dev_->get(), h_, nx, ny, nz));
+        return mbg_csr_stencil_kind(h_);
     }
     ~DeviceMatrix() { if (h_) mbg_csr_free(h_); }
     DeviceMatrix(const DeviceMatrix&) = delete;
@@ -170,6 +177,7 @@ public:
     const mbg_csr* get() const { return h_; }
 
 private:
+    Device* dev_ = nullptr;
     mbg_csr* h_ = nullptr;
 };
 
