@@ -131,15 +131,16 @@ __device__ __forceinline__ void digits_add_atomic(int64_t* d, double x) {
     if (s2) atomicAdd(u + c.j + 2, s2);
 }
 
-// Optimistic grow for the streaming loops: no per-element branch for
-// non-finite values -- a non-finite running sum only raises `bad` (sticky;
-// nothing is deposited once bad), and the caller recomputes this thread's
-// whole contribution with grow() below (a thread sees a non-finite product
-// or an overflowing partial sum only in pathological inputs).  Level 3 stays
-// a rarely taken branch.
-__device__ __forceinline__ void grow_fast(double (&a)[KEXP], double x, int64_t* slot, bool& bad) {
+// Lazy optimistic grow: not even a per-element finiteness test.  A non-finite
+// running sum is sticky in a[0] (inf and NaN survive every later addition), so
+// the caller tests a[0] once after its loop and re-walks the thread; the one
+// side effect before that test -- the rare level-3 deposit -- is taken only
+// while s0 is finite.  NEG = true deposits -e2 instead: the re-walk first
+// replays the fast pass with NEG to cancel what it deposited (exactly: the
+// replay repeats the same operations), then walks with the careful grow().
+template <bool NEG = false>
+__device__ __forceinline__ void grow_lazy(double (&a)[KEXP], double x, int64_t* slot) {
     const double s0 = __dadd_rn(a[0], x);
-    bad |= (static_cast<uint32_t>(__double2hiint(s0)) & 0x7ff00000u) == 0x7ff00000u;
     const double b0 = __dsub_rn(s0, a[0]);
     const double e0 = __dadd_rn(__dsub_rn(a[0], __dsub_rn(s0, b0)), __dsub_rn(x, b0));
     const double s1 = __dadd_rn(a[1], e0);
@@ -147,12 +148,12 @@ __device__ __forceinline__ void grow_fast(double (&a)[KEXP], double x, int64_t* 
     const double e1 = __dadd_rn(__dsub_rn(a[1], __dsub_rn(s1, b1)), __dsub_rn(e0, b1));
     a[0] = s0;
     a[1] = s1;
-    if (e1 != 0.0 && !bad) {
+    if (e1 != 0.0 && isfinite(s0)) {
         const double s2 = __dadd_rn(a[2], e1);
         const double b2 = __dsub_rn(s2, a[2]);
         const double e2 = __dadd_rn(__dsub_rn(a[2], __dsub_rn(s2, b2)), __dsub_rn(e1, b2));
         a[2] = s2;
-        if (e2 != 0.0) digits_add_atomic(slot, e2);
+        if (e2 != 0.0) digits_add_atomic(slot, NEG ? -e2 : e2);
     }
 }
 

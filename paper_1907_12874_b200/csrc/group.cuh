@@ -372,7 +372,7 @@ struct PPpG4 {
 
 // Programs whose dot products can be recomputed from the pass's inputs after
 // the pass (no input overwritten in place feeds a product): their streaming
-// loop uses the optimistic grow_fast and re-walks a thread's elements with the
+// loop uses the optimistic grow_lazy and re-walks a thread's elements with the
 // careful grow only if that thread met a non-finite value.
 template <class P, class = void>
 struct redo_safe_of { static constexpr bool value = false; };
@@ -577,8 +577,8 @@ __global__ void __launch_bounds__(256, minblocks_of<P>::value) group_kernel(Grou
 #pragma unroll
                 for (int d = 0; d < P::NDOT; ++d) {
                     if constexpr (RS) {
-                        grow_fast(acc[2 * d], p0[d], slot0[d], bad);
-                        grow_fast(acc[2 * d + 1], p1[d], slot1[d], bad);
+                        grow_lazy(acc[2 * d], p0[d], slot0[d]);
+                        grow_lazy(acc[2 * d + 1], p1[d], slot1[d]);
                     } else {
                         grow(acc[2 * d], p0[d], slot0[d]);
                         grow(acc[2 * d + 1], p1[d], slot1[d]);
@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(256, minblocks_of<P>::value) group_kernel(Grou
                 for (int i = 0; i < P::NOUT; ++i) a.out[i][qu] = o0[i];
 #pragma unroll
                 for (int d = 0; d < P::NDOT; ++d) {
-                    if constexpr (RS) grow_fast(acc[d], p0[d], slot0[d], bad);
+                    if constexpr (RS) grow_lazy(acc[d], p0[d], slot0[d]);
                     else grow(acc[d], p0[d], slot0[d]);
                 }
             }
@@ -606,9 +606,42 @@ __global__ void __launch_bounds__(256, minblocks_of<P>::value) group_kernel(Grou
     }
     pdl_trigger();   // streaming done: the successor may start filling freed SM slots
     if constexpr (RS) {
+#pragma unroll
+        for (int d = 0; d < P::NDOT * VEC; ++d) bad |= !isfinite(acc[d][0]);
         if (bad) {
-            // this thread met a non-finite value: recompute its products from the
-            // (unchanged) inputs and accumulate them with the careful grow
+            // this thread met a non-finite value: cancel what its fast pass
+            // deposited (replay with negated deposits), then recompute its
+            // products from the (unchanged) inputs with the careful grow
+#pragma unroll
+            for (int d = 0; d < ND * VEC; ++d)
+#pragma unroll
+                for (int i = 0; i < KEXP; ++i) acc[d][i] = 0.0;
+            for (int64_t qr = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; qr < npk; qr += stride) {
+                double in[P::NIN], o0[NO], p0[ND];
+                if constexpr (VEC == 2) {
+                    double o1[NO], p1[ND];
+                    Pk v[P::NIN];
+#pragma unroll
+                    for (int i = 0; i < P::NIN; ++i) v[i] = reinterpret_cast<const Pk*>(a.in[i])[qr];
+#pragma unroll
+                    for (int i = 0; i < P::NIN; ++i) in[i] = v[i].x;
+                    P::run(in, o0, p0, co0);
+#pragma unroll
+                    for (int i = 0; i < P::NIN; ++i) in[i] = v[i].y;
+                    P::run(in, o1, p1, co1);
+#pragma unroll
+                    for (int d = 0; d < P::NDOT; ++d) {
+                        grow_lazy<true>(acc[2 * d], p0[d], slot0[d]);
+                        grow_lazy<true>(acc[2 * d + 1], p1[d], slot1[d]);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < P::NIN; ++i) in[i] = a.in[i][qr];
+                    P::run(in, o0, p0, co0);
+#pragma unroll
+                    for (int d = 0; d < P::NDOT; ++d) grow_lazy<true>(acc[d], p0[d], slot0[d]);
+                }
+            }
 #pragma unroll
             for (int d = 0; d < ND * VEC; ++d)
 #pragma unroll
