@@ -109,7 +109,10 @@ __global__ void stencil_fill_kernel(GridMap gm, int nzg, int by, int S, int ntx,
         int xi, yi, zi;
         grid_coords(gm.row_begin + i, nx, ny, xi, yi, zi);
         const int64_t t = static_cast<int64_t>(yi / by) * ntx + xi / STENCIL_BX;
-        const int r = (yi % by) * STENCIL_BX + xi % STENCIL_BX;
+        // row slot inside the chunk: odd lines swap 4-point blocks pairwise
+        // (bank spread for the m = 8 lane layout; 4-aligned blocks stay contiguous)
+        const int ly = yi % by;
+        const int r = ly * STENCIL_BX + ((xi % STENCIL_BX) ^ ((ly & 1) << 2));
         unsigned char* c = chunks + (t * gm.nzl + (zi - gm.z0)) * chunk_bytes;
         double* V = reinterpret_cast<double*>(c);
         uint32_t* MK = reinterpret_cast<uint32_t*>(c + static_cast<int64_t>(S) * RT * 8);
@@ -391,10 +394,13 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
         gx = (warp & 1) * 4 + gl;
         gy = warp >> 1;
     } else {                        // 8 groups per warp, two lines
-        gx = (warp & 1) * 4 + (gl & 3);
-        gy = (warp >> 1) * 2 + (gl >> 2);
+        // an LDS.128 is served 8 lanes (128 B) at a time: the two groups of a
+        // quarter warp take the same x on two lines (odd line width 35 ->
+        // opposite bank halves), conflict-free
+        gx = (warp & 1) * 4 + (gl >> 1);
+        gy = (warp >> 1) * 2 + (gl & 1);
     }
-    const int lx0 = gx * 4, cp = cl * 2, r0 = gy * STENCIL_BX + lx0;
+    const int lx0 = gx * 4, cp = cl * 2, r0 = gy * STENCIL_BX + (lx0 ^ ((gy & 1) << 2));
     // one expansion per (dot, column); (one per row of the lane's 4 as well
     // -- independent chains -- was measured slower: 226 registers, 1 block/SM)
     constexpr int ND = StencilEpiDots<EPI>::value;
