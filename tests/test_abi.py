@@ -5,6 +5,7 @@ import re
 from pathlib import Path
 
 import pytest
+import torch  # noqa: F401  -- load torch before this file dlopens the C-ABI library repeatedly
 
 import paper_1907_12874_b200 as P
 
