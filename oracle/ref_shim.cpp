@@ -228,9 +228,24 @@ ColumnScalars div(const ColumnScalars& a, const ColumnScalars& b) {
 
 }  // namespace
 
+// hist (nullable): (maxit+1)*m relative recursive residuals, h_0 = sqrt(rho0/bb),
+// h_{j+1} = sqrt(max(res2,0)/bb) -- the same definition as the GPU solver's.
+extern "C" int ref_solve_hist(int method, int64_t n, const int64_t* off, const int32_t* col,
+                              const double* val, int m, const double* b, double* x, double tol,
+                              int fixed, int maxit, int threads, int* iters_out, double* loop_seconds,
+                              double* hist);
+
 extern "C" int ref_solve(int method, int64_t n, const int64_t* off, const int32_t* col,
                          const double* val, int m, const double* b, double* x, double tol,
                          int fixed, int maxit, int threads, int* iters_out, double* loop_seconds) {
+    return ref_solve_hist(method, n, off, col, val, m, b, x, tol, fixed, maxit, threads, iters_out, loop_seconds,
+                          nullptr);
+}
+
+extern "C" int ref_solve_hist(int method, int64_t n, const int64_t* off, const int32_t* col,
+                              const double* val, int m, const double* b, double* x, double tol,
+                              int fixed, int maxit, int threads, int* iters_out, double* loop_seconds,
+                              double* hist) {
     try {
         CsrMatrix A = make_csr(n, off, col, val);
         enum { X, B, R, R0, P, V, S, TT, Z, VH, TH, RT, Q, W, Y, NV };
@@ -246,6 +261,11 @@ extern "C" int ref_solve(int method, int64_t n, const int64_t* off, const int32_
         cx.run({{U(R, {T(one, B), T(mone, TT)}), U(R0, {T(one, R)}), D(R0, R0, 0), D(B, B, 1)}});
         ColumnScalars rho = cx.dots[0], bb = cx.dots[1], eps2(m);
         for (int c = 0; c < m; ++c) eps2[c] = (tol * tol) * bb[c];
+        auto record = [&](int j, const ColumnScalars& r2) {
+            if (!hist) return;
+            for (int c = 0; c < m; ++c) hist[static_cast<size_t>(j) * m + c] = std::sqrt((r2[c] > 0.0 ? r2[c] : 0.0) / bb[c]);
+        };
+        record(0, rho);
         auto below = [&](const ColumnScalars& r2) {
             for (int c = 0; c < m; ++c) if (!(r2[c] < eps2[c])) return false;
             return true;
@@ -263,6 +283,7 @@ extern "C" int ref_solve(int method, int64_t n, const int64_t* off, const int32_
                 cx.run({{D(TT, S, 0), D(TT, TT, 1), D(S, S, 2)}});
                 ColumnScalars omega = div(cx.dots[0], cx.dots[1]);
                 ColumnScalars res2 = cx.dots[2] - omega * cx.dots[0];
+                record(it + 1, res2);
                 const bool conv = !fixed && below(res2);
                 cx.run({{U(X, {T(one, X), T(alpha, P), T(omega, S)}), U(R, {T(one, S), T(-omega, TT)}),
                          D(R, R0, 0)}});
@@ -285,6 +306,7 @@ extern "C" int ref_solve(int method, int64_t n, const int64_t* off, const int32_
                 vec[Q].data = vec[TT].data;  // identity M^-1
                 ColumnScalars omega = div(cx.dots[0], cx.dots[1]);
                 ColumnScalars res2 = cx.dots[3] - omega * cx.dots[0];
+                record(it + 1, res2);
                 ColumnScalars psi = cx.dots[2];
                 cx.run({{U(R, {T(one, RT), T(-omega, TT)})}});
                 if (!fixed && below(res2)) {
@@ -311,6 +333,7 @@ extern "C" int ref_solve(int method, int64_t n, const int64_t* off, const int32_
                 core::spmv(A, vec[Z], vec[V], nullptr, threads);
                 omega = div(cx.dots[0], cx.dots[1]);
                 ColumnScalars res2 = cx.dots[2] - omega * cx.dots[0];
+                record(it + 1, res2);
                 cx.run({{U(X, {T(one, X), T(alpha, P), T(omega, Q)}), U(R, {T(one, Q), T(-omega, Y)})}});
                 if (!fixed && below(res2)) { ++it; break; }
                 cx.run({{U(W, {T(one, Y), T(-omega, TT), T(omega * alpha, V)}), D(R0, R, 0), D(R0, Z, 1),

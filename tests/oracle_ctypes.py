@@ -279,6 +279,26 @@ def ref_read_matrix_market(path):
     return Csr(n.value, off, col, val)
 
 
+def ref_solve_hist(a: Csr, b: np.ndarray, m: int, method="bicgstab", tol=1e-8, fixed=False, maxit=1000,
+                   threads=1):
+    """ref_solve plus its relative residual history ((iterations+1) x m)."""
+    lib = ref()
+    if not getattr(lib, "_hist_bound", False):
+        lib.ref_solve_hist.argtypes = [C.c_int, C.c_int64, _i64p, _i32p, _f64p, C.c_int, _f64p, _f64p,
+                                       C.c_double, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int),
+                                       C.POINTER(C.c_double), _f64p]
+        lib.ref_solve_hist.restype = C.c_int
+        lib._hist_bound = True
+    x = np.zeros(a.n * m)
+    hist = np.full((maxit + 1) * m, np.nan)
+    its = C.c_int()
+    secs = C.c_double()
+    rc = lib.ref_solve_hist(METHODS[method], a.n, a.off, a.col, a.val, m, np.ascontiguousarray(b), x, tol,
+                            int(bool(fixed)), maxit, threads, C.byref(its), C.byref(secs), hist)
+    assert rc == 0, lib.ref_last_error()
+    return x, its.value, hist.reshape(maxit + 1, m)[: its.value + 1].copy()
+
+
 def ref_write_matrix_market(a: Csr, path) -> None:
     assert ref().ref_write_matrix_market(str(path).encode(), a.n, a.off, a.col, a.val) == 0
 

@@ -365,3 +365,20 @@ def test_poisson5_solves_dense_oracle():
     for method in METHODS:
         r = O.solve(a, b, 1, method, tol=1e-10)
         assert r["converged"] and np.max(np.abs(r["x"] - x)) <= 1e-8, method
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("method", METHODS[:3])
+def test_unmodified_reference_history_context(method):
+    """the unmodified reference (naive thread-blocked dots)
+    against the exact oracle (= the GPU path, bitwise): relative residual
+    histories agree to 1e-10 over the first 10 iterations; iteration counts
+    drift by a few, as they do between the reference's own thread counts
+    (profiles/r01m_naive_dot_context.md)."""
+    a = O.gen_stencil("poisson7", 20, 20, 20)
+    b = O.rhs(a.n, 2, 0)
+    ex = O.solve(a, b, 2, method, "merged", 1e-8)
+    _, its, h = O.ref_solve_hist(a, b, 2, method, 1e-8, threads=1)
+    assert abs(its - ex["iterations"]) <= 6
+    k = 11
+    assert np.max(np.abs(h[:k] - ex["hist"][:k]) / ex["hist"][:k]) <= 1e-10
