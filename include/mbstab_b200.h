@@ -60,6 +60,11 @@ const char* mbg_version(void);
 int mbg_ctx_create(int device, mbg_ctx** out);
 int mbg_ctx_destroy(mbg_ctx* ctx);
 int mbg_ctx_synchronize(mbg_ctx* ctx);
+/* Small classical solves (n*m <= 2^20, m a power of two <= 32, one GPU) run
+ * their whole iteration loop in one cooperative launch -- bitwise the same
+ * iterations as the multi-kernel path.  enable = 0 forces the multi-kernel
+ * path on this context (default 1; MBG_SMALL=0 turns it off process-wide). */
+int mbg_ctx_set_small_path(mbg_ctx* ctx, int enable);
 /* Multi-GPU: join a communicator of `world` ranks (one process per GPU).
  * nccl_id is the 128-byte ncclUniqueId created by rank 0 (mbg_comm_unique_id)
  * and broadcast by the caller (e.g. torch.distributed). */

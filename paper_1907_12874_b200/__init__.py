@@ -159,6 +159,10 @@ class Context:
     def synchronize(self) -> None:
         check(lib().mbg_ctx_synchronize(self.h))
 
+    def set_small_path(self, enable: bool) -> None:
+        """Small classical solves in one cooperative launch (default on)."""
+        check(lib().mbg_ctx_set_small_path(self.h, int(bool(enable))))
+
     def launches(self) -> int:
         return int(lib().mbg_ctx_launches(self.h))
 

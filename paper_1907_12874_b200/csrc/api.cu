@@ -528,6 +528,13 @@ extern "C" int mbg_csr_reordered(const mbg_csr* a) { return a && a->reordered ? 
 
 extern "C" int mbg_csr_stencil_kind(const mbg_csr* a) { return a && a->stencil ? a->stencil->kind : 0; }
 
+extern "C" int mbg_ctx_set_small_path(mbg_ctx* ctx, int enable) {
+    return guarded([&] {
+        if (!ctx) throw Invalid("null context");
+        ctx->small_path = enable != 0;
+    });
+}
+
 extern "C" int mbg_mv_alloc(mbg_ctx* ctx, int64_t n, int m, mbg_mv** out) {
     return guarded([&] {
         use(ctx);

@@ -79,6 +79,7 @@ struct mbg_ctx {
     mbg::DevBuf<double> scratch_f64;
     mbg::DevBuf<int> scratch_ctl;
     int64_t launches = 0;            // kernels launched by this context
+    bool small_path = true;          // one-launch loop for small classical solves (small.cu)
     // pool of large work vectors reused across solves (no cudaMalloc per solve)
     std::vector<mbg::DevBuf<double>> pool;
     // pinned host memory reused across calls: control-word snapshots and the

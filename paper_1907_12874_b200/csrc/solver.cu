@@ -29,6 +29,7 @@
 #include "kernels.hpp"
 #include "scalar.cuh"
 #include "solver.hpp"
+#include "small.hpp"
 #include "stencil.hpp"
 
 namespace mbg {
@@ -622,7 +623,35 @@ void Solver::run(const double* b, double* x, bool use_graph, int chunk) {
         marks_.clear();
     }
     const int64_t setup_launches = launches_;
-    if (maxit_ > 0) {
+    // small systems (cannot fill the GPU): the whole classical loop in one
+    // cooperative launch (small.cu), bitwise the same iterations
+    const bool small = maxit_ > 0 && method_ == MBG_BICGSTAB && form_ != MBG_BASIC && !ctx_->comm && !orig_ &&
+                       !profile_ && ctx_->small_path && small_path_enabled() && len_ <= SMALL_MAX_LEN &&
+                       (m_ == 1 || m_ == 2 || m_ == 4 || m_ == 8 || m_ == 16 || m_ == 32);
+    if (small) {
+        SmallArgs sa{};
+        sa.n = n_;
+        sa.m = m_;
+        sa.off = a_->off.p;
+        sa.col = a_->col.p;
+        sa.val = a_->val.p;
+        sa.x = x_;
+        sa.r = w(V_R);
+        sa.r0 = w(V_R0);
+        sa.p = w(V_P);
+        sa.v = w(V_V);
+        sa.s = w(V_S);
+        sa.t = w(V_T);
+        sa.sc = scal_.p;
+        sa.ctl = ctl_.p;
+        sa.hist = hist_.p;
+        sa.slots = slots_.p;
+        sa.fused = form_ == MBG_FUSED;
+        sa.fixed = fixed_;
+        sa.maxit = maxit_;
+        sa.tol2 = tol_ * tol_;
+        launches_ += launch_small_classical(ctx_->stream, sa, ctx_->num_sms);
+    } else if (maxit_ > 0) {
         if (use_graph) {
             cudaGraph_t g;
             MBG_CUDA(cudaStreamBeginCapture(ctx_->stream, cudaStreamCaptureModeThreadLocal));
