@@ -26,18 +26,37 @@ namespace mbg {
 
 namespace {
 
-// y = A x over every (row, column) element, CSR order, from 0.0
-__device__ void small_spmm(const SmallArgs& a, const double* __restrict__ x, double* __restrict__ y) {
-    const int64_t len = a.n * a.m;
+// y = A x and, for the element just computed, the exact dots of program P on
+// (y, w) -- the thread owns its element, so no barrier separates the SpMM from
+// the dot pass (PDot2: (y, w); PClassicOmega: (y, w), (y, y), (w, w);
+// PClassicPhiPsi: (y, w), (y, y))
+template <class P>
+__device__ void small_spmm_dots(const SmallArgs& a, const double* __restrict__ x, double* __restrict__ y,
+                                const double* __restrict__ w, double* sh) {
+    constexpr int ND = P::NDOT;
+    const int m = a.m;
+    const int c0 = threadIdx.x % m;
+    double acc[ND][KEXP];
+#pragma unroll
+    for (int d = 0; d < ND; ++d)
+#pragma unroll
+        for (int k = 0; k < KEXP; ++k) acc[d][k] = 0.0;
+    const int64_t len = a.n * m;
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < len;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t row = e / a.m;
-        const int c = static_cast<int>(e - row * a.m);
-        double acc = 0.0;
+        const int64_t row = e / m;
+        double yv = 0.0;
         for (int k = a.off[row]; k < a.off[row + 1]; ++k)
-            acc = __dadd_rn(acc, __dmul_rn(a.val[k], x[static_cast<int64_t>(a.col[k]) * a.m + c]));
-        y[e] = acc;
+            yv = __dadd_rn(yv, __dmul_rn(a.val[k], x[static_cast<int64_t>(a.col[k]) * m + c0]));
+        y[e] = yv;
+        const double v[2] = {yv, w[e]};
+        double pr[ND];
+        P::run(v, nullptr, pr, nullptr);
+#pragma unroll
+        for (int d = 0; d < ND; ++d) grow(acc[d], pr[d], a.slots + (static_cast<int64_t>(d) * m + c0) * NSLOT);
     }
+    block_combine<ND>(acc, m, [&](int q, int k) { return a.slots + (static_cast<int64_t>(q) * m + k) * NSLOT; },
+                      sh);
 }
 
 // One merged line over all elements (group_kernel's VEC = 1 path with the
@@ -112,9 +131,7 @@ __global__ void __launch_bounds__(256) small_classical_kernel(SmallArgs a) {
         grid.sync();   // the new scalars (and the stop word) are visible to every block
     };
     for (int it = 0; it < a.maxit && !*stop; ++it) {
-        small_spmm(a, a.p, a.v);                                                  // v = A p
-        grid.sync();
-        small_group<PDot2>(a, Line{{a.v, a.r0}, {}, {}}, 0, sh);                         // delta = (v, r0)
+        small_spmm_dots<PDot2>(a, a.p, a.v, a.r0, sh);                            // v = A p ; delta = (v, r0)
         scalars(P_C_ALPHA, 1);
         if (*stop) break;
         if (a.fused)
@@ -122,12 +139,10 @@ __global__ void __launch_bounds__(256) small_classical_kernel(SmallArgs a) {
         else
             small_group<PUpd2>(a, Line{{a.r, a.v}, {a.s}, {S_ONE, S_NALPHA}}, 0, sh);     // s = r - alpha v
         grid.sync();
-        small_spmm(a, a.s, a.t);                                                  // t = A s
-        grid.sync();
         if (a.fused)
-            small_group<PClassicPhiPsi>(a, Line{{a.t, a.s}, {}, {}}, 0, sh);              // phi psi -> slots 0,1
+            small_spmm_dots<PClassicPhiPsi>(a, a.s, a.t, a.s, sh);                 // t = A s ; phi psi -> slots 0,1
         else
-            small_group<PClassicOmega>(a, Line{{a.t, a.s}, {}, {}}, 0, sh);               // phi psi theta
+            small_spmm_dots<PClassicOmega>(a, a.s, a.t, a.s, sh);                  // t = A s ; phi psi theta
         scalars(P_C_OMEGA, 3);
         if (*stop) break;
         small_group<PClassicXR>(a, Line{{a.x, a.p, a.s, a.t, a.r0}, {a.x, a.r}, {S_ALPHA, S_OMEGA, S_NOMEGA}}, 0, sh);
