@@ -148,7 +148,8 @@ double* mbg_mv_device_ptr(mbg_mv* v);
 int mbg_spmv(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* x, mbg_mv* y);
 /* core::spmv_transpose (include/mbstab/core/spmv.hpp:19-21, src/core/spmv.cpp:76-90):
  * y = A^T x, every y(j, c) summed over source rows i in ascending order from
- * 0.0 (the reference's serial loop), bit for bit.  Single-GPU matrices. */
+ * 0.0 (the reference's serial loop), bit for bit.  Partitioned matrices use
+ * the A^T halo plan built at upload (the rank's rows of y = its columns of A). */
 int mbg_spmv_transpose(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* x, mbg_mv* y);
 double mbg_spmv_traffic_bytes(int64_t n, int64_t nnz, int m);           /* Eq. (3) */
 double mbg_spmv_compulsory_bytes(int64_t n, int64_t nnz, int m);        /* x once */

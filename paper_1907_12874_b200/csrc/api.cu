@@ -638,9 +638,19 @@ extern "C" int mbg_spmv_transpose(mbg_ctx* ctx, const mbg_csr* a, const mbg_mv* 
         if (!a || !x || !y) throw Invalid("spmv_transpose: null argument");
         if (x->n != a->n || y->n != a->n || x->m != y->m) throw Invalid("spmv: dimension mismatch");
         if (x == y || x->data.p == y->data.p) throw Invalid("spmv: x and y must be distinct storage");
-        if (!a->peers.empty() || a->n_halo) throw Invalid("spmv_transpose: single-GPU matrices only");
-        const mbg_csr* at = csr_transpose(ctx, a);
-        ctx->launches += apply_operator(ctx, at, x->m, x->data.p, y->data.p, nullptr);
+        const bool part = !a->peers.empty() || a->n_halo;
+        // partitioned: A^T with its own halo plan, built at upload
+        const mbg_csr* at = part ? a->transposed.get() : csr_transpose(ctx, a);
+        if (!at) throw Invalid("spmv_transpose: partitioned matrix without its A^T plan");
+        const int m = x->m;
+        double* xin = x->data.p;
+        if (at->n_halo) {   // stage x in a buffer with A^T's halo room
+            ctx->scratch_f64.ensure(static_cast<size_t>(at->n + at->n_halo) * m);
+            MBG_CUDA(cudaMemcpyAsync(ctx->scratch_f64.p, xin, static_cast<size_t>(at->n) * m * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, ctx->stream));
+            xin = ctx->scratch_f64.p;
+        }
+        ctx->launches += apply_operator(ctx, at, m, xin, y->data.p, nullptr);
         MBG_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }

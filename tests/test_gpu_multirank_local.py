@@ -115,3 +115,39 @@ def test_ibicgstab_banded_partition_transpose_halo(ctx, world):
     for r, (rep, x) in enumerate(parts):
         assert np.array_equal(bits(rep.residual_history), bits(want["hist"])), r
         assert np.array_equal(bits(x), bits(want["x"][bounds[r] * m:bounds[r + 1] * m])), r
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_spmv_transpose(ctx, world):
+    # core::spmv_transpose across ranks (A^T halo plan), bitwise the serial order
+    a = O.gen_banded(12_000, 3_000, 6, 12, 5)
+    m = 3
+    x = np.random.default_rng(9).standard_normal(a.n * m)
+    want = O.spmv_transpose(a, x, m)
+    bounds = [a.n * p // world for p in range(world + 1)]
+    ctxs = [P.Context(0) for _ in range(world)]
+    P.local_group(ctxs)
+    A = P.CsrMatrix(a.n, a.off, a.col, a.val)
+    out, err = [None] * world, [None] * world
+
+    def rank(r):
+        try:
+            d = ctxs[r].upload(A, bounds, r)
+            r0, r1 = bounds[r], bounds[r + 1]
+            X = ctxs[r].multivector(r1 - r0, m, x[r0 * m:r1 * m])
+            Y = ctxs[r].multivector(r1 - r0, m)
+            P.spmv_transpose(ctxs[r], d, X, Y)
+            out[r] = Y.download()
+        except Exception as e:  # noqa: BLE001
+            err[r] = e
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    for c in ctxs:
+        c.close()
+    assert not any(err), err
+    for r in range(world):
+        assert np.array_equal(bits(out[r]), bits(want[bounds[r] * m:bounds[r + 1] * m])), r
