@@ -8,17 +8,25 @@
 // present slots in slot order IS the CSR order.  The twin built at
 // mbg_csr_set_grid therefore drops the column indices:
 //
-//   chunk (tile t, plane z) = values[S][32*BY] (slot-major, 0 where a slot is
-//                             absent) | mask[32*BY] (bit s: slot s present)
+//   chunk (tile t, plane z) = values[S][32*BY] (slot-major; -0.0 where a slot
+//                             is absent) | mask[32*BY] (bit s: slot s present;
+//                             bit 31: the row misses an in-grid neighbour)
 //
-// for xy-tiles of 32 x BY points.  One block computes one tile over a range
-// of planes ("z-march"): a ring of four x planes, each a TMA tensor box
-// (m, 34|35, BY+2, 1) of the x block viewed as an (nz, ny, nx, m) tensor
-// (out-of-grid points zero-filled, never used: their slots are absent),
-// and a ring of two value chunks (cp.async.bulk); plane z+2 and chunk z+1
-// are in flight while plane z computes.  A lane owns 4 consecutive points
-// along x and 2 columns: the 6 x points of one stencil line are loaded from
-// shared memory once and reused by the 3 dx slots of the 4 rows.
+// for xy-tiles of 32 x BY points (rows of odd lines swap 4-point blocks: bank
+// spread).  An absent slot's x operand is the TMA zero fill of an out-of-grid
+// point, and (-0.0)*(+0.0) = -0.0 is the exact identity of IEEE addition, so
+// only bit-31 rows need a predicate.
+//
+// Kernel: persistent and warp-specialised.  Block ranges of whole tiles (or
+// z-segments) start at the same z and march through the planes, so an x plane
+// is fetched from HBM about once and its halo lines hit L2 for the
+// neighbouring tiles.  A producer warp streams the x planes as TMA tensor
+// boxes (m, 34|35, BY+2, 1) of x viewed as (planes, ny, nx, m) -- a second
+// tensor map addresses the halo planes of a z-slab partition -- into a 5-deep
+// ring and the value chunks (cp.async.bulk) into a 3-deep ring, gated by
+// full / empty mbarriers.  A compute lane owns 4 consecutive points along x
+// and 2 columns: the 6 x points of a stencil line are loaded once from shared
+// memory and reused by the 3 dx slots of the 4 rows.
 //
 // Bytes per SpMM (the roofline's algorithmic count): 16*N*m (x once, y once)
 // + 8*nnz (values) + 4*N (masks); versus 16*N*m + 12*nnz + 4*N for CSR.
@@ -27,7 +35,6 @@
 
 #include <algorithm>
 #include <cstdlib>
-#include <cstdio>
 #include <mutex>
 #include <vector>
 
