@@ -19,6 +19,7 @@ GRIDS = {
     "stencil27_33x10x7": ("stencil27", (33, 10, 7), 2),
     "stencil27_3x3x3": ("stencil27", (3, 3, 3), 2),
     "convdiff7_1x1x40": ("convdiff7", (1, 1, 40), 1),
+    "poisson5_45x23x1": ("poisson5", (45, 23, 1), 0),   # 2-D 5-point: one plane
 }
 
 
