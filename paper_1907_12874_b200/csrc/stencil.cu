@@ -319,17 +319,27 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
     const int rb = blockIdx.x / CS;
     // ranges move through z in lockstep (every range starts at the same z), so
     // a plane of x is read by all its neighbouring tiles at about the same time
-    int64_t s0, s1;
-    if (g.kt > 0) {
-        s0 = static_cast<int64_t>(rb) * g.kt * g.nz;
-        s1 = s0 + static_cast<int64_t>(g.kt) * g.nz;
-    } else {
-        const int nseg = (g.nz + g.zseg - 1) / g.zseg;
-        const int t = rb / nseg, sg = rb % nseg;
-        s0 = static_cast<int64_t>(t) * g.nz + static_cast<int64_t>(sg) * g.zseg;
-        s1 = static_cast<int64_t>(t) * g.nz + min(g.nz, (sg + 1) * g.zseg);
-    }
-    if (s1 > g.steps) s1 = g.steps;
+    // the block's segments (tile, first plane, planes): with whole tiles per
+    // block the tiles are strided by the number of ranges, so at any moment all
+    // blocks work on one contiguous band of tiles at about the same plane --
+    // a tile's y neighbours (t +- ntx) are in the band and their shared halo
+    // lines hit L2 (C4 320^3 m=32: DRAM reads 15.0 -> 11.0 GB, 3.67 -> 3.38 ms
+    // per SpMM, against contiguous tile ranges); else one z-segment of a tile
+    const int ntiles = static_cast<int>(g.steps / g.nz);
+    const int nsegs_b = g.kt > 0 ? g.kt : 1;
+    auto segment = [&](int si, int& t, int& za, int& steps) {
+        if (g.kt > 0) {
+            t = rb + si * g.nranges;
+            za = 0;
+            steps = t < ntiles ? g.nz : 0;
+        } else {
+            const int nseg = (g.nz + g.zseg - 1) / g.zseg;
+            t = rb / nseg;
+            const int sg = rb % nseg;
+            za = sg * g.zseg;
+            steps = t < ntiles ? min(g.nz, za + g.zseg) - za : 0;
+        }
+    };
     const int tid = threadIdx.x;
     if (tid == 0) {
         for (int b = 0; b < XR; ++b) {
@@ -373,17 +383,16 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
                          static_cast<uint32_t>(CB), &vfull[b]);
                 ++j;
             };
-            for (int64_t s = s0; s < s1;) {
-                const int t = static_cast<int>(s / g.nz), za = static_cast<int>(s % g.nz);
-                const int64_t left = s1 - s;
-                const int steps = static_cast<int>(left < g.nz - za ? left : g.nz - za);
+            for (int si = 0; si < nsegs_b; ++si) {
+                int t, za, steps;
+                segment(si, t, za, steps);
+                if (steps <= 0) break;
                 plane(t, za - 1);
                 plane(t, za);
                 for (int i = 0; i < steps; ++i) {
                     plane(t, za + i + 1);
                     chunk(t, za + i);
                 }
-                s += steps;
             }
         }
         // no griddepcontrol.launch_dependents here: the producer finishes long
@@ -419,10 +428,10 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
         for (int i = 0; i < KEXP; ++i) ex[q][i] = 0.0;
     const int col0 = h * MC + cp;   // this lane's first column
     int64_t Q = 0, j = 0;
-    for (int64_t s = s0; s < s1;) {
-        const int t = static_cast<int>(s / g.nz), za = static_cast<int>(s % g.nz);
-        const int64_t left = s1 - s;
-                const int steps = static_cast<int>(left < g.nz - za ? left : g.nz - za);
+    for (int si = 0; si < nsegs_b; ++si) {
+        int t, za, steps;
+        segment(si, t, za, steps);
+        if (steps <= 0) break;
         const int xg0 = (t % g.ntx) * STENCIL_BX + lx0, yg = (t / g.ntx) * BY + gy;
         const bool yok = yg < g.ny;
         for (int i = 0; i < steps; ++i, ++j) {
@@ -499,7 +508,6 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
             mbar_arrive(&xempty[(Q + steps + 1) % XR]);
         }
         Q += steps + 2;
-        s += steps;
     }
     if constexpr (EPI != 0) {
         // every load was consumed: the x ring is free scratch for the combine
