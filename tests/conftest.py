@@ -12,6 +12,16 @@ sys.path.insert(0, str(Path(__file__).resolve().parent))
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
     config.addinivalue_line("markers", "slow: large-size cases")
+    # test infrastructure only: compile the sm_100a library (nvcc cross-compiles
+    # without a GPU) if a fresh checkout runs the tests before __graft_entry__.build();
+    # the product itself never builds or falls back at run time
+    lib = ROOT / "paper_1907_12874_b200" / "libmbstab_b200.so"
+    if not lib.exists():
+        import shutil
+        import subprocess
+        if shutil.which("make") and (shutil.which("nvcc") or Path("/usr/local/cuda/bin/nvcc").exists()):
+            subprocess.run(["make", "-s", "-j", str(os.cpu_count() or 4), "-C",
+                            str(ROOT / "paper_1907_12874_b200" / "csrc")], check=False)
 
 
 @pytest.fixture(scope="session")
