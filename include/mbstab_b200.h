@@ -123,7 +123,7 @@ int mbg_csr_reordered(const mbg_csr* a);   /* 1 when the solver uses a reordered
 /* Stencil twin built by mbg_csr_set_grid when every nonzero couples a grid
  * point with itself or one of its 26 neighbours: 7 (face neighbours only) or
  * 27; 0 = none.  The SpMM then reads no column indices and stages x as TMA
- * plane boxes (m in {8, 16, 32}; bitwise the CSR result; MBG_STENCIL=0 off). */
+ * plane boxes (m in {4, 8, 16, 32}; bitwise the CSR result; MBG_STENCIL=0 off). */
 int mbg_csr_stencil_kind(const mbg_csr* a);
 int mbg_csr_free(mbg_csr* a);
 int64_t mbg_csr_rows(const mbg_csr* a);   /* local rows */

@@ -212,7 +212,7 @@ class DeviceCsr:
 
     def set_grid(self, nx: int, ny: int, nz: int) -> bool:
         """Structured-grid hint: a grid-neighbour operator gets a stencil twin
-        (implicit columns, TMA-staged x planes; m in {8, 16, 32}) and long-row
+        (implicit columns, TMA-staged x planes; m in {4, 8, 16, 32}) and long-row
         stencils a brick-reordered twin for the other m (bitwise-identical
         results).  Returns True if reordered."""
         check(lib().mbg_csr_set_grid(self.ctx.h, self.h, nx, ny, nz))

@@ -50,6 +50,12 @@ namespace mbg {
 
 // ---- analysis and layout (device kernels over the uploaded CSR) -----------
 
+// Row slot swizzle inside a chunk: odd lines (BY = 4 layout) or lines 1-3 of
+// each 4 (BY = 8 layout, m = 4) swap 4-point blocks, so the value / mask loads
+// of the groups that share a quarter warp fall on different banks.
+__host__ __device__ constexpr int stencil_swz(int by, int ly) { return by == 8 ? ((ly & 3) << 2) : ((ly & 1) << 2); }
+
+
 __device__ __forceinline__ void grid_coords(int64_t i, int nx, int ny, int& x, int& y, int& z) {
     x = static_cast<int>(i % nx);
     const int64_t t = i / nx;
@@ -119,7 +125,7 @@ __global__ void stencil_fill_kernel(GridMap gm, int nzg, int by, int S, int ntx,
         // row slot inside the chunk: odd lines swap 4-point blocks pairwise
         // (bank spread for the m = 8 lane layout; 4-aligned blocks stay contiguous)
         const int ly = yi % by;
-        const int r = ly * STENCIL_BX + ((xi % STENCIL_BX) ^ ((ly & 1) << 2));
+        const int r = ly * STENCIL_BX + ((xi % STENCIL_BX) ^ stencil_swz(by, ly));
         unsigned char* c = chunks + (t * gm.nzl + (zi - gm.z0)) * chunk_bytes;
         double* V = reinterpret_cast<double*>(c);
         uint32_t* MK = reinterpret_cast<uint32_t*>(c + static_cast<int64_t>(S) * RT * 8);
@@ -170,9 +176,10 @@ struct StencilShape {
     static constexpr int LPR = MC / 2;                       // lanes per 4-point group (2 columns each)
     static constexpr int THREADS = 8 * BY * LPR;             // compute threads: 8 groups along x, BY along y
     static constexpr int NCW = THREADS / 32;                 // compute warps (+1 producer warp)
-    static constexpr int LW = MC == 8 ? 35 : 34;             // x-plane line width (35: bank spread at m = 8)
+    static constexpr int LW = MC <= 8 ? 35 : 34;             // x-plane line width (35: bank spread at m <= 8)
     static constexpr int RT = STENCIL_BX * BY;               // rows per tile plane
-    static constexpr int PLANE = LW * (BY + 2) * MC;         // doubles per x plane
+    static constexpr int PLANE = LW * (BY + 2) * MC;         // doubles per x plane (the TMA box)
+    static constexpr int PSTRIDE = (PLANE + 15) / 16 * 16;   // ring slot stride: 128-byte aligned boxes
 };
 
 template <int ST, int BY>
@@ -192,7 +199,7 @@ constexpr int STENCIL_HEAD = 256;               // mbarriers
 
 template <int MC, int ST, int BY>
 __host__ __device__ constexpr int stencil_smem() {
-    return STENCIL_HEAD + StencilRings<MC>::XR * StencilShape<MC, BY>::PLANE * 8 +
+    return STENCIL_HEAD + StencilRings<MC>::XR * StencilShape<MC, BY>::PSTRIDE * 8 +
            StencilRings<MC>::VR * stencil_chunk_bytes<ST, BY>();
 }
 
@@ -305,6 +312,7 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
     constexpr int CS = MT / MC;
     constexpr int XR = StencilRings<MC>::XR, VR = StencilRings<MC>::VR;
     constexpr int CB = stencil_chunk_bytes<ST, BY>();
+    static_assert(CB % 16 == 0 && (SH::PSTRIDE * 8) % 128 == 0, "ring slot alignment");
     pdl_wait();
     if (ctl && ctl[0]) return;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -313,7 +321,7 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
     uint64_t* vfull = xempty + XR;
     uint64_t* vempty = vfull + VR;
     double* xr = reinterpret_cast<double*>(smem + STENCIL_HEAD);
-    unsigned char* vr = smem + STENCIL_HEAD + XR * SH::PLANE * 8;
+    unsigned char* vr = smem + STENCIL_HEAD + XR * SH::PSTRIDE * 8;
 
     const int h = blockIdx.x % CS;
     const int rb = blockIdx.x / CS;
@@ -371,7 +379,7 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
                     map = &hmap;
                     pz = g.lower;
                 }
-                tensor4d_g2s(xr + b * SH::PLANE, map, h * MC, (t % g.ntx) * STENCIL_BX - 1, (t / g.ntx) * BY - 1, pz,
+                tensor4d_g2s(xr + b * SH::PSTRIDE, map, h * MC, (t % g.ntx) * STENCIL_BX - 1, (t / g.ntx) * BY - 1, pz,
                              &xfull[b]);
                 ++Q;
             };
@@ -409,6 +417,11 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
     if constexpr (SH::LPR == 8) {   // 4 groups per warp, one line
         gx = (warp & 1) * 4 + gl;
         gy = warp >> 1;
+    } else if constexpr (SH::LPR == 2) {   // m = 4: 16 groups per warp, four lines
+        // a quarter warp = 4 groups at the same x on four consecutive lines:
+        // line width 35 = 3 (mod 4) puts their 32-byte points on distinct banks
+        gx = (warp & 1) * 4 + (gl >> 2);
+        gy = (warp >> 1) * 4 + (gl & 3);
     } else {                        // 8 groups per warp, two lines
         // an LDS.128 is served 8 lanes (128 B) at a time: the two groups of a
         // quarter warp take the same x on two lines (odd line width 35 ->
@@ -416,7 +429,7 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
         gx = (warp & 1) * 4 + (gl >> 1);
         gy = (warp >> 1) * 2 + (gl & 1);
     }
-    const int lx0 = gx * 4, cp = cl * 2, r0 = gy * STENCIL_BX + (lx0 ^ ((gy & 1) << 2));
+    const int lx0 = gx * 4, cp = cl * 2, r0 = gy * STENCIL_BX + (lx0 ^ stencil_swz(BY, gy));
     // one expansion per (dot, column); (one per row of the lane's 4 as well
     // -- independent chains -- was measured slower: 226 registers, 1 block/SM)
     constexpr int ND = StencilEpiDots<EPI>::value;
@@ -440,9 +453,9 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
                     mbar_wait(&xfull[q % XR], static_cast<uint32_t>((q / XR) & 1));
                 mbar_wait(&vfull[j % VR], static_cast<uint32_t>((j / VR) & 1));
             }
-            const double* P0 = xr + ((Q + i) % XR) * SH::PLANE;
-            const double* P1 = xr + ((Q + i + 1) % XR) * SH::PLANE;
-            const double* P2 = xr + ((Q + i + 2) % XR) * SH::PLANE;
+            const double* P0 = xr + ((Q + i) % XR) * SH::PSTRIDE;
+            const double* P1 = xr + ((Q + i + 1) % XR) * SH::PSTRIDE;
+            const double* P2 = xr + ((Q + i + 2) % XR) * SH::PSTRIDE;
             // epilogue operand (y, aux): issued before the arithmetic so its
             // latency hides behind it
             double2 axs[4];
@@ -700,7 +713,7 @@ bool stencil_epilogues() {
 }
 
 bool stencil_handles(const mbg_csr* a, int m) {
-    return a && a->stencil && stencil_enabled() && (m == 8 || m == 16 || m == 32);
+    return a && a->stencil && stencil_enabled() && (m == 4 || m == 8 || m == 16 || m == 32);
 }
 
 double stencil_spmm_bytes(int64_t n, int64_t nnz, int m) {
@@ -727,6 +740,12 @@ void launch_by(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y
     const StencilLayout& L = layout_for(ctx, a, BY);
     const int kind = a->stencil->kind;
     switch (m) {
+        case 4:
+            if constexpr (BY == 8) {
+                if (kind == 27) launch_epi<4, 4, 27, BY>(ctx, a, L, x, y, ctl, epi, zr);
+                else launch_epi<4, 4, 7, BY>(ctx, a, L, x, y, ctl, epi, zr);
+            }
+            break;
         case 8:
             if (kind == 27) launch_epi<8, 8, 27, BY>(ctx, a, L, x, y, ctl, epi, zr);
             else launch_epi<8, 8, 7, BY>(ctx, a, L, x, y, ctl, epi, zr);
@@ -740,7 +759,7 @@ void launch_by(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y
             else launch_epi<32, 16, 7, BY>(ctx, a, L, x, y, ctl, epi, zr);
             break;
         default:
-            throw Invalid("stencil SpMM: m must be 8, 16 or 32");
+            throw Invalid("stencil SpMM: m must be 4, 8, 16 or 32");
     }
 }
 
@@ -751,7 +770,9 @@ int launch_stencil_spmm(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, 
     zbeg = std::max(0, zbeg);
     zend = std::min(nz, zend);
     if (zend <= zbeg) return 0;
-    launch_by<4>(ctx, a, m, x, y, ctl, epi, ZRange{zbeg, zend});
+    // m = 4: 32 x 8 tiles (128 compute threads per block, four lines per warp)
+    if (m == 4) launch_by<8>(ctx, a, m, x, y, ctl, epi, ZRange{zbeg, zend});
+    else launch_by<4>(ctx, a, m, x, y, ctl, epi, ZRange{zbeg, zend});
     return 1;
 }
 

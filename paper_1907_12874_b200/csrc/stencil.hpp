@@ -66,7 +66,7 @@ struct StencilOp {
 // Analyse the device CSR of `a` on the grid; returns nullptr when some
 // nonzero is not a grid neighbour (the CSR SpMM stays in use).
 std::shared_ptr<StencilOp> build_stencil(mbg_ctx* ctx, const mbg_csr* a, int nx, int ny, int nz);
-// True when the stencil SpMM handles m (and it is not disabled by MBG_STENCIL=0).
+// True when the stencil SpMM handles m (4, 8, 16, 32; not disabled by MBG_STENCIL=0).
 bool stencil_handles(const mbg_csr* a, int m);
 // MBG_STENCIL_EPI=1: the solver moves exact dots into the stencil SpMM's
 // epilogue (classical delta, phi/psi; Reordered delta).  Measured slower on

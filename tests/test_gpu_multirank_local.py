@@ -84,6 +84,7 @@ def test_banded_uneven_partition(ctx):
 
 @pytest.mark.parametrize("world,planes", [(2, 5), (3, 1), (4, 2), (2, 1)])
 @pytest.mark.parametrize("kind,m,method,form", [("convdiff7", 8, "bicgstab", "fused"),
+                                                ("convdiff7", 4, "rbicgstab", "merged"),
                                                 ("stencil27", 16, "rbicgstab", "fused"),
                                                 ("convdiff7", 32, "pipebicgstab", "merged")])
 def test_zslab_stencil_twin_equals_single_gpu(ctx, world, planes, kind, m, method, form):

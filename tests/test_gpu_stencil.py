@@ -29,7 +29,7 @@ def grid_matrix(name):
 
 
 @pytest.mark.parametrize("name", list(GRIDS))
-@pytest.mark.parametrize("m", [8, 16, 32])
+@pytest.mark.parametrize("m", [4, 8, 16, 32])
 def test_stencil_spmv_bitwise(ctx, name, m):
     a, dims, kind = grid_matrix(name)
     d = ctx.upload(to_prod(a))
@@ -62,7 +62,7 @@ def test_stencil_absent_slots(ctx, kind, dims):
     d = ctx.upload(to_prod(a))
     d.set_grid(*dims)
     assert d.stencil_kind in (7, 27)
-    for m in (8, 16, 32):
+    for m in (4, 8, 16, 32):
         x = np.random.default_rng(11).standard_normal(a.n * m)
         X, Y = ctx.multivector(a.n, m, x), ctx.multivector(a.n, m)
         P.spmv(ctx, d, X, Y)
@@ -109,7 +109,7 @@ def test_stencil_rejects_non_grid(ctx):
 @pytest.mark.parametrize("method,form", [("bicgstab", "fused"), ("rbicgstab", "fused"), ("pipebicgstab", "merged"),
                                          ("pbicgstab", "fused"), ("ibicgstab", "merged")])
 @pytest.mark.parametrize("kind,dims,m", [("convdiff7", (36, 9, 8), 8), ("stencil27", (20, 12, 9), 16),
-                                         ("convdiff7", (33, 5, 6), 32)])
+                                         ("convdiff7", (33, 5, 6), 32), ("stencil27", (37, 17, 7), 4)])
 def test_stencil_solve_bitwise(ctx, method, form, kind, dims, m):
     a = O.gen_stencil(kind, *dims, seed=2)
     b = O.rhs(a.n, m, 3)

@@ -37,7 +37,7 @@ for _ in range(args.reps):
 ctx.synchronize()
 dt = (time.perf_counter() - t) / args.reps
 sk = d.stencil_kind if args.hint else 0
-byt = (16.0 * a.n_rows * m + 8.0 * a.nnz() + 4.0 * a.n_rows) if sk and m in (8, 16, 32) else \
+byt = (16.0 * a.n_rows * m + 8.0 * a.nnz() + 4.0 * a.n_rows) if sk and m in (4, 8, 16, 32) else \
     P.spmv_compulsory_bytes(a.n_rows, a.nnz(), m)
 print(f"{args.kind} {g}^3 m={m} stencil={sk}: {dt*1e6:.1f} us/spmv (host-timed, includes launch), "
       f"{byt/dt/1e9:.0f} GB/s algorithmic")
