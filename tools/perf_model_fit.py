@@ -67,6 +67,12 @@ rel = M.relative_performance(b200, spec_of, list(M.VEC), range(1, 9), compulsory
 out["c4_relative_performance_p1_8"] = {"assumptions": "b fitted on C2; T_G = 10us + 0.5us l^0.21 p^0.5, "
                                        "T_L = 8us + l/450GB/s, gamma = 0 (not measured: one GPU here)",
                                        "R": {p: {k: round(v, 4) for k, v in r.items()} for p, r in rel.items()}}
+# predicted parallel efficiency T(1) / (p T(p)) of C4 Pipelined (the north-star 8-GPU target)
+# under the same assumed NVLink fits -- a model prediction, not a measurement
+t1 = M.t_iteration(b200, spec_of("pipebicgstab"), "pipebicgstab", 1, compulsory=True)
+out["c4_pipelined_predicted_efficiency"] = {
+    str(p): round(t1 / (p * M.t_iteration(b200, spec_of("pipebicgstab"), "pipebicgstab", p, compulsory=True)), 4)
+    for p in (1, 2, 4, 8)}
 json.dump(out, open(args.out + ".json", "w"), indent=1)
 lines = ["# r01h -- the paper's time model fitted on B200 (tools/perf_model_fit.py)", "",
          f"C2 conv-diff 128^3, m=8, merged formulation, one GPU; measured copy peak {peak} GB/s.", ""]
@@ -82,5 +88,9 @@ lines += ["## C4 (320^3, m=32) relative performance R^i(p), B200 preset (assumed
           "| p | " + " | ".join(M.VEC) + " |", "|---" * (len(M.VEC) + 1) + "|"]
 for p, r in out["c4_relative_performance_p1_8"]["R"].items():
     lines.append(f"| {p} | " + " | ".join(f"{r[k]:.3f}" for k in M.VEC) + " |")
+lines += ["", "## C4 Pipelined: predicted parallel efficiency T(1)/(p T(p)) (same assumed NVLink fits)", "",
+          "| p | " + " | ".join(out["c4_pipelined_predicted_efficiency"]) + " |",
+          "|---" * (len(out["c4_pipelined_predicted_efficiency"]) + 1) + "|",
+          "| efficiency | " + " | ".join(f"{v:.3f}" for v in out["c4_pipelined_predicted_efficiency"].values()) + " |"]
 open(args.out + ".md", "w").write("\n".join(lines) + "\n")
 print("\n".join(lines))
