@@ -28,6 +28,7 @@ KEYS = [
 
 
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+TSCALE = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}   # -> microseconds
 
 
 def raw(rep):
@@ -42,6 +43,11 @@ def raw(rep):
             if u in SCALE and d.get(k):
                 try:
                     d[k] = str(float(d[k].replace(",", "")) * SCALE[u] / 1e6)
+                except ValueError:
+                    pass
+            elif u in TSCALE and d.get(k):
+                try:
+                    d[k] = str(float(d[k].replace(",", "")) * TSCALE[u])
                 except ValueError:
                     pass
         res.append(d)
