@@ -164,7 +164,32 @@ def cpu_baseline(a_np, b, args, steps=1):
         kind = "port"
         threads = O.orc().orc_num_threads()
         sample = f"same matrix and RHS, {iters} fixed iterations of the oracle port (OpenMP {threads} threads)"
-    return {"value": float(np.median(vals)), "unit": UNIT, "cores": threads, "kind": kind, "sample": sample}, vals
+    return {"value": float(np.median(vals)), "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
+            "host": host_info()}, vals
+
+
+def host_info():
+    """the CPU model, memory and triad bandwidth beside the baseline."""
+    import ctypes as C
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_ctypes as O
+    model, mem = None, None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal:"):
+                mem = round(int(line.split()[1]) / 1e6, 1)
+                break
+    except OSError:
+        pass
+    lib = O.orc()
+    lib.orc_triad_gbs.restype = C.c_double
+    lib.orc_triad_gbs.argtypes = [C.c_long, C.c_int]
+    return {"cpu_model": model, "nproc": os.cpu_count(), "mem_total_GB": mem,
+            "triad_GBps": round(lib.orc_triad_gbs(40_000_000, 5), 1)}
 
 
 def run_reference(args):

@@ -10,6 +10,7 @@
 
 #include <math.h>
 #include <stdlib.h>
+#include <time.h>
 #include <string.h>
 #ifdef _OPENMP
 #include <omp.h>
@@ -43,6 +44,30 @@ double orc_u11(uint64_t seed, uint64_t stream, uint64_t a, uint64_t b) {
 }
 
 enum { ST_RHS = 1, ST_MAT = 2, ST_CNT = 3, ST_COL = 4, ST_VAL = 5 };
+
+/* Host STREAM-style triad a = b + s*c over n doubles, all OpenMP threads, best of
+ * reps: the host bandwidth recorded beside the CPU baseline. */
+double orc_triad_gbs(long n, int reps) {
+    double* a = (double*)malloc(sizeof(double) * (size_t)n);
+    double* b = (double*)malloc(sizeof(double) * (size_t)n);
+    double* c = (double*)malloc(sizeof(double) * (size_t)n);
+    if (!a || !b || !c) { free(a); free(b); free(c); return 0.0; }
+#pragma omp parallel for schedule(static)
+    for (long i = 0; i < n; ++i) { a[i] = 0.0; b[i] = 1.0; c[i] = 2.0; }
+    double best = 0.0;
+    for (int r = 0; r < reps; ++r) {
+        struct timespec t0, t1;
+        clock_gettime(CLOCK_MONOTONIC, &t0);
+#pragma omp parallel for schedule(static)
+        for (long i = 0; i < n; ++i) a[i] = b[i] + 3.0 * c[i];
+        clock_gettime(CLOCK_MONOTONIC, &t1);
+        const double sec = (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
+        const double gbs = 24.0 * (double)n / sec / 1e9;
+        if (gbs > best) best = gbs;
+    }
+    free(a); free(b); free(c);
+    return best;
+}
 
 int orc_num_threads(void) {
 #ifdef _OPENMP

@@ -101,6 +101,7 @@ int orc_solve_pc(const orc_csr* a, int m, const double* b, double* x, int method
 int orc_method_preconditioned(int method);
 
 int orc_num_threads(void);
+double orc_triad_gbs(long n, int reps);
 
 #ifdef __cplusplus
 }
