@@ -167,3 +167,22 @@ def check_fused_multistep(ctx, method):
     rep = P.solve(ctx, d, B, X, method, "fused", 1e-8, fixed=True, max_iters=6)
     assert_bitwise(rep.residual_history, want["hist"], f"{method} fused history")
     assert_bitwise(X.download(), want["x"], f"{method} fused x")
+
+
+def test_stencil_random_shapes(ctx):
+    # randomized grid shapes (partial tiles in x and y, 1..20 planes) for every
+    # supported m: the twin's work split (whole tiles or z-segments per block),
+    # tile padding and halo zero fill against the CSR oracle
+    rng = np.random.default_rng(2024)
+    for _ in range(24):
+        kind = ["poisson7", "convdiff7", "stencil27"][int(rng.integers(3))]
+        nx, ny, nz = int(rng.integers(1, 70)), int(rng.integers(1, 19)), int(rng.integers(1, 21))
+        m = [4, 8, 16, 32][int(rng.integers(4))]
+        a = O.gen_stencil(kind, nx, ny, nz, seed=int(rng.integers(100)))
+        d = ctx.upload(to_prod(a))
+        d.set_grid(nx, ny, nz)
+        assert d.stencil_kind in (7, 27)
+        x = rng.standard_normal(a.n * m)
+        X, Y = ctx.multivector(a.n, m, x), ctx.multivector(a.n, m)
+        P.spmv(ctx, d, X, Y)
+        assert_bitwise(Y.download(), O.spmv(a, x, m), f"{kind} {nx}x{ny}x{nz} m={m}")
