@@ -150,6 +150,8 @@ public:
     Device(const Device&) = delete;
     Device& operator=(const Device&) = delete;
     mbg_ctx* get() const { return ctx_; }
+    // small classical solves in one cooperative launch (default on; same bits)
+    void set_small_path(bool enable) { check(mbg_ctx_set_small_path(ctx_, enable ? 1 : 0)); }
     static Device& default_device() {
         static Device d(0);
         return d;
