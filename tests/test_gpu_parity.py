@@ -349,3 +349,30 @@ def test_too_many_columns_rejected(ctx):
     Y = ctx.multivector(a.n, m)
     P.spmv(ctx, d, B, Y)
     assert_bitwise(Y.download(), O.spmv(a, np.ones(a.n * m), m), "spmv m=300")
+
+
+def test_empty_inputs(ctx):
+    """0 rows and 0 nonzeros: spmv writes zeros, dots over no element are +0 (the
+    reference's loops simply do not run: spmv.cpp:54-74, execute.cpp:123-172)."""
+    m = 4
+    # n > 0, no nonzero at all
+    n = 37
+    a = O.Csr(n, np.zeros(n + 1, np.int64), np.zeros(0, np.int32), np.zeros(0))
+    d = ctx.upload(to_prod(a))
+    X = ctx.multivector(n, m, np.random.default_rng(0).standard_normal(n * m))
+    Y = ctx.multivector(n, m, np.full(n * m, 7.0))
+    P.spmv(ctx, d, X, Y)
+    assert_bitwise(Y.download(), O.spmv(a, X.download(), m), "nnz = 0")
+    # 0 rows
+    a0 = O.Csr(0, np.zeros(1, np.int64), np.zeros(0, np.int32), np.zeros(0))
+    d0 = ctx.upload(to_prod(a0))
+    X0, Y0 = ctx.multivector(0, m), ctx.multivector(0, m)
+    # two empty std::vectors share data() == nullptr, so the reference's storage check
+    # (spmv.cpp:20-25) rejects a 0-row spmv; so does the device path
+    with pytest.raises(ValueError, match="distinct storage"):
+        P.spmv(ctx, d0, X0, Y0)
+    dev = [ctx.multivector(0, m), ctx.multivector(0, m)]
+    one = np.ones(m)
+    dots = P.execute_group(ctx, [P.UpdateStatement(1, [(one, 0)]), P.DotStatement(0, 1, 0)], dev)
+    assert np.array_equal(np.asarray(dots[0]), np.zeros(m))
+    assert not np.signbit(np.asarray(dots[0])).any()
