@@ -376,3 +376,29 @@ def test_empty_inputs(ctx):
     dots = P.execute_group(ctx, [P.UpdateStatement(1, [(one, 0)]), P.DotStatement(0, 1, 0)], dev)
     assert np.array_equal(np.asarray(dots[0]), np.zeros(m))
     assert not np.signbit(np.asarray(dots[0])).any()
+
+
+@pytest.mark.parametrize("m", [1, 3, 8])
+def test_execute_group_write_through(ctx, m):
+    """Statements see the outputs of earlier statements of the same group, including an
+    input overwritten in place (execute.cpp:97-119): u = a + c b ; a = a - d u ;
+    dots (a, u), (u, u), (b, a) into slots 2, 0, 1."""
+    n = 5_003
+    rng = np.random.default_rng(11 + m)
+    a, b = rng.standard_normal(n * m), rng.standard_normal(n * m)
+    c, dd = rng.standard_normal(m), rng.standard_normal(m)
+    one = np.ones(m)
+    dev = [ctx.multivector(n, m, a), ctx.multivector(n, m, b), ctx.multivector(n, m)]
+    grp = [P.UpdateStatement(2, [(one, 0), (c, 1)]),
+           P.UpdateStatement(0, [(one, 0), (-dd, 2)]),
+           P.DotStatement(0, 2, 2), P.DotStatement(2, 2, 0), P.DotStatement(1, 0, 1)]
+    dots = P.execute_group(ctx, grp, dev, nslots=3)
+    u = np.empty_like(a)
+    O.update(n, m, [(one, a), (c, b)], u)
+    a2 = np.empty_like(a)
+    O.update(n, m, [(one, a), (-dd, u)], a2)
+    assert_bitwise(dev[2].download(), u, "u")
+    assert_bitwise(dev[0].download(), a2, "a in place")
+    assert_bitwise(dots[2], O.dot_exact(a2, u, m), "(a, u)")
+    assert_bitwise(dots[0], O.dot_exact(u, u, m), "(u, u)")
+    assert_bitwise(dots[1], O.dot_exact(b, a2, m), "(b, a)")
