@@ -51,6 +51,7 @@ __device__ __forceinline__ double fmadd_rn(double acc, double c, double v) {
 // Dot (a, b)                                   e.g. delta = (v, r0)
 struct PDot2 {
     static constexpr bool REDO_SAFE = true;
+    static constexpr int UNROLL = 4, MINB = 2;   // 4 packets in flight per trip (C2: dot2 61.6 -> 57.8 us, upd2_sq 71.2 -> 64.2)
     static constexpr const char* NAME = "dot2";
     static constexpr int NIN = 2, NOUT = 0, NCO = 0, NDOT = 1;
     __device__ static void run(const double* in, double*, double* prod, const double*) {
@@ -98,6 +99,7 @@ struct PUpd3 {
 //   s = 1*r + (-alpha)*v ; theta = (s, s)
 struct PUpd2Sq {
     static constexpr bool REDO_SAFE = true;
+    static constexpr int UNROLL = 4, MINB = 2;   // 4 packets in flight per trip (C2: dot2 61.6 -> 57.8 us, upd2_sq 71.2 -> 64.2)
     static constexpr const char* NAME = "upd2_sq";
     static constexpr int NIN = 2, NOUT = 1, NCO = 2, NDOT = 1;
     __device__ static void run(const double* in, double* out, double* prod, const double* co) {
