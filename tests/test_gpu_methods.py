@@ -231,3 +231,16 @@ def test_true_residual_after_solve(ctx, method):
     host = np.linalg.norm(r, axis=0) / np.linalg.norm(b.reshape(a.n, m), axis=0)
     assert rep.converged and np.all(tr < 1e-8)
     assert np.allclose(tr, host, rtol=1e-6, atol=1e-14)
+
+
+@pytest.mark.parametrize("m", [3, 5])
+@pytest.mark.parametrize("form", ["basic", "merged", "fused"])
+@pytest.mark.parametrize("method", ["bicgstab", "pbicgstab"])
+def test_multi_trip_tails(ctx, method, form, m):
+    """Odd m at ~150k rows: the one-column-per-thread passes run several grid-stride trips of
+    4 packets with a partial last trip (dot1 / dot2 / upd2_sq / pbcg_r) -- same bits."""
+    a = O.gen_stencil("poisson7", 53, 53, 53)
+    b = O.rhs(a.n, m, 4)
+    want, rep, X = run_both(ctx, a, b, m, method, form, fixed=True, maxit=12)
+    assert rep.iterations == 12
+    assert_same_solve(want, rep, X, f"{method}/{form} m={m}")
