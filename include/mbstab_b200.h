@@ -182,7 +182,7 @@ int mbg_execute_group(mbg_ctx* ctx, const mbg_statement* stmts, int nstmts, mbg_
 #define MBG_BICGSTAB 0
 #define MBG_RBICGSTAB 1       /* preconditioned (Alg. 6) */
 #define MBG_PIPEBICGSTAB 2
-#define MBG_IBICGSTAB 3       /* Improved, Alg. 3; needs A^T r0 (single GPU) */
+#define MBG_IBICGSTAB 3       /* Improved, Alg. 3; f0 = A^T r0 through a local A^T + its halo plan when partitioned */
 #define MBG_PBICGSTAB 4       /* preconditioned, Alg. 5 */
 #define MBG_PPIPEBICGSTAB 5   /* preconditioned Pipelined, Alg. 7 */
 #define MBG_MERGED 0

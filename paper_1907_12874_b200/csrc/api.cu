@@ -859,6 +859,10 @@ public:
             std::memcpy(dst, src, bytes);
             return;
         }
+        // one job at a time: the workers read dst_/src_/bytes_ until pending_
+        // drops to 0, so a second caller (another context's thread) must not
+        // publish its job before this one has finished
+        std::lock_guard<std::mutex> job(job_mu_);
         std::unique_lock<std::mutex> lk(mu_);
         dst_ = static_cast<char*>(dst);
         src_ = static_cast<const char*>(src);
@@ -900,10 +904,11 @@ private:
             const size_t b = n * t / nt, e = n * (t + 1) / nt;
             if (b < e) std::memcpy(d + b, s + b, e - b);
             std::lock_guard<std::mutex> lk(mu_);
-            if (--pending_ == 0) done_cv_.notify_one();
+            if (--pending_ == 0) done_cv_.notify_all();
         }
     }
     std::vector<std::thread> workers_;
+    std::mutex job_mu_;
     std::mutex mu_;
     std::condition_variable cv_, done_cv_;
     char* dst_ = nullptr;

@@ -1,7 +1,9 @@
 #include <cstdlib>
 // kernels.cu -- SpMM, exact-dot fold/round and the generic group interpreter
 // for sm_100a.
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <unordered_map>
 
 #include "common.hpp"
@@ -31,22 +33,38 @@ void launch_round(cudaStream_t st, int64_t* D, int nslots, int m, double* out) {
     MBG_CUDA(cudaGetLastError());
 }
 
-int group_grid(const void* kernel, int block, size_t smem, int num_sms, int64_t len) {
-    static std::mutex mu;
-    static std::unordered_map<const void*, int> cache;
-    int occ;
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        auto it = cache.find(kernel);
-        if (it == cache.end()) {
-            MBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, block, smem));
-            if (occ < 1) occ = 1;
-            if (occ > 8) occ = 8;
-            cache[kernel] = occ;
-        } else {
-            occ = it->second;
+int kernel_occupancy(const void* kernel, int threads, size_t smem) {
+    // keyed by (device, kernel, threads, smem): the dynamic shared-memory
+    // attribute is per device, so a second context on another device sets it
+    // again before its first launch (function-static caches did not)
+    struct Key {
+        int dev;
+        const void* k;
+        int threads;
+        size_t smem;
+        bool operator<(const Key& o) const {
+            return std::tie(dev, k, threads, smem) < std::tie(o.dev, o.k, o.threads, o.smem);
         }
-    }
+    };
+    static std::mutex mu;
+    static std::map<Key, int> cache;
+    int dev = 0;
+    MBG_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    const Key key{dev, kernel, threads, smem};
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    if (smem > (48u << 10))
+        MBG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int occ = 0;
+    MBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem));
+    if (occ < 1) occ = 1;
+    cache[key] = occ;
+    return occ;
+}
+
+int group_grid(const void* kernel, int block, size_t smem, int num_sms, int64_t len) {
+    const int occ = std::min(8, kernel_occupancy(kernel, block, smem));
     const int64_t need = (len + block - 1) / block;
     const int64_t cap = static_cast<int64_t>(num_sms) * occ;
     return static_cast<int>(need < cap ? (need < 1 ? 1 : need) : cap);

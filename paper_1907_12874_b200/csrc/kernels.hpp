@@ -102,6 +102,9 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 }
 
 // Occupancy-sized persistent grid for a group kernel instantiation.
+// blocks/SM of `kernel` on the current device (sets its dynamic shared-memory
+// attribute there first); cached per device, thread-safe
+int kernel_occupancy(const void* kernel, int threads, size_t smem);
 int group_grid(const void* kernel, int block, size_t smem, int num_sms, int64_t len);
 
 template <class P>

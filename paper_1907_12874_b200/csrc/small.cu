@@ -164,12 +164,8 @@ bool small_path_enabled() {
 }
 
 int launch_small_classical(cudaStream_t st, const SmallArgs& a, int num_sms) {
-    static int occ = -1;
     const size_t smem = static_cast<size_t>(256) * KEXP * sizeof(double);
-    if (occ < 0) {
-        MBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, small_classical_kernel, 256, smem));
-        if (occ < 1) occ = 1;
-    }
+    const int occ = kernel_occupancy(reinterpret_cast<const void*>(&small_classical_kernel), 256, smem);
     // one element per thread as far as co-residency allows: the phases are
     // latency-bound, so more blocks win (C1: 128 blocks 0.049 ms/it, 32 blocks 0.062)
     const int64_t need = (a.n * a.m + 255) / 256;

@@ -454,13 +454,7 @@ template <int M, int EPI>
 static void launch_tma(cudaStream_t st, const SpmmTiles& tl, const int32_t* off, const int32_t* col,
                        const double* val, const double* x, double* y, const int* ctl, int num_sms,
                        const SpmmEpi& epi) {
-    static int occ = -1;
-    if (occ < 0) {
-        MBG_CUDA(cudaFuncSetAttribute(spmm_tma_kernel<M, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      SPMM_SMEM));
-        MBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmm_tma_kernel<M, EPI>, 256, SPMM_SMEM));
-        if (occ < 1) occ = 1;
-    }
+    const int occ = kernel_occupancy(reinterpret_cast<const void*>(&spmm_tma_kernel<M, EPI>), 256, SPMM_SMEM);
     const int grid = static_cast<int>(std::min<int64_t>(tl.count, static_cast<int64_t>(num_sms) * occ));
     launch_pdl(spmm_tma_kernel<M, EPI>, dim3(grid), dim3(256), SPMM_SMEM, st, tl.tiles, static_cast<int>(tl.count),
                off, col, val, x, y, ctl, epi);
@@ -485,13 +479,8 @@ static void launch_tma_epi(cudaStream_t st, const SpmmTiles& tl, const int32_t* 
 template <int M, int EPI>
 static void launch_stage(cudaStream_t st, const SpmmTiles& tl, const int32_t* off, const double* val,
                          const double* x, double* y, const int* ctl, int num_sms, const SpmmEpi& epi) {
-    static int occ = -1;
     constexpr int smem = stage_smem(M);
-    if (occ < 0) {
-        MBG_CUDA(cudaFuncSetAttribute(spmm_stage_kernel<M, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        MBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmm_stage_kernel<M, EPI>, 256, smem));
-        if (occ < 1) occ = 1;
-    }
+    const int occ = kernel_occupancy(reinterpret_cast<const void*>(&spmm_stage_kernel<M, EPI>), 256, smem);
     const int grid = static_cast<int>(std::min<int64_t>(tl.scount, static_cast<int64_t>(num_sms) * occ));
     launch_pdl(spmm_stage_kernel<M, EPI>, dim3(grid), dim3(256), static_cast<size_t>(smem), st, tl.stiles, tl.umeta,
                static_cast<int>(tl.scount), off,

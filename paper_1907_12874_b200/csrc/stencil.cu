@@ -604,14 +604,8 @@ void launch_one(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const do
     constexpr int smem = stencil_smem<MC, ST, BY>();
     constexpr int threads = StencilShape<MC, BY>::THREADS + 32;   // + producer warp
     constexpr int CS = MT / MC;
-    static int occ = -1;
-    if (occ < 0) {
-        MBG_CUDA(cudaFuncSetAttribute(stencil_spmm_kernel<MT, MC, ST, BY, EPI>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        MBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil_spmm_kernel<MT, MC, ST, BY, EPI>, threads,
-                                                               smem));
-        if (occ < 1) occ = 1;
-    }
+    const int occ =
+        kernel_occupancy(reinterpret_cast<const void*>(&stencil_spmm_kernel<MT, MC, ST, BY, EPI>), threads, smem);
     // x viewed as a (planes, ny, nx, MT) fp64 tensor; box (MC, LW, BY + 2, 1):
     // the owned planes, and the halo planes appended after them (z-slabs)
     auto encode = [&](CUtensorMap& tm, const double* base, int planes) {
