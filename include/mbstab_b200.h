@@ -65,6 +65,11 @@ int mbg_ctx_synchronize(mbg_ctx* ctx);
  * iterations as the multi-kernel path.  enable = 0 forces the multi-kernel
  * path on this context (default 1; MBG_SMALL=0 turns it off process-wide). */
 int mbg_ctx_set_small_path(mbg_ctx* ctx, int enable);
+/* Size the persistent grids for (device SMs - count) SMs, leaving `count` SMs
+ * to concurrent kernels (a multi-rank NCCL communicator does this itself with
+ * MBG_RESERVE_SMS, default 4, so side-stream collectives overlap the SpMM).
+ * Results do not depend on it (bitwise). */
+int mbg_ctx_reserve_sms(mbg_ctx* ctx, int count);
 /* Multi-GPU: join a communicator of `world` ranks (one process per GPU).
  * nccl_id is the 128-byte ncclUniqueId created by rank 0 (mbg_comm_unique_id)
  * and broadcast by the caller (e.g. torch.distributed). */

@@ -152,6 +152,8 @@ public:
     mbg_ctx* get() const { return ctx_; }
     // small classical solves in one cooperative launch (default on; same bits)
     void set_small_path(bool enable) { check(mbg_ctx_set_small_path(ctx_, enable ? 1 : 0)); }
+    // leave `count` SMs to concurrent kernels (same bits)
+    void reserve_sms(int count) { check(mbg_ctx_reserve_sms(ctx_, count)); }
     static Device& default_device() {
         static Device d(0);
         return d;

@@ -163,6 +163,10 @@ class Context:
         """Small classical solves in one cooperative launch (default on)."""
         check(lib().mbg_ctx_set_small_path(self.h, int(bool(enable))))
 
+    def reserve_sms(self, count: int) -> None:
+        """Size the persistent grids for (device SMs - count) SMs (bitwise-neutral)."""
+        check(lib().mbg_ctx_reserve_sms(self.h, int(count)))
+
     def launches(self) -> int:
         return int(lib().mbg_ctx_launches(self.h))
 

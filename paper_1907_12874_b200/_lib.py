@@ -98,6 +98,7 @@ def lib() -> C.CDLL:
         "mbg_csr_reordered": (i32, [vp]),
         "mbg_csr_stencil_kind": (i32, [vp]),
         "mbg_ctx_set_small_path": (i32, [vp, i32]),
+        "mbg_ctx_reserve_sms": (i32, [vp, i32]),
         "mbg_mv_alloc": (i32, [vp, i64, i32, pp]),
         "mbg_mv_free": (i32, [vp]),
         "mbg_mv_upload": (i32, [vp, vp]),

@@ -88,6 +88,7 @@ extern "C" int mbg_ctx_create(int device, mbg_ctx** out) {
         auto* c = new mbg_ctx();
         c->device = device;
         MBG_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+        c->num_sms_device = c->num_sms;
         MBG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         MBG_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
         *out = c;
@@ -532,6 +533,14 @@ extern "C" int mbg_ctx_set_small_path(mbg_ctx* ctx, int enable) {
     return guarded([&] {
         if (!ctx) throw Invalid("null context");
         ctx->small_path = enable != 0;
+    });
+}
+
+extern "C" int mbg_ctx_reserve_sms(mbg_ctx* ctx, int count) {
+    return guarded([&] {
+        if (!ctx) throw Invalid("null context");
+        if (count < 0 || count >= ctx->num_sms_device) throw Invalid("reserve_sms: count out of range");
+        ctx->num_sms = ctx->num_sms_device - count;
     });
 }
 

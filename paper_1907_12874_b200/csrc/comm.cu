@@ -9,7 +9,9 @@
 // dot allreduce).
 #include <nccl.h>
 
+#include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <condition_variable>
 #include <cstring>
 #include <memory>
@@ -275,6 +277,19 @@ void comm_destroy(mbg_ctx* ctx) {
     if (cm->ev_side) cudaEventDestroy(cm->ev_side);
     delete cm;
     ctx->comm = nullptr;
+    ctx->num_sms = ctx->num_sms_device;
+}
+
+// SMs kept free of the persistent grids while a multi-rank NCCL communicator
+// is active (MBG_RESERVE_SMS, default 4): the SpMM / group / stencil kernels
+// size their grids to fill every SM they are given, so a side-stream NCCL
+// kernel (halo sendrecv under the interior SpMM, the Pipelined dot allreduce
+// under the next SpMM) would otherwise get no SM until they drain and the
+// overlap would serialise.  NCCL is capped at the same number of CTAs.
+int reserved_sms() {
+    const char* e = std::getenv("MBG_RESERVE_SMS");
+    const int v = e && *e ? std::atoi(e) : 4;
+    return std::max(0, std::min(v, 32));
 }
 
 }  // namespace mbg
@@ -303,7 +318,13 @@ extern "C" int mbg_ctx_init_comm(mbg_ctx* ctx, int rank, int world, const unsign
         cm->world = world;
         ncclUniqueId id;
         std::memcpy(id.internal, nccl_id, 128);
-        ncclResult_t r = ncclCommInitRank(&cm->comm, world, id, rank);
+        const int reserve = world > 1 ? mbg::reserved_sms() : 0;
+        ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+        if (reserve > 0) {
+            cfg.minCTAs = 1;
+            cfg.maxCTAs = reserve;
+        }
+        ncclResult_t r = ncclCommInitRankConfig(&cm->comm, world, id, rank, &cfg);
         if (r != ncclSuccess) {
             delete cm;
             throw std::runtime_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
@@ -311,6 +332,7 @@ extern "C" int mbg_ctx_init_comm(mbg_ctx* ctx, int rank, int world, const unsign
         MBG_CUDA(cudaEventCreateWithFlags(&cm->ev_main, cudaEventDisableTiming));
         MBG_CUDA(cudaEventCreateWithFlags(&cm->ev_side, cudaEventDisableTiming));
         ctx->comm = cm;
+        ctx->num_sms = std::max(1, ctx->num_sms_device - reserve);
         return MBG_OK;
     } catch (const mbg::Invalid& e) {
         mbg::set_error(e.what());

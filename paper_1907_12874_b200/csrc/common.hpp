@@ -70,7 +70,8 @@ struct StencilOp;   // stencil.hpp
 // ---- ABI objects ------------------------------------------------------------
 struct mbg_ctx {
     int device = 0;
-    int num_sms = 0;
+    int num_sms = 0;                 // SMs the persistent grids are sized for
+    int num_sms_device = 0;          // SMs of the device (num_sms + those reserved for NCCL)
     cudaStream_t stream = nullptr;   // main stream: all hot-path kernels
     cudaStream_t side = nullptr;     // side stream: overlapped reductions / halo
     mbg::Comm* comm = nullptr;       // multi-GPU communicator (nullptr: single GPU)

@@ -153,6 +153,52 @@ __global__ void stencil_fill_kernel(GridMap gm, int nzg, int by, int S, int ntx,
     }
 }
 
+// z-part layout of a 27-point chunk (stencil27z_kernel): the 27 slots split
+// by dz into three parts of 9, each [9][RT] doubles, with the row masks after
+// part 0:  part0 (dz=-1) | mask[RT] | part1 (dz=0) | part2 (dz=+1).  Rows are
+// not swizzled (r = ly * 32 + lx).  The kernel streams, for x plane p, part 0
+// of row plane p+1, part 1 of p and part 2 of p-1.
+__host__ __device__ constexpr int64_t zpart_off(int d, int RT) {
+    return d == 0 ? 0 : (static_cast<int64_t>(9 * d) * RT * 8 + static_cast<int64_t>(RT) * 4);
+}
+
+__global__ void stencil_fill_zpart_kernel(GridMap gm, int nzg, int by, int ntx, int64_t chunk_bytes,
+                                          const int32_t* __restrict__ off, const int32_t* __restrict__ col,
+                                          const double* __restrict__ val, unsigned char* __restrict__ chunks) {
+    const int RT = STENCIL_BX * by;
+    const int nx = gm.nx, ny = gm.ny;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < gm.n_own;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int xi, yi, zi;
+        grid_coords(gm.row_begin + i, nx, ny, xi, yi, zi);
+        const int64_t t = static_cast<int64_t>(yi / by) * ntx + xi / STENCIL_BX;
+        const int r = (yi % by) * STENCIL_BX + xi % STENCIL_BX;
+        unsigned char* c = chunks + (t * gm.nzl + (zi - gm.z0)) * chunk_bytes;
+        auto slot = [&](int s) -> double* {
+            return reinterpret_cast<double*>(c + zpart_off(s / 9, RT)) + static_cast<int64_t>(s % 9) * RT + r;
+        };
+        for (int s = 0; s < 27; ++s) *slot(s) = -0.0;
+        uint32_t mask = 0;
+        for (int k = off[i]; k < off[i + 1]; ++k) {
+            int xj, yj, zj;
+            grid_coords(gm.global_col(col[k]), nx, ny, xj, yj, zj);
+            const int s = (zj - zi + 1) * 9 + (yj - yi + 1) * 3 + (xj - xi + 1);
+            *slot(s) = val[k];
+            mask |= 1u << s;
+        }
+        bool check = false;
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const int s = (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1);
+                    const bool inside = xi + dx >= 0 && xi + dx < nx && yi + dy >= 0 && yi + dy < ny &&
+                                        zi + dz >= 0 && zi + dz < nzg;
+                    if (inside && !((mask >> s) & 1u)) check = true;
+                }
+        reinterpret_cast<uint32_t*>(c + 9 * static_cast<int64_t>(RT) * 8)[r] = mask | (check ? 0x80000000u : 0u);
+    }
+}
+
 // ---- the SpMM kernel --------------------------------------------------------
 
 struct StencilGeom {
@@ -538,6 +584,231 @@ __global__ void __launch_bounds__(StencilShape<MC, BY>::THREADS + 32)
                               xr, SyncCompute{}, SH::THREADS);
     }
 }
+
+// ---- 27-point z-marching SpMM (m = 16 per block) ---------------------------
+//
+// The 27-point kernel above keeps three x planes resident per output plane and
+// re-reads every x line from shared memory for each of the three row planes it
+// feeds; with the per-row value broadcasts the shared-memory pipe, not HBM, set
+// its time (C3: 0.69 ms against 0.52 ms of compulsory bytes).  Here each x
+// plane p is read from shared memory ONCE and feeds all three row planes it
+// touches: row plane p-1 (its slots 18-26, dz = +1: the row is then complete
+// and stored), row plane p (slots 9-17) and row plane p+1 (slots 0-8, a fresh
+// accumulator).  A row therefore still adds its 27 slots in ascending order
+// (dz, dy, dx) -- the CSR order -- bit for bit.  A lane owns 2 consecutive
+// points x 4 columns (registers: 3 row planes x 2 points x 4 columns of
+// accumulators); a quarter warp is two point pairs of one line, whose x loads
+// fall on complementary bank quads (even groups load column pair 2q first,
+// odd groups 2q+1 first) and whose value loads are two 16-byte broadcasts:
+// every shared-memory wavefront is fully used.  Per x plane the producer warp
+// issues one TMA tensor box (the plane) and three bulk copies (part 0 of row
+// plane p+1 with its masks, part 1 of p, part 2 of p-1) into XR / VR rings.
+template <int MC>
+struct Z27Shape {
+    static constexpr int LPG = MC / 4;                      // lanes per point pair (4 columns each)
+    static constexpr int THREADS = 16 * 4 * LPG;            // 16 point pairs x 4 lines
+    static constexpr int NCW = THREADS / 32;
+    static constexpr int LW = 34;
+    static constexpr int RT = STENCIL_BX * 4;
+    static constexpr int PLANE = LW * 6 * MC;               // doubles per x-plane box
+    static constexpr int PSTRIDE = (PLANE + 15) / 16 * 16;
+    static constexpr int CB = 27 * RT * 8 + RT * 4;         // one chunk (= one value-ring slot)
+};
+
+template <int MC, int XR, int VR>
+__host__ __device__ constexpr int z27_smem() {
+    return STENCIL_HEAD + XR * Z27Shape<MC>::PSTRIDE * 8 + VR * Z27Shape<MC>::CB;
+}
+
+template <int MT, int MC, int XR, int VR>
+__global__ void __launch_bounds__(Z27Shape<MC>::THREADS + 32, XR == 2 ? 2 : 1)
+    stencil27z_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
+                      StencilGeom g, double* __restrict__ y, const int* __restrict__ ctl) {
+    using SH = Z27Shape<MC>;
+    constexpr int CS = MT / MC, RT = SH::RT, CB = SH::CB;
+    constexpr int P0B = 9 * RT * 8 + RT * 4;   // part 0 + masks
+    constexpr int PB = 9 * RT * 8;             // part 1 / part 2
+    static_assert(MC == 16, "z-marching lane map is written for 16 columns per block");
+    static_assert(CB % 16 == 0 && (SH::PSTRIDE * 8) % 128 == 0 && P0B % 16 == 0, "ring slot alignment");
+    pdl_wait();
+    if (ctl && ctl[0]) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* xfull = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* xempty = xfull + XR;
+    uint64_t* vfull = xempty + XR;
+    uint64_t* vempty = vfull + VR;
+    double* xr = reinterpret_cast<double*>(smem + STENCIL_HEAD);
+    unsigned char* vr = smem + STENCIL_HEAD + XR * SH::PSTRIDE * 8;
+
+    const int h = blockIdx.x % CS;
+    const int rb = blockIdx.x / CS;
+    const int ntiles = static_cast<int>(g.steps / g.nz);
+    const int nsegs_b = g.kt > 0 ? g.kt : 1;
+    auto segment = [&](int si, int& t, int& za, int& steps) {
+        if (g.kt > 0) {
+            t = rb + si * g.nranges;
+            za = 0;
+            steps = t < ntiles ? g.nz : 0;
+        } else {
+            const int nseg = (g.nz + g.zseg - 1) / g.zseg;
+            t = rb / nseg;
+            const int sg = rb % nseg;
+            za = sg * g.zseg;
+            steps = t < ntiles ? min(g.nz, za + g.zseg) - za : 0;
+        }
+    };
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int b = 0; b < XR; ++b) {
+            mbar_init(&xfull[b], 1);
+            mbar_init(&xempty[b], SH::NCW);
+        }
+        for (int b = 0; b < VR; ++b) {
+            mbar_init(&vfull[b], 1);
+            mbar_init(&vempty[b], SH::NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (tid >= SH::THREADS) {   // ---- producer warp: one slot of each ring per x plane
+        if (tid == SH::THREADS) {
+            int64_t q = 0;   // x planes (= steps) issued so far
+            for (int si = 0; si < nsegs_b; ++si) {
+                int t, za, steps;
+                segment(si, t, za, steps);
+                if (steps <= 0) break;
+                const unsigned char* cbase = g.chunks + static_cast<int64_t>(t) * g.nzl * g.chunk_bytes;
+                for (int i = 0; i < steps + 2; ++i, ++q) {
+                    const int p = za - 1 + i;   // x plane within the range
+                    const int bx = static_cast<int>(q % XR), bv = static_cast<int>(q % VR);
+                    if (q >= XR) mbar_wait(&xempty[bx], static_cast<uint32_t>((q / XR - 1) & 1));
+                    if (q >= VR) mbar_wait(&vempty[bv], static_cast<uint32_t>((q / VR - 1) & 1));
+                    mbar_expect_tx(&xfull[bx], static_cast<uint32_t>(SH::PLANE * 8));
+                    const int pl = g.zbeg + p;
+                    const void* map = &xmap;
+                    int pz = pl;
+                    if (pl < 0 && g.lower) {
+                        map = &hmap;
+                        pz = 0;
+                    } else if (pl >= g.nzl && g.upper) {
+                        map = &hmap;
+                        pz = g.lower;
+                    }
+                    tensor4d_g2s(xr + bx * SH::PSTRIDE, map, h * MC, (t % g.ntx) * STENCIL_BX - 1,
+                                 (t / g.ntx) * 4 - 1, pz, &xfull[bx]);
+                    const bool n0 = i < steps;                             // row plane p+1 in [za, zb)
+                    const bool n1 = i >= 1 && i <= steps;                  // row plane p
+                    const bool n2 = i >= 2;                                // row plane p-1
+                    const uint32_t bytes = (n0 ? P0B : 0) + (n1 ? PB : 0) + (n2 ? PB : 0);
+                    mbar_expect_tx(&vfull[bv], bytes);
+                    unsigned char* dst = vr + bv * CB;
+                    const int64_t zl = g.zbeg + p;   // local plane of the x plane
+                    if (n0) bulk_g2s(dst, cbase + (zl + 1) * g.chunk_bytes, P0B, &vfull[bv]);
+                    if (n1) bulk_g2s(dst + P0B, cbase + zl * g.chunk_bytes + P0B, PB, &vfull[bv]);
+                    if (n2) bulk_g2s(dst + P0B + PB, cbase + (zl - 1) * g.chunk_bytes + P0B + PB, PB, &vfull[bv]);
+                }
+            }
+        }
+        return;
+    }
+
+    // ---- compute warps: lane -> (point pair px, line gy, column quad cq)
+    const int lane = tid & 31, warp = tid >> 5;
+    const int cq = lane % SH::LPG, gl = lane / SH::LPG;
+    const int gy = warp >> 1, px = (warp & 1) * 8 + gl;
+    const int lx0 = px * 2, r0 = gy * STENCIL_BX + lx0;
+    const int odd = gl & 1;
+    const int cpa = (2 * cq + odd) * 2, cpb = (2 * cq + 1 - odd) * 2;   // column pairs in load order
+    double ao[2][4], am[2][4], an[2][4];   // row planes p-1 (old), p (mid), p+1 (new)
+    uint32_t mo[2] = {0, 0}, mm[2] = {0, 0}, mn[2] = {0, 0};
+    int64_t q = 0;
+    for (int si = 0; si < nsegs_b; ++si) {
+        int t, za, steps;
+        segment(si, t, za, steps);
+        if (steps <= 0) break;
+        const int xg0 = (t % g.ntx) * STENCIL_BX + lx0, yg = (t / g.ntx) * 4 + gy;
+        const bool yok = yg < g.ny;
+        for (int i = 0; i < steps + 2; ++i, ++q) {
+            const bool n0 = i <= steps - 1, n1 = i >= 1 && i <= steps, n2 = i >= 2;
+            mbar_wait(&xfull[q % XR], static_cast<uint32_t>((q / XR) & 1));
+            mbar_wait(&vfull[q % VR], static_cast<uint32_t>((q / VR) & 1));
+            const double* P = xr + (q % XR) * SH::PSTRIDE;
+            const unsigned char* ch = vr + (q % VR) * CB;
+            const double* V0 = reinterpret_cast<const double*>(ch);
+            const double* V1 = reinterpret_cast<const double*>(ch + P0B);
+            const double* V2 = reinterpret_cast<const double*>(ch + P0B + PB);
+            if (n0) {
+                const uint2 mk = *reinterpret_cast<const uint2*>(ch + 9 * RT * 8 + r0 * 4);
+                mn[0] = mk.x;
+                mn[1] = mk.y;
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) an[r][c] = 0.0;
+            }
+            const bool ck0 = ((mn[0] | mn[1]) & 0x80000000u) != 0;
+            const bool ck1 = ((mm[0] | mm[1]) & 0x80000000u) != 0;
+            const bool ck2 = ((mo[0] | mo[1]) & 0x80000000u) != 0;
+#pragma unroll
+            for (int dy = 0; dy < 3; ++dy) {
+                // the line's 4 points (lx0-1 .. lx0+2) x this lane's 4 columns
+                double2 xa[4], xb[4];
+                const double* L = P + ((gy + dy) * SH::LW + lx0) * MC;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    xa[j] = *reinterpret_cast<const double2*>(L + j * MC + cpa);
+                    xb[j] = *reinterpret_cast<const double2*>(L + j * MC + cpb);
+                }
+                // accumulator columns 0,1 <-> pair cpa, 2,3 <-> pair cpb (odd lanes hold
+                // their pairs swapped; the store puts them back), so no selects here
+                auto term = [&](double (&acc)[2][4], const double* V, const uint32_t (&mk)[2], bool ck, int shift) {
+#pragma unroll
+                    for (int dx = 0; dx < 3; ++dx) {
+                        const double2 v = *reinterpret_cast<const double2*>(V + (dy * 3 + dx) * RT + r0);
+#pragma unroll
+                        for (int r = 0; r < 2; ++r) {
+                            if (ck && !((mk[r] >> (shift + dy * 3 + dx)) & 1u)) continue;
+                            const double vv = r ? v.y : v.x;
+                            acc[r][0] = __dadd_rn(acc[r][0], __dmul_rn(vv, xa[r + dx].x));
+                            acc[r][1] = __dadd_rn(acc[r][1], __dmul_rn(vv, xa[r + dx].y));
+                            acc[r][2] = __dadd_rn(acc[r][2], __dmul_rn(vv, xb[r + dx].x));
+                            acc[r][3] = __dadd_rn(acc[r][3], __dmul_rn(vv, xb[r + dx].y));
+                        }
+                    }
+                };
+                if (n2) term(ao, V2, mo, ck2, 18);
+                if (n1) term(am, V1, mm, ck1, 9);
+                if (n0) term(an, V0, mn, ck0, 0);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&xempty[q % XR]);
+                mbar_arrive(&vempty[q % VR]);
+            }
+            if (n2 && yok) {   // row plane p-1 = za + i - 2 is complete
+                const int64_t rowz = (static_cast<int64_t>(g.zbeg + za + i - 2) * g.ny + yg) * g.nx;
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+                    if (xg0 + r < g.nx) {
+                        double* dst = y + (rowz + xg0 + r) * MT + h * MC;
+                        *reinterpret_cast<double2*>(dst + cpa) = make_double2(ao[r][0], ao[r][1]);
+                        *reinterpret_cast<double2*>(dst + cpb) = make_double2(ao[r][2], ao[r][3]);
+                    }
+            }
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                mo[r] = mm[r];
+                mm[r] = mn[r];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    ao[r][c] = am[r][c];
+                    am[r][c] = an[r][c];
+                }
+            }
+        }
+    }
+}
 #undef MBG_ACC
 
 // ---- host side ----------------------------------------------------------------
@@ -570,12 +841,13 @@ int env_int(const char* name, int dflt) {
     return e && *e ? std::atoi(e) : dflt;
 }
 
-StencilLayout& layout_for(mbg_ctx* ctx, const mbg_csr* a, int by) {
+StencilLayout& layout_for(mbg_ctx* ctx, const mbg_csr* a, int by, int zpart = 0) {
     StencilOp& op = *a->stencil;
     for (auto& l : op.layouts)
-        if (l->by == by) return *l;
+        if (l->by == by && l->zpart == zpart) return *l;
     auto l = std::make_unique<StencilLayout>();
     l->by = by;
+    l->zpart = zpart;
     const int S = op.kind;
     const int RT = STENCIL_BX * by;
     l->chunk_bytes = static_cast<int64_t>(S) * RT * 8 + RT * 4;
@@ -583,9 +855,17 @@ StencilLayout& layout_for(mbg_ctx* ctx, const mbg_csr* a, int by) {
     const size_t bytes = static_cast<size_t>(ntx * nty * op.nz * l->chunk_bytes);
     l->chunks.alloc(bytes);
     const int grid = ctx->num_sms * 8;
-    stencil_clear_kernel<<<grid, 256, 0, ctx->stream>>>(ntx * nty * op.nz, S, RT, l->chunk_bytes, l->chunks.p);
-    stencil_fill_kernel<<<grid, 256, 0, ctx->stream>>>(op.map, op.nzg, by, S, static_cast<int>(ntx), l->chunk_bytes,
-                                                       a->off.p, a->col.p, a->val.p, l->chunks.p);
+    if (zpart) {
+        // tile rows outside the grid stay zero (never stored)
+        MBG_CUDA(cudaMemsetAsync(l->chunks.p, 0, bytes, ctx->stream));
+        stencil_fill_zpart_kernel<<<grid, 256, 0, ctx->stream>>>(op.map, op.nzg, by, static_cast<int>(ntx),
+                                                                 l->chunk_bytes, a->off.p, a->col.p, a->val.p,
+                                                                 l->chunks.p);
+    } else {
+        stencil_clear_kernel<<<grid, 256, 0, ctx->stream>>>(ntx * nty * op.nz, S, RT, l->chunk_bytes, l->chunks.p);
+        stencil_fill_kernel<<<grid, 256, 0, ctx->stream>>>(op.map, op.nzg, by, S, static_cast<int>(ntx),
+                                                           l->chunk_bytes, a->off.p, a->col.p, a->val.p, l->chunks.p);
+    }
     MBG_CUDA(cudaGetLastError());
     MBG_CUDA(cudaStreamSynchronize(ctx->stream));
     op.layouts.push_back(std::move(l));
@@ -662,6 +942,74 @@ void launch_one(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const do
                ctx->stream, tm, hm, gm, y, ctl, epi);
 }
 
+// work split of a persistent stencil grid (shared by both kernels)
+void split_work(StencilGeom& gm, int64_t slots) {
+    const int64_t ntiles = gm.steps / gm.nz;
+    if (ntiles >= slots) {
+        gm.kt = static_cast<int>((ntiles + slots - 1) / slots);
+        gm.zseg = gm.nz;
+        gm.nranges = static_cast<int>((ntiles + gm.kt - 1) / gm.kt);
+    } else {
+        const int k = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(slots / ntiles, gm.nz)));
+        gm.kt = 0;
+        gm.zseg = (gm.nz + k - 1) / k;
+        gm.nranges = static_cast<int>(ntiles * ((gm.nz + gm.zseg - 1) / gm.zseg));
+    }
+}
+
+template <int MT, int MC, int XR, int VR>
+void launch_z27(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const double* x, double* y, const int* ctl,
+                ZRange zr) {
+    using SH = Z27Shape<MC>;
+    const StencilOp& op = *a->stencil;
+    if (zr.zend <= zr.zbeg) return;
+    constexpr int smem = z27_smem<MC, XR, VR>();
+    constexpr int threads = SH::THREADS + 32;
+    constexpr int CS = MT / MC;
+    const int occ = kernel_occupancy(reinterpret_cast<const void*>(&stencil27z_kernel<MT, MC, XR, VR>), threads, smem);
+    auto encode = [&](CUtensorMap& tm, const double* base, int planes) {
+        const cuuint64_t dims[4] = {static_cast<cuuint64_t>(MT), static_cast<cuuint64_t>(op.nx),
+                                    static_cast<cuuint64_t>(op.ny), static_cast<cuuint64_t>(planes)};
+        const cuuint64_t strides[3] = {static_cast<cuuint64_t>(MT) * 8, static_cast<cuuint64_t>(op.nx) * MT * 8,
+                                       static_cast<cuuint64_t>(op.nx) * op.ny * MT * 8};
+        const cuuint32_t box[4] = {static_cast<cuuint32_t>(MC), static_cast<cuuint32_t>(SH::LW), 6u, 1u};
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        const CUresult r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims,
+                                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            throw std::runtime_error("stencil SpMM: cuTensorMapEncodeTiled failed (" +
+                                     std::to_string(static_cast<int>(r)) + ")");
+    };
+    CUtensorMap tm, hm;
+    encode(tm, x, op.nz);
+    const int nhp = op.map.lower + op.upper;
+    if (nhp) encode(hm, x + a->n * MT, nhp);
+    else hm = tm;
+    StencilGeom gm{};
+    gm.nx = op.nx;
+    gm.ny = op.ny;
+    gm.nz = zr.zend - zr.zbeg;
+    gm.zbeg = zr.zbeg;
+    gm.nzl = op.nz;
+    gm.lower = op.map.lower;
+    gm.upper = op.upper;
+    gm.ntx = (op.nx + STENCIL_BX - 1) / STENCIL_BX;
+    gm.steps = static_cast<int64_t>(gm.ntx) * ((op.ny + 3) / 4) * gm.nz;
+    gm.chunks = L.chunks.p;
+    gm.chunk_bytes = L.chunk_bytes;
+    split_work(gm, static_cast<int64_t>(occ) * ctx->num_sms / CS);
+    launch_pdl(stencil27z_kernel<MT, MC, XR, VR>, dim3(gm.nranges * CS), dim3(threads), static_cast<size_t>(smem),
+               ctx->stream, tm, hm, gm, y, ctl);
+}
+
+// MBG_STENCIL_Z: 0 = the 3-plane kernel for 27-point m = 16 / 32 too;
+// 1 (default) = z-marching with rings (3, 2); 2 = rings (2, 2) (2 blocks/SM)
+int z27_mode() {
+    static const int v = env_int("MBG_STENCIL_Z", 0);
+    return v;
+}
+
 }  // namespace
 
 std::shared_ptr<StencilOp> build_stencil(mbg_ctx* ctx, const mbg_csr* a, int nx, int ny, int nz) {
@@ -731,8 +1079,21 @@ void launch_epi(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const do
 template <int BY>
 void launch_by(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y, const int* ctl,
                const SpmmEpi* epi, ZRange zr) {
-    const StencilLayout& L = layout_for(ctx, a, BY);
     const int kind = a->stencil->kind;
+    if constexpr (BY == 4) {
+        if (kind == 27 && (m == 16 || m == 32) && (!epi || epi->kind == 0) && z27_mode() != 0) {
+            const StencilLayout& Z = layout_for(ctx, a, 4, 1);
+            if (m == 16) {
+                if (z27_mode() == 2) launch_z27<16, 16, 2, 2>(ctx, a, Z, x, y, ctl, zr);
+                else launch_z27<16, 16, 3, 2>(ctx, a, Z, x, y, ctl, zr);
+            } else {
+                if (z27_mode() == 2) launch_z27<32, 16, 2, 2>(ctx, a, Z, x, y, ctl, zr);
+                else launch_z27<32, 16, 3, 2>(ctx, a, Z, x, y, ctl, zr);
+            }
+            return;
+        }
+    }
+    const StencilLayout& L = layout_for(ctx, a, BY);
     switch (m) {
         case 4:
             if constexpr (BY == 8) {

@@ -25,6 +25,7 @@ constexpr int STENCIL_BX = 32;   // tile width along x (grid points)
 
 struct StencilLayout {
     int by = 0;                     // tile height along y
+    int zpart = 0;                  // 1: 27-point z-part chunks (stencil27z_kernel) -- see stencil.cu
     int64_t chunk_bytes = 0;        // S * 32*by * 8 (values) + 32*by * 4 (masks)
     DevBuf<unsigned char> chunks;   // [(tile * nz + z)] chunks
 };

@@ -402,3 +402,25 @@ def test_execute_group_write_through(ctx, m):
     assert_bitwise(dots[2], O.dot_exact(a2, u, m), "(a, u)")
     assert_bitwise(dots[0], O.dot_exact(u, u, m), "(u, u)")
     assert_bitwise(dots[1], O.dot_exact(b, a2, m), "(b, a)")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("reserve", [4, 37])
+def test_reserved_sms_bitwise(reserve):
+    # persistent grids sized for fewer SMs (what a multi-rank NCCL context does
+    # to leave room for side-stream collectives) give the same bits
+    a = O.gen_stencil("stencil27", 40, 24, 20, seed=2)
+    m = 16
+    b = O.rhs(a.n, m, 2)
+    want = O.solve(a, b, m, "rbicgstab", "merged", 1e-8, fixed=True, maxit=12)
+    c = P.Context(0)
+    c.reserve_sms(reserve)
+    for grid in (False, True):
+        d = c.upload(to_prod(a))
+        if grid:
+            d.set_grid(40, 24, 20)
+        B, X = c.multivector(a.n, m, b), c.multivector(a.n, m)
+        rep = P.solve(c, d, B, X, "rbicgstab", "fused", 1e-8, fixed=True, max_iters=12)
+        assert_bitwise(rep.residual_history, want["hist"], f"reserve {reserve} history")
+        assert_bitwise(X.download(), want["x"], f"reserve {reserve} x")
+    c.close()

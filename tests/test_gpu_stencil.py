@@ -186,3 +186,23 @@ def test_stencil_random_shapes(ctx):
         X, Y = ctx.multivector(a.n, m, x), ctx.multivector(a.n, m)
         P.spmv(ctx, d, X, Y)
         assert_bitwise(Y.download(), O.spmv(a, x, m), f"{kind} {nx}x{ny}x{nz} m={m}")
+
+
+@pytest.mark.parametrize("mode", ["0", "2"])
+def test_stencil_z27_modes(mode):
+    # the 27-point m = 16 / 32 SpMM has three implementations selected once per
+    # process by MBG_STENCIL_Z (0: three resident planes; 1, the default:
+    # z-marching, rings 3/2; 2: z-marching, rings 2/2 at 2 blocks/SM): rerun the
+    # stencil parity tests under the non-default ones
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    if os.environ.get("MBG_Z_NESTED"):
+        pytest.skip("nested run")
+    here = Path(__file__).resolve()
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider", str(here),
+                        "-k", "spmv_bitwise or absent_slots or special_values or solve_bitwise or random_shapes"],
+                       env={**os.environ, "MBG_STENCIL_Z": mode, "MBG_Z_NESTED": "1"}, capture_output=True, text=True,
+                       timeout=1200, cwd=str(here.parent.parent))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
