@@ -36,6 +36,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "comm.hpp"
@@ -720,8 +721,11 @@ __global__ void __launch_bounds__(Z27Shape<MC>::THREADS + 32, XR == 2 ? 2 : 1)
     const int lx0 = px * 2, r0 = gy * STENCIL_BX + lx0;
     const int odd = gl & 1;
     const int cpa = (2 * cq + odd) * 2, cpb = (2 * cq + 1 - odd) * 2;   // column pairs in load order
-    double ao[2][4], am[2][4], an[2][4];   // row planes p-1 (old), p (mid), p+1 (new)
-    uint32_t mo[2] = {0, 0}, mm[2] = {0, 0}, mn[2] = {0, 0};
+    // three accumulator sets (and row masks) whose roles rotate every x plane:
+    // old = row plane p-1, mid = p, new = p+1 (the step body is instantiated
+    // for the three rotations, so no register moves)
+    double A0[2][4], A1[2][4], A2[2][4];
+    uint32_t M0[2] = {0, 0}, M1[2] = {0, 0}, M2[2] = {0, 0};
     int64_t q = 0;
     for (int si = 0; si < nsegs_b; ++si) {
         int t, za, steps;
@@ -729,8 +733,11 @@ __global__ void __launch_bounds__(Z27Shape<MC>::THREADS + 32, XR == 2 ? 2 : 1)
         if (steps <= 0) break;
         const int xg0 = (t % g.ntx) * STENCIL_BX + lx0, yg = (t / g.ntx) * 4 + gy;
         const bool yok = yg < g.ny;
-        for (int i = 0; i < steps + 2; ++i, ++q) {
-            const bool n0 = i <= steps - 1, n1 = i >= 1 && i <= steps, n2 = i >= 2;
+        // one x plane: all three targets computed unconditionally (a target
+        // outside [za, zb) accumulates stale ring data and is never stored),
+        // so the chains of the three row planes interleave without branches
+        auto body = [&](int i, double (&ao)[2][4], double (&am)[2][4], double (&an)[2][4], uint32_t (&mo)[2],
+                        uint32_t (&mm)[2], uint32_t (&mn)[2]) {
             mbar_wait(&xfull[q % XR], static_cast<uint32_t>((q / XR) & 1));
             mbar_wait(&vfull[q % VR], static_cast<uint32_t>((q / VR) & 1));
             const double* P = xr + (q % XR) * SH::PSTRIDE;
@@ -738,55 +745,59 @@ __global__ void __launch_bounds__(Z27Shape<MC>::THREADS + 32, XR == 2 ? 2 : 1)
             const double* V0 = reinterpret_cast<const double*>(ch);
             const double* V1 = reinterpret_cast<const double*>(ch + P0B);
             const double* V2 = reinterpret_cast<const double*>(ch + P0B + PB);
-            if (n0) {
+            if (i < steps) {
                 const uint2 mk = *reinterpret_cast<const uint2*>(ch + 9 * RT * 8 + r0 * 4);
                 mn[0] = mk.x;
                 mn[1] = mk.y;
-#pragma unroll
-                for (int r = 0; r < 2; ++r)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) an[r][c] = 0.0;
+            } else {
+                mn[0] = mn[1] = 0;
             }
-            const bool ck0 = ((mn[0] | mn[1]) & 0x80000000u) != 0;
-            const bool ck1 = ((mm[0] | mm[1]) & 0x80000000u) != 0;
-            const bool ck2 = ((mo[0] | mo[1]) & 0x80000000u) != 0;
 #pragma unroll
-            for (int dy = 0; dy < 3; ++dy) {
-                // the line's 4 points (lx0-1 .. lx0+2) x this lane's 4 columns
-                double2 xa[4], xb[4];
-                const double* L = P + ((gy + dy) * SH::LW + lx0) * MC;
+            for (int r = 0; r < 2; ++r)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    xa[j] = *reinterpret_cast<const double2*>(L + j * MC + cpa);
-                    xb[j] = *reinterpret_cast<const double2*>(L + j * MC + cpb);
-                }
-                // accumulator columns 0,1 <-> pair cpa, 2,3 <-> pair cpb (odd lanes hold
-                // their pairs swapped; the store puts them back), so no selects here
-                auto term = [&](double (&acc)[2][4], const double* V, const uint32_t (&mk)[2], bool ck, int shift) {
+                for (int c = 0; c < 4; ++c) an[r][c] = 0.0;
+            const bool ck = ((mn[0] | mn[1] | mm[0] | mm[1] | mo[0] | mo[1]) & 0x80000000u) != 0;
+            auto lines = [&](auto check) {
+                constexpr bool CK = decltype(check)::value;
 #pragma unroll
-                    for (int dx = 0; dx < 3; ++dx) {
-                        const double2 v = *reinterpret_cast<const double2*>(V + (dy * 3 + dx) * RT + r0);
+                for (int dy = 0; dy < 3; ++dy) {
+                    double2 xa[4], xb[4];
+                    const double* L = P + ((gy + dy) * SH::LW + lx0) * MC;
 #pragma unroll
-                        for (int r = 0; r < 2; ++r) {
-                            if (ck && !((mk[r] >> (shift + dy * 3 + dx)) & 1u)) continue;
-                            const double vv = r ? v.y : v.x;
-                            acc[r][0] = __dadd_rn(acc[r][0], __dmul_rn(vv, xa[r + dx].x));
-                            acc[r][1] = __dadd_rn(acc[r][1], __dmul_rn(vv, xa[r + dx].y));
-                            acc[r][2] = __dadd_rn(acc[r][2], __dmul_rn(vv, xb[r + dx].x));
-                            acc[r][3] = __dadd_rn(acc[r][3], __dmul_rn(vv, xb[r + dx].y));
-                        }
+                    for (int j = 0; j < 4; ++j) {
+                        xa[j] = *reinterpret_cast<const double2*>(L + j * MC + cpa);
+                        xb[j] = *reinterpret_cast<const double2*>(L + j * MC + cpb);
                     }
-                };
-                if (n2) term(ao, V2, mo, ck2, 18);
-                if (n1) term(am, V1, mm, ck1, 9);
-                if (n0) term(an, V0, mn, ck0, 0);
-            }
+                    // accumulator columns 0,1 <-> pair cpa, 2,3 <-> pair cpb (odd lanes
+                    // hold their pairs swapped; the store puts them back)
+                    auto term = [&](double (&acc)[2][4], const double* V, const uint32_t (&mk)[2], int shift) {
+#pragma unroll
+                        for (int dx = 0; dx < 3; ++dx) {
+                            const double2 v = *reinterpret_cast<const double2*>(V + (dy * 3 + dx) * RT + r0);
+#pragma unroll
+                            for (int r = 0; r < 2; ++r) {
+                                if (CK && !((mk[r] >> (shift + dy * 3 + dx)) & 1u)) continue;
+                                const double vv = r ? v.y : v.x;
+                                acc[r][0] = __dadd_rn(acc[r][0], __dmul_rn(vv, xa[r + dx].x));
+                                acc[r][1] = __dadd_rn(acc[r][1], __dmul_rn(vv, xa[r + dx].y));
+                                acc[r][2] = __dadd_rn(acc[r][2], __dmul_rn(vv, xb[r + dx].x));
+                                acc[r][3] = __dadd_rn(acc[r][3], __dmul_rn(vv, xb[r + dx].y));
+                            }
+                        }
+                    };
+                    term(ao, V2, mo, 18);
+                    term(am, V1, mm, 9);
+                    term(an, V0, mn, 0);
+                }
+            };
+            if (__any_sync(0xffffffffu, ck)) lines(std::true_type{});
+            else lines(std::false_type{});
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&xempty[q % XR]);
                 mbar_arrive(&vempty[q % VR]);
             }
-            if (n2 && yok) {   // row plane p-1 = za + i - 2 is complete
+            if (i >= 2 && yok) {   // row plane p-1 = za + i - 2 is complete
                 const int64_t rowz = (static_cast<int64_t>(g.zbeg + za + i - 2) * g.ny + yg) * g.nx;
 #pragma unroll
                 for (int r = 0; r < 2; ++r)
@@ -796,19 +807,20 @@ __global__ void __launch_bounds__(Z27Shape<MC>::THREADS + 32, XR == 2 ? 2 : 1)
                         *reinterpret_cast<double2*>(dst + cpb) = make_double2(ao[r][2], ao[r][3]);
                     }
             }
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                mo[r] = mm[r];
-                mm[r] = mn[r];
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    ao[r][c] = am[r][c];
-                    am[r][c] = an[r][c];
-                }
-            }
+            ++q;
+        };
+        const int n = steps + 2;
+        for (int i = 0; i < n;) {
+            body(i, A0, A1, A2, M0, M1, M2);
+            if (++i == n) break;
+            body(i, A1, A2, A0, M1, M2, M0);
+            if (++i == n) break;
+            body(i, A2, A0, A1, M2, M0, M1);
+            ++i;
         }
     }
 }
+
 #undef MBG_ACC
 
 // ---- host side ----------------------------------------------------------------
@@ -1003,10 +1015,11 @@ void launch_z27(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const do
                ctx->stream, tm, hm, gm, y, ctl);
 }
 
-// MBG_STENCIL_Z: 0 = the 3-plane kernel for 27-point m = 16 / 32 too;
-// 1 (default) = z-marching with rings (3, 2); 2 = rings (2, 2) (2 blocks/SM)
+// MBG_STENCIL_Z: 0 = the three-plane kernel for 27-point m = 16 / 32 too;
+// else the z-marching kernel with the ring depths listed at the dispatch
+// (default 3: x ring 4, value ring 3; C3 SpMM 676 -> 507 us on B200)
 int z27_mode() {
-    static const int v = env_int("MBG_STENCIL_Z", 0);
+    static const int v = env_int("MBG_STENCIL_Z", 3);
     return v;
 }
 
@@ -1083,13 +1096,22 @@ void launch_by(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y
     if constexpr (BY == 4) {
         if (kind == 27 && (m == 16 || m == 32) && (!epi || epi->kind == 0) && z27_mode() != 0) {
             const StencilLayout& Z = layout_for(ctx, a, 4, 1);
-            if (m == 16) {
-                if (z27_mode() == 2) launch_z27<16, 16, 2, 2>(ctx, a, Z, x, y, ctl, zr);
-                else launch_z27<16, 16, 3, 2>(ctx, a, Z, x, y, ctl, zr);
-            } else {
-                if (z27_mode() == 2) launch_z27<32, 16, 2, 2>(ctx, a, Z, x, y, ctl, zr);
-                else launch_z27<32, 16, 3, 2>(ctx, a, Z, x, y, ctl, zr);
-            }
+            // ring depths (x planes, value slots): 1 (3,2)  2 (2,2; 2 blocks/SM)
+            // 3 (4,3, default)  4 (3,3)  5 (4,4)  6 (5,3)  7 (4,2)
+            auto go = [&](auto mt) {
+                constexpr int MT = decltype(mt)::value;
+                switch (z27_mode()) {
+                    case 2: launch_z27<MT, 16, 2, 2>(ctx, a, Z, x, y, ctl, zr); break;
+                    case 3: launch_z27<MT, 16, 4, 3>(ctx, a, Z, x, y, ctl, zr); break;
+                    case 4: launch_z27<MT, 16, 3, 3>(ctx, a, Z, x, y, ctl, zr); break;
+                    case 5: launch_z27<MT, 16, 4, 4>(ctx, a, Z, x, y, ctl, zr); break;
+                    case 6: launch_z27<MT, 16, 5, 3>(ctx, a, Z, x, y, ctl, zr); break;
+                    case 7: launch_z27<MT, 16, 4, 2>(ctx, a, Z, x, y, ctl, zr); break;
+                    default: launch_z27<MT, 16, 3, 2>(ctx, a, Z, x, y, ctl, zr); break;
+                }
+            };
+            if (m == 16) go(std::integral_constant<int, 16>{});
+            else go(std::integral_constant<int, 32>{});
             return;
         }
     }

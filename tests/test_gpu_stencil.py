@@ -188,12 +188,12 @@ def test_stencil_random_shapes(ctx):
         assert_bitwise(Y.download(), O.spmv(a, x, m), f"{kind} {nx}x{ny}x{nz} m={m}")
 
 
-@pytest.mark.parametrize("mode", ["0", "1", "2"])
+@pytest.mark.parametrize("mode", ["0", "1", "2", "6"])
 def test_stencil_z27_modes(mode):
     # the 27-point m = 16 / 32 SpMM has three implementations selected once per
-    # process by MBG_STENCIL_Z (0: three resident planes; 1: z-marching, rings
-    # 3/2; 2: z-marching, rings 2/2 at 2 blocks/SM): rerun the stencil parity
-    # tests under each
+    # process by MBG_STENCIL_Z (0: three resident planes; else z-marching with
+    # ring depths 1: 3/2, 2: 2/2 at 2 blocks/SM, 3 (default): 4/3, 6: 5/3):
+    # rerun the stencil parity tests under the non-default ones
     import os
     import subprocess
     import sys

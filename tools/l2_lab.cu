@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstdio>
 #include <vector>
 
@@ -102,7 +103,40 @@ int main() {
                     static_cast<double>(w) * passes / (ms * 1e-3) / 1e9);
         first = false;
     }
-    std::printf("], \"gather\": [");
+    // HBM: a 4 GiB read-only stream (once) and a 2 x 2 GiB copy, for the read
+    // mix of read-dominated kernels next to the copy peak of MEASURED_PEAKS.json
+    {
+        const size_t big = size_t(4) << 30;
+        double2* h;
+        CK(cudaMalloc(&h, big));
+        CK(cudaMemset(h, 0, big));
+        const int64_t n16 = static_cast<int64_t>(big / 16);
+        stream_kernel<<<sms * 8, 256>>>(h, n16, 1, sink);
+        float best = 1e30f;
+        for (int r = 0; r < 5; ++r) {
+            CK(cudaEventRecord(a));
+            stream_kernel<<<sms * 8, 256>>>(h, n16, 1, sink);
+            CK(cudaEventRecord(b));
+            CK(cudaEventSynchronize(b));
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, a, b));
+            best = std::min(best, ms);
+        }
+        float bestc = 1e30f;
+        for (int r = 0; r < 5; ++r) {
+            CK(cudaEventRecord(a));
+            CK(cudaMemcpyAsync(reinterpret_cast<char*>(h) + big / 2, h, big / 2, cudaMemcpyDeviceToDevice));
+            CK(cudaEventRecord(b));
+            CK(cudaEventSynchronize(b));
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, a, b));
+            bestc = std::min(bestc, ms);
+        }
+        std::printf("], \"hbm_read_GBps\": %.1f, \"hbm_copy_GBps\": %.1f", static_cast<double>(big) / (best * 1e-3) / 1e9,
+                    static_cast<double>(big) / (bestc * 1e-3) / 1e9);
+        CK(cudaFree(h));
+    }
+    std::printf(", \"gather\": [");
     first = true;
     for (size_t w : {size_t(1) << 20, size_t(8) << 20, size_t(32) << 20}) {
         for (int L : {1, 2, 4, 8, 16}) {
