@@ -112,6 +112,7 @@ struct PUpd2Sq {
 // ... and phi = (t,s), psi = (t,t) in the pass after t = A s
 struct PClassicPhiPsi {
     static constexpr bool REDO_SAFE = true;
+    static constexpr bool FAST_SUM = true;   // FastTwoSum grows: -6 % (tools/ncu_ab.sh, C2)
     static constexpr const char* NAME = "classic_phipsi";
     static constexpr int NIN = 2, NOUT = 0, NCO = 0, NDOT = 2;   // in: t s
     __device__ static void run(const double* in, double*, double* prod, const double*) {
@@ -175,6 +176,23 @@ struct PReordG12 {
         const double z = fmadd_rn(fmadd_rn(0.0, 1.0, in[2]), co[2], in[3]);
         out[1] = z;
         out[2] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, z), co[3], in[1]), co[4], in[4]);
+    }
+};
+
+// Reordered, fused formulation with identity M^-1 (q = t, s = v elided): Alg. 6
+// line 17's r = 1*rt + (-omega)*t merged into the lines 20-22 pass, which reads
+// t (as q) anyway -- one vector read less per iteration, same expressions
+//   x = 1*x + alpha*vh + omega*th ; z = 1*th + (-omega)*q ;
+//   vh = 1*z + beta*vh + (-(beta*omega))*s ; r = 1*rt + (-omega)*q
+struct PReordG12R {
+    static constexpr const char* NAME = "reord_g12r";
+    static constexpr int NIN = 6, NOUT = 4, NCO = 5, NDOT = 0;   // in: x vh th q s rt; co: alpha omega -omega beta -(beta*omega)
+    __device__ static void run(const double* in, double* out, double*, const double* co) {
+        out[0] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, in[0]), co[0], in[1]), co[1], in[2]);
+        const double z = fmadd_rn(fmadd_rn(0.0, 1.0, in[2]), co[2], in[3]);
+        out[1] = z;
+        out[2] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, z), co[3], in[1]), co[4], in[4]);
+        out[3] = fmadd_rn(fmadd_rn(0.0, 1.0, in[5]), co[2], in[3]);
     }
 };
 
@@ -383,6 +401,12 @@ struct redo_safe_of { static constexpr bool value = false; };
 template <class P>
 struct redo_safe_of<P, decltype(void(P::REDO_SAFE))> { static constexpr bool value = P::REDO_SAFE; };
 
+// FastTwoSum in the streaming grows (exact.cuh two_sum_lazy) where it measured faster.
+template <class P, class = void>
+struct fast_sum_of { static constexpr bool value = false; };
+template <class P>
+struct fast_sum_of<P, decltype(void(P::FAST_SUM))> { static constexpr bool value = P::FAST_SUM; };
+
 // Widest packet a program may use (2 unless it declares VEC = 1).
 template <class P, class = void>
 struct vec_of { static constexpr int value = 2; };
@@ -455,8 +479,10 @@ __device__ __forceinline__ void block_combine(double (&acc)[NX][KEXP], int class
 #pragma unroll
                 for (int i = 0; i < KEXP; ++i) t[i] = __shfl_down_sync(0xffffffffu, mine[i], off);
                 if (lane < off) {
+                    // the lower terms are almost always exactly zero: skip their grows
 #pragma unroll
-                    for (int i = 0; i < KEXP; ++i) grow(mine, t[i], slot);
+                    for (int i = 0; i < KEXP; ++i)
+                        if (i == 0 || t[i] != 0.0) grow(mine, t[i], slot);
                 }
             }
             const int nw = nthr >> 5;
@@ -468,7 +494,10 @@ __device__ __forceinline__ void block_combine(double (&acc)[NX][KEXP], int class
             for (int s = nw >> 1; s >= 1; s >>= 1) {
                 if (warp < s && lane < classes) {
 #pragma unroll
-                    for (int i = 0; i < KEXP; ++i) grow(mine, sh[((warp + s) * 32 + lane) * KEXP + i], slot);
+                    for (int i = 0; i < KEXP; ++i) {
+                        const double v = sh[((warp + s) * 32 + lane) * KEXP + i];
+                        if (i == 0 || v != 0.0) grow(mine, v, slot);
+                    }
 #pragma unroll
                     for (int i = 0; i < KEXP; ++i) sh[(warp * 32 + lane) * KEXP + i] = mine[i];
                 }
@@ -481,7 +510,10 @@ __device__ __forceinline__ void block_combine(double (&acc)[NX][KEXP], int class
             for (int s = (nthr / classes) >> 1; s >= 1; s >>= 1) {
                 if (tid < s * classes) {
 #pragma unroll
-                    for (int i = 0; i < KEXP; ++i) grow(mine, sh[(tid + s * classes) * KEXP + i], slot);
+                    for (int i = 0; i < KEXP; ++i) {
+                        const double v = sh[(tid + s * classes) * KEXP + i];
+                        if (i == 0 || v != 0.0) grow(mine, v, slot);
+                    }
 #pragma unroll
                     for (int i = 0; i < KEXP; ++i) sh[tid * KEXP + i] = mine[i];
                 }
@@ -581,8 +613,8 @@ __global__ void __launch_bounds__(256, minblocks_of<P>::value) group_kernel(Grou
 #pragma unroll
                 for (int d = 0; d < P::NDOT; ++d) {
                     if constexpr (RS) {
-                        grow_lazy(acc[2 * d], p0[d], slot0[d]);
-                        grow_lazy(acc[2 * d + 1], p1[d], slot1[d]);
+                        grow_lazy<false, fast_sum_of<P>::value>(acc[2 * d], p0[d], slot0[d]);
+                        grow_lazy<false, fast_sum_of<P>::value>(acc[2 * d + 1], p1[d], slot1[d]);
                     } else {
                         grow(acc[2 * d], p0[d], slot0[d]);
                         grow(acc[2 * d + 1], p1[d], slot1[d]);
@@ -596,7 +628,7 @@ __global__ void __launch_bounds__(256, minblocks_of<P>::value) group_kernel(Grou
                 for (int i = 0; i < P::NOUT; ++i) a.out[i][qu] = o0[i];
 #pragma unroll
                 for (int d = 0; d < P::NDOT; ++d) {
-                    if constexpr (RS) grow_lazy(acc[d], p0[d], slot0[d]);
+                    if constexpr (RS) grow_lazy<false, fast_sum_of<P>::value>(acc[d], p0[d], slot0[d]);
                     else grow(acc[d], p0[d], slot0[d]);
                 }
             }
@@ -635,15 +667,15 @@ __global__ void __launch_bounds__(256, minblocks_of<P>::value) group_kernel(Grou
                     P::run(in, o1, p1, co1);
 #pragma unroll
                     for (int d = 0; d < P::NDOT; ++d) {
-                        grow_lazy<true>(acc[2 * d], p0[d], slot0[d]);
-                        grow_lazy<true>(acc[2 * d + 1], p1[d], slot1[d]);
+                        grow_lazy<true, fast_sum_of<P>::value>(acc[2 * d], p0[d], slot0[d]);
+                        grow_lazy<true, fast_sum_of<P>::value>(acc[2 * d + 1], p1[d], slot1[d]);
                     }
                 } else {
 #pragma unroll
                     for (int i = 0; i < P::NIN; ++i) in[i] = a.in[i][qr];
                     P::run(in, o0, p0, co0);
 #pragma unroll
-                    for (int d = 0; d < P::NDOT; ++d) grow_lazy<true>(acc[d], p0[d], slot0[d]);
+                    for (int d = 0; d < P::NDOT; ++d) grow_lazy<true, fast_sum_of<P>::value>(acc[d], p0[d], slot0[d]);
                 }
             }
 #pragma unroll

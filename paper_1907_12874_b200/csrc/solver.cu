@@ -446,14 +446,20 @@ void Solver::iteration() {
         } else {
             group<PReordG7>({r, v, t, r0}, {rt}, {S_NALPHA}, 0, P_R_OMEGA, 4);
         }
-        group<PUpd2>({rt, t}, {r}, {S_ONE, S_NOMEGA}, 0);        // r = rt - omega t
-        if (basic) {
-            group<PUpd3>({x, vh, th}, {x}, {S_ONE, S_ALPHA, S_OMEGA}, 0);
-            group<PUpd2>({th, q}, {z}, {S_ONE, S_NOMEGA}, 0);
-            group<PUpd3>({z, vh, s}, {vh}, {S_ONE, S_BETA, S_NBO}, 0, P_R_END, 0);
+        if (fused && elide_) {
+            // r = rt - omega t in the x / z / vh pass (t is read there as q)
+            group<PReordG12R>({x, vh, th, q, s, rt}, {x, z, vh, r}, {S_ALPHA, S_OMEGA, S_NOMEGA, S_BETA, S_NBO}, 0,
+                              P_R_END, 0);
         } else {
-            group<PReordG12>({x, vh, th, q, s}, {x, z, vh}, {S_ALPHA, S_OMEGA, S_NOMEGA, S_BETA, S_NBO}, 0,
-                             P_R_END, 0);
+            group<PUpd2>({rt, t}, {r}, {S_ONE, S_NOMEGA}, 0);        // r = rt - omega t
+            if (basic) {
+                group<PUpd3>({x, vh, th}, {x}, {S_ONE, S_ALPHA, S_OMEGA}, 0);
+                group<PUpd2>({th, q}, {z}, {S_ONE, S_NOMEGA}, 0);
+                group<PUpd3>({z, vh, s}, {vh}, {S_ONE, S_BETA, S_NBO}, 0, P_R_END, 0);
+            } else {
+                group<PReordG12>({x, vh, th, q, s}, {x, z, vh}, {S_ALPHA, S_OMEGA, S_NOMEGA, S_BETA, S_NBO}, 0,
+                                 P_R_END, 0);
+            }
         }
     } else if (method_ == MBG_PIPEBICGSTAB) {
         double *p = w(V_P), *s = w(V_S), *wv = w(V_W), *z = w(V_Z), *t = w(V_T), *v = w(V_V);
@@ -722,6 +728,9 @@ void Solver::report(double* hist_host, mbg_report* rep) {
     // TrafficCounter semantics: the preconditioner's transfers are tallied too
     // (alpha/2 reads + alpha/2 writes per application)
     if (method_ == MBG_RBICGSTAB && form_ == MBG_FUSED && !epi_delta_) reads += 1;   // delta pass: v, r0 vs aux r0
+    // fused Reordered merges r = rt - omega t into the x/z/vh pass only when
+    // q = t is elided (identity M^-1); otherwise that update is its own pass
+    if (method_ == MBG_RBICGSTAB && form_ == MBG_FUSED && !elide_) reads += 1;
     // classical fused on the stencil SpMM: delta pass (v, r0) -> aux r0 in the
     // SpMM epilogue; phi/psi pass (t, s) -> the second SpMM's epilogue
     const int classic_epi = (method_ == MBG_BICGSTAB && form_ == MBG_FUSED && stencil_ && stencil_epilogues()) ? 3 : 0;

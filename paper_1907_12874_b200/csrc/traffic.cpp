@@ -169,10 +169,10 @@ std::vector<Group> schedule_fused(int method, int* aux_reads, int* spmm_dots) {
             *aux_reads = 1;                 // r0 in v = A vh
             spmm_dots[0] = 1;
             spmm_dots[1] = 0;
+            // r = rt - omega t merged into the x / z / vh pass (t is read there as q)
             return {{U(TH, {Z, V})},
                     {U(RT, {R, V}), Dt(T, RT, 0), Dt(T, T, 1), Dt(T, R0, 2), Dt(RT, RT, 3)},
-                    {U(R, {RT, T})},
-                    {U(X, {X, VH, TH}), U(Z, {TH, T}), U(VH, {Z, VH, V})}};
+                    {U(X, {X, VH, TH}), U(Z, {TH, T}), U(VH, {Z, VH, V}), U(R, {RT, T})}};
         case MBG_PIPEBICGSTAB:
             *aux_reads = 0;
             spmm_dots[0] = spmm_dots[1] = 0;

@@ -243,3 +243,11 @@ def test_halo_plan_consistent(nparts):
             theirs = [x for x in plans[q]["peers"] if x["part"] == p]
             sent = theirs[0]["send_rows"] + bounds[q] if theirs else np.zeros(0, np.int64)
             assert np.array_equal(mine, sent)
+
+
+def test_method_schedule_fused_reordered():
+    # fused Reordered (identity M^-1 elided): the delta dot in the SpMM epilogue
+    # reads one aux vector; r = rt - omega t rides in the x / z / vh pass:
+    # 18 group transfers + 1 aux = 19 (merged listing: 21 + 4 for the copies)
+    s = P.method_schedule_pc("rbicgstab", "fused")
+    assert s["vec"] == 19 and s["precond"] == 0 and s["reductions"] == [1, 4]
