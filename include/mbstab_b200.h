@@ -70,6 +70,13 @@ int mbg_ctx_set_small_path(mbg_ctx* ctx, int enable);
  * MBG_RESERVE_SMS, default 4, so side-stream collectives overlap the SpMM).
  * Results do not depend on it (bitwise). */
 int mbg_ctx_reserve_sms(mbg_ctx* ctx, int count);
+/* Checked builds only (make checked -> libmbstab_b200_checked.so): every device
+ * allocation has guard zones on both sides; verify all live ones now and
+ * return the number of damaged buffers found so far.  Plain builds return an
+ * error.  mbg_debug_write_past_end deliberately writes one double past v's
+ * allocation (tests of the guard mechanism). */
+int mbg_debug_guard_check(int64_t* violations);
+int mbg_debug_write_past_end(mbg_mv* v);
 /* Multi-GPU: join a communicator of `world` ranks (one process per GPU).
  * nccl_id is the 128-byte ncclUniqueId created by rank 0 (mbg_comm_unique_id)
  * and broadcast by the caller (e.g. torch.distributed). */

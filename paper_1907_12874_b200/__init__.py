@@ -278,6 +278,20 @@ class MultiVector:
 # ---------------------------------------------------------------------------
 # operators
 # ---------------------------------------------------------------------------
+def debug_guard_check() -> int:
+    """Checked builds (MBG_CHECKED=1): damaged guard zones found so far (0 = none)."""
+    v = C.c_int64(0)
+    rc = lib().mbg_debug_guard_check(C.byref(v))
+    if rc != 0 and v.value == 0:
+        check(rc)
+    return int(v.value)
+
+
+def debug_write_past_end(v: "MultiVector") -> None:
+    """Checked builds: write one double past v's allocation (tests the guards)."""
+    check(lib().mbg_debug_write_past_end(v.h))
+
+
 def spmv(ctx: Context, a: DeviceCsr, x: MultiVector, y: MultiVector) -> None:
     """y = A x (core::spmv).  Raises ValueError on shape mismatch or x is y."""
     check(lib().mbg_spmv(ctx.h, a.h, x.h, y.h))

@@ -11,7 +11,9 @@ import os
 from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
-LIB_PATH = HERE / "libmbstab_b200.so"
+# MBG_CHECKED=1: the guard-zone build (csrc/Makefile `checked`), for the
+# out-of-bounds tests that stand in for compute-sanitizer on this pool
+LIB_PATH = HERE / ("libmbstab_b200_checked.so" if os.environ.get("MBG_CHECKED") == "1" else "libmbstab_b200.so")
 
 MBG_OK, MBG_ERR_INVALID, MBG_ERR_RUNTIME, MBG_ERR_BREAKDOWN = 0, 1, 2, 3
 MBG_MAX_TERMS = 8
@@ -99,6 +101,8 @@ def lib() -> C.CDLL:
         "mbg_csr_stencil_kind": (i32, [vp]),
         "mbg_ctx_set_small_path": (i32, [vp, i32]),
         "mbg_ctx_reserve_sms": (i32, [vp, i32]),
+        "mbg_debug_guard_check": (i32, [C.POINTER(C.c_int64)]),
+        "mbg_debug_write_past_end": (i32, [vp]),
         "mbg_mv_alloc": (i32, [vp, i64, i32, pp]),
         "mbg_mv_free": (i32, [vp]),
         "mbg_mv_upload": (i32, [vp, vp]),

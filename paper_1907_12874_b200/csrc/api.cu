@@ -11,6 +11,7 @@
 #include <mutex>
 #include <thread>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -533,6 +534,111 @@ extern "C" int mbg_ctx_set_small_path(mbg_ctx* ctx, int enable) {
     return guarded([&] {
         if (!ctx) throw Invalid("null context");
         ctx->small_path = enable != 0;
+    });
+}
+
+#ifdef MBG_CHECKED
+namespace mbg {
+namespace {
+struct GuardRegistry {
+    std::mutex mu;
+    std::map<void*, size_t> live;   // user pointer -> user bytes
+    int64_t violations = 0;
+    std::string first;
+};
+GuardRegistry& guards() {
+    static GuardRegistry g;
+    return g;
+}
+// number of guard bytes (of the two zones of `user`) that no longer hold GUARD_BYTE
+int64_t guard_damage(void* user, size_t bytes) {
+    std::vector<unsigned char> h(GUARD_BYTES);
+    int64_t bad = 0;
+    for (int side = 0; side < 2; ++side) {
+        const unsigned char* z = static_cast<unsigned char*>(user) + (side ? bytes : 0) - (side ? 0 : GUARD_BYTES);
+        if (cudaMemcpy(h.data(), z, GUARD_BYTES, cudaMemcpyDeviceToHost) != cudaSuccess) {
+            (void)cudaGetLastError();
+            return -1;
+        }
+        for (unsigned char c : h) bad += c != GUARD_BYTE;
+    }
+    return bad;
+}
+}  // namespace
+
+void* guarded_alloc(size_t bytes) {
+    const size_t padded = (bytes + 255) / 256 * 256;
+    unsigned char* raw = nullptr;
+    MBG_CUDA(cudaMalloc(&raw, padded + 2 * GUARD_BYTES));
+    MBG_CUDA(cudaMemset(raw, GUARD_BYTE, padded + 2 * GUARD_BYTES));
+    void* user = raw + GUARD_BYTES;
+    std::lock_guard<std::mutex> lk(guards().mu);
+    guards().live[user] = padded;
+    return user;
+}
+
+void guarded_free(void* user) {
+    size_t bytes = 0;
+    {
+        std::lock_guard<std::mutex> lk(guards().mu);
+        auto it = guards().live.find(user);
+        if (it == guards().live.end()) return;
+        bytes = it->second;
+        guards().live.erase(it);
+    }
+    cudaDeviceSynchronize();
+    const int64_t bad = guard_damage(user, bytes);
+    if (bad != 0) {
+        std::lock_guard<std::mutex> lk(guards().mu);
+        guards().violations += bad > 0 ? 1 : 0;
+        if (guards().first.empty())
+            guards().first = "guard zone of a " + std::to_string(bytes) + "-byte buffer overwritten (" +
+                             std::to_string(bad) + " bytes)";
+    }
+    cudaFree(static_cast<unsigned char*>(user) - GUARD_BYTES);
+}
+
+__global__ void write_past_end_kernel(double* p, int64_t n) { p[n] = 1.0; }
+}  // namespace mbg
+#endif
+
+// Checked builds only: verify the guard zones of every live device buffer
+// now; *violations = buffers found damaged so far (live or freed).
+extern "C" int mbg_debug_guard_check(int64_t* violations) {
+    return guarded([&] {
+        if (!violations) throw Invalid("null output");
+#ifdef MBG_CHECKED
+        MBG_CUDA(cudaDeviceSynchronize());
+        std::lock_guard<std::mutex> lk(guards().mu);
+        for (const auto& [user, bytes] : guards().live) {
+            const int64_t bad = guard_damage(user, bytes);
+            if (bad != 0) {
+                ++guards().violations;
+                if (guards().first.empty())
+                    guards().first = "guard zone of a live " + std::to_string(bytes) + "-byte buffer overwritten";
+            }
+        }
+        *violations = guards().violations;
+        if (*violations) set_error(guards().first.c_str());
+#else
+        throw std::runtime_error("mbg_debug_guard_check: not a checked build (make checked)");
+#endif
+    });
+}
+
+// Checked builds only (tests of the guard mechanism): one kernel writes the
+// element just past the end of v's n*m doubles.
+extern "C" int mbg_debug_write_past_end(mbg_mv* v) {
+    return guarded([&] {
+        if (!v) throw Invalid("null multivector");
+#ifdef MBG_CHECKED
+        MBG_CUDA(cudaSetDevice(v->device));
+        // the first element past the 256-byte-rounded allocation: the guard zone
+        write_past_end_kernel<<<1, 1>>>(v->data.p, static_cast<int64_t>((v->data.n * 8 + 255) / 256 * 256 / 8));
+        MBG_CUDA(cudaDeviceSynchronize());
+#else
+        throw std::runtime_error("mbg_debug_write_past_end: not a checked build (make checked)");
+#endif
     });
 }
 

@@ -36,6 +36,22 @@ void set_error(const std::string& msg);
 
 // Device buffer with RAII.
 template <class T>
+struct DevBuf;
+
+#ifdef MBG_CHECKED
+// Checked builds (make checked -> libmbstab_b200_checked.so; MBG_CHECKED=1
+// selects it in the Python binding): every device allocation carries guard
+// zones of GUARD_BYTES filled with GUARD_BYTE on both sides; they are verified
+// when the buffer is freed and on demand (mbg_debug_guard_check), so an
+// out-of-bounds write by any kernel is caught -- the substitute for
+// compute-sanitizer memcheck, which this GPU pool does not allow.
+constexpr size_t GUARD_BYTES = 64u << 10;
+constexpr unsigned char GUARD_BYTE = 0xA5;
+void* guarded_alloc(size_t bytes);     // returns the user pointer
+void guarded_free(void* user);         // verifies, then frees
+#endif
+
+template <class T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
@@ -51,12 +67,20 @@ struct DevBuf {
     ~DevBuf() { release(); }
     void alloc(size_t count) {
         release();
+#ifdef MBG_CHECKED
+        if (count) p = static_cast<T*>(guarded_alloc(count * sizeof(T)));
+#else
         if (count) MBG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+#endif
         n = count;
     }
     void ensure(size_t count) { if (count > n) alloc(count); }
     void release() {
+#ifdef MBG_CHECKED
+        if (p) guarded_free(p);
+#else
         if (p) cudaFree(p);
+#endif
         p = nullptr;
         n = 0;
     }
