@@ -196,6 +196,22 @@ struct PReordG12R {
     }
 };
 
+// ... and with th never stored (formed inside the second SpMM, stencil.cu):
+// th = 1*z + (-alpha)*s recomputed here with the expression of its update pass
+//   in: x vh z q s rt ; out: x z vh r ; co: alpha omega -omega beta -(beta*omega) -alpha
+struct PReordG12RZ {
+    static constexpr const char* NAME = "reord_g12rz";
+    static constexpr int NIN = 6, NOUT = 4, NCO = 6, NDOT = 0;
+    __device__ static void run(const double* in, double* out, double*, const double* co) {
+        const double th = fmadd_rn(fmadd_rn(0.0, 1.0, in[2]), co[5], in[4]);
+        out[0] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, in[0]), co[0], in[1]), co[1], th);
+        const double z = fmadd_rn(fmadd_rn(0.0, 1.0, th), co[2], in[3]);
+        out[1] = z;
+        out[2] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, z), co[3], in[1]), co[4], in[4]);
+        out[3] = fmadd_rn(fmadd_rn(0.0, 1.0, in[5]), co[2], in[3]);
+    }
+};
+
 // Pipelined, Alg. 4 line 4:
 //   p = 1*r + beta*p + nbo*s ; s = 1*w + beta*s + nbo*z ; z = 1*t + beta*z + nbo*v ;
 //   q = 1*r + (-alpha)*s ; y = 1*w + (-alpha)*z ; theta=(q,y), phi=(y,y), pi=(q,q)

@@ -95,6 +95,9 @@ Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulatio
     // 8.90 vs 8.07 ms/iteration, C5 m=8 5.28 vs 4.97; C2 7-point 0.76 vs 0.84)
     // (stencil SpMM: only with MBG_STENCIL_EPI=1 -- measured slower)
     epi_delta_ = formulation == MBG_FUSED && (stencil_ ? stencil_epilogues() : a->nnz <= 12 * a->n);
+    // fused Reordered on a single-GPU 27-point twin (m = 16 / 32): the th update
+    // pass is folded into the second SpMM, th is never stored (2 transfers less)
+    ax_ = elide_ && method == MBG_RBICGSTAB && !ctx->comm && stencil_ && !epi_delta_ && stencil_axpy_handles(a, m);
     if (method == MBG_IBICGSTAB) {
         if (!a->peers.empty() || a->n_halo) {
             // partitioned: A^T and its own halo plan were built at upload
@@ -113,7 +116,8 @@ Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulatio
     switch (method) {
         case MBG_BICGSTAB: need = {V_R, V_R0, V_P, V_V, V_S, V_T}; break;
         case MBG_RBICGSTAB:
-            need = {V_R, V_R0, V_V, V_T, V_Z, V_VH, V_TH, V_RT};
+            need = {V_R, V_R0, V_V, V_T, V_Z, V_VH, V_RT};
+            if (!ax_) need.push_back(V_TH);
             if (!elide_) need.insert(need.end(), {V_S, V_Q});
             break;
         case MBG_PIPEBICGSTAB: need = {V_R, V_R0, V_P, V_V, V_S, V_T, V_Z, V_Q, V_W, V_Y, V_TMP}; break;
@@ -219,6 +223,13 @@ void Solver::spmm(const double* x, double* y, int epi_kind, const double* aux, i
         if (nred > 0) reductions_++;
     }
     if (post_point >= 0) scalars(post_point, post_nd);
+}
+
+void Solver::spmm_axpy(const double* z, const double* v, const double* na, double* y) {
+    // algorithmic bytes: the stencil SpMM's, plus the second input vector
+    mark_begin("spmm+axpy", stencil_spmm_bytes(a_->n, a_->nnz, m_) + 8.0 * len_);
+    launches_ += launch_stencil_spmm_axpy(ctx_, a_, m_, z, v, na, y, ctl_.p);
+    mark_end();
 }
 
 template <class P>
@@ -434,8 +445,12 @@ void Solver::iteration() {
             if (!elide_) minv(v, s);                              // s = M^-1 v
             group<PDot2>({v, r0}, {}, {}, 0, P_C_ALPHA, 1);
         }
-        group<PUpd2>({z, s}, {th}, {S_ONE, S_NALPHA}, 0);        // th = z - alpha s
-        spmm(th, t);
+        if (ax_) {
+            spmm_axpy(z, s, sc(S_NALPHA), t);                    // t = A (z - alpha s), th never stored
+        } else {
+            group<PUpd2>({z, s}, {th}, {S_ONE, S_NALPHA}, 0);    // th = z - alpha s
+            spmm(th, t);
+        }
         if (!elide_) minv(t, q);                                  // q = M^-1 t
         if (basic) {
             group<PUpd2>({r, v}, {rt}, {S_ONE, S_NALPHA}, 0);
@@ -446,7 +461,11 @@ void Solver::iteration() {
         } else {
             group<PReordG7>({r, v, t, r0}, {rt}, {S_NALPHA}, 0, P_R_OMEGA, 4);
         }
-        if (fused && elide_) {
+        if (ax_) {
+            // th recomputed from z and s (same expression as its update pass)
+            group<PReordG12RZ>({x, vh, z, q, s, rt}, {x, z, vh, r},
+                               {S_ALPHA, S_OMEGA, S_NOMEGA, S_BETA, S_NBO, S_NALPHA}, 0, P_R_END, 0);
+        } else if (fused && elide_) {
             // r = rt - omega t in the x / z / vh pass (t is read there as q)
             group<PReordG12R>({x, vh, th, q, s, rt}, {x, z, vh, r}, {S_ALPHA, S_OMEGA, S_NOMEGA, S_BETA, S_NBO}, 0,
                               P_R_END, 0);
@@ -731,6 +750,12 @@ void Solver::report(double* hist_host, mbg_report* rep) {
     // fused Reordered merges r = rt - omega t into the x/z/vh pass only when
     // q = t is elided (identity M^-1); otherwise that update is its own pass
     if (method_ == MBG_RBICGSTAB && form_ == MBG_FUSED && !elide_) reads += 1;
+    // th formed inside the second SpMM: its update pass (z, s -> th) is gone and
+    // the SpMM reads s beside z (the SpMM-side read is counted as a vector read)
+    if (ax_) {
+        reads -= 1;
+        writes -= 1;
+    }
     // classical fused on the stencil SpMM: delta pass (v, r0) -> aux r0 in the
     // SpMM epilogue; phi/psi pass (t, s) -> the second SpMM's epilogue
     const int classic_epi = (method_ == MBG_BICGSTAB && form_ == MBG_FUSED && stencil_ && stencil_epilogues()) ? 3 : 0;
@@ -740,7 +765,9 @@ void Solver::report(double* hist_host, mbg_report* rep) {
     rep->spmv_bytes = static_cast<double>(spmvs) * its * spmv_traffic_bytes(a_->n, a_->nnz, m_);
     rep->compulsory_bytes =
         (iteration_bytes(method_, form_, pa_, a_->n, a_->nnz, m_) +
-         ((method_ == MBG_RBICGSTAB && form_ == MBG_FUSED && !epi_delta_) ? 8.0 * static_cast<double>(len_) : 0.0) -
+         ((method_ == MBG_RBICGSTAB && form_ == MBG_FUSED && !epi_delta_) ? 8.0 * static_cast<double>(len_) : 0.0) +
+         ((method_ == MBG_RBICGSTAB && form_ == MBG_FUSED && !elide_) ? 8.0 * static_cast<double>(len_) : 0.0) -
+         (ax_ ? 16.0 * static_cast<double>(len_) : 0.0) -
          8.0 * classic_epi * static_cast<double>(len_) -
          // stencil SpMM: no column indices (8 B instead of 12 B per nonzero)
          (stencil_ ? 4.0 * spmvs * static_cast<double>(a_->nnz) : 0.0)) *

@@ -54,6 +54,8 @@ private:
     // footprint slowed the streaming kernels; removed.)
     void spmm(const double* x, double* y, int epi_kind = 0, const double* aux = nullptr, int post_point = -1,
               int post_nd = 0, int first_slot = 0, int reduce = -1);
+    // y = A ((0 + 1*z) + na*v), the input formed per x plane inside the stencil SpMM
+    void spmm_axpy(const double* z, const double* v, const double* na, double* y);
     template <class P>
     void group(std::initializer_list<const double*> in, std::initializer_list<double*> out,
                std::initializer_list<int> co, int first_slot, int post_point = -1, int post_nd = 0,
@@ -72,6 +74,7 @@ private:
     int pa_ = 0;            // preconditioner alpha (0 none, 2 identity, >= 4 synthetic)
     bool elide_ = false;    // fused formulation with identity M^-1: applications aliased away
     bool epi_delta_ = false;
+    bool ax_ = false;         // fused Reordered: th = z - alpha s formed inside the second SpMM (stencil.cu)
     bool stencil_ = false;    // the operator's SpMM runs on its stencil twin (stencil.cu)  // fused Reordered: delta = (v, r0) in the SpMM epilogue
     const mbg_csr* at_ = nullptr;   // A^T (IBiCGStab setup)
     const mbg_csr* orig_ = nullptr; // caller's operator when a_ is its reordered twin

@@ -616,15 +616,25 @@ struct Z27Shape {
     static constexpr int CB = 27 * RT * 8 + RT * 4;         // one chunk (= one value-ring slot)
 };
 
-template <int MC, int XR, int VR>
+// VS > 0 (the fused-input variant): the SpMM input is xin = (0 + 1*z) + na*v
+// with na a per-column coefficient (Reordered: th = z - alpha s, Alg. 6 line 6
+// in the same expression and rounding as the separate update pass).  The x
+// ring then holds z boxes, converted in place to xin boxes once their v box
+// (a VS-deep staging ring) has landed, before the step reads them.
+template <int MC, int XR, int VR, int VS = 0>
 __host__ __device__ constexpr int z27_smem() {
-    return STENCIL_HEAD + XR * Z27Shape<MC>::PSTRIDE * 8 + VR * Z27Shape<MC>::CB;
+    return STENCIL_HEAD + (XR + VS) * Z27Shape<MC>::PSTRIDE * 8 + VR * Z27Shape<MC>::CB;
 }
 
-template <int MT, int MC, int XR, int VR>
-__global__ void __launch_bounds__(Z27Shape<MC>::THREADS + 32, XR == 2 ? 2 : 1)
+// converter warps of the fused-input variant (they form xin one plane ahead of
+// the compute warps, so the conversion never stalls them)
+constexpr int Z27_CONV = 64;
+
+template <int MT, int MC, int XR, int VR, int VS = 0>
+__global__ void __launch_bounds__(Z27Shape<MC>::THREADS + (VS > 0 ? Z27_CONV : 0) + 32, XR == 2 ? 2 : 1)
     stencil27z_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
-                      StencilGeom g, double* __restrict__ y, const int* __restrict__ ctl) {
+                      StencilGeom g, double* __restrict__ y, const int* __restrict__ ctl,
+                      const __grid_constant__ CUtensorMap vmap, const double* __restrict__ na) {
     using SH = Z27Shape<MC>;
     constexpr int CS = MT / MC, RT = SH::RT, CB = SH::CB;
     constexpr int P0B = 9 * RT * 8 + RT * 4;   // part 0 + masks
@@ -638,8 +648,14 @@ __global__ void __launch_bounds__(Z27Shape<MC>::THREADS + 32, XR == 2 ? 2 : 1)
     uint64_t* xempty = xfull + XR;
     uint64_t* vfull = xempty + XR;
     uint64_t* vempty = vfull + VR;
+    uint64_t* sempty = vempty + VR;   // v staging ring (VS > 0)
+    uint64_t* ready = sempty + VS;    // xin box formed (VS > 0)
     double* xr = reinterpret_cast<double*>(smem + STENCIL_HEAD);
-    unsigned char* vr = smem + STENCIL_HEAD + XR * SH::PSTRIDE * 8;
+    double* vs = xr + XR * SH::PSTRIDE;
+    unsigned char* vr = smem + STENCIL_HEAD + (XR + VS) * SH::PSTRIDE * 8;
+    static_assert(3 * XR + 2 * VR + VS <= STENCIL_HEAD / 8, "barrier header");
+    constexpr int NCONV = VS > 0 ? Z27_CONV : 0;
+    constexpr int PROD = SH::THREADS + NCONV;   // first thread of the producer warp
 
     const int h = blockIdx.x % CS;
     const int rb = blockIdx.x / CS;
@@ -668,12 +684,41 @@ __global__ void __launch_bounds__(Z27Shape<MC>::THREADS + 32, XR == 2 ? 2 : 1)
             mbar_init(&vfull[b], 1);
             mbar_init(&vempty[b], SH::NCW);
         }
+        for (int b = 0; b < VS; ++b) mbar_init(&sempty[b], NCONV);
+        for (int b = 0; b < (VS > 0 ? XR : 0); ++b) mbar_init(&ready[b], NCONV);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
-    if (tid >= SH::THREADS) {   // ---- producer warp: one slot of each ring per x plane
-        if (tid == SH::THREADS) {
+    if constexpr (VS > 0) {
+        if (tid >= SH::THREADS && tid < PROD) {   // ---- converter warps: xin = (0 + 1*z) + na*v, in place
+            const int ct = tid - SH::THREADS;
+            // the thread's column pair is fixed (NCONV pairs per sweep, MC columns)
+            const double2 nc = make_double2(na[h * MC + (2 * ct) % MC], na[h * MC + (2 * ct) % MC + 1]);
+            int64_t q = 0;
+            for (int si = 0; si < nsegs_b; ++si) {
+                int t, za, steps;
+                segment(si, t, za, steps);
+                if (steps <= 0) break;
+                for (int i = 0; i < steps + 2; ++i, ++q) {
+                    mbar_wait(&xfull[q % XR], static_cast<uint32_t>((q / XR) & 1));
+                    double2* zb = reinterpret_cast<double2*>(xr + (q % XR) * SH::PSTRIDE);
+                    const double2* vb = reinterpret_cast<const double2*>(vs + (q % VS) * SH::PSTRIDE);
+#pragma unroll 4
+                    for (int e = ct; e < SH::PLANE / 2; e += NCONV) {
+                        const double2 zz = zb[e], vv = vb[e];
+                        zb[e] = make_double2(__dadd_rn(__dadd_rn(0.0, __dmul_rn(1.0, zz.x)), __dmul_rn(nc.x, vv.x)),
+                                             __dadd_rn(__dadd_rn(0.0, __dmul_rn(1.0, zz.y)), __dmul_rn(nc.y, vv.y)));
+                    }
+                    mbar_arrive(&sempty[q % VS]);   // v box consumed
+                    mbar_arrive(&ready[q % XR]);    // (release: this thread's xin stores)
+                }
+            }
+            return;
+        }
+    }
+    if (tid >= PROD) {   // ---- producer warp: one slot of each ring per x plane
+        if (tid == PROD) {
             int64_t q = 0;   // x planes (= steps) issued so far
             for (int si = 0; si < nsegs_b; ++si) {
                 int t, za, steps;
@@ -685,7 +730,16 @@ __global__ void __launch_bounds__(Z27Shape<MC>::THREADS + 32, XR == 2 ? 2 : 1)
                     const int bx = static_cast<int>(q % XR), bv = static_cast<int>(q % VR);
                     if (q >= XR) mbar_wait(&xempty[bx], static_cast<uint32_t>((q / XR - 1) & 1));
                     if (q >= VR) mbar_wait(&vempty[bv], static_cast<uint32_t>((q / VR - 1) & 1));
-                    mbar_expect_tx(&xfull[bx], static_cast<uint32_t>(SH::PLANE * 8));
+                    if constexpr (VS > 0) {
+                        const int bs = static_cast<int>(q % VS);
+                        if (q >= VS) mbar_wait(&sempty[bs], static_cast<uint32_t>((q / VS - 1) & 1));
+                        // z box into the x ring, v box into the staging ring, one barrier
+                        mbar_expect_tx(&xfull[bx], static_cast<uint32_t>(2 * SH::PLANE * 8));
+                        tensor4d_g2s(vs + bs * SH::PSTRIDE, &vmap, h * MC, (t % g.ntx) * STENCIL_BX - 1,
+                                     (t / g.ntx) * 4 - 1, g.zbeg + p, &xfull[bx]);
+                    } else {
+                        mbar_expect_tx(&xfull[bx], static_cast<uint32_t>(SH::PLANE * 8));
+                    }
                     const int pl = g.zbeg + p;
                     const void* map = &xmap;
                     int pz = pl;
@@ -738,7 +792,8 @@ __global__ void __launch_bounds__(Z27Shape<MC>::THREADS + 32, XR == 2 ? 2 : 1)
         // so the chains of the three row planes interleave without branches
         auto body = [&](int i, double (&ao)[2][4], double (&am)[2][4], double (&an)[2][4], uint32_t (&mo)[2],
                         uint32_t (&mm)[2], uint32_t (&mn)[2]) {
-            mbar_wait(&xfull[q % XR], static_cast<uint32_t>((q / XR) & 1));
+            if constexpr (VS > 0) mbar_wait(&ready[q % XR], static_cast<uint32_t>((q / XR) & 1));
+            else mbar_wait(&xfull[q % XR], static_cast<uint32_t>((q / XR) & 1));
             mbar_wait(&vfull[q % VR], static_cast<uint32_t>((q / VR) & 1));
             const double* P = xr + (q % XR) * SH::PSTRIDE;
             const unsigned char* ch = vr + (q % VR) * CB;
@@ -969,16 +1024,18 @@ void split_work(StencilGeom& gm, int64_t slots) {
     }
 }
 
-template <int MT, int MC, int XR, int VR>
+// VS > 0: the fused-input variant, x = z, v / na as stencil27z_kernel describes
+template <int MT, int MC, int XR, int VR, int VS = 0>
 void launch_z27(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const double* x, double* y, const int* ctl,
-                ZRange zr) {
+                ZRange zr, const double* v = nullptr, const double* na = nullptr) {
     using SH = Z27Shape<MC>;
     const StencilOp& op = *a->stencil;
     if (zr.zend <= zr.zbeg) return;
-    constexpr int smem = z27_smem<MC, XR, VR>();
-    constexpr int threads = SH::THREADS + 32;
+    constexpr int smem = z27_smem<MC, XR, VR, VS>();
+    constexpr int threads = SH::THREADS + (VS > 0 ? Z27_CONV : 0) + 32;
     constexpr int CS = MT / MC;
-    const int occ = kernel_occupancy(reinterpret_cast<const void*>(&stencil27z_kernel<MT, MC, XR, VR>), threads, smem);
+    const int occ =
+        kernel_occupancy(reinterpret_cast<const void*>(&stencil27z_kernel<MT, MC, XR, VR, VS>), threads, smem);
     auto encode = [&](CUtensorMap& tm, const double* base, int planes) {
         const cuuint64_t dims[4] = {static_cast<cuuint64_t>(MT), static_cast<cuuint64_t>(op.nx),
                                     static_cast<cuuint64_t>(op.ny), static_cast<cuuint64_t>(planes)};
@@ -1011,8 +1068,10 @@ void launch_z27(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const do
     gm.chunks = L.chunks.p;
     gm.chunk_bytes = L.chunk_bytes;
     split_work(gm, static_cast<int64_t>(occ) * ctx->num_sms / CS);
-    launch_pdl(stencil27z_kernel<MT, MC, XR, VR>, dim3(gm.nranges * CS), dim3(threads), static_cast<size_t>(smem),
-               ctx->stream, tm, hm, gm, y, ctl);
+    CUtensorMap vm = tm;
+    if constexpr (VS > 0) encode(vm, v, op.nz);
+    launch_pdl(stencil27z_kernel<MT, MC, XR, VR, VS>, dim3(gm.nranges * CS), dim3(threads), static_cast<size_t>(smem),
+               ctx->stream, tm, hm, gm, y, ctl, vm, na);
 }
 
 // MBG_STENCIL_Z: 0 = the three-plane kernel for 27-point m = 16 / 32 too;
@@ -1138,6 +1197,32 @@ void launch_by(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y
         default:
             throw Invalid("stencil SpMM: m must be 4, 8, 16 or 32");
     }
+}
+
+bool stencil_axpy_handles(const mbg_csr* a, int m) {
+    static const bool on = env_int("MBG_STENCIL_AX", 1) != 0;
+    return on && stencil_handles(a, m) && a->stencil->kind == 27 && (m == 16 || m == 32) && z27_mode() != 0 &&
+           a->stencil->map.lower == 0 && a->stencil->upper == 0 && a->peers.empty() && a->n_halo == 0;
+}
+
+int launch_stencil_spmm_axpy(mbg_ctx* ctx, const mbg_csr* a, int m, const double* z, const double* v,
+                             const double* na, double* y, const int* ctl) {
+    if (!stencil_axpy_handles(a, m)) throw Invalid("stencil SpMM: fused input needs a 27-point m = 16 / 32 twin");
+    const StencilLayout& Z = layout_for(ctx, a, 4, 1);
+    const ZRange zr{0, a->stencil->nz};
+    // rings: x (z boxes) 3, v staging 2, values 3 (the 227 KB budget; value
+    // depth 3 is what matters, tools/spmm_time.py sweep in DESIGN.md)
+    // MBG_STENCIL_AXR (lab): ring depths x / values / v staging  1: 3/3/2  2: 4/3/1  3: 4/2/2
+    static const int rings = env_int("MBG_STENCIL_AXR", 1);
+    auto go = [&](auto mt) {
+        constexpr int MT = decltype(mt)::value;
+        if (rings == 2) launch_z27<MT, 16, 4, 3, 1>(ctx, a, Z, z, y, ctl, zr, v, na);
+        else if (rings == 3) launch_z27<MT, 16, 4, 2, 2>(ctx, a, Z, z, y, ctl, zr, v, na);
+        else launch_z27<MT, 16, 3, 3, 2>(ctx, a, Z, z, y, ctl, zr, v, na);
+    };
+    if (m == 16) go(std::integral_constant<int, 16>{});
+    else go(std::integral_constant<int, 32>{});
+    return 1;
 }
 
 int launch_stencil_spmm(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y, const int* ctl,

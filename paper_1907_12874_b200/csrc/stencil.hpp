@@ -81,6 +81,13 @@ struct SpmmEpi;
 // runs its interior planes while the halo planes travel, then the two faces.
 int launch_stencil_spmm(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y, const int* ctl,
                         const SpmmEpi* epi = nullptr, int zbeg = 0, int zend = -1);
+// y = A xin with xin = (0 + 1*z) + na*v (na: m per-column coefficients),
+// formed per x plane in shared memory -- the Reordered th = z - alpha s update
+// fused into its SpMM (same expression, same bits).  Single-GPU 27-point
+// operators at m = 16 / 32 (stencil_axpy_handles); returns kernel launches.
+bool stencil_axpy_handles(const mbg_csr* a, int m);
+int launch_stencil_spmm_axpy(mbg_ctx* ctx, const mbg_csr* a, int m, const double* z, const double* v,
+                             const double* na, double* y, const int* ctl);
 // Algorithmic bytes of one stencil SpMM: x read once, y written once, 8 B per
 // nonzero value, 4 B per row mask.
 double stencil_spmm_bytes(int64_t n, int64_t nnz, int m);

@@ -109,7 +109,8 @@ def test_stencil_rejects_non_grid(ctx):
 @pytest.mark.parametrize("method,form", [("bicgstab", "fused"), ("rbicgstab", "fused"), ("pipebicgstab", "merged"),
                                          ("pbicgstab", "fused"), ("ibicgstab", "merged")])
 @pytest.mark.parametrize("kind,dims,m", [("convdiff7", (36, 9, 8), 8), ("stencil27", (20, 12, 9), 16),
-                                         ("convdiff7", (33, 5, 6), 32), ("stencil27", (37, 17, 7), 4)])
+                                         ("convdiff7", (33, 5, 6), 32), ("stencil27", (37, 17, 7), 4),
+                                         ("stencil27", (35, 9, 11), 32)])
 def test_stencil_solve_bitwise(ctx, method, form, kind, dims, m):
     a = O.gen_stencil(kind, *dims, seed=2)
     b = O.rhs(a.n, m, 3)
@@ -206,3 +207,26 @@ def test_stencil_z27_modes(mode):
                        env={**os.environ, "MBG_STENCIL_Z": mode, "MBG_Z_NESTED": "1"}, capture_output=True, text=True,
                        timeout=1200, cwd=str(here.parent.parent))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("m,dims", [(16, (40, 13, 24)), (32, (33, 8, 10))])
+def test_reordered_fused_axpy_spmm(ctx, m, dims):
+    # fused Reordered on a 27-point twin forms th = z - alpha s inside the second
+    # SpMM (th never stored) and recomputes it in the x/z/vh pass: many planes
+    # per block, converged solve and a fixed-iteration one, bitwise vs the oracle
+    a = O.gen_stencil("stencil27", *dims, seed=2)
+    b = O.rhs(a.n, m, 5)
+    d = ctx.upload(to_prod(a))
+    d.set_grid(*dims)
+    for fixed, maxit in ((False, 400), (True, 7)):
+        want = O.solve(a, b, m, "rbicgstab", "fused", 1e-8, fixed=fixed, maxit=maxit)
+        B, X = ctx.multivector(a.n, m, b), ctx.multivector(a.n, m)
+        rep = P.solve(ctx, d, B, X, "rbicgstab", "fused", 1e-8, fixed=fixed, max_iters=maxit)
+        assert rep.iterations == want["iterations"]
+        assert_bitwise(rep.residual_history, want["hist"], "history")
+        assert_bitwise(X.download(), want["x"], "x")
+        # byte model: delta pass 2 + (s read by the SpMM) 1 + 4-dot pass 5 +
+        # x/z/vh/r pass 10 = 18 vector transfers, + 2 stencil SpMMs
+        per_it = rep.compulsory_bytes / rep.iterations
+        spmm = 16.0 * a.n * m + 8.0 * a.nnz + 4.0 * (a.n + 1)
+        assert abs(per_it - (18 * 8.0 * a.n * m + 2 * spmm)) < 16.0, per_it
