@@ -552,6 +552,23 @@ def main():
             traffic = json.loads(ncu.read_text()).get(f"{cfg['name']}:{dname}")   # per launch, ncu --set full
         except Exception:
             traffic = None
+    # gather-bound CSR SpMM (C5): its x gathers against the measured L2 gather
+    # ceiling for their segment size (tools/l2_lab.cu -> profiles/l2_ceilings.json)
+    gather = None
+    ceil_f = ROOT / "profiles" / "l2_ceilings.json"
+    if dname == "spmm" and not stencil and ceil_f.exists():
+        try:
+            ceil = json.loads(ceil_f.read_text())
+            seg = max(16, 8 * m)
+            cg = ceil["gather_GBps_by_segment_B"][str(min(256, seg))]
+            gb = 8.0 * m * nnz_loc   # useful x bytes gathered per SpMM (one m-wide row of x per nonzero)
+            ach = gb / (dms / dn / 1000.0) / 1e9
+            gather = {"bound": "l2-gather", "achieved": ach, "peak": cg, "unit": "GB/s", "frac": ach / cg,
+                      "bytes_per_launch": gb, "segment_B": 8 * m,
+                      "peak_source": "tools/l2_lab.cu random L2-resident gathers of min(256, max(16, 8m))-byte "
+                                     "segments (profiles/l2_ceilings.json)"}
+        except Exception:
+            gather = None
     kernels = {k: {"launches": v[0], "ms": round(v[1], 3), "share": round(v[1] / total_ms, 4),
                    "GB/s": round(v[2] / (v[1] / v[0] / 1000.0) / 1e9, 1) if v[2] > 0 else None}
                for k, v in prof.items()}
@@ -580,6 +597,8 @@ def main():
                             "timed solve's iterations, after the timed region"},
         "kernels": kernels,
     }
+    if gather:
+        line["roofline_l2_gather"] = gather
     if world == 1 and rank == 0 and not args.no_compare:
         line["variants"] = variants(P, ctx, a, cfg, d, B, X, peak, min(args.steps, 3))
         if cfg["name"] != "C2":
