@@ -561,6 +561,8 @@ def main():
             ceil = json.loads(ceil_f.read_text())
             seg = max(16, 8 * m)
             cg = ceil["gather_GBps_by_segment_B"][str(min(256, seg))]
+            if 8 * m < 16:   # 8-byte gathers move the same sectors as 16-byte ones
+                cg *= 8.0 * m / 16.0
             gb = 8.0 * m * nnz_loc   # useful x bytes gathered per SpMM (one m-wide row of x per nonzero)
             ach = gb / (dms / dn / 1000.0) / 1e9
             gather = {"bound": "l2-gather", "achieved": ach, "peak": cg, "unit": "GB/s", "frac": ach / cg,
