@@ -269,6 +269,7 @@ struct PPipeG5 {
 // w = 1*y + (-omega)*t + (omega*alpha)*v ; rho'=(r0,r), psi=(r0,z), sigma=(r0,w), delta=(r0,s)
 struct PPipeG45 {
     static constexpr bool REDO_SAFE = true;
+    static constexpr bool NO_BATCH = true;   // batched grows +2.6 % here (C4, locked clock)
     static constexpr const char* NAME = "pipe_g45";
     static constexpr int NIN = 9, NOUT = 3, NCO = 4, NDOT = 4, UNROLL = 1;
     // in: x p q y t v r0 z s ; out: x r w ; co: alpha omega -omega omega*alpha
@@ -416,6 +417,18 @@ template <class P, class = void>
 struct redo_safe_of { static constexpr bool value = false; };
 template <class P>
 struct redo_safe_of<P, decltype(void(P::REDO_SAFE))> { static constexpr bool value = P::REDO_SAFE; };
+
+#ifndef MBG_GROW_BATCH
+#define MBG_GROW_BATCH 1
+#endif
+// Batched lazy grows (exact.cuh grow_lazy_batch) unless a program opts out
+// (NO_BATCH): measured at ncu's locked clock, Reordered 4-dot pass -11 %, dot2
+// -5 %, phi/psi -3.5 %; the fused Pipelined 4-dot pass +2.6 % (and the careful
+// grows of Alg. 4 line 4 spill when batched: +45 %), so those keep per-grow code.
+template <class P, class = void>
+struct batch_of { static constexpr bool value = true; };
+template <class P>
+struct batch_of<P, decltype(void(P::NO_BATCH))> { static constexpr bool value = !P::NO_BATCH; };
 
 // FastTwoSum in the streaming grows (exact.cuh two_sum_lazy) where it measured faster.
 template <class P, class = void>
@@ -626,6 +639,20 @@ __global__ void __launch_bounds__(256, minblocks_of<P>::value) group_kernel(Grou
                 P::run(in, o1, p1, co1);
 #pragma unroll
                 for (int i = 0; i < P::NOUT; ++i) reinterpret_cast<double2*>(a.out[i])[qu] = make_double2(o0[i], o1[i]);
+#if MBG_GROW_BATCH
+                if constexpr (RS && batch_of<P>::value) {
+                    double px[2 * ND];
+                    int64_t* sl[2 * ND];
+#pragma unroll
+                    for (int d = 0; d < ND; ++d) {
+                        px[2 * d] = p0[d];
+                        px[2 * d + 1] = p1[d];
+                        sl[2 * d] = slot0[d];
+                        sl[2 * d + 1] = slot1[d];
+                    }
+                    grow_lazy_batch<2 * ND, false, fast_sum_of<P>::value>(acc, px, sl);
+                } else
+#endif
 #pragma unroll
                 for (int d = 0; d < P::NDOT; ++d) {
                     if constexpr (RS) {
@@ -681,6 +708,20 @@ __global__ void __launch_bounds__(256, minblocks_of<P>::value) group_kernel(Grou
 #pragma unroll
                     for (int i = 0; i < P::NIN; ++i) in[i] = v[i].y;
                     P::run(in, o1, p1, co1);
+#if MBG_GROW_BATCH
+                    if constexpr (batch_of<P>::value) {   // the replay repeats the fast pass's operations exactly
+                        double px[2 * ND];
+                        int64_t* sl[2 * ND];
+#pragma unroll
+                        for (int d = 0; d < ND; ++d) {
+                            px[2 * d] = p0[d];
+                            px[2 * d + 1] = p1[d];
+                            sl[2 * d] = slot0[d];
+                            sl[2 * d + 1] = slot1[d];
+                        }
+                        grow_lazy_batch<2 * ND, true, fast_sum_of<P>::value>(acc, px, sl);
+                    } else
+#endif
 #pragma unroll
                     for (int d = 0; d < P::NDOT; ++d) {
                         grow_lazy<true, fast_sum_of<P>::value>(acc[2 * d], p0[d], slot0[d]);
