@@ -165,6 +165,23 @@ struct PReordG7 {
         prod[3] = __dmul_rn(rt, rt);
     }
 };
+// ... fused formulation: the same four dots with rt kept in registers only
+// (rt is recomputed where r = rt - omega t is formed), one vector write less
+struct PReordG7D {
+    static constexpr bool REDO_SAFE = true;
+    static constexpr bool PREFETCH = true;
+    static constexpr int MINB = 2;
+    static constexpr int UNROLL = 1;
+    static constexpr const char* NAME = "reord_g7d";
+    static constexpr int NIN = 4, NOUT = 0, NCO = 1, NDOT = 4;   // in: r v t r0; co: -alpha
+    __device__ static void run(const double* in, double*, double* prod, const double* co) {
+        const double rt = fmadd_rn(fmadd_rn(0.0, 1.0, in[0]), co[0], in[1]);
+        prod[0] = __dmul_rn(in[2], rt);
+        prod[1] = __dmul_rn(in[2], in[2]);
+        prod[2] = __dmul_rn(in[2], in[3]);
+        prod[3] = __dmul_rn(rt, rt);
+    }
+};
 // Reordered, Alg. 6 lines 20-22 (footnote-5 form):
 //   x = 1*x + alpha*vh + omega*th ; z = 1*th + (-omega)*q ;
 //   vh = 1*z + beta*vh + (-(beta*omega))*s
@@ -181,34 +198,39 @@ struct PReordG12 {
 
 // Reordered, fused formulation with identity M^-1 (q = t, s = v elided): Alg. 6
 // line 17's r = 1*rt + (-omega)*t merged into the lines 20-22 pass, which reads
-// t (as q) anyway -- one vector read less per iteration, same expressions
+// t (as q) and v (as s) anyway, with rt = 1*r + (-alpha)*v recomputed from r
+// (the 4-dot pass keeps it in registers) -- same expressions, same bits
 //   x = 1*x + alpha*vh + omega*th ; z = 1*th + (-omega)*q ;
-//   vh = 1*z + beta*vh + (-(beta*omega))*s ; r = 1*rt + (-omega)*q
+//   vh = 1*z + beta*vh + (-(beta*omega))*s ; r = 1*(1*r + (-alpha)*s) + (-omega)*q
 struct PReordG12R {
     static constexpr const char* NAME = "reord_g12r";
-    static constexpr int NIN = 6, NOUT = 4, NCO = 5, NDOT = 0;   // in: x vh th q s rt; co: alpha omega -omega beta -(beta*omega)
+    // in: x vh th q s r; co: alpha omega -omega beta -(beta*omega) -alpha
+    // (rt = 1*r + (-alpha)*s recomputed as in the dot pass: s = v here)
+    static constexpr int NIN = 6, NOUT = 4, NCO = 6, NDOT = 0;
     __device__ static void run(const double* in, double* out, double*, const double* co) {
         out[0] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, in[0]), co[0], in[1]), co[1], in[2]);
         const double z = fmadd_rn(fmadd_rn(0.0, 1.0, in[2]), co[2], in[3]);
         out[1] = z;
         out[2] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, z), co[3], in[1]), co[4], in[4]);
-        out[3] = fmadd_rn(fmadd_rn(0.0, 1.0, in[5]), co[2], in[3]);
+        const double rt = fmadd_rn(fmadd_rn(0.0, 1.0, in[5]), co[5], in[4]);
+        out[3] = fmadd_rn(fmadd_rn(0.0, 1.0, rt), co[2], in[3]);
     }
 };
 
 // ... and with th never stored (formed inside the second SpMM, stencil.cu):
 // th = 1*z + (-alpha)*s recomputed here with the expression of its update pass
-//   in: x vh z q s rt ; out: x z vh r ; co: alpha omega -omega beta -(beta*omega) -alpha
+//   in: x vh z q s r ; out: x z vh r ; co: alpha omega -omega beta -(beta*omega) -alpha
 struct PReordG12RZ {
     static constexpr const char* NAME = "reord_g12rz";
-    static constexpr int NIN = 6, NOUT = 4, NCO = 6, NDOT = 0;
+    static constexpr int NIN = 6, NOUT = 4, NCO = 6, NDOT = 0;   // in: x vh z q s r
     __device__ static void run(const double* in, double* out, double*, const double* co) {
         const double th = fmadd_rn(fmadd_rn(0.0, 1.0, in[2]), co[5], in[4]);
         out[0] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, in[0]), co[0], in[1]), co[1], th);
         const double z = fmadd_rn(fmadd_rn(0.0, 1.0, th), co[2], in[3]);
         out[1] = z;
         out[2] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, z), co[3], in[1]), co[4], in[4]);
-        out[3] = fmadd_rn(fmadd_rn(0.0, 1.0, in[5]), co[2], in[3]);
+        const double rt = fmadd_rn(fmadd_rn(0.0, 1.0, in[5]), co[5], in[4]);
+        out[3] = fmadd_rn(fmadd_rn(0.0, 1.0, rt), co[2], in[3]);
     }
 };
 

@@ -116,8 +116,9 @@ Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulatio
     switch (method) {
         case MBG_BICGSTAB: need = {V_R, V_R0, V_P, V_V, V_S, V_T}; break;
         case MBG_RBICGSTAB:
-            need = {V_R, V_R0, V_V, V_T, V_Z, V_VH, V_RT};
+            need = {V_R, V_R0, V_V, V_T, V_Z, V_VH};
             if (!ax_) need.push_back(V_TH);
+            if (!elide_) need.push_back(V_RT);   // fused + identity: rt lives in registers only
             if (!elide_) need.insert(need.end(), {V_S, V_Q});
             break;
         case MBG_PIPEBICGSTAB: need = {V_R, V_R0, V_P, V_V, V_S, V_T, V_Z, V_Q, V_W, V_Y, V_TMP}; break;
@@ -433,7 +434,7 @@ void Solver::iteration() {
         group<PUpd3>({r, p, v}, {p}, {S_ONE, S_BETA, S_NBO}, 0);
     } else if (method_ == MBG_RBICGSTAB) {
         double *z = w(V_Z), *vh = w(V_VH), *v = w(V_V), *th = w(V_TH), *t = w(V_T);
-        double *rt = w(V_RT);
+        double* rt = elide_ ? nullptr : w(V_RT);
         // identity M^-1: the fused formulation aliases s = v and q = t instead of copying
         double* s = elide_ ? v : w(V_S);
         double* q = elide_ ? t : w(V_Q);
@@ -458,17 +459,19 @@ void Solver::iteration() {
             group<PDot1>({t}, {}, {}, 1);
             group<PDot2>({t, r0}, {}, {}, 2);
             group<PDot1>({rt}, {}, {}, 3, P_R_OMEGA, 4);
+        } else if (fused && elide_) {
+            group<PReordG7D>({r, v, t, r0}, {}, {S_NALPHA}, 0, P_R_OMEGA, 4);   // rt in registers only
         } else {
             group<PReordG7>({r, v, t, r0}, {rt}, {S_NALPHA}, 0, P_R_OMEGA, 4);
         }
         if (ax_) {
-            // th recomputed from z and s (same expression as its update pass)
-            group<PReordG12RZ>({x, vh, z, q, s, rt}, {x, z, vh, r},
+            // th and rt recomputed from z, s and r (the expressions of their passes)
+            group<PReordG12RZ>({x, vh, z, q, s, r}, {x, z, vh, r},
                                {S_ALPHA, S_OMEGA, S_NOMEGA, S_BETA, S_NBO, S_NALPHA}, 0, P_R_END, 0);
         } else if (fused && elide_) {
-            // r = rt - omega t in the x / z / vh pass (t is read there as q)
-            group<PReordG12R>({x, vh, th, q, s, rt}, {x, z, vh, r}, {S_ALPHA, S_OMEGA, S_NOMEGA, S_BETA, S_NBO}, 0,
-                              P_R_END, 0);
+            // r = (r - alpha s) - omega t in the x / z / vh pass (t, s are read there as q, s)
+            group<PReordG12R>({x, vh, th, q, s, r}, {x, z, vh, r},
+                              {S_ALPHA, S_OMEGA, S_NOMEGA, S_BETA, S_NBO, S_NALPHA}, 0, P_R_END, 0);
         } else {
             group<PUpd2>({rt, t}, {r}, {S_ONE, S_NOMEGA}, 0);        // r = rt - omega t
             if (basic) {
@@ -749,7 +752,10 @@ void Solver::report(double* hist_host, mbg_report* rep) {
     if (method_ == MBG_RBICGSTAB && form_ == MBG_FUSED && !epi_delta_) reads += 1;   // delta pass: v, r0 vs aux r0
     // fused Reordered merges r = rt - omega t into the x/z/vh pass only when
     // q = t is elided (identity M^-1); otherwise that update is its own pass
-    if (method_ == MBG_RBICGSTAB && form_ == MBG_FUSED && !elide_) reads += 1;
+    if (method_ == MBG_RBICGSTAB && form_ == MBG_FUSED && !elide_) {
+        reads += 1;    // the separate r = rt - omega t pass ...
+        writes += 1;   // ... and rt stored by the 4-dot pass
+    }
     // th formed inside the second SpMM: its update pass (z, s -> th) is gone and
     // the SpMM reads s beside z (the SpMM-side read is counted as a vector read)
     if (ax_) {
@@ -766,7 +772,7 @@ void Solver::report(double* hist_host, mbg_report* rep) {
     rep->compulsory_bytes =
         (iteration_bytes(method_, form_, pa_, a_->n, a_->nnz, m_) +
          ((method_ == MBG_RBICGSTAB && form_ == MBG_FUSED && !epi_delta_) ? 8.0 * static_cast<double>(len_) : 0.0) +
-         ((method_ == MBG_RBICGSTAB && form_ == MBG_FUSED && !elide_) ? 8.0 * static_cast<double>(len_) : 0.0) -
+         ((method_ == MBG_RBICGSTAB && form_ == MBG_FUSED && !elide_) ? 16.0 * static_cast<double>(len_) : 0.0) -
          (ax_ ? 16.0 * static_cast<double>(len_) : 0.0) -
          8.0 * classic_epi * static_cast<double>(len_) -
          // stencil SpMM: no column indices (8 B instead of 12 B per nonzero)

@@ -169,10 +169,12 @@ std::vector<Group> schedule_fused(int method, int* aux_reads, int* spmm_dots) {
             *aux_reads = 1;                 // r0 in v = A vh
             spmm_dots[0] = 1;
             spmm_dots[1] = 0;
-            // r = rt - omega t merged into the x / z / vh pass (t is read there as q)
+            // rt = r - alpha v lives in registers only: the 4-dot pass reads r, v,
+            // t, r0 and stores nothing (modelled by dots over the same vectors);
+            // r = rt - omega t is formed in the x / z / vh pass from r, v, t
             return {{U(TH, {Z, V})},
-                    {U(RT, {R, V}), Dt(T, RT, 0), Dt(T, T, 1), Dt(T, R0, 2), Dt(RT, RT, 3)},
-                    {U(X, {X, VH, TH}), U(Z, {TH, T}), U(VH, {Z, VH, V}), U(R, {RT, T})}};
+                    {Dt(T, R, 0), Dt(T, T, 1), Dt(T, R0, 2), Dt(V, V, 3)},
+                    {U(X, {X, VH, TH}), U(Z, {TH, T}), U(VH, {Z, VH, V}), U(R, {R, V, T})}};
         case MBG_PIPEBICGSTAB:
             *aux_reads = 0;
             spmm_dots[0] = spmm_dots[1] = 0;

@@ -247,7 +247,7 @@ def test_halo_plan_consistent(nparts):
 
 def test_method_schedule_fused_reordered():
     # fused Reordered (identity M^-1 elided): the delta dot in the SpMM epilogue
-    # reads one aux vector; r = rt - omega t rides in the x / z / vh pass:
-    # 18 group transfers + 1 aux = 19 (merged listing: 21 + 4 for the copies)
+    # reads one aux vector; rt stays in registers and r = rt - omega t rides in
+    # the x / z / vh pass: 17 group transfers + 1 aux = 18 (merged listing: 21 + 4)
     s = P.method_schedule_pc("rbicgstab", "fused")
-    assert s["vec"] == 19 and s["precond"] == 0 and s["reductions"] == [1, 4]
+    assert s["vec"] == 18 and s["precond"] == 0 and s["reductions"] == [1, 4]
