@@ -237,6 +237,35 @@ __device__ __forceinline__ void grow(double (&a)[KEXP], double x, int64_t* slot)
 }
 #endif
 
+#ifdef __CUDACC__
+// grow over N independent expansions as one basic block (see grow_lazy_batch):
+// levels 1-2 of all N into temporaries and one test; if any expansion met a
+// non-finite sum or a level-2 error, all N take grow()'s careful path from
+// their untouched state -- the same result as N sequential grow() calls.
+template <int N>
+__device__ __forceinline__ void grow_batch(double (&acc)[N][KEXP], const double (&x)[N], int64_t* const (&slot)[N]) {
+    double s0[N], s1[N];
+    bool rare = false;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        double e0, e1;
+        two_sum_lazy(acc[k][0], x[k], s0[k], e0);
+        two_sum_lazy(acc[k][1], e0, s1[k], e1);
+        rare |= !isfinite(s0[k]) || e1 != 0.0;
+    }
+    if (!rare) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            acc[k][0] = s0[k];
+            acc[k][1] = s1[k];
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < N; ++k) grow(acc[k], x[k], slot[k]);
+    }
+}
+#endif
+
 // Carry-normalise in place: words 0..NDIG-2 in [0, 2^32), top word signed.
 __host__ __device__ __forceinline__ void digits_normalize(int64_t* d) {
     int64_t carry = 0;

@@ -630,11 +630,15 @@ __host__ __device__ constexpr int z27_smem() {
 // the compute warps, so the conversion never stalls them)
 constexpr int Z27_CONV = 64;
 
-template <int MT, int MC, int XR, int VR, int VS = 0>
+// EPI = 1: delta = (y, aux) of the finished rows accumulated exactly in the
+// epilogue (the Reordered delta = (v, r0), SpmmEpi kind 1), one expansion per
+// (lane, column), combined per block at the end.
+template <int MT, int MC, int XR, int VR, int VS = 0, int EPI = 0>
 __global__ void __launch_bounds__(Z27Shape<MC>::THREADS + (VS > 0 ? Z27_CONV : 0) + 32, XR == 2 ? 2 : 1)
     stencil27z_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
                       StencilGeom g, double* __restrict__ y, const int* __restrict__ ctl,
-                      const __grid_constant__ CUtensorMap vmap, const double* __restrict__ na) {
+                      const __grid_constant__ CUtensorMap vmap, const double* __restrict__ na, SpmmEpi epi) {
+    static_assert(EPI == 0 || (EPI == 1 && VS == 0), "z-marching epilogue: kind 1 on the plain input only");
     using SH = Z27Shape<MC>;
     constexpr int CS = MT / MC, RT = SH::RT, CB = SH::CB;
     constexpr int P0B = 9 * RT * 8 + RT * 4;   // part 0 + masks
@@ -780,6 +784,13 @@ __global__ void __launch_bounds__(Z27Shape<MC>::THREADS + (VS > 0 ? Z27_CONV : 0
     // for the three rotations, so no register moves)
     double A0[2][4], A1[2][4], A2[2][4];
     uint32_t M0[2] = {0, 0}, M1[2] = {0, 0}, M2[2] = {0, 0};
+    // EPI: one expansion per accumulator column (cpa, cpa + 1, cpb, cpb + 1)
+    constexpr int NEX = EPI ? 4 : 1;
+    double ex[NEX][KEXP];
+#pragma unroll
+    for (int c = 0; c < NEX; ++c)
+#pragma unroll
+        for (int k = 0; k < KEXP; ++k) ex[c][k] = 0.0;
     int64_t q = 0;
     for (int si = 0; si < nsegs_b; ++si) {
         int t, za, steps;
@@ -812,6 +823,19 @@ __global__ void __launch_bounds__(Z27Shape<MC>::THREADS + (VS > 0 ? Z27_CONV : 0
 #pragma unroll
                 for (int c = 0; c < 4; ++c) an[r][c] = 0.0;
             const bool ck = ((mn[0] | mn[1] | mm[0] | mm[1] | mo[0] | mo[1]) & 0x80000000u) != 0;
+            // epilogue operand of the rows finished this step, issued before the
+            // arithmetic so its latency hides behind it
+            double2 axa[2], axb[2];
+            if constexpr (EPI == 1) {
+                const int64_t rowz = (static_cast<int64_t>(g.zbeg + za + i - 2) * g.ny + yg) * g.nx;
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const bool ok = i >= 2 && yok && xg0 + r < g.nx;
+                    const double* src = epi.aux + (rowz + xg0 + r) * MT + h * MC;
+                    axa[r] = ok ? __ldg(reinterpret_cast<const double2*>(src + cpa)) : make_double2(0.0, 0.0);
+                    axb[r] = ok ? __ldg(reinterpret_cast<const double2*>(src + cpb)) : make_double2(0.0, 0.0);
+                }
+            }
             auto lines = [&](auto check) {
                 constexpr bool CK = decltype(check)::value;
 #pragma unroll
@@ -860,6 +884,16 @@ __global__ void __launch_bounds__(Z27Shape<MC>::THREADS + (VS > 0 ? Z27_CONV : 0
                         double* dst = y + (rowz + xg0 + r) * MT + h * MC;
                         *reinterpret_cast<double2*>(dst + cpa) = make_double2(ao[r][0], ao[r][1]);
                         *reinterpret_cast<double2*>(dst + cpb) = make_double2(ao[r][2], ao[r][3]);
+                        if constexpr (EPI == 1) {   // PDot2 order: v * r0
+                            int64_t* s0 = epi.slot[0] + static_cast<int64_t>(h * MC) * NSLOT;
+                            int64_t* const sl[4] = {s0 + static_cast<int64_t>(cpa) * NSLOT,
+                                                    s0 + static_cast<int64_t>(cpa + 1) * NSLOT,
+                                                    s0 + static_cast<int64_t>(cpb) * NSLOT,
+                                                    s0 + static_cast<int64_t>(cpb + 1) * NSLOT};
+                            const double pr[4] = {__dmul_rn(ao[r][0], axa[r].x), __dmul_rn(ao[r][1], axa[r].y),
+                                                  __dmul_rn(ao[r][2], axb[r].x), __dmul_rn(ao[r][3], axb[r].y)};
+                            grow_batch<4>(ex, pr, sl);
+                        }
                     }
             }
             ++q;
@@ -873,6 +907,22 @@ __global__ void __launch_bounds__(Z27Shape<MC>::THREADS + (VS > 0 ? Z27_CONV : 0
             body(i, A2, A0, A1, M2, M0, M1);
             ++i;
         }
+    }
+    if constexpr (EPI == 1) {
+        // every load was consumed: the x ring is scratch for the block combine
+        // (compute warps only: named barrier 1); class = lane % 8 fixes (cq, odd)
+        struct SyncCompute {
+            __device__ void operator()() const { asm volatile("bar.sync 1, %0;" ::"n"(SH::THREADS) : "memory"); }
+        };
+        SyncCompute{}();
+        block_combine<4>(ex, 8,
+                         [&](int xi, int k) {
+                             const int kq = k % 4, ko = (k / 4) & 1;
+                             const int ca = (2 * kq + ko) * 2, cb = (2 * kq + 1 - ko) * 2;
+                             const int col = xi < 2 ? ca + xi : cb + xi - 2;
+                             return epi.slot[0] + static_cast<int64_t>(h * MC + col) * NSLOT;
+                         },
+                         xr, SyncCompute{}, SH::THREADS);
     }
 }
 
@@ -1024,10 +1074,11 @@ void split_work(StencilGeom& gm, int64_t slots) {
     }
 }
 
-// VS > 0: the fused-input variant, x = z, v / na as stencil27z_kernel describes
-template <int MT, int MC, int XR, int VR, int VS = 0>
+// VS > 0: the fused-input variant, x = z, v / na as stencil27z_kernel describes;
+// EPI = 1: the delta epilogue (epi kind 1)
+template <int MT, int MC, int XR, int VR, int VS = 0, int EPI = 0>
 void launch_z27(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const double* x, double* y, const int* ctl,
-                ZRange zr, const double* v = nullptr, const double* na = nullptr) {
+                ZRange zr, const double* v = nullptr, const double* na = nullptr, const SpmmEpi& epi = SpmmEpi{}) {
     using SH = Z27Shape<MC>;
     const StencilOp& op = *a->stencil;
     if (zr.zend <= zr.zbeg) return;
@@ -1035,7 +1086,7 @@ void launch_z27(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const do
     constexpr int threads = SH::THREADS + (VS > 0 ? Z27_CONV : 0) + 32;
     constexpr int CS = MT / MC;
     const int occ =
-        kernel_occupancy(reinterpret_cast<const void*>(&stencil27z_kernel<MT, MC, XR, VR, VS>), threads, smem);
+        kernel_occupancy(reinterpret_cast<const void*>(&stencil27z_kernel<MT, MC, XR, VR, VS, EPI>), threads, smem);
     auto encode = [&](CUtensorMap& tm, const double* base, int planes) {
         const cuuint64_t dims[4] = {static_cast<cuuint64_t>(MT), static_cast<cuuint64_t>(op.nx),
                                     static_cast<cuuint64_t>(op.ny), static_cast<cuuint64_t>(planes)};
@@ -1070,8 +1121,8 @@ void launch_z27(mbg_ctx* ctx, const mbg_csr* a, const StencilLayout& L, const do
     split_work(gm, static_cast<int64_t>(occ) * ctx->num_sms / CS);
     CUtensorMap vm = tm;
     if constexpr (VS > 0) encode(vm, v, op.nz);
-    launch_pdl(stencil27z_kernel<MT, MC, XR, VR, VS>, dim3(gm.nranges * CS), dim3(threads), static_cast<size_t>(smem),
-               ctx->stream, tm, hm, gm, y, ctl, vm, na);
+    launch_pdl(stencil27z_kernel<MT, MC, XR, VR, VS, EPI>, dim3(gm.nranges * CS), dim3(threads),
+               static_cast<size_t>(smem), ctx->stream, tm, hm, gm, y, ctl, vm, na, epi);
 }
 
 // MBG_STENCIL_Z: 0 = the three-plane kernel for 27-point m = 16 / 32 too;
@@ -1153,6 +1204,12 @@ void launch_by(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y
                const SpmmEpi* epi, ZRange zr) {
     const int kind = a->stencil->kind;
     if constexpr (BY == 4) {
+        if (kind == 27 && (m == 16 || m == 32) && epi && epi->kind == 1 && z27_mode() != 0) {
+            const StencilLayout& Z = layout_for(ctx, a, 4, 1);
+            if (m == 16) launch_z27<16, 16, 4, 3, 0, 1>(ctx, a, Z, x, y, ctl, zr, nullptr, nullptr, *epi);
+            else launch_z27<32, 16, 4, 3, 0, 1>(ctx, a, Z, x, y, ctl, zr, nullptr, nullptr, *epi);
+            return;
+        }
         if (kind == 27 && (m == 16 || m == 32) && (!epi || epi->kind == 0) && z27_mode() != 0) {
             const StencilLayout& Z = layout_for(ctx, a, 4, 1);
             // ring depths (x planes, value slots): 1 (3,2)  2 (2,2; 2 blocks/SM)
@@ -1197,6 +1254,11 @@ void launch_by(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, double* y
         default:
             throw Invalid("stencil SpMM: m must be 4, 8, 16 or 32");
     }
+}
+
+bool stencil_delta_epilogue(const mbg_csr* a, int m) {
+    static const bool on = env_int("MBG_Z27_EPI", 0) != 0;
+    return on && stencil_handles(a, m) && a->stencil->kind == 27 && (m == 16 || m == 32) && z27_mode() != 0;
 }
 
 bool stencil_axpy_handles(const mbg_csr* a, int m) {

@@ -86,6 +86,10 @@ int launch_stencil_spmm(mbg_ctx* ctx, const mbg_csr* a, int m, const double* x, 
 // fused into its SpMM (same expression, same bits).  Single-GPU 27-point
 // operators at m = 16 / 32 (stencil_axpy_handles); returns kernel launches.
 bool stencil_axpy_handles(const mbg_csr* a, int m);
+// The z-marching 27-point kernel (m = 16 / 32) carries the delta = (y, aux)
+// epilogue (SpmmEpi kind 1) -- the fused Reordered delta pass folded into the
+// first SpMM.  Opt-in (MBG_Z27_EPI=1): measured slower on B200.
+bool stencil_delta_epilogue(const mbg_csr* a, int m);
 int launch_stencil_spmm_axpy(mbg_ctx* ctx, const mbg_csr* a, int m, const double* z, const double* v,
                              const double* na, double* y, const int* ctl);
 // Algorithmic bytes of one stencil SpMM: x read once, y written once, 8 B per

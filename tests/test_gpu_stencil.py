@@ -189,7 +189,7 @@ def test_stencil_random_shapes(ctx):
         assert_bitwise(Y.download(), O.spmv(a, x, m), f"{kind} {nx}x{ny}x{nz} m={m}")
 
 
-@pytest.mark.parametrize("mode", ["0", "1", "2", "6"])
+@pytest.mark.parametrize("mode", ["0", "1", "2", "6", "epi"])
 def test_stencil_z27_modes(mode):
     # the 27-point m = 16 / 32 SpMM has three implementations selected once per
     # process by MBG_STENCIL_Z (0: three resident planes; else z-marching with
@@ -202,10 +202,12 @@ def test_stencil_z27_modes(mode):
     if os.environ.get("MBG_Z_NESTED"):
         pytest.skip("nested run")
     here = Path(__file__).resolve()
+    # "epi": the default kernel with the opt-in delta epilogue (MBG_Z27_EPI=1)
+    env = {**os.environ, "MBG_Z_NESTED": "1"}
+    env.update({"MBG_Z27_EPI": "1"} if mode == "epi" else {"MBG_STENCIL_Z": mode})
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider", str(here),
-                        "-k", "spmv_bitwise or absent_slots or special_values or solve_bitwise or random_shapes"],
-                       env={**os.environ, "MBG_STENCIL_Z": mode, "MBG_Z_NESTED": "1"}, capture_output=True, text=True,
-                       timeout=1200, cwd=str(here.parent.parent))
+                        "-k", "spmv_bitwise or absent_slots or special_values or solve_bitwise or random_shapes or axpy"],
+                       env=env, capture_output=True, text=True, timeout=1200, cwd=str(here.parent.parent))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
@@ -225,8 +227,13 @@ def test_reordered_fused_axpy_spmm(ctx, m, dims):
         assert rep.iterations == want["iterations"]
         assert_bitwise(rep.residual_history, want["hist"], "history")
         assert_bitwise(X.download(), want["x"], "x")
-        # byte model: delta pass 2 + (s read by the SpMM) 1 + 4-dot pass 4 +
-        # x/z/vh/r pass 10 = 17 vector transfers, + 2 stencil SpMMs
+        # byte model: delta pass 2 (or r0 read by the SpMM epilogue: 1) + (s read
+        # by the SpMM) 1 + 4-dot pass 4 + x/z/vh/r pass 10 = 17 (16) vector
+        # transfers, + 2 stencil SpMMs
+        import os
+        nvec = 16 if os.environ.get("MBG_Z27_EPI") == "1" else 17
+        if os.environ.get("MBG_STENCIL_Z") == "0":   # no z-marching kernel: th has its own pass
+            nvec = 19
         per_it = rep.compulsory_bytes / rep.iterations
         spmm = 16.0 * a.n * m + 8.0 * a.nnz + 4.0 * (a.n + 1)
-        assert abs(per_it - (17 * 8.0 * a.n * m + 2 * spmm)) < 16.0, per_it
+        assert abs(per_it - (nvec * 8.0 * a.n * m + 2 * spmm)) < 16.0, per_it
