@@ -285,6 +285,53 @@ struct PPipeG5 {
     }
 };
 
+// Pipelined, fused formulation: q = 1*r + (-alpha)*s and y = 1*w + (-alpha)*z
+// live in registers only -- the line-4 pass forms them for its three dots and
+// the line-7/12 pass recomputes them from r, w and the new s, z (which it
+// reads anyway), with the same expressions, so the bits do not change and q, y
+// are never stored (2 vector writes less per iteration, 2 vectors less memory)
+//   in: r p s w z t v ; out: p s z ; co: beta nbo -alpha
+struct PPipeG1F {
+    static constexpr bool PREFETCH = true;
+    static constexpr int MINB = 2;
+    static constexpr int UNROLL = 1;
+    static constexpr const char* NAME = "pipe_g1f";
+    static constexpr int NIN = 7, NOUT = 3, NCO = 3, NDOT = 3;
+    __device__ static void run(const double* in, double* out, double* prod, const double* co) {
+        const double r = in[0], p = in[1], s = in[2], w = in[3], z = in[4], t = in[5], v = in[6];
+        const double pn = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, r), co[0], p), co[1], s);
+        const double sn = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, w), co[0], s), co[1], z);
+        const double zn = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, t), co[0], z), co[1], v);
+        const double q = fmadd_rn(fmadd_rn(0.0, 1.0, r), co[2], sn);
+        const double y = fmadd_rn(fmadd_rn(0.0, 1.0, w), co[2], zn);
+        out[0] = pn; out[1] = sn; out[2] = zn;
+        prod[0] = __dmul_rn(q, y);
+        prod[1] = __dmul_rn(y, y);
+        prod[2] = __dmul_rn(q, q);
+    }
+};
+//   in: x p r w t v r0 z s ; out: x r w ; co: alpha omega -omega omega*alpha -alpha
+struct PPipeG45F {
+    static constexpr bool REDO_SAFE = true;
+    static constexpr bool NO_BATCH = true;
+    static constexpr const char* NAME = "pipe_g45f";
+    static constexpr int NIN = 9, NOUT = 3, NCO = 5, NDOT = 4, UNROLL = 1;
+    __device__ static void run(const double* in, double* out, double* prod, const double* co) {
+        const double q = fmadd_rn(fmadd_rn(0.0, 1.0, in[2]), co[4], in[8]);
+        const double y = fmadd_rn(fmadd_rn(0.0, 1.0, in[3]), co[4], in[7]);
+        out[0] = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, in[0]), co[0], in[1]), co[1], q);
+        const double r = fmadd_rn(fmadd_rn(0.0, 1.0, q), co[2], y);
+        out[1] = r;
+        const double w = fmadd_rn(fmadd_rn(fmadd_rn(0.0, 1.0, y), co[2], in[4]), co[3], in[5]);
+        out[2] = w;
+        const double r0 = in[6];
+        prod[0] = __dmul_rn(r0, r);
+        prod[1] = __dmul_rn(r0, in[7]);
+        prod[2] = __dmul_rn(r0, w);
+        prod[3] = __dmul_rn(r0, in[8]);
+    }
+};
+
 // Pipelined, fused formulation: Alg. 4 lines 7 and 12 in ONE pass (the
 // convergence break between them only skips w, which the GPU may compute and
 // discard): x = 1*x + alpha*p + omega*q ; r = 1*q + (-omega)*y ;

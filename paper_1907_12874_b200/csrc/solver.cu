@@ -123,7 +123,10 @@ Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulatio
             if (!elide_) need.push_back(V_RT);   // fused + identity: rt lives in registers only
             if (!elide_) need.insert(need.end(), {V_S, V_Q});
             break;
-        case MBG_PIPEBICGSTAB: need = {V_R, V_R0, V_P, V_V, V_S, V_T, V_Z, V_Q, V_W, V_Y, V_TMP}; break;
+        case MBG_PIPEBICGSTAB:
+            need = {V_R, V_R0, V_P, V_V, V_S, V_T, V_Z, V_W};
+            if (formulation != MBG_FUSED) need.insert(need.end(), {V_Q, V_Y, V_TMP});   // fused: q, y in registers
+            break;
         case MBG_IBICGSTAB: need = {V_R, V_R0, V_V, V_S, V_T, V_Z, V_Q, V_U, V_F0}; break;
         case MBG_PBICGSTAB:
             need = {V_R, V_R0, V_P, V_V, V_S, V_T};
@@ -487,10 +490,12 @@ void Solver::iteration() {
         }
     } else if (method_ == MBG_PIPEBICGSTAB) {
         double *p = w(V_P), *s = w(V_S), *wv = w(V_W), *z = w(V_Z), *t = w(V_T), *v = w(V_V);
-        double *q = w(V_Q), *y = w(V_Y), *tmp = w(V_TMP);
+        double *q = fused ? nullptr : w(V_Q), *y = fused ? nullptr : w(V_Y), *tmp = fused ? nullptr : w(V_TMP);
         // The scalar steps wait for the reductions, which overlap the following
         // SpMM (on the side stream when a communicator allreduces them).
-        if (basic) {
+        if (fused) {
+            group<PPipeG1F>({r, p, s, wv, z, t, v}, {p, s, z}, {S_BETA, S_NBO, S_NALPHA}, 0, -1, 3);
+        } else if (basic) {
             group<PUpd3>({r, p, s}, {p}, {S_ONE, S_BETA, S_NBO}, 0);
             group<PUpd3>({wv, s, z}, {s}, {S_ONE, S_BETA, S_NBO}, 0);
             group<PUpd3>({t, z, v}, {z}, {S_ONE, S_BETA, S_NBO}, 0);
@@ -515,8 +520,9 @@ void Solver::iteration() {
             group<PDot2>({r0, wv}, {}, {}, 2);
             group<PDot2>({r0, s}, {}, {}, 3, -1, 4);
         } else if (fused) {
-            group<PPipeG45>({x, p, q, y, t, v, r0, z, s}, {x, r, wv}, {S_ALPHA, S_OMEGA, S_NOMEGA, S_OA}, 0,
-                            -1, 4);
+            // q, y recomputed from r, w (read before this pass overwrites them) and the new s, z
+            group<PPipeG45F>({x, p, r, wv, t, v, r0, z, s}, {x, r, wv}, {S_ALPHA, S_OMEGA, S_NOMEGA, S_OA, S_NALPHA},
+                             0, -1, 4);
         } else {
             group<PPipeG4>({x, p, q, y}, {x, r}, {S_ALPHA, S_OMEGA, S_NOMEGA}, 0);
             group<PPipeG5>({y, t, v, r0, r, z, s}, {wv}, {S_NOMEGA, S_OA}, 0, -1, 4);

@@ -178,10 +178,13 @@ std::vector<Group> schedule_fused(int method, int* aux_reads, int* spmm_dots) {
         case MBG_PIPEBICGSTAB:
             *aux_reads = 0;
             spmm_dots[0] = spmm_dots[1] = 0;
-            return {{U(P, {R, P, S}), U(S, {W, S, Z}), U(Z, {T, Z, V}), U(Q, {R, S}), U(Y, {W, Z}),
-                     Dt(Q, Y, 0), Dt(Y, Y, 1), Dt(Q, Q, 2)},
-                    {U(X, {X, P, Q}), U(R, {Q, Y}), U(W, {Y, T, V}), Dt(R0, R, 0), Dt(R0, Z, 1), Dt(R0, W, 2),
-                     Dt(R0, S, 3)}};
+            // q = r - alpha s, y = w - alpha z in registers only: the line-4 pass
+            // dots them where they are formed (modelled by dots over the vectors
+            // they come from) and the line-7/12 pass recomputes them from r, w,
+            // s, z -- Alg. 4 lines 7 + 12 in one pass, 22 transfers
+            return {{U(P, {R, P, S}), U(S, {W, S, Z}), U(Z, {T, Z, V}), Dt(R, S, 0), Dt(W, Z, 1), Dt(R, W, 2)},
+                    {U(X, {X, P, R, S}), U(R, {R, S, W, Z}), U(W, {W, Z, T, V}), Dt(R0, R, 0), Dt(R0, Z, 1),
+                     Dt(R0, W, 2), Dt(R0, S, 3)}};
     }
     throw Invalid("unknown method");
 }

@@ -251,3 +251,10 @@ def test_method_schedule_fused_reordered():
     # the x / z / vh pass: 17 group transfers + 1 aux = 18 (merged listing: 21 + 4)
     s = P.method_schedule_pc("rbicgstab", "fused")
     assert s["vec"] == 18 and s["precond"] == 0 and s["reductions"] == [1, 4]
+
+
+def test_method_schedule_fused_pipelined():
+    # fused Pipelined: lines 7 + 12 in one pass and q, y in registers only
+    # (formed for the line-4 dots, recomputed in the line-7/12 pass): 22 (merged 26)
+    s = P.method_schedule_pc("pipebicgstab", "fused")
+    assert s["vec"] == 22 and s["reductions"] == [3, 4]
