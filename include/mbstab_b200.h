@@ -145,6 +145,19 @@ int64_t mbg_csr_nnz(const mbg_csr* a);    /* local nnz */
  * tiles, e.g. 27-point stencils; MBG_SPMM_STAGE=0/1 forces it off/on),
  * reuse = nonzeros per distinct column per tile of that tiling (0 if none). */
 int mbg_csr_stage_info(const mbg_csr* a, int* staged, double* reuse);
+/* sorted = 1 when the CSR SpMM walks a length-sorted twin of the rows (rows
+ * stored by descending length inside windows of 4096 and padded to groups of
+ * 4 nonzeros, each row's nonzeros in CSR order: spmv.cpp:38-47's per-row sums
+ * are unchanged, only which lane computes which row); lane_efficiency = share of the natural order's gather
+ * slots that do useful work (the twin is built below 0.92, e.g. the random
+ * band of BASELINE config 5; MBG_SPMM_SORT=0/1 forces it off/on). */
+int mbg_csr_sort_info(const mbg_csr* a, int* sorted, double* lane_efficiency);
+/* Host-only view of that twin's plan (no device): rowid[n] = the row stored in
+ * each slot, tiles[4*ntiles] = (slot0, slot1, k0, k1) per tile with k indexing
+ * the permuted nonzeros, every row padded to a multiple of 4 entries; call
+ * with tiles == NULL for ntiles first. */
+int mbg_sorted_twin_plan(int64_t n, const int64_t* offsets, int window, int32_t* rowid, double* lane_efficiency,
+                         int64_t* ntiles, int32_t* tiles);
 
 /* ---- multivector: n x m fp64, row-interleaved (element (i,c) at i*m+c) -- */
 int mbg_mv_alloc(mbg_ctx* ctx, int64_t n, int m, mbg_mv** out);

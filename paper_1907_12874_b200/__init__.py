@@ -233,6 +233,13 @@ class DeviceCsr:
         check(lib().mbg_csr_stage_info(self.h, C.byref(st), C.byref(ru)))
         return bool(st.value), float(ru.value)
 
+    def sort_info(self):
+        """(sorted, lane_efficiency): whether the CSR SpMM walks the
+        length-sorted twin, and the natural order's useful share of gather slots."""
+        so, ef = C.c_int(0), C.c_double(0.0)
+        check(lib().mbg_csr_sort_info(self.h, C.byref(so), C.byref(ef)))
+        return bool(so.value), float(ef.value)
+
     def __del__(self):
         try:
             if self.h:
@@ -479,6 +486,20 @@ def solve_host(ctx: Context, a: DeviceCsr, b: np.ndarray, x: np.ndarray, m: int,
 # ---------------------------------------------------------------------------
 # partition / exact-dot host hooks (used by the multi-rank CPU tests)
 # ---------------------------------------------------------------------------
+def sorted_twin_plan(row_offsets, window: int = 4096) -> dict:
+    """Host-only plan of the CSR SpMM's length-sorted twin: the row stored in
+    each slot, the tile list over slots and the natural order's lane efficiency."""
+    off = np.ascontiguousarray(row_offsets, dtype=np.int64)
+    n = off.size - 1
+    rowid = np.empty(max(1, n), np.int32)
+    eff, nt = C.c_double(0.0), C.c_int64(0)
+    check(lib().mbg_sorted_twin_plan(n, _ptr(off), window, _ptr(rowid), C.byref(eff), C.byref(nt), None))
+    tiles = np.empty(max(1, 4 * nt.value), np.int32)
+    check(lib().mbg_sorted_twin_plan(n, _ptr(off), window, None, None, C.byref(nt), _ptr(tiles)))
+    return {"rowid": rowid[:n].copy(), "tiles": tiles[: 4 * nt.value].reshape(-1, 4).copy(),
+            "lane_efficiency": float(eff.value)}
+
+
 def halo_plan(a: CsrMatrix, bounds: Sequence[int], my_part: int, transpose: bool = False) -> dict:
     """Host-only halo plan of part `my_part` (of A^T when transpose=True)."""
     L = lib()

@@ -14,6 +14,8 @@ HERE = Path(__file__).resolve().parent
 # MBG_CHECKED=1: the guard-zone build (csrc/Makefile `checked`), for the
 # out-of-bounds tests that stand in for compute-sanitizer on this pool
 LIB_PATH = HERE / ("libmbstab_b200_checked.so" if os.environ.get("MBG_CHECKED") == "1" else "libmbstab_b200.so")
+if os.environ.get("MBG_LIB"):   # A/B measurements: another build of the same library (tools/ncu_ab.sh)
+    LIB_PATH = Path(os.environ["MBG_LIB"]).resolve()
 
 MBG_OK, MBG_ERR_INVALID, MBG_ERR_RUNTIME, MBG_ERR_BREAKDOWN = 0, 1, 2, 3
 MBG_MAX_TERMS = 8
@@ -93,6 +95,8 @@ def lib() -> C.CDLL:
         "mbg_csr_rows": (i64, [vp]),
         "mbg_csr_nnz": (i64, [vp]),
         "mbg_csr_stage_info": (i32, [vp, vp, vp]),
+        "mbg_csr_sort_info": (i32, [vp, vp, vp]),
+        "mbg_sorted_twin_plan": (i32, [i64, vp, i32, vp, vp, vp, vp]),
         "mbg_csr_upload_any_order": (i32, [vp, i64, vp, vp, vp, pp]),
         "mbg_csr_set_grid": (i32, [vp, vp, i32, i32, i32]),
         "mbg_spmv_transpose": (i32, [vp, vp, vp, vp]),
@@ -138,6 +142,8 @@ def lib() -> C.CDLL:
         "mbg_ctx_launches": (i64, [vp]),
     }
     for name, (res, args) in sig.items():
+        if os.environ.get("MBG_LIB") and not hasattr(L, name):
+            continue   # an older build under A/B measurement: entry points added since are absent
         f = getattr(L, name)
         f.restype = res
         f.argtypes = args

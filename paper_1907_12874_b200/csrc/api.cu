@@ -169,6 +169,42 @@ static void stage_tilings(mbg_ctx* ctx, mbg_csr* a, const std::vector<int32_t>& 
     }
 }
 
+// Length-sorted twin of one row class (spmm.cu): built when fewer than 92 % of
+// the natural order's gather slots do useful work (rows of widely different
+// lengths side by side, e.g. the random band of BASELINE config 5; stencil
+// operators stay above 0.97).  MBG_SPMM_SORT=0 / 1 forces it off / on,
+// MBG_SPMM_SORT_WINDOW sets the sorting window (rows; default 4096).
+static int sort_mode() {
+    const char* e = std::getenv("MBG_SPMM_SORT");
+    return e ? std::atoi(e) : -1;
+}
+
+static void sorted_twin_to_device(mbg_ctx* ctx, mbg_csr* a, mbg_csr::SortedDev& d, const std::vector<int32_t>& off32,
+                                  const int32_t* col, const double* val, const std::vector<int32_t>& rows) {
+    const int mode = sort_mode();
+    if (mode == 0 || rows.empty()) return;
+    const double eff = spmm_lane_efficiency(off32, rows);
+    a->lane_efficiency = std::min(a->lane_efficiency, eff);
+    if (mode != 1 && eff >= 0.92) return;
+    int window = 4096;
+    if (const char* e = std::getenv("MBG_SPMM_SORT_WINDOW")) window = std::max(64, std::atoi(e));
+    SortedTwin t;
+    build_sorted_twin(off32, col, val, rows, window, t);
+    constexpr int PAD = 8;   // the tile kernel's bulk copies round ranges up
+    t.off.resize(t.off.size() + PAD, t.off.back());
+    t.col.resize(t.col.size() + PAD, 0);
+    t.val.resize(t.val.size() + PAD, 0.0);
+    upload(d.off, t.off.data(), t.off.size(), ctx->stream);
+    upload(d.col, t.col.data(), t.col.size(), ctx->stream);
+    upload(d.val, t.val.data(), t.val.size(), ctx->stream);
+    upload(d.rowid, t.rowid.data(), t.rowid.size(), ctx->stream);
+    upload(d.tiles, t.tiles.data(), t.tiles.size(), ctx->stream);
+    upload(d.long_rows, t.long_rows.data(), t.long_rows.size(), ctx->stream);
+    d.sched.alloc(2);
+    MBG_CUDA(cudaMemsetAsync(d.sched.p, 0, 2 * sizeof(int), ctx->stream));
+    MBG_CUDA(cudaStreamSynchronize(ctx->stream));   // t's vectors are the copy sources
+}
+
 // Upload a (local) CSR with int32 offsets.  Arrays are padded by 8 entries so
 // the SpMM's 16-byte-aligned TMA bulk copies may round a tile's range up.
 static void csr_arrays_to_device(mbg_ctx* ctx, mbg_csr* a, int64_t n, const std::vector<int32_t>& off32,
@@ -194,6 +230,7 @@ static void csr_arrays_to_device(mbg_ctx* ctx, mbg_csr* a, int64_t n, const std:
     auto lr = long_rows_of(t);
     upload(a->long_all, lr.data(), lr.size(), ctx->stream);
     stage_tilings(ctx, a, off32, col, &all, nullptr, nullptr);
+    sorted_twin_to_device(ctx, a, a->sorted_all, off32, col, val, all);
     MBG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
@@ -368,6 +405,8 @@ static std::unique_ptr<mbg_csr> csr_from_plan(mbg_ctx* ctx, int64_t n, int64_t r
         upload(a->long_interior, li.data(), li.size(), ctx->stream);
         upload(a->long_boundary, lb.data(), lb.size(), ctx->stream);
         stage_tilings(ctx, a.get(), pl.off, pl.col.data(), nullptr, &pl.interior, &pl.boundary);
+        sorted_twin_to_device(ctx, a.get(), a->sorted_interior, pl.off, pl.col.data(), pl.val.data(), pl.interior);
+        sorted_twin_to_device(ctx, a.get(), a->sorted_boundary, pl.off, pl.col.data(), pl.val.data(), pl.boundary);
         upload(a->interior_rows, pl.interior.data(), pl.interior.size(), ctx->stream);
         upload(a->boundary_rows, pl.boundary.data(), pl.boundary.size(), ctx->stream);
         a->n_interior = static_cast<int64_t>(pl.interior.size());
@@ -526,6 +565,40 @@ extern "C" int mbg_csr_stage_info(const mbg_csr* a, int* staged, double* reuse) 
     });
 }
 
+extern "C" int mbg_csr_sort_info(const mbg_csr* a, int* sorted, double* lane_efficiency) {
+    return guarded([&] {
+        if (!a) throw Invalid("null matrix");
+        if (sorted) *sorted = (a->sorted_all.rowid.n || a->sorted_interior.rowid.n || a->sorted_boundary.rowid.n) ? 1 : 0;
+        if (lane_efficiency) *lane_efficiency = a->lane_efficiency;
+    });
+}
+
+extern "C" int mbg_sorted_twin_plan(int64_t n, const int64_t* off, int window, int32_t* rowid,
+                                    double* lane_efficiency, int64_t* ntiles, int32_t* tiles) {
+    return guarded([&] {
+        if (n < 0 || !off) throw Invalid("sorted twin plan: null offsets");
+        if (window < 1) throw Invalid("sorted twin plan: window < 1");
+        std::vector<int32_t> off32(static_cast<size_t>(n) + 1), rows(static_cast<size_t>(n));
+        for (int64_t i = 0; i <= n; ++i) off32[i] = static_cast<int32_t>(off[i]);
+        for (int64_t i = 0; i < n; ++i) rows[i] = static_cast<int32_t>(i);
+        if (lane_efficiency) *lane_efficiency = spmm_lane_efficiency(off32, rows);
+        // the plan does not depend on the columns or values
+        std::vector<int32_t> col(static_cast<size_t>(off32[n]), 0);
+        std::vector<double> val(static_cast<size_t>(off32[n]), 0.0);
+        SortedTwin t;
+        build_sorted_twin(off32, col.data(), val.data(), rows, window, t);
+        if (rowid) std::copy(t.rowid.begin(), t.rowid.end(), rowid);
+        if (ntiles) *ntiles = static_cast<int64_t>(t.tiles.size());
+        if (tiles)
+            for (size_t i = 0; i < t.tiles.size(); ++i) {
+                tiles[4 * i] = t.tiles[i].x;
+                tiles[4 * i + 1] = t.tiles[i].y;
+                tiles[4 * i + 2] = t.tiles[i].z;
+                tiles[4 * i + 3] = t.tiles[i].w;
+            }
+    });
+}
+
 extern "C" int mbg_csr_reordered(const mbg_csr* a) { return a && a->reordered ? 1 : 0; }
 
 extern "C" int mbg_csr_stencil_kind(const mbg_csr* a) { return a && a->stencil ? a->stencil->kind : 0; }
@@ -571,6 +644,9 @@ void* guarded_alloc(size_t bytes) {
     unsigned char* raw = nullptr;
     MBG_CUDA(cudaMalloc(&raw, padded + 2 * GUARD_BYTES));
     MBG_CUDA(cudaMemset(raw, GUARD_BYTE, padded + 2 * GUARD_BYTES));
+    // the fill runs on the legacy stream, the buffer's first use on a
+    // non-blocking one: without this the fill can land after an upload
+    MBG_CUDA(cudaDeviceSynchronize());
     void* user = raw + GUARD_BYTES;
     std::lock_guard<std::mutex> lk(guards().mu);
     guards().live[user] = padded;

@@ -104,9 +104,25 @@ static void side_to_main(mbg_ctx* ctx) {
 int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, const int* ctl,
                    const SpmmEpi* epi) {
     const bool hint = a->n > 0 && a->nnz > 12 * a->n;
-    auto tiles = [hint](const mbg::DevBuf<int4>& t, const mbg::DevBuf<int32_t>& l, const mbg::DevBuf<int4>& st,
-                        const mbg::DevBuf<int2>& um, const mbg::DevBuf<int32_t>& uc, const mbg::DevBuf<uint16_t>& lc) {
+    // the length-sorted twin pays off from m = 8 (B200, config 5's random band,
+    // locked clocks: m = 8 -24 %, 16 -36 %, 32 -49 % per SpMM; m <= 4 is bound by
+    // 8- and 16-byte gather wavefronts either way and loses 1-8 % to the scattered y rows)
+    const bool tile_m = m == 8 || m == 16 || m == 32;
+    auto tiles = [hint, tile_m](const mbg::DevBuf<int4>& t, const mbg::DevBuf<int32_t>& l, const mbg::DevBuf<int4>& st,
+                                const mbg::DevBuf<int2>& um, const mbg::DevBuf<int32_t>& uc,
+                                const mbg::DevBuf<uint16_t>& lc, const mbg_csr::SortedDev& sd) {
         SpmmTiles r{t.p, static_cast<int64_t>(t.n), l.p, static_cast<int64_t>(l.n), hint};
+        if (sd.rowid.p && tile_m) {   // length-sorted twin of this row class
+            r.tiles = sd.tiles.p;
+            r.count = static_cast<int64_t>(sd.tiles.n);
+            r.long_rows = sd.long_rows.p;
+            r.nlong = static_cast<int64_t>(sd.long_rows.n);
+            r.rowid = sd.rowid.p;
+            r.s_off = sd.off.p;
+            r.s_col = sd.col.p;
+            r.s_val = sd.val.p;
+            r.sched = sd.sched.p;
+        }
         if (st.n && lc.p) {
             r.stiles = st.p;
             r.umeta = um.p;
@@ -118,7 +134,7 @@ int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, 
     };
     if (a->peers.empty()) {
         if (stencil_handles(a, m)) return launch_stencil_spmm(ctx, a, m, x, y, ctl, epi);
-        return launch_spmm(ctx->stream, tiles(a->tiles_all, a->long_all, a->stiles_all, a->umeta_all, a->ucols_all, a->lcol_all), a->n, nullptr, a->off.p, a->col.p, a->val.p, m, x,
+        return launch_spmm(ctx->stream, tiles(a->tiles_all, a->long_all, a->stiles_all, a->umeta_all, a->ucols_all, a->lcol_all, a->sorted_all), a->n, nullptr, a->off.p, a->col.p, a->val.p, m, x,
                            y, ctl, ctx->num_sms, epi);
     }
     Comm* cm = ctx->comm;
@@ -198,11 +214,11 @@ int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, 
     }
     // interior rows overlap the exchange; boundary rows wait for the halo
     launches += launch_spmm(ctx->stream, tiles(a->tiles_interior, a->long_interior, a->stiles_interior, a->umeta_interior,
-                                                      a->ucols_interior, a->lcol_split), a->n_interior, a->interior_rows.p, a->off.p,
+                                                      a->ucols_interior, a->lcol_split, a->sorted_interior), a->n_interior, a->interior_rows.p, a->off.p,
                             a->col.p, a->val.p, m, x, y, ctl, ctx->num_sms, epi);
     side_to_main(ctx);
     launches += launch_spmm(ctx->stream, tiles(a->tiles_boundary, a->long_boundary, a->stiles_boundary, a->umeta_boundary,
-                                                      a->ucols_boundary, a->lcol_split), a->n_boundary, a->boundary_rows.p, a->off.p,
+                                                      a->ucols_boundary, a->lcol_split, a->sorted_boundary), a->n_boundary, a->boundary_rows.p, a->off.p,
                             a->col.p, a->val.p, m, x, y, ctl, ctx->num_sms, epi);
     return launches;
 }

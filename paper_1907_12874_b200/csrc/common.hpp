@@ -158,6 +158,16 @@ struct mbg_csr {
     mbg::DevBuf<int32_t> ucols_all, ucols_interior, ucols_boundary;
     mbg::DevBuf<uint16_t> lcol_all, lcol_split;    // per nonzero, for the all / interior+boundary tilings
     double stage_reuse = 0.0;
+    // length-sorted twins of the row classes (spmm.cu build_sorted_twin): built
+    // when the natural row order leaves warps waiting on their longest row
+    struct SortedDev {
+        mbg::DevBuf<int32_t> off, col, rowid, long_rows;
+        mbg::DevBuf<double> val;
+        mbg::DevBuf<int4> tiles;
+        mbg::DevBuf<int> sched;               // {next tile, finished blocks}, self-rewinding
+    };
+    SortedDev sorted_all, sorted_interior, sorted_boundary;
+    double lane_efficiency = 1.0;             // spmm_lane_efficiency of the natural order
     struct Peer {
         int rank;
         int64_t send_count, recv_count;

@@ -30,6 +30,16 @@ struct SpmmTiles {
     const int32_t* ucols = nullptr;
     const uint16_t* lcol = nullptr;      // indexed by the global nonzero k
     int64_t scount = 0;
+    // length-sorted twin (build_sorted_twin): `tiles` then index slots of the
+    // row-permuted copy (s_off / s_col / s_val) and rowid[slot] is the row the
+    // slot's result belongs to; long_rows stay original row ids
+    const int32_t* rowid = nullptr;
+    const int32_t* s_off = nullptr;
+    const int32_t* s_col = nullptr;
+    const double* s_val = nullptr;
+    // {next tile, finished blocks}: the twin's tiles differ in work (rows of one
+    // length per tile), so blocks claim them from a counter instead of striding
+    int* sched = nullptr;
 };
 // Optional fused epilogue of the SpMM y = A x (beyond-paper merge):
 //   kind 1: slot[0] += exact (y, aux)                    e.g. delta = (v, r0)
@@ -44,8 +54,27 @@ struct SpmmEpi {
 int launch_spmm(cudaStream_t st, const SpmmTiles& tl, int64_t nrows, const int32_t* rows, const int32_t* off,
                 const int32_t* col, const double* val, int m, const double* x, double* y, const int* ctl,
                 int num_sms, const SpmmEpi* epi = nullptr);
-std::vector<int4> build_spmm_tiles(const std::vector<int32_t>& off, const std::vector<int32_t>& rows);
+std::vector<int4> build_spmm_tiles(const std::vector<int32_t>& off, const std::vector<int32_t>& rows,
+                                   bool sorted = false);
 std::vector<int32_t> long_rows_of(const std::vector<int4>& tiles);
+
+// Length-sorted twin of one row class (SELL-C-sigma's sigma step without the
+// padding): inside windows of `window` consecutive rows of the class the rows
+// are stored by descending length, every row's nonzeros in their CSR order, so
+// the lanes of a warp and the warps of a tile walk rows of (nearly) one length
+// and finish together.  Only the storage order of the rows changes: each
+// (row, column) sum is the same sequence of operations.
+struct SortedTwin {
+    std::vector<int32_t> off, col, rowid;
+    std::vector<double> val;
+    std::vector<int4> tiles;          // over slots
+    std::vector<int32_t> long_rows;   // original row ids of the one-row tiles beyond SPMM_TILE_NNZ
+};
+// Share of the gather slots of 8-row warps (batches of 4 nonzeros) that do
+// useful work in the natural row order; the twin is built below ~0.92.
+double spmm_lane_efficiency(const std::vector<int32_t>& off, const std::vector<int32_t>& rows);
+void build_sorted_twin(const std::vector<int32_t>& off, const int32_t* col, const double* val,
+                       const std::vector<int32_t>& rows, int window, SortedTwin& out);
 
 // Gather-once tiling: tiles of <= STAGE_ROWS rows, <= STAGE_NNZ nonzeros and
 // <= STAGE_UCOLS distinct columns.  lcol (size >= nnz, shared by disjoint row

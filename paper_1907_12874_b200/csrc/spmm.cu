@@ -80,13 +80,20 @@ __device__ __forceinline__ void spmm_epi_row(double (&ex)[ND * VW][KEXP], const 
 // EPI: 0 plain; 1/2/3 fused dot epilogues (kernels.hpp SpmmEpi kinds); 4 plain
 // for long rows (> 12 nonzeros on average) at m = 32: 6 gathers in flight per
 // lane, 3-block register budget.
-template <int M, int EPI>
+// SORTED: the length-sorted twin (build_sorted_twin) -- slots instead of rows,
+// every row padded to a multiple of 4 nonzeros (column -1 = padding) so that a
+// lane reads 4 columns and 4 values with three 16-byte shared-memory loads
+// instead of eight narrow ones (the load/store pipe, shared by the x gathers
+// and these reads, is what bounds the kernel at m = 8), and tiles claimed from
+// a counter.
+template <int M, int EPI, bool SORTED = false>
 __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_tma_kernel(const int4* __restrict__ tiles, int ntiles,
                                                        const int32_t* __restrict__ off,
                                                        const int32_t* __restrict__ col,
                                                        const double* __restrict__ val,
                                                        const double* __restrict__ x, double* __restrict__ y,
-                                                       const int* __restrict__ ctl, SpmmEpi epi) {
+                                                       const int* __restrict__ ctl, SpmmEpi epi,
+                                                       const int32_t* __restrict__ rowid, int* sched) {
     pdl_wait();
     if (ctl && ctl[0]) return;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -101,9 +108,18 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
     }
     __syncthreads();
 
+    // sched == nullptr: block b walks tiles b, b + grid, ...; else (length-sorted
+    // twin: tiles of unequal work) the next unclaimed tile, a tile row of -1
+    // telling the block that none is left
     auto issue = [&](int i, int b) {
-        const int t = blockIdx.x + i * gridDim.x;
-        if (t >= ntiles) return;
+        const int t = SORTED ? atomicAdd(&sched[0], 1) : static_cast<int>(blockIdx.x + i * gridDim.x);
+        if (t >= ntiles) {
+            if constexpr (SORTED) {
+                meta[b] = make_int4(-1, 0, 0, 0);
+                mbar_arrive(&bars[b]);
+            }
+            return;
+        }
         const int4 tl = tiles[t];
         const int r0a = tl.x & ~3, r1a = (tl.y + 1 + 3) & ~3;
         const int k0a = tl.z & ~3, k1a = (tl.w + 3) & ~3;
@@ -143,12 +159,12 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
     auto epilogue = [&](int row, double t0, double t1) { spmm_epi_row<M, EPI, VW, ND>(ex, epi, cp, row, t0, t1, x); };
 
     for (int i = 0;; ++i) {
-        const int t = blockIdx.x + i * gridDim.x;
-        if (t >= ntiles) break;
+        if (!SORTED && static_cast<int>(blockIdx.x + i * gridDim.x) >= ntiles) break;
         const int b = i % STAGES;
         while (!mbar_try_wait(&bars[b], static_cast<uint32_t>((i / STAGES) & 1))) {
         }
         const int4 mt = meta[b];
+        if (SORTED && mt.x < 0) break;   // claimed past the last tile
         const int r0 = mt.x, r1 = mt.y, r0a = mt.z, k0a = mt.w;
         const unsigned char* buf = bufs + b * BUF_BYTES;
         const int32_t* s_off = reinterpret_cast<const int32_t*>(buf);
@@ -160,41 +176,59 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
             // spmm_long_rows_kernel; only its fused epilogue runs here
             if constexpr (EPI >= 1 && EPI <= 3) {
                 if (tid < LPR) {
+                    const int row = SORTED ? rowid[r0] : r0;
                     double a0, a1 = 0.0;
                     if constexpr (VW == 2) {
-                        const double2 yv = *reinterpret_cast<const double2*>(y + static_cast<int64_t>(r0) * M + cp);
+                        const double2 yv = *reinterpret_cast<const double2*>(y + static_cast<int64_t>(row) * M + cp);
                         a0 = yv.x;
                         a1 = yv.y;
                     } else {
-                        a0 = y[r0];
+                        a0 = y[row];
                     }
-                    epilogue(r0, a0, a1);
+                    epilogue(row, a0, a1);
                 }
             }
         } else {
             const int32_t* cs = s_col - k0a;   // index with the global k
             const double* vs = s_val - k0a;
             for (int rr = tid / LPR; rr < r1 - r0; rr += RPP) {
-                const int row = r0 + rr;
-                const int k0 = s_off[row - r0a], k1 = s_off[row + 1 - r0a];
+                // slot = position in the (possibly length-sorted) row storage;
+                // row = where its result goes (sorted twin: rowid[slot])
+                const int slot = r0 + rr;
+                const int row = SORTED ? __ldg(rowid + slot) : slot;
+                const int k0 = s_off[slot - r0a], k1 = s_off[slot + 1 - r0a];
                 double a0 = 0.0, a1 = 0.0;
                 // batches of BATCH nonzeros: index/value loads, then the gathers, then
                 // the ordered adds (BATCH gathers in flight per lane)
                 for (int k = k0; k < k1; k += BATCH) {
                     int j[BATCH];
                     double va[BATCH];
+                    bool ok[BATCH];
+                    if constexpr (SORTED) {
+                        static_assert(!SORTED || BATCH == 4, "padded rows come in groups of 4");
+                        const int4 jj = *reinterpret_cast<const int4*>(cs + k);
+                        const double2 v01 = *reinterpret_cast<const double2*>(vs + k);
+                        const double2 v23 = *reinterpret_cast<const double2*>(vs + k + 2);
+                        j[0] = jj.x; j[1] = jj.y; j[2] = jj.z; j[3] = jj.w;
+                        va[0] = v01.x; va[1] = v01.y; va[2] = v23.x; va[3] = v23.y;
 #pragma unroll
-                    for (int q = 0; q < BATCH; ++q)
-                        if (k + q < k1) { j[q] = cs[k + q]; va[q] = vs[k + q]; }
+                        for (int q = 0; q < BATCH; ++q) ok[q] = j[q] >= 0;
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < BATCH; ++q) {
+                            ok[q] = k + q < k1;
+                            if (ok[q]) { j[q] = cs[k + q]; va[q] = vs[k + q]; }
+                        }
+                    }
                     if constexpr (VW == 2) {
                         double2 xa[BATCH];
 #pragma unroll
                         for (int q = 0; q < BATCH; ++q)
-                            if (k + q < k1)
+                            if (ok[q])
                                 xa[q] = __ldg(reinterpret_cast<const double2*>(x + static_cast<int64_t>(j[q]) * M + cp));
 #pragma unroll
                         for (int q = 0; q < BATCH; ++q)
-                            if (k + q < k1) {
+                            if (ok[q]) {
                                 a0 = __dadd_rn(a0, __dmul_rn(va[q], xa[q].x));
                                 a1 = __dadd_rn(a1, __dmul_rn(va[q], xa[q].y));
                             }
@@ -202,10 +236,10 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
                         double xa[BATCH];
 #pragma unroll
                         for (int q = 0; q < BATCH; ++q)
-                            if (k + q < k1) xa[q] = __ldg(x + j[q]);
+                            if (ok[q]) xa[q] = __ldg(x + j[q]);
 #pragma unroll
                         for (int q = 0; q < BATCH; ++q)
-                            if (k + q < k1) a0 = __dadd_rn(a0, __dmul_rn(va[q], xa[q]));
+                            if (ok[q]) a0 = __dadd_rn(a0, __dmul_rn(va[q], xa[q]));
                     }
                 }
                 if constexpr (VW == 2)
@@ -222,6 +256,17 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
         if (tid == 0) issue(i + STAGES, b);
     }
     pdl_trigger();
+    if (SORTED && tid == 0) {
+        // the last block out rewinds the tile counter for the next launch (the
+        // fences order every block's claims before its count and the rewind
+        // after the last count)
+        __threadfence();
+        const unsigned last = gridDim.x - 1;
+        if (atomicInc(reinterpret_cast<unsigned*>(&sched[1]), last) == last) {
+            __threadfence();
+            atomicExch(&sched[0], 0);
+        }
+    }
     if constexpr (EPI >= 1 && EPI <= 3) {
         // no bulk copy is in flight any more: the stage memory is free scratch
         double* sh = reinterpret_cast<double*>(bufs);
@@ -450,21 +495,33 @@ __global__ void __launch_bounds__(256) spmm_generic_kernel(int64_t nrows, const 
     y[row * m + c] = acc;
 }
 
+template <int M, int EPI, bool SORTED>
+static void launch_tma_s(cudaStream_t st, const SpmmTiles& tl, const int32_t* off, const int32_t* col,
+                         const double* val, const double* x, double* y, const int* ctl, int num_sms,
+                         const SpmmEpi& epi) {
+    const int occ =
+        kernel_occupancy(reinterpret_cast<const void*>(&spmm_tma_kernel<M, EPI, SORTED>), 256, SPMM_SMEM);
+    const int grid = static_cast<int>(std::min<int64_t>(tl.count, static_cast<int64_t>(num_sms) * occ));
+    launch_pdl(spmm_tma_kernel<M, EPI, SORTED>, dim3(grid), dim3(256), SPMM_SMEM, st, tl.tiles,
+               static_cast<int>(tl.count), off, col, val, x, y, ctl, epi, tl.rowid, tl.sched);
+}
+
 template <int M, int EPI>
 static void launch_tma(cudaStream_t st, const SpmmTiles& tl, const int32_t* off, const int32_t* col,
                        const double* val, const double* x, double* y, const int* ctl, int num_sms,
                        const SpmmEpi& epi) {
-    const int occ = kernel_occupancy(reinterpret_cast<const void*>(&spmm_tma_kernel<M, EPI>), 256, SPMM_SMEM);
-    const int grid = static_cast<int>(std::min<int64_t>(tl.count, static_cast<int64_t>(num_sms) * occ));
-    launch_pdl(spmm_tma_kernel<M, EPI>, dim3(grid), dim3(256), SPMM_SMEM, st, tl.tiles, static_cast<int>(tl.count),
-               off, col, val, x, y, ctl, epi);
+    if constexpr (EPI != 4 && M >= 8) {   // apply_operator offers the twin from m = 8
+        if (tl.rowid) return launch_tma_s<M, EPI, true>(st, tl, off, col, val, x, y, ctl, num_sms, epi);
+    }
+    if (tl.rowid) throw Invalid("spmv: internal: length-sorted twin below m = 8");
+    launch_tma_s<M, EPI, false>(st, tl, off, col, val, x, y, ctl, num_sms, epi);
 }
 
 template <int M>
 static void launch_tma_epi(cudaStream_t st, const SpmmTiles& tl, const int32_t* off, const int32_t* col,
                            const double* val, const double* x, double* y, const int* ctl, int num_sms,
                            const SpmmEpi* epi) {
-    if ((!epi || epi->kind == 0) && tl.long_rows_hint && M >= 32)
+    if ((!epi || epi->kind == 0) && tl.long_rows_hint && M >= 32 && !tl.rowid)
         launch_tma<M, 4>(st, tl, off, col, val, x, y, ctl, num_sms, SpmmEpi{});
     else if (!epi || epi->kind == 0)
         launch_tma<M, 0>(st, tl, off, col, val, x, y, ctl, num_sms, SpmmEpi{});
@@ -521,6 +578,11 @@ int launch_spmm(cudaStream_t st, const SpmmTiles& tl, int64_t nrows, const int32
             static_cast<int>(tl.nlong), tl.long_rows, off, col, val, m, x, y, ctl);
         ++launched;
     }
+    if (tl.rowid) {   // the tile kernel walks the length-sorted twin
+        off = tl.s_off;
+        col = tl.s_col;
+        val = tl.s_val;
+    }
     switch (m) {
         case 1: launch_tma_epi<1>(st, tl, off, col, val, x, y, ctl, num_sms, epi); break;
         case 2: launch_tma_epi<2>(st, tl, off, col, val, x, y, ctl, num_sms, epi); break;
@@ -530,6 +592,7 @@ int launch_spmm(cudaStream_t st, const SpmmTiles& tl, int64_t nrows, const int32
         case 32: launch_tma_epi<32>(st, tl, off, col, val, x, y, ctl, num_sms, epi); break;
         default: {
             if (epi && epi->kind != 0) throw Invalid("spmv: fused epilogue needs m in {1,2,4,8,16,32}");
+            if (tl.rowid) throw Invalid("spmv: internal: sorted twin with a generic m");
             const int64_t total = nrows * m;
             spmm_generic_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(nrows, rows, off, col,
                                                                                             val, m, x, y, ctl);
@@ -603,7 +666,58 @@ static bool tile_align() {
     return on;
 }
 
-std::vector<int4> build_spmm_tiles(const std::vector<int32_t>& off, const std::vector<int32_t>& rows) {
+double spmm_lane_efficiency(const std::vector<int32_t>& off, const std::vector<int32_t>& rows) {
+    int64_t useful = 0, slots = 0;
+    for (size_t i = 0; i < rows.size(); i += 8) {
+        int mx = 0;
+        const size_t e = std::min(rows.size(), i + 8);
+        for (size_t j = i; j < e; ++j) {
+            const int b = (off[rows[j] + 1] - off[rows[j]] + 3) / 4;
+            useful += b;
+            mx = std::max(mx, b);
+        }
+        slots += static_cast<int64_t>(mx) * static_cast<int64_t>(e - i);
+    }
+    return slots ? static_cast<double>(useful) / static_cast<double>(slots) : 1.0;
+}
+
+void build_sorted_twin(const std::vector<int32_t>& off, const int32_t* col, const double* val,
+                       const std::vector<int32_t>& rows, int window, SortedTwin& out) {
+    out = SortedTwin{};
+    const size_t n = rows.size();
+    out.rowid.resize(n);
+    std::vector<int32_t> idx;
+    for (size_t w0 = 0; w0 < n; w0 += static_cast<size_t>(window)) {
+        const size_t w1 = std::min(n, w0 + static_cast<size_t>(window));
+        idx.assign(rows.begin() + static_cast<std::ptrdiff_t>(w0), rows.begin() + static_cast<std::ptrdiff_t>(w1));
+        std::stable_sort(idx.begin(), idx.end(),
+                         [&](int32_t a, int32_t b) { return off[a + 1] - off[a] > off[b + 1] - off[b]; });
+        std::copy(idx.begin(), idx.end(), out.rowid.begin() + static_cast<std::ptrdiff_t>(w0));
+    }
+    // every row starts at a multiple of 4 entries; padding: column -1, value 0
+    out.off.resize(n + 1);
+    out.off[0] = 0;
+    for (size_t s = 0; s < n; ++s) {
+        const int64_t next = static_cast<int64_t>(out.off[s]) + ((off[out.rowid[s] + 1] - off[out.rowid[s]] + 3) & ~3);
+        if (next > INT32_MAX - 64) throw Invalid("csr: the padded length-sorted copy needs 64-bit offsets");
+        out.off[s + 1] = static_cast<int32_t>(next);
+    }
+    const size_t nnz = static_cast<size_t>(out.off[n]);
+    out.col.assign(nnz, -1);
+    out.val.assign(nnz, 0.0);
+    for (size_t s = 0; s < n; ++s) {
+        const int32_t r = out.rowid[s];
+        std::copy(col + off[r], col + off[r + 1], out.col.begin() + out.off[s]);
+        std::copy(val + off[r], val + off[r + 1], out.val.begin() + out.off[s]);
+    }
+    std::vector<int32_t> slots(n);
+    for (size_t s = 0; s < n; ++s) slots[s] = static_cast<int32_t>(s);
+    out.tiles = build_spmm_tiles(out.off, slots, /*sorted=*/true);
+    for (const auto& t : out.tiles)
+        if (t.w - t.z > SPMM_TILE_NNZ) out.long_rows.push_back(out.rowid[t.x]);
+}
+
+std::vector<int4> build_spmm_tiles(const std::vector<int32_t>& off, const std::vector<int32_t>& rows, bool sorted) {
     std::vector<int4> out;
     size_t i = 0;
     while (i < rows.size()) {
@@ -623,7 +737,9 @@ std::vector<int4> build_spmm_tiles(const std::vector<int32_t>& off, const std::v
         // its grid it runs on the stencil twin anyway; MBG_TILE_ALIGN=0: off)
         if (tile_align() && r1 - r0 < SPMM_TILE_ROWS) {
             const int len = r1 - r0;
-            const int al = len >= 64 ? (len & ~63) : (len >= 16 ? (len & ~15) : len);
+            // (length-sorted twin: a tile's rows have one length, the longest
+            // ones -- 60 rows of 32 -- keep their single nearly full pass)
+            const int al = len >= 64 ? (len & ~63) : (len >= 16 && !sorted ? (len & ~15) : len);
             j -= static_cast<size_t>(len - al);
             r1 = r0 + al;
         }

@@ -258,3 +258,37 @@ def test_method_schedule_fused_pipelined():
     # (formed for the line-4 dots, recomputed in the line-7/12 pass): 22 (merged 26)
     s = P.method_schedule_pc("pipebicgstab", "fused")
     assert s["vec"] == 22 and s["reductions"] == [3, 4]
+
+
+def test_sorted_twin_plan_properties():
+    """Host logic of the CSR SpMM's length-sorted twin: a permutation of the
+    rows, descending lengths inside each window, stable (ties keep the row
+    order), tiles partition the slots within the stage capacity (every row
+    padded to a multiple of 4 nonzeros)."""
+    rng = np.random.default_rng(5)
+    n, window = 10_000, 512
+    lens = rng.integers(0, 41, n)
+    lens[[17, 4000]] = [1920, 3000]          # one row at the stage capacity, one beyond it
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    plan = P.sorted_twin_plan(off, window)
+    rowid = plan["rowid"]
+    assert np.array_equal(np.sort(rowid), np.arange(n))
+    for w0 in range(0, n, window):
+        seg = rowid[w0:w0 + window]
+        assert seg.min() >= w0 and seg.max() < min(n, w0 + window)
+        ls = lens[seg]
+        assert np.all(np.diff(ls) <= 0)
+        for v in np.unique(ls):                  # stable: equal lengths keep ascending rows
+            assert np.all(np.diff(seg[ls == v]) > 0)
+    tiles = plan["tiles"]
+    soff = np.concatenate([[0], np.cumsum((lens[rowid] + 3) & ~3)])   # rows padded to groups of 4
+    assert tiles[0, 0] == 0 and tiles[-1, 1] == n
+    assert np.array_equal(tiles[1:, 0], tiles[:-1, 1])
+    assert np.array_equal(tiles[:, 2], soff[tiles[:, 0]]) and np.array_equal(tiles[:, 3], soff[tiles[:, 1]])
+    nnz_t = tiles[:, 3] - tiles[:, 2]
+    rows_t = tiles[:, 1] - tiles[:, 0]
+    assert np.all(rows_t >= 1) and np.all(rows_t <= 192)
+    assert np.all((nnz_t <= 1920) | (rows_t == 1))
+    assert 0.5 < plan["lane_efficiency"] < 0.9
+    # uniform rows: nothing to gain
+    assert P.sorted_twin_plan(np.arange(0, 7 * 1000 + 1, 7), 4096)["lane_efficiency"] == 1.0
