@@ -131,8 +131,15 @@ int mbg_csr_upload_any_order(mbg_ctx* ctx, int64_t n, const int64_t* offsets, co
  * P A P^T (8x8x4 bricks; each row keeps its summation order) used for the m
  * the stencil twin does not cover.  Results are bitwise identical (exact dots). */
 int mbg_csr_set_grid(mbg_ctx* ctx, mbg_csr* a, int nx, int ny, int nz);
+/* mbg_csr_upload and mbg_csr_upload_partitioned detect a lexicographic 7- or
+ * 27-point grid operator themselves (the longest row's column offsets give
+ * nx, ny, nz; every row is then verified on the device), so the reference's
+ * own calls -- CsrMatrix + core::spmv / solve, no grid argument anywhere --
+ * reach the stencil twin; MBG_AUTO_GRID=0 turns the detection off and
+ * mbg_csr_clear_grid drops a twin (A/B measurements of the CSR path). */
+int mbg_csr_clear_grid(mbg_csr* a);
 int mbg_csr_reordered(const mbg_csr* a);   /* 1 when the solver uses a reordered twin */
-/* Stencil twin built by mbg_csr_set_grid when every nonzero couples a grid
+/* Stencil twin built at upload or by mbg_csr_set_grid when every nonzero couples a grid
  * point with itself or one of its 26 neighbours: 7 (face neighbours only) or
  * 27; 0 = none.  The SpMM then reads no column indices and stages x as TMA
  * plane boxes (m in {4, 8, 16, 32}; bitwise the CSR result; MBG_STENCIL=0 off). */

@@ -175,6 +175,10 @@ public:
         check(mbg_csr_set_grid(dev_->get(), h_, nx, ny, nz));
         return mbg_csr_stencil_kind(h_);
     }
+    // The upload detects a lexicographic 7- / 27-point grid operator itself
+    // (mbstab_b200.h); stencil_kind() tells, clear_grid() drops the twin.
+    int stencil_kind() const { return mbg_csr_stencil_kind(h_); }
+    void clear_grid() { check(mbg_csr_clear_grid(h_)); }
     ~DeviceMatrix() { if (h_) mbg_csr_free(h_); }
     DeviceMatrix(const DeviceMatrix&) = delete;
     DeviceMatrix& operator=(const DeviceMatrix&) = delete;

@@ -222,6 +222,11 @@ class DeviceCsr:
         check(lib().mbg_csr_set_grid(self.ctx.h, self.h, nx, ny, nz))
         return bool(lib().mbg_csr_reordered(self.h))
 
+    def clear_grid(self) -> None:
+        """Drop the stencil twin (detected at upload or set by set_grid): the
+        SpMM takes the CSR path (A/B measurements)."""
+        check(lib().mbg_csr_clear_grid(self.h))
+
     @property
     def stencil_kind(self) -> int:
         """7 or 27 when the stencil twin is in place, else 0."""

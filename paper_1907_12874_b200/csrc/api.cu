@@ -339,6 +339,60 @@ static void csr_to_device(mbg_ctx* ctx, mbg_csr* a, int64_t n, const int64_t* of
     csr_arrays_to_device(ctx, a, n, off32, col, val, nnz);
 }
 
+// Structured-grid detection at upload (the reference's operator API has no
+// grid call: a maintainer who swaps core::spmv / solve gets the stencil twin
+// without one).  The longest row of a lexicographic 7- or 27-point operator
+// is an interior point whose column offsets spell the grid: {+-1, +-nx,
+// +-nx*ny} or dz*nx*ny + dy*nx + dx.  The guess is then verified against
+// every row on the device (build_stencil); anything else keeps the CSR path.
+// MBG_AUTO_GRID=0 turns the detection off.
+static bool infer_grid(int64_t n, const int64_t* off, const int32_t* col, int& nx, int& ny, int& nz) {
+    if (const char* e = std::getenv("MBG_AUTO_GRID"))
+        if (e[0] == '0') return false;
+    if (n < 27) return false;
+    int64_t best = 0, len = 0;
+    for (int64_t i = 0; i < n; ++i)
+        if (off[i + 1] - off[i] > len) {
+            len = off[i + 1] - off[i];
+            best = i;
+        }
+    if (len != 7 && len != 27) return false;
+    std::vector<int64_t> pos;   // the positive offsets, ascending (columns are sorted)
+    for (int64_t k = off[best]; k < off[best + 1]; ++k) {
+        const int64_t d = col[k] - best;
+        if (d > 0) pos.push_back(d);
+    }
+    const size_t half = static_cast<size_t>(len / 2);
+    if (pos.size() != half || col[off[best] + static_cast<int64_t>(half)] != best) return false;
+    for (size_t i = 0; i < half; ++i)   // symmetric pattern
+        if (col[off[best] + static_cast<int64_t>(half) - 1 - static_cast<int64_t>(i)] - best != -pos[i]) return false;
+    const int64_t gx = len == 7 ? pos[1] : pos[2], gxy = len == 7 ? pos[2] : pos[8];
+    if (pos[0] != 1 || gx < 3 || gxy % gx || n % gxy || gxy / gx < 3 || n / gxy < 3 || gx > INT32_MAX) return false;
+    if (len == 27) {
+        const int64_t want[13] = {1, gx - 1, gx, gx + 1, gxy - gx - 1, gxy - gx, gxy - gx + 1, gxy - 1, gxy, gxy + 1,
+                                  gxy + gx - 1, gxy + gx, gxy + gx + 1};
+        for (int i = 0; i < 13; ++i)
+            if (pos[static_cast<size_t>(i)] != want[i]) return false;
+    }
+    nx = static_cast<int>(gx);
+    ny = static_cast<int>(gxy / gx);
+    nz = static_cast<int>(n / gxy);
+    return true;
+}
+
+static void detect_grid(mbg_ctx* ctx, mbg_csr* a, int64_t n, const int64_t* off, const int32_t* col) {
+    int nx = 0, ny = 0, nz = 0;
+    if (a->stencil || !infer_grid(n, off, col, nx, ny, nz)) return;
+    a->stencil = build_stencil(ctx, a, nx, ny, nz);   // nullptr unless every row fits the grid
+}
+
+extern "C" int mbg_csr_clear_grid(mbg_csr* a) {
+    return guarded([&] {
+        if (!a) throw Invalid("clear_grid: null matrix");
+        a->stencil.reset();
+    });
+}
+
 extern "C" int mbg_csr_upload(mbg_ctx* ctx, int64_t n, const int64_t* off, const int32_t* col,
                               const double* val, mbg_csr** out) {
     return guarded([&] {
@@ -351,6 +405,7 @@ extern "C" int mbg_csr_upload(mbg_ctx* ctx, int64_t n, const int64_t* off, const
             a->device = ctx->device;
             a->n_global = n;
             csr_to_device(ctx, a, n, off, col, val);
+            detect_grid(ctx, a, n, off, col);
         } catch (...) {
             delete a;
             throw;
@@ -442,6 +497,7 @@ extern "C" int mbg_csr_upload_partitioned(mbg_ctx* ctx, int64_t n, const int64_t
                 a->transposed =
                     csr_from_plan(ctx, n, bounds[my_part], nparts,
                                   build_transpose_plan(n, off, col, val, nparts, bounds, my_part));
+            detect_grid(ctx, a, n, off, col);   // z-slabs of whole planes get the twin of their slab
             MBG_CUDA(cudaStreamSynchronize(ctx->stream));
         } catch (...) {
             delete a;

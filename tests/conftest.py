@@ -9,6 +9,13 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(Path(__file__).resolve().parent))
 
 
+# The upload detects 7- / 27-point grid operators and gives them the stencil
+# twin (tests/test_gpu_autogrid.py covers that).  Everywhere else the tests
+# decide themselves which SpMM a matrix takes (set_grid = stencil twin, none =
+# the CSR kernels), so the detection is off unless a test turns it on.
+os.environ.setdefault("MBG_AUTO_GRID", "0")
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
     config.addinivalue_line("markers", "slow: large-size cases")

@@ -18,7 +18,7 @@ def bits(x):
     return np.ascontiguousarray(x, dtype=np.float64).view(np.int64)
 
 
-def run_partitioned(a, b, m, bounds, method, form, grid=None, **kw):
+def run_partitioned(a, b, m, bounds, method, form, grid=None, expect_stencil=None, **kw):
     world = len(bounds) - 1
     ctxs = [P.Context(0) for _ in range(world)]
     P.local_group(ctxs)
@@ -32,6 +32,8 @@ def run_partitioned(a, b, m, bounds, method, form, grid=None, **kw):
             if grid is not None:   # z-slab on the stencil twin
                 d.set_grid(*grid)
                 assert d.stencil_kind in (7, 27), "slab stencil twin not built"
+            if expect_stencil is not None:   # detected by the partitioned upload itself
+                assert d.stencil_kind == expect_stencil, d.stencil_kind
             r0, r1 = bounds[r], bounds[r + 1]
             B = ctxs[r].multivector(r1 - r0, m, b[r0 * m:r1 * m])
             X = ctxs[r].multivector(r1 - r0, m)

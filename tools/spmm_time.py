@@ -25,6 +25,8 @@ ctx = P.Context(0)
 d = ctx.upload(a)
 if args.hint and args.kind != "banded":
     d.set_grid(g, g, g)
+else:
+    d.clear_grid()   # the upload detects grid operators: without --hint time the CSR kernels
 m = args.m
 X = ctx.multivector(a.n_rows, m, P.gen_rhs(a.n_rows, m, 1))
 Y = ctx.multivector(a.n_rows, m)

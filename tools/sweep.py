@@ -50,6 +50,8 @@ def main():
                 d = ctx.upload(a)
                 if kind != "banded" and not args.natural:
                     d.set_grid(*dims)   # brick-reordered twin for long-row stencils (C3)
+                elif args.natural:
+                    d.clear_grid()      # drop the stencil twin the upload detects: CSR kernels
                 cache[key] = (a, d, time.time() - t)
             a, d, tgen = cache[key]
             b = P.gen_rhs(a.n_rows, m, seed)
