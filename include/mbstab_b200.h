@@ -152,19 +152,22 @@ int64_t mbg_csr_nnz(const mbg_csr* a);    /* local nnz */
  * tiles, e.g. 27-point stencils; MBG_SPMM_STAGE=0/1 forces it off/on),
  * reuse = nonzeros per distinct column per tile of that tiling (0 if none). */
 int mbg_csr_stage_info(const mbg_csr* a, int* staged, double* reuse);
-/* sorted = 1 when the CSR SpMM walks a length-sorted twin of the rows (rows
- * stored by descending length inside windows of 4096 and padded to groups of
- * 4 nonzeros, each row's nonzeros in CSR order: spmv.cpp:38-47's per-row sums
- * are unchanged, only which lane computes which row); lane_efficiency = share of the natural order's gather
+/* sorted = 1 when the CSR SpMM (m >= 8) walks a length-sorted twin of the rows:
+ * rows stored by descending length inside windows of 4096, in groups of 8
+ * whose nonzeros lie batch-major (4 per batch, padded), each row's nonzeros in
+ * CSR order: spmv.cpp:38-47's per-row sums are unchanged, only which lane
+ * computes which row; lane_efficiency = share of the natural order's gather
  * slots that do useful work (the twin is built below 0.92, e.g. the random
  * band of BASELINE config 5; MBG_SPMM_SORT=0/1 forces it off/on). */
 int mbg_csr_sort_info(const mbg_csr* a, int* sorted, double* lane_efficiency);
-/* Host-only view of that twin's plan (no device): rowid[n] = the row stored in
- * each slot, tiles[4*ntiles] = (slot0, slot1, k0, k1) per tile with k indexing
- * the permuted nonzeros, every row padded to a multiple of 4 entries; call
- * with tiles == NULL for ntiles first. */
-int mbg_sorted_twin_plan(int64_t n, const int64_t* offsets, int window, int32_t* rowid, double* lane_efficiency,
-                         int64_t* ntiles, int32_t* tiles);
+/* Host-only view of that twin's plan (no device).  rowid[nslots] = the row
+ * stored in each slot (-1: padding of the last group; nslots <= n + 7: rows
+ * of more than 240 nonzeros come last, one slot each, and go to the long-row
+ * kernel); group_off[g] = first batch of group g (8 slots), n/8 + 2 entries;
+ * tiles[4*ntiles] = (slot0, slot1, batch0, batch1) of whole groups, batch0 = -1
+ * for a long row's slot.  Call with the array arguments NULL for the sizes. */
+int mbg_sorted_twin_plan(int64_t n, const int64_t* offsets, int window, int64_t* nslots, int32_t* rowid,
+                         double* lane_efficiency, int64_t* ntiles, int32_t* tiles, int32_t* group_off);
 
 /* ---- multivector: n x m fp64, row-interleaved (element (i,c) at i*m+c) -- */
 int mbg_mv_alloc(mbg_ctx* ctx, int64_t n, int m, mbg_mv** out);

@@ -493,16 +493,18 @@ def solve_host(ctx: Context, a: DeviceCsr, b: np.ndarray, x: np.ndarray, m: int,
 # ---------------------------------------------------------------------------
 def sorted_twin_plan(row_offsets, window: int = 4096) -> dict:
     """Host-only plan of the CSR SpMM's length-sorted twin: the row stored in
-    each slot, the tile list over slots and the natural order's lane efficiency."""
+    each slot (-1 = padding), the groups' first batches, the tile list and the
+    natural order's lane efficiency."""
     off = np.ascontiguousarray(row_offsets, dtype=np.int64)
     n = off.size - 1
-    rowid = np.empty(max(1, n), np.int32)
-    eff, nt = C.c_double(0.0), C.c_int64(0)
-    check(lib().mbg_sorted_twin_plan(n, _ptr(off), window, _ptr(rowid), C.byref(eff), C.byref(nt), None))
+    eff, nt, ns = C.c_double(0.0), C.c_int64(0), C.c_int64(0)
+    check(lib().mbg_sorted_twin_plan(n, _ptr(off), window, C.byref(ns), None, C.byref(eff), C.byref(nt), None, None))
+    rowid = np.empty(max(1, ns.value), np.int32)
     tiles = np.empty(max(1, 4 * nt.value), np.int32)
-    check(lib().mbg_sorted_twin_plan(n, _ptr(off), window, None, None, C.byref(nt), _ptr(tiles)))
-    return {"rowid": rowid[:n].copy(), "tiles": tiles[: 4 * nt.value].reshape(-1, 4).copy(),
-            "lane_efficiency": float(eff.value)}
+    goff = np.empty(n // 8 + 2, np.int32)
+    check(lib().mbg_sorted_twin_plan(n, _ptr(off), window, None, _ptr(rowid), None, None, _ptr(tiles), _ptr(goff)))
+    return {"rowid": rowid[: ns.value].copy(), "tiles": tiles[: 4 * nt.value].reshape(-1, 4).copy(),
+            "group_off": goff, "lane_efficiency": float(eff.value)}
 
 
 def halo_plan(a: CsrMatrix, bounds: Sequence[int], my_part: int, transpose: bool = False) -> dict:

@@ -96,7 +96,7 @@ def lib() -> C.CDLL:
         "mbg_csr_nnz": (i64, [vp]),
         "mbg_csr_stage_info": (i32, [vp, vp, vp]),
         "mbg_csr_sort_info": (i32, [vp, vp, vp]),
-        "mbg_sorted_twin_plan": (i32, [i64, vp, i32, vp, vp, vp, vp]),
+        "mbg_sorted_twin_plan": (i32, [i64, vp, i32, vp, vp, vp, vp, vp, vp]),
         "mbg_csr_upload_any_order": (i32, [vp, i64, vp, vp, vp, pp]),
         "mbg_csr_set_grid": (i32, [vp, vp, i32, i32, i32]),
         "mbg_csr_clear_grid": (i32, [vp]),

@@ -629,8 +629,8 @@ extern "C" int mbg_csr_sort_info(const mbg_csr* a, int* sorted, double* lane_eff
     });
 }
 
-extern "C" int mbg_sorted_twin_plan(int64_t n, const int64_t* off, int window, int32_t* rowid,
-                                    double* lane_efficiency, int64_t* ntiles, int32_t* tiles) {
+extern "C" int mbg_sorted_twin_plan(int64_t n, const int64_t* off, int window, int64_t* nslots, int32_t* rowid,
+                                    double* lane_efficiency, int64_t* ntiles, int32_t* tiles, int32_t* group_off) {
     return guarded([&] {
         if (n < 0 || !off) throw Invalid("sorted twin plan: null offsets");
         if (window < 1) throw Invalid("sorted twin plan: window < 1");
@@ -643,7 +643,9 @@ extern "C" int mbg_sorted_twin_plan(int64_t n, const int64_t* off, int window, i
         std::vector<double> val(static_cast<size_t>(off32[n]), 0.0);
         SortedTwin t;
         build_sorted_twin(off32, col.data(), val.data(), rows, window, t);
+        if (nslots) *nslots = static_cast<int64_t>(t.rowid.size());
         if (rowid) std::copy(t.rowid.begin(), t.rowid.end(), rowid);
+        if (group_off) std::copy(t.off.begin(), t.off.end(), group_off);
         if (ntiles) *ntiles = static_cast<int64_t>(t.tiles.size());
         if (tiles)
             for (size_t i = 0; i < t.tiles.size(); ++i) {

@@ -81,11 +81,14 @@ __device__ __forceinline__ void spmm_epi_row(double (&ex)[ND * VW][KEXP], const 
 // for long rows (> 12 nonzeros on average) at m = 32: 6 gathers in flight per
 // lane, 3-block register budget.
 // SORTED: the length-sorted twin (build_sorted_twin) -- slots instead of rows,
-// every row padded to a multiple of 4 nonzeros (column -1 = padding) so that a
-// lane reads 4 columns and 4 values with three 16-byte shared-memory loads
-// instead of eight narrow ones (the load/store pipe, shared by the x gathers
-// and these reads, is what bounds the kernel at m = 8), and tiles claimed from
-// a counter.
+// in groups of 8 slots whose nonzeros are stored batch-major (batch = 4
+// nonzeros; column -1 = padding): for batch b the 8 rows' column quadruples
+// are 128 contiguous bytes and their value pairs 2 x 128, so a lane reads 4
+// columns and 4 values with three 16-byte shared-memory loads and the 8 rows a
+// warp walks hit 8 different bank groups -- one wavefront per load, not the 2-8
+// of rows stored one after the other (the load/store pipe, shared by the x
+// gathers and these reads, is what bounds the kernel at m = 8).  `off` holds
+// the groups' cumulative batch counts; tiles are claimed from a counter.
 template <int M, int EPI, bool SORTED = false>
 __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_tma_kernel(const int4* __restrict__ tiles, int ntiles,
                                                        const int32_t* __restrict__ off,
@@ -121,6 +124,23 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
             return;
         }
         const int4 tl = tiles[t];
+        if constexpr (SORTED) {
+            // (slot0, slot1, first batch, end batch) of whole groups; a negative
+            // batch marks a row beyond a stage (long-row kernel; epilogue only)
+            meta[b] = tl;
+            if (tl.z < 0) {
+                mbar_arrive(&bars[b]);
+                return;
+            }
+            unsigned char* buf = bufs + b * BUF_BYTES;
+            const uint32_t cnt = static_cast<uint32_t>(tl.w - tl.z) * 32u;   // entries (8 rows x 4 per batch)
+            mbar_expect_tx(&bars[b], cnt * 12u);
+            if (cnt) {
+                bulk_g2s(buf + OFF_CAP * 4, col + static_cast<int64_t>(tl.z) * 32, cnt * 4u, &bars[b]);
+                bulk_g2s(buf + OFF_CAP * 4 + NNZ_PAD * 4, val + static_cast<int64_t>(tl.z) * 32, cnt * 8u, &bars[b]);
+            }
+            return;
+        }
         const int r0a = tl.x & ~3, r1a = (tl.y + 1 + 3) & ~3;
         const int k0a = tl.z & ~3, k1a = (tl.w + 3) & ~3;
         const bool lng = tl.w - tl.z > SPMM_TILE_NNZ;
@@ -170,7 +190,7 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
         const int32_t* s_off = reinterpret_cast<const int32_t*>(buf);
         const int32_t* s_col = reinterpret_cast<const int32_t*>(buf + OFF_CAP * 4);
         const double* s_val = reinterpret_cast<const double*>(buf + OFF_CAP * 4 + NNZ_PAD * 4);
-        const bool lng = s_off[r1 - r0a] - s_off[r0 - r0a] > SPMM_TILE_NNZ;
+        const bool lng = SORTED ? mt.z < 0 : s_off[r1 - r0a] - s_off[r0 - r0a] > SPMM_TILE_NNZ;
         if (lng) {
             // a row longer than the stage capacity was multiplied beforehand by
             // spmm_long_rows_kernel; only its fused epilogue runs here
@@ -193,22 +213,35 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
             const double* vs = s_val - k0a;
             for (int rr = tid / LPR; rr < r1 - r0; rr += RPP) {
                 // slot = position in the (possibly length-sorted) row storage;
-                // row = where its result goes (sorted twin: rowid[slot])
+                // row = where its result goes (sorted twin: rowid[slot], -1 = no row)
                 const int slot = r0 + rr;
                 const int row = SORTED ? __ldg(rowid + slot) : slot;
-                const int k0 = s_off[slot - r0a], k1 = s_off[slot + 1 - r0a];
+                int k0, k1;
+                const int4* c4 = nullptr;
+                const double2* v2 = nullptr;
+                if constexpr (SORTED) {
+                    // batches of this slot's group: [k0, k1) counts batches, not nonzeros
+                    const int g = slot >> 3;
+                    k0 = __ldg(off + g) - r0a;        // r0a = the tile's first batch
+                    k1 = __ldg(off + g + 1) - r0a;
+                    c4 = reinterpret_cast<const int4*>(s_col) + k0 * 8 + (slot & 7);
+                    v2 = reinterpret_cast<const double2*>(s_val) + k0 * 16 + (slot & 7);
+                } else {
+                    k0 = s_off[slot - r0a];
+                    k1 = s_off[slot + 1 - r0a];
+                }
                 double a0 = 0.0, a1 = 0.0;
                 // batches of BATCH nonzeros: index/value loads, then the gathers, then
                 // the ordered adds (BATCH gathers in flight per lane)
-                for (int k = k0; k < k1; k += BATCH) {
+                for (int k = k0; k < k1; k += SORTED ? 1 : BATCH) {
                     int j[BATCH];
                     double va[BATCH];
                     bool ok[BATCH];
                     if constexpr (SORTED) {
-                        static_assert(!SORTED || BATCH == 4, "padded rows come in groups of 4");
-                        const int4 jj = *reinterpret_cast<const int4*>(cs + k);
-                        const double2 v01 = *reinterpret_cast<const double2*>(vs + k);
-                        const double2 v23 = *reinterpret_cast<const double2*>(vs + k + 2);
+                        static_assert(!SORTED || BATCH == 4, "the twin stores batches of 4");
+                        const int4 jj = c4[(k - k0) * 8];
+                        const double2 v01 = v2[(k - k0) * 16];
+                        const double2 v23 = v2[(k - k0) * 16 + 8];
                         j[0] = jj.x; j[1] = jj.y; j[2] = jj.z; j[3] = jj.w;
                         va[0] = v01.x; va[1] = v01.y; va[2] = v23.x; va[3] = v23.y;
 #pragma unroll
@@ -242,6 +275,7 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
                             if (ok[q]) a0 = __dadd_rn(a0, __dmul_rn(va[q], xa[q]));
                     }
                 }
+                if (SORTED && row < 0) continue;   // a padding slot of the last group
                 if constexpr (VW == 2)
                     *reinterpret_cast<double2*>(y + static_cast<int64_t>(row) * M + cp) = make_double2(a0, a1);
                 else
@@ -684,37 +718,70 @@ double spmm_lane_efficiency(const std::vector<int32_t>& off, const std::vector<i
 void build_sorted_twin(const std::vector<int32_t>& off, const int32_t* col, const double* val,
                        const std::vector<int32_t>& rows, int window, SortedTwin& out) {
     out = SortedTwin{};
-    const size_t n = rows.size();
-    out.rowid.resize(n);
+    // rows beyond a stage (a group's batches must fit one) go to the long-row kernel
+    constexpr int MAX_BATCHES = SPMM_TILE_NNZ / 32;
+    std::vector<int32_t> reg;
+    reg.reserve(rows.size());
+    for (int32_t r : rows) {
+        if ((off[r + 1] - off[r] + 3) / 4 > MAX_BATCHES) out.long_rows.push_back(r);
+        else reg.push_back(r);
+    }
+    const size_t n = reg.size();
+    const size_t nslots = (n + 7) & ~size_t(7);
+    out.rowid.assign(nslots + out.long_rows.size(), -1);
     std::vector<int32_t> idx;
     for (size_t w0 = 0; w0 < n; w0 += static_cast<size_t>(window)) {
         const size_t w1 = std::min(n, w0 + static_cast<size_t>(window));
-        idx.assign(rows.begin() + static_cast<std::ptrdiff_t>(w0), rows.begin() + static_cast<std::ptrdiff_t>(w1));
+        idx.assign(reg.begin() + static_cast<std::ptrdiff_t>(w0), reg.begin() + static_cast<std::ptrdiff_t>(w1));
         std::stable_sort(idx.begin(), idx.end(),
                          [&](int32_t a, int32_t b) { return off[a + 1] - off[a] > off[b + 1] - off[b]; });
         std::copy(idx.begin(), idx.end(), out.rowid.begin() + static_cast<std::ptrdiff_t>(w0));
     }
-    // every row starts at a multiple of 4 entries; padding: column -1, value 0
-    out.off.resize(n + 1);
-    out.off[0] = 0;
-    for (size_t s = 0; s < n; ++s) {
-        const int64_t next = static_cast<int64_t>(out.off[s]) + ((off[out.rowid[s] + 1] - off[out.rowid[s]] + 3) & ~3);
-        if (next > INT32_MAX - 64) throw Invalid("csr: the padded length-sorted copy needs 64-bit offsets");
-        out.off[s + 1] = static_cast<int32_t>(next);
+    // groups of 8 slots, each with the batches of its longest row
+    const size_t G = nslots / 8;
+    out.off.assign(G + 1, 0);
+    for (size_t g = 0; g < G; ++g) {
+        int nb = 0;
+        for (int r8 = 0; r8 < 8; ++r8) {
+            const int32_t r = out.rowid[g * 8 + r8];
+            if (r >= 0) nb = std::max(nb, (off[r + 1] - off[r] + 3) / 4);
+        }
+        const int64_t next = static_cast<int64_t>(out.off[g]) + nb;
+        if (next * 32 > INT32_MAX - 64) throw Invalid("csr: the length-sorted copy needs 64-bit offsets");
+        out.off[g + 1] = static_cast<int32_t>(next);
     }
-    const size_t nnz = static_cast<size_t>(out.off[n]);
-    out.col.assign(nnz, -1);
-    out.val.assign(nnz, 0.0);
-    for (size_t s = 0; s < n; ++s) {
-        const int32_t r = out.rowid[s];
-        std::copy(col + off[r], col + off[r + 1], out.col.begin() + out.off[s]);
-        std::copy(val + off[r], val + off[r + 1], out.val.begin() + out.off[s]);
+    // batch-major inside a group: columns [batch][row][4], values [batch][half][row][2]
+    const size_t entries = static_cast<size_t>(out.off[G]) * 32;
+    out.col.assign(entries, -1);
+    out.val.assign(entries, 0.0);
+    for (size_t g = 0; g < G; ++g)
+        for (int r8 = 0; r8 < 8; ++r8) {
+            const int32_t r = out.rowid[g * 8 + r8];
+            if (r < 0) continue;
+            const int len = off[r + 1] - off[r];
+            for (int e = 0; e < len; ++e) {
+                const size_t b = static_cast<size_t>(out.off[g]) + static_cast<size_t>(e / 4);
+                const int q = e & 3;
+                out.col[(b * 8 + static_cast<size_t>(r8)) * 4 + static_cast<size_t>(q)] = col[off[r] + e];
+                out.val[((b * 2 + static_cast<size_t>(q >> 1)) * 8 + static_cast<size_t>(r8)) * 2 + static_cast<size_t>(q & 1)] =
+                    val[off[r] + e];
+            }
+        }
+    // tiles of whole groups: <= SPMM_TILE_ROWS slots, <= MAX_BATCHES batches; one cut by
+    // the batch cap keeps a multiple of 64 slots (whole block passes at m = 8)
+    size_t g = 0;
+    while (g < G) {
+        size_t h = g;
+        while (h < G && (h - g) * 8 < static_cast<size_t>(SPMM_TILE_ROWS) && out.off[h + 1] - out.off[g] <= MAX_BATCHES) ++h;
+        if ((h - g) * 8 < static_cast<size_t>(SPMM_TILE_ROWS) && h < G && h - g >= 8) h = g + ((h - g) & ~size_t(7));
+        out.tiles.push_back(make_int4(static_cast<int>(g * 8), static_cast<int>(h * 8), out.off[g], out.off[h]));
+        g = h;
     }
-    std::vector<int32_t> slots(n);
-    for (size_t s = 0; s < n; ++s) slots[s] = static_cast<int32_t>(s);
-    out.tiles = build_spmm_tiles(out.off, slots, /*sorted=*/true);
-    for (const auto& t : out.tiles)
-        if (t.w - t.z > SPMM_TILE_NNZ) out.long_rows.push_back(out.rowid[t.x]);
+    // one epilogue-only tile per long row (slot after the groups, batch -1)
+    for (size_t i = 0; i < out.long_rows.size(); ++i) {
+        out.rowid[nslots + i] = out.long_rows[i];
+        out.tiles.push_back(make_int4(static_cast<int>(nslots + i), static_cast<int>(nslots + i + 1), -1, -1));
+    }
 }
 
 std::vector<int4> build_spmm_tiles(const std::vector<int32_t>& off, const std::vector<int32_t>& rows, bool sorted) {

@@ -80,11 +80,11 @@ def test_spmv_sorted_forced(ctx, mname, m, window):
 
 @pytest.mark.parametrize("m", [1, 2, 3, 8, 32])
 def test_spmv_sorted_ragged_long_and_empty_rows(ctx, m):
-    """Empty rows, rows at a stage's capacity (1920) and beyond it (multiplied
-    by the long-row kernel); m = 3 takes the generic kernel on the original
-    storage."""
-    n = 6000
-    a = ragged(n, 11, long_rows={5: 1919, 700: 1920, 701: 1921, 3000: 5000, 5999: 2500})
+    """Empty rows, rows at the twin's longest (240 nonzeros = the 60 batches of
+    a stage) and beyond it (multiplied by the long-row kernel); m = 3 takes the
+    generic kernel on the original storage."""
+    n = 6001                      # not a multiple of 8: the last group has padding slots
+    a = ragged(n, 11, long_rows={5: 239, 6: 240, 7: 241, 700: 1920, 701: 1921, 3000: 5000, 5999: 2500})
     x = np.random.default_rng(m).standard_normal(n * m)
     with env(MBG_SPMM_SORT_WINDOW=512):
         d = ctx.upload(to_prod(a))
@@ -94,6 +94,37 @@ def test_spmv_sorted_ragged_long_and_empty_rows(ctx, m):
     Y.fill(7.0)
     P.spmv(ctx, d, X, Y)
     assert_bitwise(Y.download(), O.spmv(a, x, m), f"ragged sorted spmv m={m}")
+
+
+@pytest.mark.parametrize("m", [8, 16])
+def test_solve_sorted_long_rows_fused_epilogue(ctx, m):
+    """Fused SpMM epilogues (exact dots of finished rows) when some rows take
+    the long-row kernel: their terms come from the epilogue-only tiles."""
+    n = 3000
+    rng = np.random.default_rng(3)
+    off, cols, vals = [0], [], []
+    for i in range(n):
+        k = 400 if i in (11, 1500) else int(rng.integers(3, 12))
+        c = np.unique(np.concatenate([[i], rng.choice(n, size=k - 1, replace=False)])).astype(np.int32)
+        v = -rng.random(c.size)
+        v[c == i] = 1.1 * (np.abs(v).sum() + 1.0)       # diagonally dominant
+        cols.append(c)
+        vals.append(v)
+        off.append(off[-1] + c.size)
+    a = O.Csr(n, np.array(off, np.int64), np.concatenate(cols), np.concatenate(vals))
+    b = O.rhs(n, m, 7)
+    ctx.set_small_path(False)
+    try:
+        with env(MBG_SPMM_SORT=1):
+            d = ctx.upload(to_prod(a))
+        assert d.sort_info()[0]
+        for method in ("bicgstab", "rbicgstab"):
+            want = O.solve(a, b, m, method, "fused", 1e-8, True, 12)
+            B, X = ctx.multivector(n, m, b), ctx.multivector(n, m)
+            rep = P.solve(ctx, d, B, X, method, "fused", 1e-8, True, 12)
+            assert_same_solve(want, rep, X, f"long rows {method} m={m}")
+    finally:
+        ctx.set_small_path(True)
 
 
 @pytest.mark.parametrize("form", ["merged", "basic", "fused"])

@@ -262,33 +262,39 @@ def test_method_schedule_fused_pipelined():
 
 def test_sorted_twin_plan_properties():
     """Host logic of the CSR SpMM's length-sorted twin: a permutation of the
-    rows, descending lengths inside each window, stable (ties keep the row
-    order), tiles partition the slots within the stage capacity (every row
-    padded to a multiple of 4 nonzeros)."""
+    rows (long rows last, one slot each), descending lengths inside each
+    window, stable (ties keep the row order), groups of 8 slots with the
+    batches of their longest row, tiles of whole groups within a stage."""
     rng = np.random.default_rng(5)
-    n, window = 10_000, 512
+    n, window = 10_001, 512
     lens = rng.integers(0, 41, n)
-    lens[[17, 4000]] = [1920, 3000]          # one row at the stage capacity, one beyond it
+    lens[[17, 4000, 9000]] = [240, 241, 3000]   # the longest row of the twin, two beyond it
     off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
     plan = P.sorted_twin_plan(off, window)
-    rowid = plan["rowid"]
-    assert np.array_equal(np.sort(rowid), np.arange(n))
-    for w0 in range(0, n, window):
-        seg = rowid[w0:w0 + window]
-        assert seg.min() >= w0 and seg.max() < min(n, w0 + window)
+    rowid, tiles, goff = plan["rowid"], plan["tiles"], plan["group_off"]
+    nreg = n - 2
+    nslots = (nreg + 7) // 8 * 8
+    assert rowid.size == nslots + 2
+    assert list(rowid[nslots:]) == [4000, 9000]
+    assert np.all(rowid[nreg:nslots] == -1)
+    assert np.array_equal(np.sort(rowid[rowid >= 0]), np.arange(n))
+    reg = np.array([r for r in range(n) if r not in (4000, 9000)])
+    for w0 in range(0, nreg, window):
+        seg = rowid[w0:min(nreg, w0 + window)]
+        assert set(seg.tolist()) == set(reg[w0:w0 + window].tolist())
         ls = lens[seg]
         assert np.all(np.diff(ls) <= 0)
         for v in np.unique(ls):                  # stable: equal lengths keep ascending rows
             assert np.all(np.diff(seg[ls == v]) > 0)
-    tiles = plan["tiles"]
-    soff = np.concatenate([[0], np.cumsum((lens[rowid] + 3) & ~3)])   # rows padded to groups of 4
-    assert tiles[0, 0] == 0 and tiles[-1, 1] == n
-    assert np.array_equal(tiles[1:, 0], tiles[:-1, 1])
-    assert np.array_equal(tiles[:, 2], soff[tiles[:, 0]]) and np.array_equal(tiles[:, 3], soff[tiles[:, 1]])
-    nnz_t = tiles[:, 3] - tiles[:, 2]
-    rows_t = tiles[:, 1] - tiles[:, 0]
-    assert np.all(rows_t >= 1) and np.all(rows_t <= 192)
-    assert np.all((nnz_t <= 1920) | (rows_t == 1))
+    G = nslots // 8
+    nb = np.array([max([(lens[r] + 3) // 4 for r in rowid[8 * g:8 * g + 8] if r >= 0], default=0) for g in range(G)])
+    assert np.array_equal(goff[:G + 1], np.concatenate([[0], np.cumsum(nb)]))
+    reg_t, long_t = tiles[tiles[:, 2] >= 0], tiles[tiles[:, 2] < 0]
+    assert reg_t[0, 0] == 0 and reg_t[-1, 1] == nslots
+    assert np.array_equal(reg_t[1:, 0], reg_t[:-1, 1]) and np.all(reg_t[:, 0] % 8 == 0)
+    assert np.array_equal(reg_t[:, 2], goff[reg_t[:, 0] // 8]) and np.array_equal(reg_t[:, 3], goff[reg_t[:, 1] // 8])
+    assert np.all(reg_t[:, 3] - reg_t[:, 2] <= 60) and np.all(reg_t[:, 1] - reg_t[:, 0] <= 192)
+    assert np.array_equal(long_t[:, 0], [nslots, nslots + 1]) and np.all(long_t[:, 3] == -1)
     assert 0.5 < plan["lane_efficiency"] < 0.9
     # uniform rows: nothing to gain
     assert P.sorted_twin_plan(np.arange(0, 7 * 1000 + 1, 7), 4096)["lane_efficiency"] == 1.0
