@@ -285,7 +285,9 @@ __global__ void __launch_bounds__(256, EPI == 0 ? 4 : (EPI == 2 ? 2 : 3)) spmm_t
         }
         // (a warp-asynchronous release of the stage -- last warp out refills --
         // measured 6% slower on C3: warps drifting onto different tiles split
-        // the L1 working set that the 27-point gathers depend on)
+        // the L1 working set that the 27-point gathers depend on; on the
+        // length-sorted twin of config 5's band it changes nothing at m = 8 / 16
+        // and loses 1-6 % at m = 32)
         __syncthreads();  // every thread is done with stage b
         if (tid == 0) issue(i + STAGES, b);
     }
