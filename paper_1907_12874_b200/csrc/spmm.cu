@@ -24,7 +24,9 @@
 #include <cstdint>
 #include <algorithm>
 #include <cstdlib>
+#include <thread>
 #include <type_traits>
+#include <vector>
 
 #include "common.hpp"
 #include "kernels.hpp"
@@ -717,6 +719,26 @@ double spmm_lane_efficiency(const std::vector<int32_t>& off, const std::vector<i
     return slots ? static_cast<double>(useful) / static_cast<double>(slots) : 1.0;
 }
 
+// Host helper: fn(begin, end) over [0, n) in chunks that are multiples of
+// `grain`, on up to 16 threads (the twin of an 8M-row matrix is built at upload).
+template <class F>
+static void host_parallel(size_t n, size_t grain, F fn) {
+    const size_t units = (n + grain - 1) / grain;
+    const unsigned nt = static_cast<unsigned>(
+        std::min<size_t>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())), std::max<size_t>(1, units / 64)));
+    if (nt <= 1) {
+        fn(size_t(0), n);
+        return;
+    }
+    std::vector<std::thread> th;
+    const size_t per = (units + nt - 1) / nt * grain;
+    for (unsigned t = 0; t < nt; ++t) {
+        const size_t b = std::min(n, t * per), e = std::min(n, (t + 1) * per);
+        if (b < e) th.emplace_back([=] { fn(b, e); });
+    }
+    for (auto& x : th) x.join();
+}
+
 void build_sorted_twin(const std::vector<int32_t>& off, const int32_t* col, const double* val,
                        const std::vector<int32_t>& rows, int window, SortedTwin& out) {
     out = SortedTwin{};
@@ -731,14 +753,16 @@ void build_sorted_twin(const std::vector<int32_t>& off, const int32_t* col, cons
     const size_t n = reg.size();
     const size_t nslots = (n + 7) & ~size_t(7);
     out.rowid.assign(nslots + out.long_rows.size(), -1);
-    std::vector<int32_t> idx;
-    for (size_t w0 = 0; w0 < n; w0 += static_cast<size_t>(window)) {
-        const size_t w1 = std::min(n, w0 + static_cast<size_t>(window));
-        idx.assign(reg.begin() + static_cast<std::ptrdiff_t>(w0), reg.begin() + static_cast<std::ptrdiff_t>(w1));
-        std::stable_sort(idx.begin(), idx.end(),
-                         [&](int32_t a, int32_t b) { return off[a + 1] - off[a] > off[b + 1] - off[b]; });
-        std::copy(idx.begin(), idx.end(), out.rowid.begin() + static_cast<std::ptrdiff_t>(w0));
-    }
+    host_parallel(n, static_cast<size_t>(window), [&](size_t begin, size_t end) {
+        std::vector<int32_t> idx;
+        for (size_t w0 = begin; w0 < end; w0 += static_cast<size_t>(window)) {
+            const size_t w1 = std::min(n, w0 + static_cast<size_t>(window));
+            idx.assign(reg.begin() + static_cast<std::ptrdiff_t>(w0), reg.begin() + static_cast<std::ptrdiff_t>(w1));
+            std::stable_sort(idx.begin(), idx.end(),
+                             [&](int32_t a, int32_t b) { return off[a + 1] - off[a] > off[b + 1] - off[b]; });
+            std::copy(idx.begin(), idx.end(), out.rowid.begin() + static_cast<std::ptrdiff_t>(w0));
+        }
+    });
     // groups of 8 slots, each with the batches of its longest row
     const size_t G = nslots / 8;
     out.off.assign(G + 1, 0);
@@ -754,21 +778,27 @@ void build_sorted_twin(const std::vector<int32_t>& off, const int32_t* col, cons
     }
     // batch-major inside a group: columns [batch][row][4], values [batch][half][row][2]
     const size_t entries = static_cast<size_t>(out.off[G]) * 32;
-    out.col.assign(entries, -1);
-    out.val.assign(entries, 0.0);
-    for (size_t g = 0; g < G; ++g)
-        for (int r8 = 0; r8 < 8; ++r8) {
-            const int32_t r = out.rowid[g * 8 + r8];
-            if (r < 0) continue;
-            const int len = off[r + 1] - off[r];
-            for (int e = 0; e < len; ++e) {
-                const size_t b = static_cast<size_t>(out.off[g]) + static_cast<size_t>(e / 4);
-                const int q = e & 3;
-                out.col[(b * 8 + static_cast<size_t>(r8)) * 4 + static_cast<size_t>(q)] = col[off[r] + e];
-                out.val[((b * 2 + static_cast<size_t>(q >> 1)) * 8 + static_cast<size_t>(r8)) * 2 + static_cast<size_t>(q & 1)] =
-                    val[off[r] + e];
+    out.col.resize(entries);
+    out.val.resize(entries);
+    host_parallel(G, 1, [&](size_t gb, size_t ge) {   // groups own disjoint ranges of col / val
+        std::fill(out.col.begin() + static_cast<std::ptrdiff_t>(out.off[gb]) * 32,
+                  out.col.begin() + static_cast<std::ptrdiff_t>(out.off[ge]) * 32, -1);
+        std::fill(out.val.begin() + static_cast<std::ptrdiff_t>(out.off[gb]) * 32,
+                  out.val.begin() + static_cast<std::ptrdiff_t>(out.off[ge]) * 32, 0.0);
+        for (size_t g = gb; g < ge; ++g)
+            for (int r8 = 0; r8 < 8; ++r8) {
+                const int32_t r = out.rowid[g * 8 + static_cast<size_t>(r8)];
+                if (r < 0) continue;
+                const int len = off[r + 1] - off[r];
+                for (int e = 0; e < len; ++e) {
+                    const size_t b = static_cast<size_t>(out.off[g]) + static_cast<size_t>(e / 4);
+                    const int q = e & 3;
+                    out.col[(b * 8 + static_cast<size_t>(r8)) * 4 + static_cast<size_t>(q)] = col[off[r] + e];
+                    out.val[((b * 2 + static_cast<size_t>(q >> 1)) * 8 + static_cast<size_t>(r8)) * 2 +
+                            static_cast<size_t>(q & 1)] = val[off[r] + e];
+                }
             }
-        }
+    });
     // tiles of whole groups: <= SPMM_TILE_ROWS slots, <= MAX_BATCHES batches; one cut by
     // the batch cap keeps a multiple of 64 slots (whole block passes at m = 8)
     size_t g = 0;
