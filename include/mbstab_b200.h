@@ -148,9 +148,10 @@ int mbg_csr_free(mbg_csr* a);
 int64_t mbg_csr_rows(const mbg_csr* a);   /* local rows */
 int64_t mbg_csr_nnz(const mbg_csr* a);    /* local nnz */
 /* SpMM kernel choice made at upload (no reference counterpart; diagnostics):
- * staged = 1 when the gather-once tiling is in use (x rows reused inside
- * tiles, e.g. 27-point stencils; MBG_SPMM_STAGE=0/1 forces it off/on),
- * reuse = nonzeros per distinct column per tile of that tiling (0 if none). */
+ * staged = 1 when the gather-once tiling is in use (opt-in, MBG_SPMM_STAGE=1:
+ * x rows reused inside tiles, e.g. 27-point stencils; measured slower than the
+ * register gathers), reuse = nonzeros per distinct column per tile of that
+ * tiling (0 if none). */
 int mbg_csr_stage_info(const mbg_csr* a, int* staged, double* reuse);
 /* sorted = 1 when the CSR SpMM (m >= 8) walks a length-sorted twin of the rows:
  * rows stored by descending length inside windows of 4096, in groups of 8

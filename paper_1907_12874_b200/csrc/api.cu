@@ -127,9 +127,9 @@ extern "C" int mbg_csr_validate(int64_t n, const int64_t* off, const int32_t* co
     return guarded([&] { validate_csr(n, off, col, nnz); });
 }
 
-// Gather-once SpMM tilings (spmm.cu spmm_stage_kernel): built when the tiles
-// reuse x rows (>= 2 nonzeros per distinct column, e.g. 27-point stencils);
-// MBG_SPMM_STAGE=0 / 1 forces them off / on (tests, A/B measurements).
+// Gather-once SpMM tilings (spmm.cu spmm_stage_kernel), for tiles that reuse
+// x rows (>= 2 nonzeros per distinct column, e.g. 27-point stencils): opt-in
+// with MBG_SPMM_STAGE=1 (tests, A/B measurements; measured slower).
 static int stage_mode() {
     const char* e = std::getenv("MBG_SPMM_STAGE");
     return e ? std::atoi(e) : -1;
@@ -139,7 +139,7 @@ static void stage_tilings(mbg_ctx* ctx, mbg_csr* a, const std::vector<int32_t>& 
                           const std::vector<int32_t>* all, const std::vector<int32_t>* interior,
                           const std::vector<int32_t>* boundary) {
     const int mode = stage_mode();
-    if (mode == 0) return;
+    if (mode != 1) return;   // opt-in (measured slower): no O(nnz) host pass at every upload
     const int64_t ncols = a->n + a->n_halo;
     std::vector<uint16_t> lcol(static_cast<size_t>(a->nnz) + 16, 0);
     if (all) {

@@ -94,9 +94,12 @@ Solver::Solver(mbg_ctx* ctx, const mbg_csr* a, int m, int method, int formulatio
     // registers than the separate 2-vector dot pass costs (B200: C3 27-point
     // 8.90 vs 8.07 ms/iteration, C5 m=8 5.28 vs 4.97; C2 7-point 0.76 vs 0.84)
     // (stencil SpMM: only with MBG_STENCIL_EPI=1 -- measured slower)
+    // (MBG_SPMM_EPI_DELTA=0 / 1 forces the CSR choice for A/B measurements)
+    bool csr_delta = a->nnz <= 12 * a->n;
+    if (const char* e = std::getenv("MBG_SPMM_EPI_DELTA")) csr_delta = e[0] != '0';
     epi_delta_ = formulation == MBG_FUSED &&
                  (stencil_ ? (stencil_epilogues() || (method == MBG_RBICGSTAB && stencil_delta_epilogue(a, m)))
-                           : a->nnz <= 12 * a->n);
+                           : csr_delta);
     // fused Reordered on a single-GPU 27-point twin (m = 16 / 32): the th update
     // pass is folded into the second SpMM, th is never stored (2 transfers less)
     ax_ = elide_ && method == MBG_RBICGSTAB && !ctx->comm && stencil_ && stencil_axpy_handles(a, m);
