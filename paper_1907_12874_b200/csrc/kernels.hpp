@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <utility>
 #include <vector>
 
@@ -64,9 +65,27 @@ std::vector<int32_t> long_rows_of(const std::vector<int4>& tiles);
 // the lanes of a warp and the warps of a tile walk rows of (nearly) one length
 // and finish together.  Only the storage order of the rows changes: each
 // (row, column) sum is the same sequence of operations.
+// std::vector without value-initialisation on resize (the twin's 2.4 GB of
+// columns / values are first touched by the threads that fill them)
+template <class T>
+struct DefaultInitAlloc : std::allocator<T> {
+    template <class U>
+    struct rebind { using other = DefaultInitAlloc<U>; };
+    DefaultInitAlloc() = default;
+    template <class U>
+    DefaultInitAlloc(const DefaultInitAlloc<U>&) {}
+    template <class U>
+    void construct(U* p) noexcept { ::new (static_cast<void*>(p)) U; }
+    template <class U, class... A>
+    void construct(U* p, A&&... a) { ::new (static_cast<void*>(p)) U(std::forward<A>(a)...); }
+};
+template <class T>
+using RawVec = std::vector<T, DefaultInitAlloc<T>>;
+
 struct SortedTwin {
-    std::vector<int32_t> off, col, rowid;
-    std::vector<double> val;
+    std::vector<int32_t> off, rowid;
+    RawVec<int32_t> col;
+    RawVec<double> val;
     std::vector<int4> tiles;          // over slots
     std::vector<int32_t> long_rows;   // original row ids of the one-row tiles beyond SPMM_TILE_NNZ
 };

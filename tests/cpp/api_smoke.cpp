@@ -3,6 +3,7 @@
 // and checks it against plain host loops.  Built and run by
 // tests/test_gpu_cpp_api.py on the GPU box.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <vector>
 
@@ -100,12 +101,23 @@ int main() {
         core::CsrMatrix R = core::read_matrix_market(path);
         if (R.values != P5.values || R.col_indices != P5.col_indices) { std::puts("matrix market"); return 1; }
     }
-    // device-resident solve on the stencil twin (structured-grid hint): the
-    // same bits as the CSR operator (exact dots, same summation order)
+    // device-resident solve on the stencil twin -- detected by the upload itself
+    // (no grid call, as in the reference) unless MBG_AUTO_GRID=0, then declared
+    // with set_grid -- and on the CSR kernels (twin dropped): the same bits
+    // (exact dots, same summation order)
     {
         Device dev;
         DeviceMatrix dA(dev, A), dC(dev, A);
+        const char* ag = std::getenv("MBG_AUTO_GRID");
+        if (!(ag && ag[0] == '0')) {
+            if (dA.stencil_kind() != 7) { std::puts("stencil twin not detected at upload"); return 1; }
+        } else if (dA.stencil_kind() != 0) {
+            std::puts("MBG_AUTO_GRID=0 ignored");
+            return 1;
+        }
         if (dA.set_grid(12, 10, 8) != 7) { std::puts("stencil twin not built"); return 1; }
+        dC.clear_grid();
+        if (dC.stencil_kind() != 0) { std::puts("clear_grid"); return 1; }
         const int m8 = 8;
         core::MultiVector B8(A.n_rows, m8), Xs(A.n_rows, m8), Xc(A.n_rows, m8);
         for (std::size_t i = 0; i < B8.data.size(); ++i) B8.data[i] = std::sin(0.1 * double(i));

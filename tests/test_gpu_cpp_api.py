@@ -20,9 +20,13 @@ def test_cpp_api_compiles(tmp_path):
 
 
 @pytest.mark.gpu
-def test_cpp_api_runs(tmp_path):
+@pytest.mark.parametrize("auto_grid", ["1", "0"])
+def test_cpp_api_runs(tmp_path, auto_grid):
+    """auto_grid 1 = the product default: the upload detects the 7-point grid."""
+    import os
     exe = tmp_path / "api_smoke"
     build_demo(exe)
-    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300,
+                       env={**os.environ, "MBG_AUTO_GRID": auto_grid})
     assert r.returncode == 0, r.stdout + r.stderr
     assert "cpp api ok" in r.stdout
