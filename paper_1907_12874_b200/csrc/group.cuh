@@ -36,6 +36,10 @@ struct GroupArgs {
     const double* coef[GMAX_CO]; // device arrays of m doubles
     int64_t* slot[GMAX_DOT];     // long accumulators: m * NSLOT words each
     const int* ctl;              // ctl[0] != 0: solve stopped -> no-op
+    // 1: every thread walks its trips from the last one down, so the pass sweeps
+    // the vectors from their end -- where the pass before it (walking up) left the
+    // L2 warm.  Same elements per thread, exact dots: same bits either way.
+    int reverse;
 };
 
 __device__ __forceinline__ double fmadd_rn(double acc, double c, double v) {
@@ -685,11 +689,17 @@ __global__ void __launch_bounds__(256, minblocks_of<P>::value) group_kernel(Grou
     constexpr bool PF = prefetch_of<P>::value;
     constexpr bool RS = redo_safe_of<P>::value && P::NDOT > 0;
     bool bad = false;
-    if constexpr (PF) load(cur, q);
-    for (; q < npk; q += UNR * stride) {
-        const int64_t qn = q + UNR * stride;
+    // trips of this thread: T of UNR packets each, walked up or (a.reverse) down
+    const int64_t q_first = q, step = UNR * stride;
+    const int64_t T = q_first < npk ? (npk - q_first + step - 1) / step : 0;
+    const int64_t dq = a.reverse ? -step : step;
+    if (a.reverse) q = q_first + (T - 1) * step;
+    if constexpr (PF) {
+        if (T > 0) load(cur, q);
+    }
+    for (int64_t trip = 0; trip < T; ++trip, q += dq) {
         if constexpr (PF) {
-            if (qn < npk) load(nxt, qn);
+            if (trip + 1 < T) load(nxt, q + dq);
         } else {
             load(cur, q);
         }
@@ -764,7 +774,12 @@ __global__ void __launch_bounds__(256, minblocks_of<P>::value) group_kernel(Grou
             for (int d = 0; d < ND * VEC; ++d)
 #pragma unroll
                 for (int i = 0; i < KEXP; ++i) acc[d][i] = 0.0;
-            for (int64_t qr = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; qr < npk; qr += stride) {
+            // (the fast pass's order: trips up or down, the packets of a trip ascending)
+            int64_t qt = a.reverse ? q_first + (T - 1) * step : q_first;
+            for (int64_t trip = 0; trip < T; ++trip, qt += dq)
+            for (int u = 0; u < UNR; ++u) {
+                const int64_t qr = qt + u * stride;
+                if (qr >= npk) break;
                 double in[P::NIN], o0[NO], p0[ND];
                 if constexpr (VEC == 2) {
                     double o1[NO], p1[ND];

@@ -210,6 +210,15 @@ std::string Solver::profile_json() {
     return out + "}";
 }
 
+// Alternating sweep direction of the group passes (solver.hpp rev_next_).
+static bool group_reverse_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("MBG_GROUP_REVERSE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void Solver::spmm(const double* x, double* y, int epi_kind, const double* aux, int post_point, int post_nd,
                   int first_slot, int reduce) {
     SpmmEpi e;
@@ -222,6 +231,7 @@ void Solver::spmm(const double* x, double* y, int epi_kind, const double* aux, i
                    extra);
     launches_ += apply_operator(ctx_, a_, m_, const_cast<double*>(x), y, ctl_.p, epi_kind ? &e : nullptr);
     mark_end();
+    rev_next_ = group_reverse_enabled();
     if (epi_kind) {
         const int nred = reduce < 0 ? (epi_kind == 2 ? 3 : 1) : reduce;
         if (ctx_->comm && nred > 0) {
@@ -239,6 +249,7 @@ void Solver::spmm_axpy(const double* z, const double* v, const double* na, doubl
     mark_begin("spmm+axpy", stencil_spmm_bytes(a_->n, a_->nnz, m_) + 8.0 * len_);
     launches_ += launch_stencil_spmm_axpy(ctx_, a_, m_, z, v, na, y, ctl_.p);
     mark_end();
+    rev_next_ = group_reverse_enabled();
 }
 
 template <class P>
@@ -255,6 +266,8 @@ void Solver::group(std::initializer_list<const double*> in, std::initializer_lis
     for (int s : co) g.coef[i++] = sc(s);
     for (int d = 0; d < P::NDOT; ++d) g.slot[d] = slot(first_slot + d);
     g.ctl = ctl_.p;
+    g.reverse = rev_next_ ? 1 : 0;
+    rev_next_ = group_reverse_enabled() && !rev_next_;
     mark_begin(std::string("group:") + P::NAME, static_cast<double>(P::NIN + P::NOUT) * 8.0 * len_);
     launch_group<P>(ctx_->stream, g, ctx_->num_sms);
     MBG_CUDA(cudaGetLastError());

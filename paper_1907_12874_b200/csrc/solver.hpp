@@ -95,6 +95,10 @@ private:
     int64_t launches_ = 0;
     int64_t reductions_ = 0;
     bool pending_join_ = false;
+    // direction of the next group pass: after an SpMM (which walks up) the first
+    // pass walks down, the next up, ... -- each starts where its predecessor left
+    // the L2 warm (group.cuh GroupArgs::reverse; MBG_GROUP_REVERSE=0 off)
+    bool rev_next_ = false;
     float loop_ms_ = 0.f;
     // profiling
     bool profile_ = false;
