@@ -138,6 +138,9 @@ int mbg_csr_set_grid(mbg_ctx* ctx, mbg_csr* a, int nx, int ny, int nz);
  * reach the stencil twin; MBG_AUTO_GRID=0 turns the detection off and
  * mbg_csr_clear_grid drops a twin (A/B measurements of the CSR path). */
 int mbg_csr_clear_grid(mbg_csr* a);
+/* Host-only: the grid that detection would try for this matrix (0, 0, 0 = none;
+ * no device needed -- the device then verifies every row before the twin is built). */
+int mbg_infer_grid(int64_t n, const int64_t* offsets, const int32_t* cols, int* nx, int* ny, int* nz);
 int mbg_csr_reordered(const mbg_csr* a);   /* 1 when the solver uses a reordered twin */
 /* Stencil twin built at upload or by mbg_csr_set_grid when every nonzero couples a grid
  * point with itself or one of its 26 neighbours: 7 (face neighbours only) or

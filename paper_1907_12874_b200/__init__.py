@@ -491,6 +491,15 @@ def solve_host(ctx: Context, a: DeviceCsr, b: np.ndarray, x: np.ndarray, m: int,
 # ---------------------------------------------------------------------------
 # partition / exact-dot host hooks (used by the multi-rank CPU tests)
 # ---------------------------------------------------------------------------
+def infer_grid(a: CsrMatrix) -> tuple[int, int, int]:
+    """Host-only: the (nx, ny, nz) the upload would try for a lexicographic 7- /
+    27-point grid operator, (0, 0, 0) when the matrix does not look like one."""
+    nx, ny, nz = C.c_int(0), C.c_int(0), C.c_int(0)
+    check(lib().mbg_infer_grid(a.n_rows, _ptr(a.row_offsets), _ptr(a.col_indices), C.byref(nx), C.byref(ny),
+                               C.byref(nz)))
+    return nx.value, ny.value, nz.value
+
+
 def sorted_twin_plan(row_offsets, window: int = 4096) -> dict:
     """Host-only plan of the CSR SpMM's length-sorted twin: the row stored in
     each slot (-1 = padding), the groups' first batches, the tile list and the

@@ -100,6 +100,7 @@ def lib() -> C.CDLL:
         "mbg_csr_upload_any_order": (i32, [vp, i64, vp, vp, vp, pp]),
         "mbg_csr_set_grid": (i32, [vp, vp, i32, i32, i32]),
         "mbg_csr_clear_grid": (i32, [vp]),
+        "mbg_infer_grid": (i32, [i64, vp, vp, vp, vp, vp]),
         "mbg_spmv_transpose": (i32, [vp, vp, vp, vp]),
         "mbg_true_residual": (i32, [vp, vp, vp, vp, vp]),
         "mbg_csr_reordered": (i32, [vp]),

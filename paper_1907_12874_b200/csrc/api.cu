@@ -380,6 +380,22 @@ static bool infer_grid(int64_t n, const int64_t* off, const int32_t* col, int& n
     return true;
 }
 
+// Host-only: the grid the upload would try for this matrix (0 = none).  The
+// guess is verified on the device before the stencil twin is built.
+extern "C" int mbg_infer_grid(int64_t n, const int64_t* off, const int32_t* col, int* nx, int* ny, int* nz) {
+    return guarded([&] {
+        if (n < 0 || !off || !nx || !ny || !nz) throw Invalid("infer_grid: null argument");
+        if (n > 0 && !col) throw Invalid("infer_grid: null columns");
+        *nx = *ny = *nz = 0;
+        int x = 0, y = 0, z = 0;
+        if (infer_grid(n, off, col, x, y, z)) {
+            *nx = x;
+            *ny = y;
+            *nz = z;
+        }
+    });
+}
+
 static void detect_grid(mbg_ctx* ctx, mbg_csr* a, int64_t n, const int64_t* off, const int32_t* col) {
     int nx = 0, ny = 0, nz = 0;
     if (a->stencil || !infer_grid(n, off, col, nx, ny, nz)) return;

@@ -298,3 +298,24 @@ def test_sorted_twin_plan_properties():
     assert 0.5 < plan["lane_efficiency"] < 0.9
     # uniform rows: nothing to gain
     assert P.sorted_twin_plan(np.arange(0, 7 * 1000 + 1, 7), 4096)["lane_efficiency"] == 1.0
+
+
+def test_infer_grid_host_logic(monkeypatch):
+    """Grid detection's host half (api.cu infer_grid): the longest row's column
+    offsets give nx, ny, nz for lexicographic 7- / 27-point operators; other
+    matrices give none."""
+    monkeypatch.setenv("MBG_AUTO_GRID", "1")
+    for kind, dims in (("poisson7", (16, 16, 16)), ("convdiff7", (24, 20, 9)), ("convdiff7", (3, 5, 4)),
+                       ("stencil27", (13, 11, 10)), ("stencil27", (3, 3, 3)), ("stencil27", (40, 3, 7))):
+        a = O.gen_stencil(kind, *dims, seed=2)
+        assert P.infer_grid(P.CsrMatrix(a.n, a.off, a.col, a.val)) == dims, (kind, dims)
+    band = O.gen_banded(5000, 300, 16, 32, 4)
+    assert P.infer_grid(P.CsrMatrix(band.n, band.off, band.col, band.val)) == (0, 0, 0)
+    tiny = O.gen_stencil("poisson7", 2, 2, 2)            # no interior point
+    assert P.infer_grid(P.CsrMatrix(tiny.n, tiny.off, tiny.col, tiny.val)) == (0, 0, 0)
+    # a 2-D five-point operator (one plane) is not a 3-D grid operator
+    flat = O.gen_stencil("poisson7", 12, 12, 1)
+    assert P.infer_grid(P.CsrMatrix(flat.n, flat.off, flat.col, flat.val)) == (0, 0, 0)
+    monkeypatch.setenv("MBG_AUTO_GRID", "0")
+    a = O.gen_stencil("poisson7", 8, 8, 8)
+    assert P.infer_grid(P.CsrMatrix(a.n, a.off, a.col, a.val)) == (0, 0, 0)
