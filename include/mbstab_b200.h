@@ -156,7 +156,7 @@ int64_t mbg_csr_nnz(const mbg_csr* a);    /* local nnz */
  * register gathers), reuse = nonzeros per distinct column per tile of that
  * tiling (0 if none). */
 int mbg_csr_stage_info(const mbg_csr* a, int* staged, double* reuse);
-/* sorted = 1 when the CSR SpMM (m >= 8) walks a length-sorted twin of the rows:
+/* sorted = 1 when the CSR SpMM (m >= 4) walks a length-sorted twin of the rows:
  * rows stored by descending length inside windows of 4096, in groups of 8
  * whose nonzeros lie batch-major (4 per batch, padded), each row's nonzeros in
  * CSR order: spmv.cpp:38-47's per-row sums are unchanged, only which lane

@@ -104,10 +104,11 @@ static void side_to_main(mbg_ctx* ctx) {
 int apply_operator(mbg_ctx* ctx, const mbg_csr* a, int m, double* x, double* y, const int* ctl,
                    const SpmmEpi* epi) {
     const bool hint = a->n > 0 && a->nnz > 12 * a->n;
-    // the length-sorted twin pays off from m = 8 (B200, config 5's random band,
-    // locked clocks: m = 8 -24 %, 16 -36 %, 32 -49 % per SpMM; m <= 4 is bound by
-    // 8- and 16-byte gather wavefronts either way and loses 1-8 % to the scattered y rows)
-    const bool tile_m = m == 8 || m == 16 || m == 32;
+    // the length-sorted twin pays off from m = 4 (B200, config 5's random band,
+    // per SpMM: m = 4 -3 %, 8 -9 %, 16 -8 %, 32 -17 % free-running, -29 / -38 / -50 % at
+    // m = 8 / 16 / 32 at locked clocks; m <= 2 is bound by 8- and 16-byte gather
+    // wavefronts either way and loses 1-8 % to the scattered y rows)
+    const bool tile_m = m == 4 || m == 8 || m == 16 || m == 32;
     auto tiles = [hint, tile_m](const mbg::DevBuf<int4>& t, const mbg::DevBuf<int32_t>& l, const mbg::DevBuf<int4>& st,
                                 const mbg::DevBuf<int2>& um, const mbg::DevBuf<int32_t>& uc,
                                 const mbg::DevBuf<uint16_t>& lc, const mbg_csr::SortedDev& sd) {

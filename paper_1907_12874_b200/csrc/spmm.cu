@@ -548,10 +548,10 @@ template <int M, int EPI>
 static void launch_tma(cudaStream_t st, const SpmmTiles& tl, const int32_t* off, const int32_t* col,
                        const double* val, const double* x, double* y, const int* ctl, int num_sms,
                        const SpmmEpi& epi) {
-    if constexpr (EPI != 4 && M >= 8) {   // apply_operator offers the twin from m = 8
+    if constexpr (EPI != 4 && M >= 4) {   // apply_operator offers the twin from m = 4
         if (tl.rowid) return launch_tma_s<M, EPI, true>(st, tl, off, col, val, x, y, ctl, num_sms, epi);
     }
-    if (tl.rowid) throw Invalid("spmv: internal: length-sorted twin below m = 8");
+    if (tl.rowid) throw Invalid("spmv: internal: length-sorted twin below m = 4");
     launch_tma_s<M, EPI, false>(st, tl, off, col, val, x, y, ctl, num_sms, epi);
 }
 

@@ -63,7 +63,7 @@ def test_sort_heuristic(ctx):
 
 
 @pytest.mark.parametrize("mname", list(MATRICES))
-@pytest.mark.parametrize("m", [4, 8, 16, 32])      # the twin serves m >= 8; m = 4 keeps the natural order
+@pytest.mark.parametrize("m", [2, 4, 8, 16, 32])   # the twin serves m >= 4; m = 2 keeps the natural order
 @pytest.mark.parametrize("window", [64, 4096])
 def test_spmv_sorted_forced(ctx, mname, m, window):
     a = MATRICES[mname]()
