@@ -19,7 +19,13 @@
 //   Sizing (tools/spmm_lab.cu sweep on B200, C2 shape): 4 resident blocks of
 //   256 threads (<= 64 registers, 2 x 24 KB stages) beat deeper pipelines,
 //   larger tiles, wider gather batches and two rows per lane, all of which
-//   trade occupancy for in-flight bytes and lose.
+//   trade occupancy for in-flight bytes and lose.  (A stage of 2048 nonzeros
+//   instead of 1920 pushes the block's shared memory past the 196 KB carve-out
+//   step, leaves L1 28 KB instead of 60 and nearly doubles the SpMM's time.)
+//   * ragged matrices (m >= 4): the same kernel walks a length-sorted twin of
+//     the rows (build_sorted_twin: rows by descending length, groups of 8 stored
+//     batch-major, tiles claimed from a counter) -- see the SORTED template
+//     parameter below and DESIGN.md section 8.
 // Any other m uses a thread-per-(row, column) kernel with the same arithmetic.
 #include <cstdint>
 #include <algorithm>
