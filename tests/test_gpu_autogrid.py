@@ -128,3 +128,21 @@ def test_partitioned_slabs_detected(ctx, world):
         assert np.array_equal(rep.residual_history.view(np.int64), want["hist"].view(np.int64))
         r0, r1 = bounds[r], bounds[r + 1]
         assert np.array_equal(x.view(np.int64), want["x"][r0 * m:r1 * m].view(np.int64))
+
+
+def test_partition_across_planes_keeps_csr(ctx):
+    """Row blocks that cut through a plane cannot take the slab twin: those
+    ranks stay on the CSR kernels (mixed ranks give the same bits)."""
+    nx, ny, nz = 10, 8, 6
+    a = O.gen_stencil("convdiff7", nx, ny, nz, seed=3)
+    m = 8
+    b = O.rhs(a.n, m, 3)
+    bounds = [0, 3 * nx * ny + 17, a.n]          # not a multiple of nx*ny
+    want = O.solve(a, b, m, "bicgstab", "fused", 1e-8)
+    with autogrid():
+        parts = run_partitioned(a, b, m, bounds, "bicgstab", "fused", tol=1e-8, expect_stencil=0)
+    for r, (rep, x) in enumerate(parts):
+        assert rep.iterations == want["iterations"]
+        assert np.array_equal(rep.residual_history.view(np.int64), want["hist"].view(np.int64))
+        r0, r1 = bounds[r], bounds[r + 1]
+        assert np.array_equal(x.view(np.int64), want["x"][r0 * m:r1 * m].view(np.int64))
