@@ -78,6 +78,34 @@ __global__ void __launch_bounds__(256, 4) k(const double2* __restrict__ x, uint3
     if (acc == 1.2345) sink[0] = acc;
 }
 
+// The same nonzeros with 32 bytes of x per lane (ld.global.nc.v4.f64, LDG.E.256):
+// 2 lanes per row, 16 rows per warp, the batch's columns / values from shared
+// memory as in mode "shared" (one 16-byte chunk triple per row).
+__global__ void __launch_bounds__(256, 3) k256(const double* __restrict__ x, uint32_t nrows, int iters, double* sink) {
+    extern __shared__ int4 sm[];
+    const int lane = threadIdx.x & 31, grp = lane >> 1, part = lane & 1;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    for (int i = threadIdx.x; i < 3072; i += 256) sm[i] = make_int4(i, i + 1, i + 2, i + 3);
+    __syncthreads();
+    double acc = 0.0;
+    for (int it = 0; it < iters; ++it) {
+        const int b = ((threadIdx.x >> 1) * 3 + it * 3) % 3069;
+        const int4 c = sm[b], v0 = sm[b + 1], v1 = sm[b + 2];
+        const uint32_t salt = c.x + v0.y + v1.z;
+        double g[4][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t r = mix(gw * 0x9E3779B9u + static_cast<uint32_t>(it) * 131u + grp * 7u + q * 977u + (salt & 1u)) % nrows;
+            const double* p = x + static_cast<int64_t>(r) * 8 + part * 4;
+            asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                         : "=d"(g[q][0]), "=d"(g[q][1]), "=d"(g[q][2]), "=d"(g[q][3]) : "l"(p));
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc += g[q][0] * __int_as_float(v0.x) + g[q][1] + g[q][2] + g[q][3];
+    }
+    if (acc == 1.2345) sink[0] = acc;
+}
+
 int main() {
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -130,6 +158,22 @@ int main() {
         const double nnz = double(grid) * 8 /*warps*/ * 8 /*rows*/ * 4 * iters;
         std::printf("%s\"%s\": {\"ms\": %.3f, \"gather_TBps\": %.2f, \"ns_per_nnz_per_sm\": %.4f}", mode ? ", " : "",
                     names[mode], ms, nnz * 64.0 / (ms * 1e-3) / 1e12, ms * 1e6 / (nnz / sms));
+    }
+    {
+        // 3 blocks of 256 threads per SM (the register budget of 4 x 32-byte gathers per lane)
+        const int grid3 = sms * 3;
+        CK(cudaFuncSetAttribute(k256, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+        k256<<<grid3, 256, 65536>>>(reinterpret_cast<const double*>(x), nrows, 64, sink);
+        CK(cudaEventRecord(a));
+        k256<<<grid3, 256, 65536>>>(reinterpret_cast<const double*>(x), nrows, iters, sink);
+        CK(cudaEventRecord(b));
+        CK(cudaEventSynchronize(b));
+        CK(cudaGetLastError());
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        const double nnz = double(grid3) * 8 * 16 * 4 * iters;
+        std::printf(", \"ldg256_shared\": {\"ms\": %.3f, \"gather_TBps\": %.2f, \"ns_per_nnz_per_sm\": %.4f}", ms,
+                    nnz * 64.0 / (ms * 1e-3) / 1e12, ms * 1e6 / (nnz / sms));
     }
     std::printf("}}\n");
     return 0;
